@@ -1,0 +1,133 @@
+/*
+ * cgf.h — C ABI of the B200-native CG tensor-product kernels (libcgf.so).
+ *
+ * This is the drop-in boundary for the reference's C++ operator API
+ * (/root/reference/proj/include/cgforge/ headers). The reference has no C ABI, no
+ * plugin registry and no FFI: its callers construct engine::TpPlan /
+ * conv::ConvPlan objects directly. Each entry point below replaces one of
+ * those calls (file:line cited per function); INTEGRATION.md shows the ctypes
+ * binding and the header-compatible C++ shim a maintainer would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Array pointers passed to cgf_tp_* and
+ *    cgf_conv_* are DEVICE pointers (CUDA global memory, any allocator); the
+ *    *_host variants take host pointers and do the copies themselves.
+ *  - Layouts are the reference's: row-major [rows x dim], irreps segments
+ *    [mult][2l+1] mult-major, weights concatenated per instruction with kind C
+ *    stored W[w][u] (tpspec.hpp:16-20).
+ *  - Outputs are fully overwritten (the reference zero-fills then accumulates,
+ *    engine.cpp:270-274).
+ *  - `stream` is a CUstream / cudaStream_t (0 = legacy default stream).
+ *  - Every function returns CGF_OK or an error code; the message of the last
+ *    error on the calling thread is cgf_last_error(). Codes map 1:1 onto the
+ *    reference's exception types.
+ *  - No CPU fallback: without a usable CUDA device the compute calls return
+ *    CGF_E_CUDA.
+ */
+#ifndef CGF_H
+#define CGF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum cgf_status {
+  CGF_OK = 0,
+  CGF_E_PARSE = 1,       /* irreps::ParseError, malformed problem JSON (irreps.hpp:58, tpspec.hpp:88-91) */
+  CGF_E_VALIDATION = 2,  /* tpspec::validate violations (tpspec.hpp:70-84) */
+  CGF_E_SHAPE = 3,       /* engine::ShapeError (engine.hpp:62-64) */
+  CGF_E_BUDGET = 4,      /* scheduler::BudgetError (scheduler.hpp:74-76) */
+  CGF_E_TRIANGLE = 5,    /* cg::TriangleError (cg.hpp:40-42) */
+  CGF_E_INVALID = 6,     /* std::invalid_argument, e.g. unsorted edges (conv.cpp:196-205) */
+  CGF_E_CUDA = 7,        /* CUDA driver error / no device */
+  CGF_E_JIT = 8,         /* NVRTC compilation of a generated kernel failed */
+  CGF_E_UNSUPPORTED = 9, /* configuration outside this build's coverage */
+  CGF_E_INTERNAL = 10    /* std::logic_error (engine.cpp:48, 126) */
+};
+
+enum cgf_dtype { CGF_F32 = 0, CGF_F64 = 1 };
+enum cgf_op { CGF_OP_FORWARD = 0, CGF_OP_BACKWARD = 1, CGF_OP_DOUBLE_BACKWARD = 2 };
+
+typedef struct cgf_plan cgf_plan;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* cgf_last_error(void);
+/* Library version string ("cgf <semver> nvrtc <maj.min> sm_100a"). */
+const char* cgf_version(void);
+
+/* ---- descriptors -------------------------------------------------------- */
+
+/* Real-basis CG block <l1 l2 l3>, entries sorted (k,i,j), per-k orthonormal.
+ * Replaces cg::cg_block (cg.hpp:55, cg.cpp:138-160). Returns the entry count
+ * (arrays filled up to cap) or -(error code). */
+int cgf_cg_block(int l1, int l2, int l3, int cap, int* i, int* j, int* k, double* v);
+
+/* Parse + validate + split + plan. Replaces tpspec::parse_problem_json
+ * (tpspec.hpp:88-91) -> scheduler::split_multiplicities (scheduler.hpp:82-84)
+ * -> scheduler::build_schedule (scheduler.hpp:86-89) -> engine::TpPlan ctor
+ * (engine.hpp:73). lane_width: multiplicity split width (<= 0: 32).
+ * budget_words: the reference's per-worker scratch budget; kept for API
+ * parity — a budget below the largest subkernel working set is rejected with
+ * CGF_E_BUDGET exactly as build_schedule does (scheduler.cpp:161-170); 0 means
+ * the reference default 4096. Kernels are generated and compiled lazily. */
+int cgf_plan_create(const char* problem_json, int lane_width, uint32_t budget_words, cgf_plan** out);
+void cgf_plan_destroy(cgf_plan* plan);
+
+/* dims = {dim_x, dim_y, dim_z, total_weights, split_subkernels, units}. */
+int cgf_plan_dims(const cgf_plan* plan, int64_t dims[6]);
+/* Reference flop rule per row (kernelgen::flop_count, kernelgen.cpp:253-276):
+ * flops = {forward, backward, double_backward(= 3 fwd + 4 bwd)}. */
+int cgf_plan_flops(const cgf_plan* plan, uint64_t flops[3]);
+/* Generated CUDA source for (op, dtype, w_shared, aligned); returns its length
+ * (copies up to cap-1 bytes + NUL). Debug / inspection only. */
+int cgf_plan_source(cgf_plan* plan, int op, int dtype, int w_shared, int aligned, char* buf, int cap);
+/* Generate + NVRTC-compile (sm_100a) ahead of time; no device needed. */
+int cgf_plan_compile(cgf_plan* plan, int op, int dtype, int w_shared, int aligned);
+
+/* ---- batched tensor product (device pointers) --------------------------- */
+
+/* z[rows x dim_z] = TP(x, y, W). Replaces TpPlan::forward (engine.hpp:82-83,
+ * engine.cpp:278-283). w_shared != 0: w is ONE row used for every batch row
+ * (a superset of the reference API, which stores W per row). */
+int cgf_tp_forward(cgf_plan* plan, int dtype, const void* x, const void* y, const void* w, void* z,
+                   int64_t rows, int w_shared, void* stream);
+
+/* (gx, gy, gw) = backward(x, y, W, gz). Replaces TpPlan::backward
+ * (engine.hpp:85-87, engine.cpp:285-295). */
+int cgf_tp_backward(cgf_plan* plan, int dtype, const void* x, const void* y, const void* w,
+                    const void* gz, void* gx, void* gy, void* gw, int64_t rows, int w_shared,
+                    void* stream);
+
+/* Given (da, db, dC) = upstream gradients of (gx, gy, gw), returns
+ * (dL/dx, dL/dy, dL/dW, dL/dgz) in one fused pass. Replaces
+ * TpPlan::double_backward (engine.hpp:89-95, engine.cpp:297-392). */
+int cgf_tp_double_backward(cgf_plan* plan, int dtype, const void* x, const void* y, const void* w,
+                           const void* gz, const void* da, const void* db, const void* dc,
+                           void* ox, void* oy, void* ow, void* ogz, int64_t rows, int w_shared,
+                           void* stream);
+
+/* Host-pointer variants: allocate device buffers, copy in, run, copy out,
+ * synchronise. The semantics of the reference's std::vector API
+ * (TpPlan::forward/backward/double_backward on host Batch<T>). */
+int cgf_tp_forward_host(cgf_plan* plan, int dtype, const void* x, const void* y, const void* w,
+                        void* z, int64_t rows, int w_shared);
+int cgf_tp_backward_host(cgf_plan* plan, int dtype, const void* x, const void* y, const void* w,
+                         const void* gz, void* gx, void* gy, void* gw, int64_t rows, int w_shared);
+int cgf_tp_double_backward_host(cgf_plan* plan, int dtype, const void* x, const void* y,
+                                const void* w, const void* gz, const void* da, const void* db,
+                                const void* dc, void* ox, void* oy, void* ow, void* ogz,
+                                int64_t rows, int w_shared);
+
+/* Model-based traffic/flop counters of one call (engine::ExecStats,
+ * engine.hpp:19-30): {loads_words, stores_words, flops} for `rows` rows of
+ * `op` under the compulsory-traffic model (each input read once, each output
+ * written once). */
+int cgf_tp_stats(const cgf_plan* plan, int op, int64_t rows, int w_shared, uint64_t stats[3]);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CGF_H */

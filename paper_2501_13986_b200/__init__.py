@@ -1,0 +1,300 @@
+"""B200-native CG tensor-product kernels (arXiv 2501.13986), Python face.
+
+A thin ctypes binding over ``libcgf.so`` (the C ABI in ``include/cgf.h``) that
+mirrors the reference's C++ operator API (``cgforge::engine::TpPlan``,
+``cgforge::conv::ConvPlan``; /root/reference/proj/include/cgforge/) with the
+same names, argument meaning and error behaviour:
+
+    plan = TpPlan(problem_json)                  # parse -> validate -> split -> plan
+    z = plan.forward(x, y, w)                    # TpPlan::forward   (engine.hpp:82)
+    gx, gy, gw = plan.backward(x, y, w, gz)      # TpPlan::backward  (engine.hpp:85)
+    dx, dy, dw, dgz = plan.double_backward(x, y, w, gz, (da, db, dc))   # (engine.hpp:91)
+
+Arrays are torch CUDA tensors (computed in place on the device, on the current
+stream) or numpy arrays (the host path: copy in, compute, copy out). There is
+no CPU fallback: the compute path is the generated sm_100a kernels, and a
+missing ``libcgf.so`` or CUDA device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcgf.so")
+
+__all__ = [
+    "TpPlan", "cg_block", "lib", "CgfError", "ParseError", "ValidationError", "ShapeError",
+    "BudgetError", "TriangleError", "InvalidArgument", "CudaError", "JitError",
+    "UnsupportedError", "F32", "F64", "OP_FORWARD", "OP_BACKWARD", "OP_DOUBLE_BACKWARD",
+]
+
+F32, F64 = 0, 1
+OP_FORWARD, OP_BACKWARD, OP_DOUBLE_BACKWARD = 0, 1, 2
+
+
+class CgfError(RuntimeError):
+    code = 0
+
+
+class ParseError(CgfError, ValueError):  # irreps::ParseError
+    code = 1
+
+
+class ValidationError(CgfError, ValueError):  # tpspec::validate violations
+    code = 2
+
+
+class ShapeError(CgfError, ValueError):  # engine::ShapeError
+    code = 3
+
+
+class BudgetError(CgfError):  # scheduler::BudgetError
+    code = 4
+
+
+class TriangleError(CgfError, ValueError):  # cg::TriangleError
+    code = 5
+
+
+class InvalidArgument(CgfError, ValueError):  # std::invalid_argument
+    code = 6
+
+
+class CudaError(CgfError):
+    code = 7
+
+
+class JitError(CgfError):
+    code = 8
+
+
+class UnsupportedError(CgfError):
+    code = 9
+
+
+class InternalError(CgfError):
+    code = 10
+
+
+_ERRORS = {c.code: c for c in (ParseError, ValidationError, ShapeError, BudgetError, TriangleError,
+                               InvalidArgument, CudaError, JitError, UnsupportedError, InternalError)}
+
+_lib = None
+
+
+def lib():
+    """Loads libcgf.so (built by ``__graft_entry__.build()`` / ``make -C
+    paper_2501_13986_b200``). Raises if it is missing — there is no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `make -C {_HERE}` or __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    P, I64, I = C.c_void_p, C.c_int64, C.c_int
+    L.cgf_last_error.restype = C.c_char_p
+    L.cgf_version.restype = C.c_char_p
+    L.cgf_cg_block.argtypes = [I, I, I, I, P, P, P, P]
+    L.cgf_plan_create.argtypes = [C.c_char_p, I, C.c_uint32, C.POINTER(P)]
+    L.cgf_plan_destroy.argtypes = [P]
+    L.cgf_plan_dims.argtypes = [P, P]
+    L.cgf_plan_flops.argtypes = [P, P]
+    L.cgf_plan_source.argtypes = [P, I, I, I, I, C.c_char_p, I]
+    L.cgf_plan_compile.argtypes = [P, I, I, I, I]
+    L.cgf_tp_forward.argtypes = [P, I, P, P, P, P, I64, I, P]
+    L.cgf_tp_backward.argtypes = [P, I, P, P, P, P, P, P, P, I64, I, P]
+    L.cgf_tp_double_backward.argtypes = [P, I] + [P] * 11 + [I64, I, P]
+    L.cgf_tp_forward_host.argtypes = [P, I, P, P, P, P, I64, I]
+    L.cgf_tp_backward_host.argtypes = [P, I] + [P] * 7 + [I64, I]
+    L.cgf_tp_double_backward_host.argtypes = [P, I] + [P] * 11 + [I64, I]
+    L.cgf_tp_stats.argtypes = [P, I, I64, I, P]
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().cgf_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, CgfError)(msg)
+
+
+def version() -> str:
+    return lib().cgf_version().decode()
+
+
+def cg_block(l1: int, l2: int, l3: int):
+    """Real-basis CG block entries, (k,i,j)-sorted: (i, j, k, v) arrays (cg.hpp:55)."""
+    cap = (2 * l1 + 1) * (2 * l2 + 1) * (2 * l3 + 1)
+    i, j, k = (np.zeros(cap, np.int32) for _ in range(3))
+    v = np.zeros(cap, np.float64)
+    n = lib().cgf_cg_block(l1, l2, l3, cap, i.ctypes.data, j.ctypes.data, k.ctypes.data, v.ctypes.data)
+    if n < 0:
+        _check(-n)
+    return i[:n].copy(), j[:n].copy(), k[:n].copy(), v[:n].copy()
+
+
+def _is_torch(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
+def _dtype_code(a) -> int:
+    name = str(a.dtype)
+    if name.endswith("float32"):
+        return F32
+    if name.endswith("float64"):
+        return F64
+    raise ShapeError(f"unsupported dtype {a.dtype} (float32 / float64)")
+
+
+class TpPlan:
+    """Compiled CG tensor-product problem (mirrors engine::TpPlan, engine.hpp:73-104).
+
+    ``problem`` is the reference's problem JSON (str or dict). ``budget`` is
+    the reference's scratch budget in words: accepted for API parity and used
+    only for the same admission check (BudgetError)."""
+
+    def __init__(self, problem, lane_width: int = 32, budget: int = 4096):
+        if not isinstance(problem, str):
+            problem = json.dumps(problem)
+        self.problem_json = problem
+        h = C.c_void_p()
+        _check(lib().cgf_plan_create(problem.encode(), lane_width, budget, C.byref(h)))
+        self._h = h
+        d = np.zeros(6, np.int64)
+        _check(lib().cgf_plan_dims(h, d.ctypes.data))
+        self.dim_x, self.dim_y, self.dim_z, self.n_w, self.n_split, self.n_units = (int(v) for v in d)
+        f = np.zeros(3, np.uint64)
+        _check(lib().cgf_plan_flops(h, f.ctypes.data))
+        self.flops_fwd, self.flops_bwd, self.flops_dbwd = (int(v) for v in f)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.cgf_plan_destroy(h)
+            self._h = None
+
+    # -- introspection -------------------------------------------------------
+    def source(self, op=OP_FORWARD, dtype=F32, w_shared=False, aligned=True) -> str:
+        n = lib().cgf_plan_source(self._h, op, dtype, int(w_shared), int(aligned), None, 0)
+        if n < 0:
+            _check(-n)
+        buf = C.create_string_buffer(n + 1)
+        lib().cgf_plan_source(self._h, op, dtype, int(w_shared), int(aligned), buf, n + 1)
+        return buf.value.decode()
+
+    def compile(self, op=OP_FORWARD, dtype=F32, w_shared=False, aligned=True):
+        _check(lib().cgf_plan_compile(self._h, op, dtype, int(w_shared), int(aligned)))
+
+    def stats(self, op, rows, w_shared=False):
+        s = np.zeros(3, np.uint64)
+        _check(lib().cgf_tp_stats(self._h, op, rows, int(w_shared), s.ctypes.data))
+        return tuple(int(v) for v in s)
+
+    # -- shape checks (engine.cpp:206-220) ----------------------------------
+    def _rows(self, x, y, w, w_shared):
+        if x.ndim != 2 or x.shape[1] != self.dim_x:
+            raise ShapeError(f"shape mismatch for x: expected [rows, {self.dim_x}], got {tuple(x.shape)}")
+        rows = x.shape[0]
+        if tuple(y.shape) != (rows, self.dim_y):
+            raise ShapeError(f"shape mismatch for y: expected ({rows}, {self.dim_y}), got {tuple(y.shape)}")
+        wr = 1 if w_shared else rows
+        if tuple(w.shape) != (wr, self.n_w) and not (w_shared and tuple(w.shape) == (self.n_w,)):
+            raise ShapeError(f"shape mismatch for w: expected ({wr}, {self.n_w}), got {tuple(w.shape)}")
+        return rows
+
+    @staticmethod
+    def _same(ref, *arrs):
+        for a in arrs:
+            if _is_torch(a) != _is_torch(ref) or str(a.dtype) != str(ref.dtype):
+                raise ShapeError("all arrays must share one dtype and one device kind")
+            if _is_torch(a) and (not a.is_cuda or a.device != ref.device):
+                raise ShapeError("torch tensors must be CUDA tensors on one device")
+            if _is_torch(a) and not a.is_contiguous():
+                raise ShapeError("tensors must be contiguous")
+
+    @staticmethod
+    def _stream(ref):
+        import torch
+        return C.c_void_p(torch.cuda.current_stream(ref.device).cuda_stream)
+
+    @staticmethod
+    def _p(a):
+        return C.c_void_p(a.data_ptr() if _is_torch(a) else a.ctypes.data)
+
+    @staticmethod
+    def _empty_like(ref, shape):
+        if _is_torch(ref):
+            import torch
+            return torch.empty(shape, dtype=ref.dtype, device=ref.device)
+        return np.empty(shape, dtype=ref.dtype)
+
+    @staticmethod
+    def _host(a):
+        return np.ascontiguousarray(a)
+
+    # -- the three entry points ---------------------------------------------
+    def forward(self, x, y, w, z=None, w_shared=False):
+        """z = TP(x, y, W) over a batch of rows (TpPlan::forward, engine.cpp:278-283)."""
+        if not _is_torch(x):
+            x, y, w = self._host(x), self._host(y), self._host(w)
+        self._same(x, y, w)
+        rows = self._rows(x, y, w, w_shared)
+        if z is None:
+            z = self._empty_like(x, (rows, self.dim_z))
+        self._same(x, z)
+        dt = _dtype_code(x)
+        if _is_torch(x):
+            _check(lib().cgf_tp_forward(self._h, dt, self._p(x), self._p(y), self._p(w), self._p(z), rows,
+                                        int(w_shared), self._stream(x)))
+        else:
+            _check(lib().cgf_tp_forward_host(self._h, dt, self._p(x), self._p(y), self._p(w), self._p(z),
+                                             rows, int(w_shared)))
+        return z
+
+    def backward(self, x, y, w, gz, w_shared=False):
+        """(gx, gy, gw) from gz (TpPlan::backward, engine.cpp:285-295)."""
+        if not _is_torch(x):
+            x, y, w, gz = (self._host(a) for a in (x, y, w, gz))
+        self._same(x, y, w, gz)
+        rows = self._rows(x, y, w, w_shared)
+        if tuple(gz.shape) != (rows, self.dim_z):
+            raise ShapeError(f"shape mismatch for g_z: expected ({rows}, {self.dim_z}), got {tuple(gz.shape)}")
+        gx = self._empty_like(x, (rows, self.dim_x))
+        gy = self._empty_like(x, (rows, self.dim_y))
+        gw = self._empty_like(x, (1 if w_shared else rows, self.n_w))
+        dt = _dtype_code(x)
+        args = [self._p(a) for a in (x, y, w, gz, gx, gy, gw)]
+        if _is_torch(x):
+            _check(lib().cgf_tp_backward(self._h, dt, *args, rows, int(w_shared), self._stream(x)))
+        else:
+            _check(lib().cgf_tp_backward_host(self._h, dt, *args, rows, int(w_shared)))
+        return gx, gy, gw
+
+    def double_backward(self, x, y, w, gz, upstream, w_shared=False):
+        """Given upstream = (dL/da, dL/db, dL/dC) of backward's outputs, returns
+        (dL/dx, dL/dy, dL/dW, dL/dg_z) (TpPlan::double_backward, engine.cpp:297-392)."""
+        da, db, dc = upstream
+        if not _is_torch(x):
+            x, y, w, gz, da, db, dc = (self._host(a) for a in (x, y, w, gz, da, db, dc))
+        self._same(x, y, w, gz, da, db, dc)
+        rows = self._rows(x, y, w, w_shared)
+        if tuple(gz.shape) != (rows, self.dim_z):
+            raise ShapeError(f"shape mismatch for g_z: expected ({rows}, {self.dim_z}), got {tuple(gz.shape)}")
+        for name, a, shp in (("dL/da", da, x.shape), ("dL/db", db, y.shape), ("dL/dC", dc, w.shape)):
+            if tuple(a.shape) != tuple(shp):
+                raise ShapeError(f"shape mismatch for {name}: expected {tuple(shp)}, got {tuple(a.shape)}")
+        ox = self._empty_like(x, (rows, self.dim_x))
+        oy = self._empty_like(x, (rows, self.dim_y))
+        ow = self._empty_like(x, tuple(w.shape))
+        ogz = self._empty_like(x, (rows, self.dim_z))
+        dt = _dtype_code(x)
+        args = [self._p(a) for a in (x, y, w, gz, da, db, dc, ox, oy, ow, ogz)]
+        if _is_torch(x):
+            _check(lib().cgf_tp_double_backward(self._h, dt, *args, rows, int(w_shared), self._stream(x)))
+        else:
+            _check(lib().cgf_tp_double_backward_host(self._h, dt, *args, rows, int(w_shared)))
+        return ox, oy, ow, ogz
