@@ -126,6 +126,56 @@ int cgf_tp_double_backward_host(cgf_plan* plan, int dtype, const void* x, const 
  * written once). */
 int cgf_tp_stats(const cgf_plan* plan, int op, int64_t rows, int w_shared, uint64_t stats[3]);
 
+/* ---- kernel introspection ------------------------------------------------ */
+
+/* comp: 0 fwd, 1 bwd, 2 fused double-backward, 3 conv dbwd pass 1 (dgz),
+ * 4 conv dbwd pass 2 (dx, dy, dW). loop: 0 batched rows, 1 conv by output
+ * node, 2 conv by neighbour node (transposed CSR). */
+int cgf_plan_kernel_source(cgf_plan* plan, int comp, int loop, int dtype, int w_shared, int aligned, char* buf,
+                           int cap);
+int cgf_plan_kernel_compile(cgf_plan* plan, int comp, int loop, int dtype, int w_shared, int aligned);
+
+/* ---- fused tensor product + graph convolution (device pointers) ---------- */
+
+/* Edge convention of the reference (conv.hpp:15-18): edge e = (s, d)
+ * contributes node_z[s] += TP(node_x[d], edge_y[e], edge_w[e]). The graph is
+ * the reference's GraphCSR (conv.hpp:44-50): edges sorted strictly by (s, d),
+ * row_ptr[nodes + 1] (int64) by output node s, nbr[e] = d (int32).
+ * Deterministic: every output row is owned by one warp and summed in edge
+ * order; no atomics. */
+enum cgf_conv_mode { CGF_CONV_DETERMINISTIC = 0, CGF_CONV_ATOMIC = 1 };
+
+/* Transposed CSR for the backward traversal (conv::transpose_permutation,
+ * conv.cpp:135-151, on host arrays): t_row_ptr[nodes + 1] by neighbour d,
+ * t_src[q] = output node s of transposed position q, t_eid[q] = its edge id
+ * (so perm[t_eid[q]] == q). */
+int cgf_conv_transpose_host(int64_t nodes, int64_t edges, const int64_t* row_ptr, const int32_t* nbr,
+                            int64_t* t_row_ptr, int32_t* t_src, int32_t* t_eid);
+
+/* node_z = sum over edges (ConvPlan::forward, conv.hpp:99-102, conv.cpp:234-355). */
+int cgf_conv_forward(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                     const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
+                     void* node_z, int mode, void* stream);
+
+/* (g_node_x, g_edge_y, g_edge_w) from g_node_z (ConvPlan::backward,
+ * conv.hpp:106-111, conv.cpp:357-528): g_node_x accumulated per neighbour
+ * over the transposed CSR, per-edge gradients written directly. */
+int cgf_conv_backward(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                      const int32_t* nbr, const int64_t* t_row_ptr, const int32_t* t_src, const int32_t* t_eid,
+                      const void* node_x, const void* edge_y, const void* edge_w, const void* g_node_z,
+                      void* g_node_x, void* g_edge_y, void* g_edge_w, int mode, void* stream);
+
+/* Conv double-backward (no reference entry point; composed per SURVEY.md §8c):
+ * given (d_gx, d_gy, d_gw) = upstream gradients of the backward outputs,
+ * returns (dL/dnode_x, dL/dedge_y, dL/dedge_w, dL/dg_node_z). Two passes:
+ * by output node (dg_node_z) and by neighbour node (the rest). */
+int cgf_conv_double_backward(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                             const int32_t* nbr, const int64_t* t_row_ptr, const int32_t* t_src,
+                             const int32_t* t_eid, const void* node_x, const void* edge_y, const void* edge_w,
+                             const void* g_node_z, const void* d_gx, const void* d_gy, const void* d_gw,
+                             void* o_node_x, void* o_edge_y, void* o_edge_w, void* o_g_node_z, int mode,
+                             void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcgf.so")
 
 __all__ = [
-    "TpPlan", "cg_block", "lib", "CgfError", "ParseError", "ValidationError", "ShapeError",
+    "TpPlan", "ConvPlan", "Graph", "cg_block", "lib", "CgfError", "ParseError", "ValidationError", "ShapeError",
     "BudgetError", "TriangleError", "InvalidArgument", "CudaError", "JitError",
     "UnsupportedError", "F32", "F64", "OP_FORWARD", "OP_BACKWARD", "OP_DOUBLE_BACKWARD",
 ]
@@ -112,6 +112,12 @@ def lib():
     L.cgf_tp_backward_host.argtypes = [P, I] + [P] * 7 + [I64, I]
     L.cgf_tp_double_backward_host.argtypes = [P, I] + [P] * 11 + [I64, I]
     L.cgf_tp_stats.argtypes = [P, I, I64, I, P]
+    L.cgf_plan_kernel_source.argtypes = [P, I, I, I, I, I, C.c_char_p, I]
+    L.cgf_plan_kernel_compile.argtypes = [P, I, I, I, I, I]
+    L.cgf_conv_transpose_host.argtypes = [I64, I64, P, P, P, P, P]
+    L.cgf_conv_forward.argtypes = [P, I, I64, I64, P, P, P, P, P, P, I, P]
+    L.cgf_conv_backward.argtypes = [P, I, I64, I64] + [P] * 12 + [I, P]
+    L.cgf_conv_double_backward.argtypes = [P, I, I64, I64] + [P] * 16 + [I, P]
     _lib = L
     return L
 
@@ -298,3 +304,148 @@ class TpPlan:
         else:
             _check(lib().cgf_tp_double_backward_host(self._h, dt, *args, rows, int(w_shared)))
         return ox, oy, ow, ogz
+
+
+# ------------------------------------------------------------ convolution --
+
+COMP_FWD, COMP_BWD, COMP_DBWD, COMP_DBWD_Z, COMP_DBWD_X = range(5)
+LOOP_ROWS, LOOP_CONV_BY_OUTPUT, LOOP_CONV_BY_INPUT = range(3)
+DETERMINISTIC, ATOMIC = 0, 1
+
+
+class Graph:
+    """The reference's GraphCSR (conv.hpp:44-50): edges sorted strictly by
+    (src, dst); ``src`` is the output node of an edge, ``nbr`` (reference
+    ``dst``) the node whose features it reads. Holds host arrays and uploads
+    CSR + transposed CSR to a device on first use."""
+
+    def __init__(self, nodes: int, src, nbr):
+        src = np.ascontiguousarray(np.asarray(src, dtype=np.int64))
+        nbr = np.ascontiguousarray(np.asarray(nbr, dtype=np.int64))
+        if src.shape != nbr.shape or src.ndim != 1:
+            raise ShapeError("src / nbr must be 1-D arrays of equal length")
+        if src.size and (src.min() < 0 or nbr.min() < 0 or src.max() >= nodes or nbr.max() >= nodes):
+            raise InvalidArgument("edge endpoint out of range")
+        key = src * max(nodes, 1) + nbr
+        if src.size > 1 and not np.all(np.diff(key) > 0):
+            raise InvalidArgument("conv: deterministic mode requires edges sorted by first coordinate")
+        self.nodes = int(nodes)
+        self.src = src.astype(np.int32)
+        self.nbr = nbr.astype(np.int32)
+        counts = np.bincount(src, minlength=nodes) if src.size else np.zeros(nodes, np.int64)
+        self.row_ptr = np.zeros(nodes + 1, np.int64)
+        np.cumsum(counts, out=self.row_ptr[1:])
+        self.t_row_ptr = np.zeros(nodes + 1, np.int64)
+        self.t_src = np.zeros(max(self.edges, 1), np.int32)
+        self.t_eid = np.zeros(max(self.edges, 1), np.int32)
+        _check(lib().cgf_conv_transpose_host(self.nodes, self.edges, self.row_ptr.ctypes.data,
+                                             self.nbr.ctypes.data if self.edges else None,
+                                             self.t_row_ptr.ctypes.data, self.t_src.ctypes.data,
+                                             self.t_eid.ctypes.data))
+        self._dev = {}
+
+    @property
+    def edges(self) -> int:
+        return int(self.src.size)
+
+    def transpose_permutation(self) -> np.ndarray:
+        """perm[e] = position of edge e in the transposed CSR (conv.hpp:62-63)."""
+        perm = np.empty(self.edges, np.int64)
+        perm[self.t_eid[:self.edges]] = np.arange(self.edges)
+        return perm
+
+    def device(self, dev):
+        import torch
+        key = str(dev)
+        if key not in self._dev:
+            t = lambda a: torch.from_numpy(a).to(dev)
+            self._dev[key] = {k: t(getattr(self, k)) for k in ("row_ptr", "nbr", "t_row_ptr", "t_src", "t_eid")}
+        return self._dev[key]
+
+
+class ConvPlan:
+    """Fused tensor product + graph convolution over a TpPlan (conv.hpp:93-115).
+    Deterministic: each output row is owned by one warp and summed in edge
+    order (no atomics, no fixup pass)."""
+
+    def __init__(self, plan: TpPlan):
+        self.plan = plan
+
+    def _ptrs(self, g: Graph, ref):
+        d = g.device(ref.device)
+        return {k: C.c_void_p(v.data_ptr()) for k, v in d.items()}
+
+    def _check_shapes(self, g, node_x, edge_y, edge_w):
+        p = self.plan
+        if tuple(node_x.shape) != (g.nodes, p.dim_x):
+            raise ShapeError("conv: node_x shape mismatch")
+        if tuple(edge_y.shape) != (g.edges, p.dim_y):
+            raise ShapeError("conv: edge_y shape mismatch")
+        if tuple(edge_w.shape) != (g.edges, p.n_w):
+            raise ShapeError("conv: edge_w shape mismatch")
+        TpPlan._same(node_x, edge_y, edge_w)
+        if not _is_torch(node_x):
+            raise ShapeError("conv: pass torch CUDA tensors")
+
+    def forward(self, g: Graph, node_x, edge_y, edge_w, mode=DETERMINISTIC):
+        """node_z[s] = sum over edges (s, d) of TP(node_x[d], edge_y[e], edge_w[e])."""
+        self._check_shapes(g, node_x, edge_y, edge_w)
+        p = self.plan
+        z = TpPlan._empty_like(node_x, (g.nodes, p.dim_z))
+        d = self._ptrs(g, node_x)
+        _check(lib().cgf_conv_forward(p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"],
+                                      TpPlan._p(node_x), TpPlan._p(edge_y), TpPlan._p(edge_w), TpPlan._p(z), mode,
+                                      TpPlan._stream(node_x)))
+        return z
+
+    def backward(self, g: Graph, node_x, edge_y, edge_w, g_node_z, mode=DETERMINISTIC):
+        """(g_node_x, g_edge_y, g_edge_w) from g_node_z (conv.cpp:357-528)."""
+        self._check_shapes(g, node_x, edge_y, edge_w)
+        p = self.plan
+        if tuple(g_node_z.shape) != (g.nodes, p.dim_z):
+            raise ShapeError("conv: g_node_z shape mismatch")
+        TpPlan._same(node_x, g_node_z)
+        gx = TpPlan._empty_like(node_x, (g.nodes, p.dim_x))
+        gy = TpPlan._empty_like(node_x, (g.edges, p.dim_y))
+        gw = TpPlan._empty_like(node_x, (g.edges, p.n_w))
+        d = self._ptrs(g, node_x)
+        _check(lib().cgf_conv_backward(p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"],
+                                       d["t_row_ptr"], d["t_src"], d["t_eid"], TpPlan._p(node_x), TpPlan._p(edge_y),
+                                       TpPlan._p(edge_w), TpPlan._p(g_node_z), TpPlan._p(gx), TpPlan._p(gy),
+                                       TpPlan._p(gw), mode, TpPlan._stream(node_x)))
+        return gx, gy, gw
+
+    def double_backward(self, g: Graph, node_x, edge_y, edge_w, g_node_z, upstream, mode=DETERMINISTIC):
+        """Given (dL/dg_node_x, dL/dg_edge_y, dL/dg_edge_w), returns
+        (dL/dnode_x, dL/dedge_y, dL/dedge_w, dL/dg_node_z)."""
+        d_gx, d_gy, d_gw = upstream
+        self._check_shapes(g, node_x, edge_y, edge_w)
+        p = self.plan
+        TpPlan._same(node_x, g_node_z, d_gx, d_gy, d_gw)
+        for name, a, shp in (("g_node_z", g_node_z, (g.nodes, p.dim_z)), ("d_gx", d_gx, (g.nodes, p.dim_x)),
+                             ("d_gy", d_gy, (g.edges, p.dim_y)), ("d_gw", d_gw, (g.edges, p.n_w))):
+            if tuple(a.shape) != shp:
+                raise ShapeError(f"conv: {name} shape mismatch")
+        ox = TpPlan._empty_like(node_x, (g.nodes, p.dim_x))
+        oy = TpPlan._empty_like(node_x, (g.edges, p.dim_y))
+        ow = TpPlan._empty_like(node_x, (g.edges, p.n_w))
+        ogz = TpPlan._empty_like(node_x, (g.nodes, p.dim_z))
+        d = self._ptrs(g, node_x)
+        _check(lib().cgf_conv_double_backward(
+            p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"], d["t_row_ptr"], d["t_src"],
+            d["t_eid"], *(TpPlan._p(a) for a in (node_x, edge_y, edge_w, g_node_z, d_gx, d_gy, d_gw, ox, oy, ow,
+                                                 ogz)), mode, TpPlan._stream(node_x)))
+        return ox, oy, ow, ogz
+
+
+def _kernel_source(plan: TpPlan, comp, loop, dtype=F32, w_shared=False, aligned=True) -> str:
+    n = lib().cgf_plan_kernel_source(plan._h, comp, loop, dtype, int(w_shared), int(aligned), None, 0)
+    if n < 0:
+        _check(-n)
+    buf = C.create_string_buffer(n + 1)
+    lib().cgf_plan_kernel_source(plan._h, comp, loop, dtype, int(w_shared), int(aligned), buf, n + 1)
+    return buf.value.decode()
+
+
+def _kernel_compile(plan: TpPlan, comp, loop, dtype=F32, w_shared=False, aligned=True):
+    _check(lib().cgf_plan_kernel_compile(plan._h, comp, loop, dtype, int(w_shared), int(aligned)))

@@ -24,7 +24,7 @@ struct cgf_plan {
   std::uint32_t budget = 4096;
   bool z_covered = true, x_covered = true;
   std::mutex mu;
-  std::map<std::tuple<int, int, int, int>, std::shared_ptr<cgf::KernelSource>> sources;
+  std::map<std::tuple<int, int, int, int, int>, std::shared_ptr<cgf::KernelSource>> sources;
 };
 
 namespace {
@@ -82,23 +82,30 @@ bool covers(const std::vector<std::pair<std::uint32_t, std::uint32_t>>& pieces, 
   return true;
 }
 
-std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, int op, int dtype, int w_shared, int aligned) {
-  if (op < 0 || op > 2) throw std::invalid_argument("bad op");
+std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype,
+                                              int w_shared, int aligned) {
   if (dtype != CGF_F32 && dtype != CGF_F64) throw std::invalid_argument("bad dtype");
   std::lock_guard<std::mutex> g(p->mu);
-  const auto key = std::make_tuple(op, dtype, w_shared ? 1 : 0, aligned ? 1 : 0);
+  const auto key = std::make_tuple(static_cast<int>(comp), static_cast<int>(loop), dtype, w_shared ? 1 : 0,
+                                   aligned ? 1 : 0);
   auto it = p->sources.find(key);
   if (it != p->sources.end()) return it->second;
-  if (w_shared && op != CGF_OP_FORWARD)
+  if (w_shared && comp != cgf::Comp::Fwd)
     throw cgf::UnsupportedError("shared-weight backward / double-backward needs the uvw tensor-core path");
   cgf::KernelConfig cfg;
-  cfg.op = static_cast<cgf::Op>(op);
+  cfg.comp = comp;
+  cfg.loop = loop;
   cfg.f64 = dtype == CGF_F64;
   cfg.w_shared = w_shared != 0;
   cfg.aligned = aligned != 0;
-  auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_tp_kernel(p->problem, p->units, cfg));
+  auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_kernel(p->problem, p->units, cfg));
   p->sources.emplace(key, ks);
   return ks;
+}
+
+std::shared_ptr<cgf::KernelSource> source_for_op(cgf_plan* p, int op, int dtype, int w_shared, int aligned) {
+  if (op < 0 || op > 2) throw std::invalid_argument("bad op");
+  return source_for(p, static_cast<cgf::Comp>(op), cgf::Loop::Rows, dtype, w_shared, aligned);
 }
 
 bool aligned16(std::initializer_list<const void*> ptrs) {
@@ -107,29 +114,48 @@ bool aligned16(std::initializer_list<const void*> ptrs) {
   return true;
 }
 
+struct Args {
+  const void *x = nullptr, *y = nullptr, *w = nullptr, *gz = nullptr, *da = nullptr, *db = nullptr, *dc = nullptr;
+  void *o0 = nullptr, *o1 = nullptr, *o2 = nullptr, *o3 = nullptr;
+  std::int64_t rows = 0;
+  const void *rp = nullptr, *nb = nullptr, *eid = nullptr;
+  std::int64_t edges = 0;
+};
+
+void run_kernel(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype, int w_shared, const Args& a, void* stream) {
+  if (a.rows <= 0) return;
+  const bool al = aligned16({a.x, a.y, a.w, a.gz, a.da, a.db, a.dc, a.o0, a.o1, a.o2, a.o3});
+  const auto ks = source_for(p, comp, loop, dtype, w_shared, al);
+  const cgf::Kernel k = cgf::load_kernel(*ks);
+  const int warps = k.threads / 32;
+  const std::int64_t need = (a.rows + warps - 1) / warps;
+  const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(need, k.max_grid));
+  Args c = a;
+  void* args[] = {&c.x, &c.y, &c.w, &c.gz, &c.da, &c.db, &c.dc, &c.o0, &c.o1, &c.o2, &c.o3, &c.rows,
+                  &c.rp, &c.nb, &c.eid, &c.edges};
+  CU_CHECK(cgf::drv::cuLaunchKernel(k.fn, grid, 1, 1, k.threads, 1, 1, k.smem_bytes,
+                                    reinterpret_cast<CUstream>(stream), args, nullptr));
+}
+
+void memzero(void* ptr, std::size_t bytes, void* stream) {
+  if (bytes) CU_CHECK(cgf::drv::cuMemsetD8Async(reinterpret_cast<CUdeviceptr>(ptr), 0, bytes, reinterpret_cast<CUstream>(stream)));
+}
+
 void launch(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, const void* x,
             const void* y, const void* w, const void* gz, const void* da, const void* db,
             const void* dc, void* o0, void* o1, void* o2, void* o3, void* stream) {
   if (rows < 0) throw cgf::ShapeError("rows must be non-negative");
   if (rows == 0) return;
-  const bool al = aligned16({x, y, w, gz, da, db, dc, o0, o1, o2, o3});
-  const auto ks = source_for(p, op, dtype, w_shared, al);
-  const cgf::Kernel k = cgf::load_kernel(*ks);
-  CUstream s = reinterpret_cast<CUstream>(stream);
+  if (op < 0 || op > 2) throw std::invalid_argument("bad op");
   const std::size_t es = dtype == CGF_F64 ? 8 : 4;
   const auto& pr = p->problem;
   // Outputs the kernel never touches must still read as zero.
-  if (op != CGF_OP_BACKWARD && !p->z_covered) {
-    void* zo = op == CGF_OP_FORWARD ? o0 : o3;
-    CU_CHECK(cgf::drv::cuMemsetD8Async(reinterpret_cast<CUdeviceptr>(zo), 0, es * rows * pr.dim_z, s));
-  }
-  if (op != CGF_OP_FORWARD && !p->x_covered)
-    CU_CHECK(cgf::drv::cuMemsetD8Async(reinterpret_cast<CUdeviceptr>(o0), 0, es * rows * pr.dim_x, s));
-  const int warps = k.threads / 32;
-  const std::int64_t need = (rows + warps - 1) / warps;
-  const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(need, k.max_grid));
-  void* args[] = {&x, &y, &w, &gz, &da, &db, &dc, &o0, &o1, &o2, &o3, &rows};
-  CU_CHECK(cgf::drv::cuLaunchKernel(k.fn, grid, 1, 1, k.threads, 1, 1, k.smem_bytes, s, args, nullptr));
+  if (op != CGF_OP_BACKWARD && !p->z_covered) memzero(op == CGF_OP_FORWARD ? o0 : o3, es * rows * pr.dim_z, stream);
+  if (op != CGF_OP_FORWARD && !p->x_covered) memzero(o0, es * rows * pr.dim_x, stream);
+  Args a;
+  a.x = x; a.y = y; a.w = w; a.gz = gz; a.da = da; a.db = db; a.dc = dc;
+  a.o0 = o0; a.o1 = o1; a.o2 = o2; a.o3 = o3; a.rows = rows;
+  run_kernel(p, static_cast<cgf::Comp>(op), cgf::Loop::Rows, dtype, w_shared, a, stream);
 }
 
 void need(const void* ptr, const char* what) {
@@ -234,7 +260,7 @@ int cgf_plan_source(cgf_plan* p, int op, int dtype, int w_shared, int aligned, c
   int n = 0;
   const int rc = guarded([&] {
     need(p, "plan");
-    const auto ks = source_for(p, op, dtype, w_shared, aligned);
+    const auto ks = source_for_op(p, op, dtype, w_shared, aligned);
     n = static_cast<int>(ks->source.size());
     if (buf && cap > 0) {
       const int m = std::min(cap - 1, n);
@@ -248,7 +274,7 @@ int cgf_plan_source(cgf_plan* p, int op, int dtype, int w_shared, int aligned, c
 int cgf_plan_compile(cgf_plan* p, int op, int dtype, int w_shared, int aligned) {
   return guarded([&] {
     need(p, "plan");
-    const auto ks = source_for(p, op, dtype, w_shared, aligned);
+    const auto ks = source_for_op(p, op, dtype, w_shared, aligned);
     cgf::compile_cubin(ks->source, ks->name);
   });
 }
@@ -406,6 +432,129 @@ int cgf_tp_stats(const cgf_plan* p, int op, int64_t rows, int w_shared, uint64_t
         break;
       default: throw std::invalid_argument("bad op");
     }
+  });
+}
+
+// ------------------------------------------------------------- convolution --
+
+int cgf_plan_kernel_source(cgf_plan* p, int comp, int loop, int dtype, int w_shared, int aligned, char* buf,
+                           int cap) {
+  int n = 0;
+  const int rc = guarded([&] {
+    need(p, "plan");
+    if (comp < 0 || comp > 4 || loop < 0 || loop > 2) throw std::invalid_argument("bad comp / loop");
+    const auto ks = source_for(p, static_cast<cgf::Comp>(comp), static_cast<cgf::Loop>(loop), dtype, w_shared, aligned);
+    n = static_cast<int>(ks->source.size());
+    if (buf && cap > 0) {
+      const int m = std::min(cap - 1, n);
+      std::memcpy(buf, ks->source.data(), m);
+      buf[m] = 0;
+    }
+  });
+  return rc == CGF_OK ? n : -rc;
+}
+
+int cgf_plan_kernel_compile(cgf_plan* p, int comp, int loop, int dtype, int w_shared, int aligned) {
+  return guarded([&] {
+    need(p, "plan");
+    if (comp < 0 || comp > 4 || loop < 0 || loop > 2) throw std::invalid_argument("bad comp / loop");
+    const auto ks = source_for(p, static_cast<cgf::Comp>(comp), static_cast<cgf::Loop>(loop), dtype, w_shared, aligned);
+    cgf::compile_cubin(ks->source, ks->name);
+  });
+}
+
+int cgf_conv_transpose_host(int64_t nodes, int64_t edges, const int64_t* row_ptr, const int32_t* nbr,
+                            int64_t* t_row_ptr, int32_t* t_out, int32_t* t_eid) {
+  return guarded([&] {
+    if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (edges > 0) {
+      need(row_ptr, "row_ptr"); need(nbr, "nbr"); need(t_row_ptr, "t_row_ptr"); need(t_out, "t_src"); need(t_eid, "t_eid");
+    }
+    if (row_ptr[0] != 0 || row_ptr[nodes] != edges) throw std::invalid_argument("row_ptr does not span the edge list");
+    // Stable counting sort by neighbour (conv.cpp:135-151): within a bucket
+    // edges keep CSR order, i.e. ascending output node.
+    std::vector<int64_t> cnt(static_cast<size_t>(nodes) + 1, 0);
+    for (int64_t e = 0; e < edges; ++e) {
+      if (nbr[e] < 0 || nbr[e] >= nodes) throw std::invalid_argument("neighbour index out of range");
+      ++cnt[static_cast<size_t>(nbr[e]) + 1];
+    }
+    for (int64_t v = 0; v < nodes; ++v) cnt[v + 1] += cnt[v];
+    std::memcpy(t_row_ptr, cnt.data(), sizeof(int64_t) * (static_cast<size_t>(nodes) + 1));
+    for (int64_t s = 0; s < nodes; ++s)
+      for (int64_t e = row_ptr[s]; e < row_ptr[s + 1]; ++e) {
+        const int64_t q = cnt[nbr[e]]++;
+        t_out[q] = static_cast<int32_t>(s);
+        t_eid[q] = static_cast<int32_t>(e);
+      }
+  });
+}
+
+int cgf_conv_forward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr, const int32_t* nbr,
+                     const void* node_x, const void* edge_y, const void* edge_w, void* node_z, int mode, void* stream) {
+  return guarded([&] {
+    need(p, "plan");
+    if (mode != CGF_CONV_DETERMINISTIC) throw cgf::UnsupportedError("only the deterministic conv mode is built");
+    if (nodes <= 0) return;
+    need(row_ptr, "row_ptr"); need(node_x, "node_x"); need(node_z, "node_z");
+    if (edges > 0) { need(nbr, "nbr"); need(edge_y, "edge_y"); need(edge_w, "edge_w"); }
+    const std::size_t es = dtype == CGF_F64 ? 8 : 4;
+    if (!p->z_covered) memzero(node_z, es * nodes * p->problem.dim_z, stream);
+    Args a;
+    a.x = node_x; a.y = edge_y; a.w = edge_w; a.o0 = node_z; a.rows = nodes;
+    a.rp = row_ptr; a.nb = nbr; a.edges = edges;
+    run_kernel(p, cgf::Comp::Fwd, cgf::Loop::ConvByOutput, dtype, 0, a, stream);
+  });
+}
+
+int cgf_conv_backward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                      const int32_t* nbr, const int64_t* t_row_ptr, const int32_t* t_out, const int32_t* t_eid,
+                      const void* node_x, const void* edge_y, const void* edge_w, const void* g_node_z,
+                      void* g_node_x, void* g_edge_y, void* g_edge_w, int mode, void* stream) {
+  return guarded([&] {
+    need(p, "plan");
+    if (mode != CGF_CONV_DETERMINISTIC) throw cgf::UnsupportedError("only the deterministic conv mode is built");
+    (void)row_ptr; (void)nbr;
+    if (nodes <= 0) return;
+    need(t_row_ptr, "t_row_ptr"); need(node_x, "node_x"); need(g_node_z, "g_node_z"); need(g_node_x, "g_node_x");
+    if (edges > 0) {
+      need(t_out, "t_src"); need(t_eid, "t_eid"); need(edge_y, "edge_y"); need(edge_w, "edge_w");
+      need(g_edge_y, "g_edge_y"); need(g_edge_w, "g_edge_w");
+    }
+    const std::size_t es = dtype == CGF_F64 ? 8 : 4;
+    if (!p->x_covered) memzero(g_node_x, es * nodes * p->problem.dim_x, stream);
+    Args a;
+    a.x = node_x; a.y = edge_y; a.w = edge_w; a.gz = g_node_z;
+    a.o0 = g_node_x; a.o1 = g_edge_y; a.o2 = g_edge_w; a.rows = nodes;
+    a.rp = t_row_ptr; a.nb = t_out; a.eid = t_eid; a.edges = edges;
+    run_kernel(p, cgf::Comp::Bwd, cgf::Loop::ConvByInput, dtype, 0, a, stream);
+  });
+}
+
+int cgf_conv_double_backward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                             const int32_t* nbr, const int64_t* t_row_ptr, const int32_t* t_out,
+                             const int32_t* t_eid, const void* node_x, const void* edge_y, const void* edge_w,
+                             const void* g_node_z, const void* d_gx, const void* d_gy, const void* d_gw,
+                             void* o_node_x, void* o_edge_y, void* o_edge_w, void* o_g_node_z, int mode,
+                             void* stream) {
+  return guarded([&] {
+    need(p, "plan");
+    if (mode != CGF_CONV_DETERMINISTIC) throw cgf::UnsupportedError("only the deterministic conv mode is built");
+    if (nodes <= 0) return;
+    const std::size_t es = dtype == CGF_F64 ? 8 : 4;
+    if (!p->z_covered) memzero(o_g_node_z, es * nodes * p->problem.dim_z, stream);
+    if (!p->x_covered) memzero(o_node_x, es * nodes * p->problem.dim_x, stream);
+    // Pass 1, by output node: dL/dg_node_z = sum_e op3 + op6 + op7.
+    Args a;
+    a.x = node_x; a.y = edge_y; a.w = edge_w; a.da = d_gx; a.db = d_gy; a.dc = d_gw;
+    a.o3 = o_g_node_z; a.rows = nodes; a.rp = row_ptr; a.nb = nbr; a.edges = edges;
+    run_kernel(p, cgf::Comp::DBwdZ, cgf::Loop::ConvByOutput, dtype, 0, a, stream);
+    // Pass 2, by neighbour node (transposed CSR): dL/dnode_x = sum_e op1.gx + op2.gx,
+    // per edge dL/dy = op1.gy + op2.gy and dL/dW = op4.gw + op5.gw.
+    Args b;
+    b.x = node_x; b.y = edge_y; b.w = edge_w; b.gz = g_node_z; b.da = d_gx; b.db = d_gy; b.dc = d_gw;
+    b.o0 = o_node_x; b.o1 = o_edge_y; b.o2 = o_edge_w; b.rows = nodes;
+    b.rp = t_row_ptr; b.nb = t_out; b.eid = t_eid; b.edges = edges;
+    run_kernel(p, cgf::Comp::DBwdX, cgf::Loop::ConvByInput, dtype, 0, b, stream);
   });
 }
 

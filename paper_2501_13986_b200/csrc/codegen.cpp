@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <functional>
 #include <map>
 #include <sstream>
 
@@ -56,6 +57,7 @@ template <class T> DEVI T warp_sum(T v) {
 )RT";
 }
 
+
 namespace {
 
 std::string hexd(double v) {
@@ -64,25 +66,31 @@ std::string hexd(double v) {
   return b;
 }
 
+std::string S(long long v) { return std::to_string(v); }
+
+enum class Src { Row, Nbr, Edge };
+
 struct SlotRange {
-  std::string arr;  // kernel parameter name
-  std::string stride;  // row stride expression (words)
+  std::string arr;     // kernel parameter name
+  std::uint32_t stride = 0;  // words per indexed row
+  Src src = Src::Row;
   std::uint32_t off = 0, words = 0, slot_off = 0;
   bool bulk = false;
+  bool window = false;  // y-like: copy the 16-byte aligned window around the row
 };
 
 struct UnitLayout {
   std::vector<SlotRange> ranges;
   std::map<std::uint32_t, std::uint32_t> x_slot, a_slot, gz_slot;  // row offset -> slot offset
   std::map<int, std::uint32_t> w_slot, c_slot;                      // sub index -> slot offset
-  std::uint32_t words = 0, bulk_bytes = 0;
+  std::uint32_t y_slot = 0, db_slot = 0;
+  std::uint32_t words = 0, fixed_bulk_bytes = 0;
 };
 
 class Gen {
  public:
   Gen(const Problem& p, const std::vector<Unit>& units, const KernelConfig& cfg)
       : p_(p), units_(units), cfg_(cfg), sz_(cfg.f64 ? 8 : 4) {}
-
   KernelSource run();
 
  private:
@@ -96,35 +104,63 @@ class Gen {
   bool has_c_ = false;
   std::uint32_t scr_words_ = 0, off_zs_ = 0, off_wt_ = 0, off_ct_ = 0;
 
-  bool bwd() const { return cfg_.op != Op::Fwd; }
-  bool dbl() const { return cfg_.op == Op::DBwd; }
-  std::uint32_t align_words() const { return 16u / sz_; }
-  std::uint32_t up(std::uint32_t w) const { return (w + align_words() - 1) / align_words() * align_words(); }
-  bool aligned16(std::uint64_t words) const { return (words * sz_) % 16 == 0; }
+  // What the compute mode reads / writes.
+  bool reads_gz() const { return cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdX; }
+  bool dual() const { return cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX; }
+  bool out_x() const { return cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdX; }
+  bool out_z() const { return cfg_.comp == Comp::Fwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ; }
+  bool out_y() const { return out_x(); }
+  bool out_w() const { return out_x(); }
+  bool conv() const { return cfg_.loop != Loop::Rows; }
+  bool by_input() const { return cfg_.loop == Loop::ConvByInput; }
+  Src x_src() const { return cfg_.loop == Loop::ConvByOutput ? Src::Nbr : Src::Row; }
+  Src z_src() const { return cfg_.loop == Loop::ConvByInput ? Src::Nbr : Src::Row; }
+  Src e_src() const { return conv() ? Src::Edge : Src::Row; }
+  const char* idx(Src s) const { return s == Src::Row ? "row" : s == Src::Nbr ? "nbr" : "eid"; }
+  std::uint32_t A() const { return 16u / sz_; }  // words per 16 bytes
+  std::uint32_t up(std::uint32_t w) const { return (w + A() - 1) / A() * A(); }
+  bool al16(std::uint64_t words) const { return (words * sz_) % 16 == 0; }
 
+  void add(UnitLayout& L, const std::string& arr, std::uint32_t stride, Src src, std::uint32_t off,
+           std::uint32_t words, std::uint32_t& so, bool window = false);
   void layout();
-  void add_range(UnitLayout& L, const std::string& arr, std::uint32_t stride, std::uint32_t off,
-                 std::uint32_t words, std::uint32_t& slot_off);
   void emit_issue();
-  void emit_unit(int u);
-  void emit_store(const std::string& dst, std::uint32_t stride, std::uint32_t off,
-                  std::uint32_t words, const std::string& guard_rows, int width,
-                  const std::string& reg);
+  void emit_unit_body(int u, const std::string& accx_prefix, const std::function<void(int)>& post_sub = {});
+  bool gy_flush() const { return out_y() && (dual() || cfg_.f64); }
+  void emit_gy_flush_row(const std::string& rowexpr);
+  std::uint32_t off_gya_ = 0;
+  void emit_wait_and_sync(int u);
+  void emit_release();
+  void emit_store(const std::string& dst, const std::string& rowexpr, std::uint32_t stride, std::uint32_t off,
+                  std::uint32_t words, int guard_rows, int width, const std::string& reg);
   std::string wsrc(const Sub& s, const std::string& arr) const;
+  std::string yv(int j) const;
+  std::string dbv(int j) const;
+  void emit_gy_reduce(const std::string& dst_rowexpr);
+  void emit_rows_loop();
+  void emit_conv_loop();
 };
 
-void Gen::add_range(UnitLayout& L, const std::string& arr, std::uint32_t stride, std::uint32_t off,
-                    std::uint32_t words, std::uint32_t& slot_off) {
+void Gen::add(UnitLayout& L, const std::string& arr, std::uint32_t stride, Src src, std::uint32_t off,
+              std::uint32_t words, std::uint32_t& so, bool window) {
   SlotRange r;
   r.arr = arr;
-  r.stride = std::to_string(stride);
+  r.stride = stride;
+  r.src = src;
   r.off = off;
   r.words = words;
+  r.window = window;
   r.slot_off = L.words;
-  r.bulk = cfg_.aligned && aligned16(stride) && aligned16(off) && aligned16(words);
-  slot_off = r.slot_off;
-  L.words = up(L.words + words);
-  if (r.bulk) L.bulk_bytes += words * sz_;
+  if (window) {
+    // Row start is only A-word aligned up to a runtime shift of < A words.
+    r.bulk = cfg_.aligned;
+    L.words = up(L.words + words + 2 * A());
+  } else {
+    r.bulk = cfg_.aligned && al16(stride) && al16(off) && al16(words);
+    L.words = up(L.words + words);
+    if (r.bulk) L.fixed_bulk_bytes += words * sz_;
+  }
+  so = r.slot_off;
   L.ranges.push_back(r);
 }
 
@@ -135,14 +171,21 @@ void Gen::layout() {
     max_piece_ = std::max({max_piece_, s.b * s.dz(), s.bp * s.dx()});
     if (s.kind == Kind::C) has_c_ = true;
   }
+  const std::uint32_t nw = cfg_.w_shared ? 0 : p_.n_w;
   for (const auto& u : units_) {
     UnitLayout L;
     std::uint32_t so = 0;
+    add(L, "Y", p_.dim_y, e_src(), 0, p_.dim_y, so, true);
+    L.y_slot = so;
+    if (dual()) {
+      add(L, "DB", p_.dim_y, e_src(), 0, p_.dim_y, so, true);
+      L.db_slot = so;
+    }
     for (const auto& xc : u.x_chunks) {
-      add_range(L, "X", p_.dim_x, xc.off, xc.words, so);
+      add(L, "X", p_.dim_x, x_src(), xc.off, xc.words, so);
       L.x_slot[xc.off] = so;
-      if (dbl()) {
-        add_range(L, "DA", p_.dim_x, xc.off, xc.words, so);
+      if (dual()) {
+        add(L, "DA", p_.dim_x, x_src(), xc.off, xc.words, so);
         L.a_slot[xc.off] = so;
       }
     }
@@ -150,134 +193,169 @@ void Gen::layout() {
       for (int si : u.subs) {
         const Sub& s = p_.subs[si];
         if (s.kind != Kind::B) continue;
-        add_range(L, "W", p_.n_w, s.w_off, s.b, so);
+        add(L, "W", nw, e_src(), s.w_off, s.b, so);
         L.w_slot[si] = so;
-        if (dbl()) {
-          add_range(L, "DC", p_.n_w, s.w_off, s.b, so);
+        if (dual()) {
+          add(L, "DC", nw, e_src(), s.w_off, s.b, so);
           L.c_slot[si] = so;
         }
       }
     }
-    if (bwd()) {
+    if (reads_gz()) {
       for (const auto& zp : u.z_pieces) {
-        add_range(L, "GZ", p_.dim_z, zp.off, zp.words, so);
+        add(L, "GZ", p_.dim_z, z_src(), zp.off, zp.words, so);
         L.gz_slot[zp.off] = so;
       }
     }
-    L.words = std::max<std::uint32_t>(L.words, align_words());
+    L.words = std::max<std::uint32_t>(L.words, A());
     lay_.push_back(std::move(L));
   }
-  // Per-warp scratch: output staging, plus z' staging and W / dC tiles for uvw.
   const std::uint32_t stage = up(static_cast<std::uint32_t>(std::max(max_piece_, 32 * max_dx_)));
   scr_words_ = stage;
+  off_gya_ = scr_words_;
+  scr_words_ += up(static_cast<std::uint32_t>(p_.dim_y));
   off_zs_ = scr_words_;
   if (has_c_) {
     scr_words_ += up(2u * 32u * max_dz_);
     off_wt_ = scr_words_;
     scr_words_ += up(32u * 33u);
     off_ct_ = scr_words_;
-    if (dbl()) scr_words_ += up(32u * 33u);
+    if (dual()) scr_words_ += up(32u * 33u);
   }
 }
 
 std::string Gen::wsrc(const Sub& s, const std::string& arr) const {
-  // Global base of this subkernel's weight tile for the current row.
-  if (cfg_.w_shared) return "(" + arr + " + " + std::to_string(s.w_off) + ")";
-  return "(" + arr + " + row * (i64)" + std::to_string(p_.n_w) + " + " + std::to_string(s.w_off) + ")";
+  if (cfg_.w_shared) return "(" + arr + " + " + S(s.w_off) + ")";
+  return "(" + arr + " + " + idx(e_src()) + " * (i64)" + S(p_.n_w) + " + " + S(s.w_off) + ")";
 }
 
+std::string Gen::yv(int j) const { return "sl[ys + " + S(j) + "]"; }
+std::string Gen::dbv(int j) const { return "sl[dbs + " + S(j) + "]"; }
+
+// issue_unit: arm the slot's mbarrier with this item's byte count and start
+// its bulk copies. Window ranges (y-like rows that are not 16-byte aligned)
+// copy the aligned window around the row unless it would run past the array.
 void Gen::emit_issue() {
-  o_ << "DEVI void issue_unit(int u, i64 row, T* sl, u64* bar, const T* __restrict__ X,"
-        " const T* __restrict__ W, const T* __restrict__ GZ, const T* __restrict__ DA,"
-        " const T* __restrict__ DC) {\n"
+  o_ << "__device__ __noinline__ void issue_unit(int u, i64 row, i64 nbr, i64 eid, i64 rows_tot, i64 edges_tot, T* sl, u64* bar,"
+        " const T* __restrict__ X, const T* __restrict__ Y, const T* __restrict__ W, const T* __restrict__ GZ,"
+        " const T* __restrict__ DA, const T* __restrict__ DB, const T* __restrict__ DC) {\n"
         "  fence_proxy_async();\n  switch (u) {\n";
   for (size_t u = 0; u < lay_.size(); ++u) {
     const auto& L = lay_[u];
-    o_ << "  case " << u << ":\n    mbar_expect_tx(bar, " << L.bulk_bytes << "u);\n";
+    o_ << "  case " << u << ": {\n    u32 tx = " << L.fixed_bulk_bytes << "u;\n";
     for (const auto& r : L.ranges)
-      if (r.bulk)
-        o_ << "    bulk_g2s(sl + " << r.slot_off << ", " << r.arr << " + row * (i64)" << r.stride
-           << " + " << r.off << ", " << r.words * sz_ << "u, bar);\n";
-    o_ << "    break;\n";
+      if (r.bulk && r.window) {
+        const std::string I = r.src == Src::Edge ? "eid" : "row";
+        const std::string tot = r.src == Src::Edge && conv() ? "edges_tot" : "rows_tot";
+        o_ << "    { const i64 b0 = " << I << " * " << r.stride << "; const i64 a0 = b0 & ~(i64)" << A() - 1
+           << "; const i64 a1 = (b0 + " << r.words << " + " << A() - 1 << ") & ~(i64)" << A() - 1 << ";\n"
+           << "      if (a1 <= " << tot << " * (i64)" << r.stride << ") { tx += (u32)((a1 - a0) * sizeof(T)); }\n    }\n";
+      }
+    o_ << "    mbar_expect_tx(bar, tx);\n";
+    for (const auto& r : L.ranges) {
+      if (!r.bulk) continue;
+      if (r.window) {
+        const std::string I = r.src == Src::Edge ? "eid" : "row";
+        const std::string tot = r.src == Src::Edge && conv() ? "edges_tot" : "rows_tot";
+        o_ << "    { const i64 b0 = " << I << " * " << r.stride << "; const i64 a0 = b0 & ~(i64)" << A() - 1
+           << "; const i64 a1 = (b0 + " << r.words << " + " << A() - 1 << ") & ~(i64)" << A() - 1 << ";\n"
+           << "      if (a1 <= " << tot << " * (i64)" << r.stride << ") bulk_g2s(sl + " << r.slot_off << ", " << r.arr
+           << " + a0, (u32)((a1 - a0) * sizeof(T)), bar); }\n";
+      } else {
+        const std::string I = (r.arr == "W" || r.arr == "DC") && cfg_.w_shared ? "0" : idx(r.src);
+        o_ << "    bulk_g2s(sl + " << r.slot_off << ", " << r.arr << " + " << I << " * (i64)" << r.stride << " + "
+           << r.off << ", " << r.words * sz_ << "u, bar);\n";
+      }
+    }
+    o_ << "    break; }\n";
   }
   o_ << "  default: break;\n  }\n}\n\n";
 }
 
-void Gen::emit_store(const std::string& dst, std::uint32_t stride, std::uint32_t off,
-                     std::uint32_t words, const std::string& guard_rows, int width,
-                     const std::string& reg) {
-  // Lane r owns `width` consecutive words of the piece; stage through smem so
-  // the global store is coalesced (and 16-byte vectorised when aligned).
+void Gen::emit_wait_and_sync(int ui) {
+  const UnitLayout& L = lay_[ui];
+  o_ << "      T* sl = wsm + slot * SLOT_WORDS;\n      mbar_wait(&bars[slot], phase);\n";
+  bool sync = false;
+  for (const auto& r : L.ranges) {
+    if (r.window) {
+      const std::string I = r.src == Src::Edge ? "eid" : "row";
+      const std::string tot = r.src == Src::Edge && conv() ? "edges_tot" : "rows";
+      const std::string var = r.arr == "Y" ? "ys" : "dbs";
+      // bulk path: data sits at (b0 - a0) inside the window; sync path: at 0.
+      if (r.bulk) {
+        o_ << "      int " << var << ";\n      { const i64 b0 = " << I << " * " << r.stride << "; const i64 a0 = b0 & ~(i64)"
+           << A() - 1 << "; const i64 a1 = (b0 + " << r.words << " + " << A() - 1 << ") & ~(i64)" << A() - 1 << ";\n"
+           << "        if (a1 <= " << tot << " * (i64)" << r.stride << ") " << var << " = " << r.slot_off
+           << " + (int)(b0 - a0);\n        else { " << var << " = " << r.slot_off << "; coop_load(sl + "
+           << r.slot_off << ", " << r.arr << " + b0, " << r.words << ", lane); __syncwarp(); } }\n";
+      } else {
+        o_ << "      const int " << var << " = " << r.slot_off << ";\n      coop_load(sl + " << r.slot_off << ", " << r.arr
+           << " + " << I << " * (i64)" << r.stride << ", " << r.words << ", lane);\n";
+        sync = true;
+      }
+      continue;
+    }
+    if (r.bulk) continue;
+    const std::string I = (r.arr == "W" || r.arr == "DC") && cfg_.w_shared ? "0" : idx(r.src);
+    o_ << "      coop_load(sl + " << r.slot_off << ", " << r.arr << " + " << I << " * (i64)" << r.stride << " + "
+       << r.off << ", " << r.words << ", lane);\n";
+    sync = true;
+  }
+  if (sync) o_ << "      __syncwarp();\n";
+}
+
+void Gen::emit_release() {
+  o_ << "      __syncwarp();\n      if (lane == 0) producer_next();\n"
+        "      if (++slot == D) { slot = 0; phase ^= 1u; }\n";
+}
+
+void Gen::emit_store(const std::string& dst, const std::string& rowexpr, std::uint32_t stride, std::uint32_t off,
+                     std::uint32_t words, int guard_rows, int width, const std::string& reg) {
   o_ << "      if (lane < " << guard_rows << ") {";
   for (int k = 0; k < width; ++k) o_ << " scr[lane * " << width << " + " << k << "] = " << reg << "[" << k << "];";
   o_ << " }\n      __syncwarp();\n";
-  const bool vec = cfg_.aligned && aligned16(stride) && aligned16(off) && aligned16(words);
+  const bool vec = cfg_.aligned && al16(stride) && al16(off) && al16(words);
   if (vec)
-    o_ << "      coop_store16(" << dst << " + row * (i64)" << stride << " + " << off << ", scr, "
+    o_ << "      coop_store16(" << dst << " + " << rowexpr << " * (i64)" << stride << " + " << off << ", scr, "
        << words * sz_ / 16 << ", lane);\n";
   else
-    o_ << "      coop_store(" << dst << " + row * (i64)" << stride << " + " << off << ", scr, " << words
+    o_ << "      coop_store(" << dst << " + " << rowexpr << " * (i64)" << stride << " + " << off << ", scr, " << words
        << ", lane);\n";
   o_ << "      __syncwarp();\n";
 }
 
-void Gen::emit_unit(int ui) {
+// Compute of one unit on its staged slot. Accumulators (ax<prefix><c> for x
+// chunks, pz<u>_<z> for z pieces, gy) are declared by the caller.
+void Gen::emit_unit_body(int ui, const std::string& axp, const std::function<void(int)>& post_sub) {
   const Unit& u = units_[ui];
   const UnitLayout& L = lay_[ui];
-  o_ << "    { // ---- unit " << ui << ": " << u.subs.size() << " subkernels\n";
-  o_ << "      T* sl = wsm + slot * " << "SLOT_WORDS;\n";
-  o_ << "      mbar_wait(&bars[slot], phase);\n";
-  bool any_sync = false;
-  for (const auto& r : L.ranges)
-    if (!r.bulk) {
-      o_ << "      coop_load(sl + " << r.slot_off << ", " << r.arr << " + row * (i64)" << r.stride << " + "
-         << r.off << ", " << r.words << ", lane);\n";
-      any_sync = true;
-    }
-  if (any_sync) o_ << "      __syncwarp();\n";
-
-  // Output accumulators: per x chunk (gx / dx) and per z piece (z / dgz).
-  std::map<std::uint32_t, int> xdx, zdz;
-  std::map<std::uint32_t, int> xb, zb;
-  for (int si : u.subs) {
-    const Sub& s = p_.subs[si];
-    xdx[s.x_off] = s.dx();
-    xb[s.x_off] = s.bp;
-    zdz[s.z_off] = s.dz();
-    zb[s.z_off] = s.b;
-  }
-  if (bwd())
-    for (size_t c = 0; c < u.x_chunks.size(); ++c)
-      o_ << "      T gx" << c << "[" << xdx[u.x_chunks[c].off] << "] = {};\n";
-  if (cfg_.op != Op::Bwd)
-    for (size_t z = 0; z < u.z_pieces.size(); ++z)
-      o_ << "      T pz" << z << "[" << zdz[u.z_pieces[z].off] << "] = {};\n";
-
-  for (int si : u.subs) {
+  const std::string nw = S(p_.n_w);
+  const std::string wrow = cfg_.w_shared ? "0" : idx(e_src());
+  for (size_t q = 0; q < u.subs.size(); ++q) {
+    const int si = u.subs[q];
     const Sub& s = p_.subs[si];
     const int dx = s.dx(), dz = s.dz();
     const int xc = u.x_chunk_of(s), zc = u.z_piece_of(s);
+    const std::string AX = axp + S(xc), PZ = "pz" + S(ui) + "_" + S(zc);
+    if (q) o_ << "      asm volatile(\"\" ::: \"memory\");\n";  // keep subkernels' live ranges apart
+    o_ << "      { // sub " << si << ": " << (s.kind == Kind::B ? "B" : "C") << " l=(" << s.l1 << "," << s.l2 << ","
+       << s.l3 << ") b=" << s.b << " b'=" << s.bp << " nnz=" << s.cg->entries.size() << "\n";
+    const bool gfl = gy_flush();
+    if (gfl) o_ << "        T gyl[" << s.dy() << "] = {};\n";
+    auto GY = [&](int j) { return gfl ? "gyl[" + S(j) + "]" : "gy[" + S(s.y_off + j) + "]"; };
     const std::uint32_t xs = L.x_slot.at(s.x_off);
-    o_ << "      { // sub " << si << ": " << (s.kind == Kind::B ? "B" : "C") << " l=(" << s.l1 << ","
-       << s.l2 << "," << s.l3 << ") b=" << s.b << " b'=" << s.bp << " nnz=" << s.cg->entries.size()
-       << "\n";
-    // x (and da) lanes t < b'
-    o_ << "        T xv[" << dx << "];";
-    if (dbl()) o_ << " T av[" << dx << "];";
-    o_ << "\n        if (lane < " << s.bp << ") {";
+    o_ << "        T xv[" << dx << "];" << (dual() ? " T av[" + S(dx) + "];" : "") << "\n        if (lane < " << s.bp << ") {";
     for (int i = 0; i < dx; ++i) o_ << " xv[" << i << "] = sl[" << xs << " + lane * " << dx << " + " << i << "];";
-    if (dbl())
-      for (int i = 0; i < dx; ++i)
-        o_ << " av[" << i << "] = sl[" << L.a_slot.at(s.x_off) << " + lane * " << dx << " + " << i << "];";
+    if (dual())
+      for (int i = 0; i < dx; ++i) o_ << " av[" << i << "] = sl[" << L.a_slot.at(s.x_off) << " + lane * " << dx << " + " << i << "];";
     o_ << " } else {";
     for (int i = 0; i < dx; ++i) o_ << " xv[" << i << "] = 0;";
-    if (dbl())
+    if (dual())
       for (int i = 0; i < dx; ++i) o_ << " av[" << i << "] = 0;";
     o_ << " }\n";
-    // gz (lanes t < b), uniform access for C
     std::string gzs;
-    if (bwd()) {
-      gzs = std::to_string(L.gz_slot.at(s.z_off));
+    if (reads_gz()) {
+      gzs = S(L.gz_slot.at(s.z_off));
       if (s.kind == Kind::B) {
         o_ << "        T gz[" << dz << "];\n        if (lane < " << s.b << ") {";
         for (int k = 0; k < dz; ++k) o_ << " gz[" << k << "] = sl[" << gzs << " + lane * " << dz << " + " << k << "];";
@@ -286,159 +364,304 @@ void Gen::emit_unit(int ui) {
         o_ << " }\n";
       }
     }
-    // weights for B: per lane scalar
     if (s.kind == Kind::B) {
       auto wexpr = [&](const std::string& arr, const std::map<int, std::uint32_t>& slot) {
         if (cfg_.w_shared) return "__ldg(" + wsrc(s, arr) + " + lane)";
-        return "sl[" + std::to_string(slot.at(si)) + " + lane]";
+        return "sl[" + S(slot.at(si)) + " + lane]";
       };
       o_ << "        const T wt = (lane < " << s.b << ") ? " << wexpr("W", L.w_slot) << " : (T)0;\n";
-      if (dbl()) o_ << "        const T ct = (lane < " << s.b << ") ? " << wexpr("DC", L.c_slot) << " : (T)0;\n";
+      if (dual()) o_ << "        const T ct = (lane < " << s.b << ") ? " << wexpr("DC", L.c_slot) << " : (T)0;\n";
     }
-    // W^T g_z (bwd): gzp (and gzc for dbl: dC^T g_z)
-    if (bwd()) {
-      o_ << "        T gzp[" << dz << "];";
-      if (dbl()) o_ << " T gzc[" << dz << "];";
-      o_ << "\n";
+    const bool need_gzc = cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdX;
+    if (reads_gz()) {
+      o_ << "        T gzp[" << dz << "];" << (need_gzc ? " T gzc[" + S(dz) + "];" : "") << "\n";
       if (s.kind == Kind::B) {
-        for (int k = 0; k < dz; ++k) {
-          o_ << "        gzp[" << k << "] = wt * gz[" << k << "];";
-          if (dbl()) o_ << " gzc[" << k << "] = ct * gz[" << k << "];";
-          o_ << "\n";
-        }
+        for (int k = 0; k < dz; ++k)
+          o_ << "        gzp[" << k << "] = wt * gz[" << k << "];" << (need_gzc ? " gzc[" + S(k) + "] = ct * gz[" + S(k) + "];" : "") << "\n";
       } else {
         o_ << "        {";
-        for (int k = 0; k < dz; ++k) {
-          o_ << " gzp[" << k << "] = 0;";
-          if (dbl()) o_ << " gzc[" << k << "] = 0;";
-        }
+        for (int k = 0; k < dz; ++k) o_ << " gzp[" << k << "] = 0;" << (need_gzc ? " gzc[" + S(k) + "] = 0;" : "");
         o_ << "\n          const T* wg = " << wsrc(s, "W") << ";\n";
-        if (dbl()) o_ << "          const T* cg = " << wsrc(s, "DC") << ";\n";
+        if (need_gzc) o_ << "          const T* cg = " << wsrc(s, "DC") << ";\n";
         o_ << "#pragma unroll 2\n          for (int r = 0; r < " << s.b << "; ++r) {\n"
            << "            const T wv = (lane < " << s.bp << ") ? __ldg(wg + r * " << s.w_stride << " + lane) : (T)0;\n";
-        if (dbl())
-          o_ << "            const T cv = (lane < " << s.bp << ") ? __ldg(cg + r * " << s.w_stride << " + lane) : (T)0;\n";
+        if (need_gzc) o_ << "            const T cv = (lane < " << s.bp << ") ? __ldg(cg + r * " << s.w_stride << " + lane) : (T)0;\n";
         for (int k = 0; k < dz; ++k) {
-          o_ << "            { const T g = sl[" << gzs << " + r * " << dz << " + " << k << "]; gzp[" << k
-             << "] = fma(wv, g, gzp[" << k << "]);";
-          if (dbl()) o_ << " gzc[" << k << "] = fma(cv, g, gzc[" << k << "]);";
+          o_ << "            { const T g = sl[" << gzs << " + r * " << dz << " + " << k << "]; gzp[" << k << "] = fma(wv, g, gzp[" << k << "]);";
+          if (need_gzc) o_ << " gzc[" << k << "] = fma(cv, g, gzc[" << k << "]);";
           o_ << " }\n";
         }
         o_ << "          }\n        }\n";
       }
     }
-    // The unrolled CG stream: one line per nonzero entry.
-    if (cfg_.op == Op::Fwd) {
-      o_ << "        T zp[" << dz << "] = {};\n";
-      for (const auto& e : s.cg->entries)
-        o_ << "        zp[" << e.k << "] = fma((T)" << hexd(e.v) << " * y[" << s.y_off + e.j << "], xv[" << e.i
-           << "], zp[" << e.k << "]);\n";
-    } else if (cfg_.op == Op::Bwd) {
-      o_ << "        T zp[" << dz << "] = {};\n";
-      for (const auto& e : s.cg->entries) {
-        const std::string v = "(T)" + hexd(e.v);
-        const std::string yj = "y[" + std::to_string(s.y_off + e.j) + "]";
-        o_ << "        { const T c = " << v << " * " << yj << "; gx" << xc << "[" << e.i << "] = fma(c, gzp["
-           << e.k << "], gx" << xc << "[" << e.i << "]); zp[" << e.k << "] = fma(c, xv[" << e.i << "], zp["
-           << e.k << "]); gy[" << s.y_off + e.j << "] = fma(" << v << " * xv[" << e.i << "], gzp[" << e.k
-           << "], gy[" << s.y_off + e.j << "]); }\n";
+    // ---- the unrolled CG stream (one line per nonzero entry) ----
+    const bool zx = cfg_.comp == Comp::Fwd || cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ;
+    const bool zab = cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX;
+    if (zx) o_ << "        T zx[" << dz << "] = {};\n";
+    if (zab) o_ << "        T za[" << dz << "] = {}; T zb[" << dz << "] = {};\n";
+    for (const auto& e : s.cg->entries) {
+      const std::string v = "(T)" + hexd(e.v), I = S(e.i), K = S(e.k);
+      const int J = s.y_off + e.j;
+      std::ostringstream l;
+      l << "        { const T cy = " << v << " * " << yv(J) << ";";
+      if (dual()) l << " const T cb = " << v << " * " << dbv(J) << ";";
+      if (zx) l << " zx[" << K << "] = fma(cy, xv[" << I << "], zx[" << K << "]);";
+      if (zab) l << " za[" << K << "] = fma(cy, av[" << I << "], za[" << K << "]); zb[" << K << "] = fma(cb, xv[" << I << "], zb[" << K << "]);";
+      if (cfg_.comp == Comp::Bwd) {
+        l << " " << AX << "[" << I << "] = fma(cy, gzp[" << K << "], " << AX << "[" << I << "]);"
+          << " " << GY(e.j) << " = fma(" << v << " * xv[" << I << "], gzp[" << K << "], " << GY(e.j) << ");";
       }
-    } else {
-      o_ << "        T zx[" << dz << "] = {}; T za[" << dz << "] = {}; T zb[" << dz << "] = {};\n";
-      for (const auto& e : s.cg->entries) {
-        const std::string v = "(T)" + hexd(e.v);
-        const std::string J = std::to_string(s.y_off + e.j), I = std::to_string(e.i), K = std::to_string(e.k);
-        const std::string X = std::to_string(xc);
-        o_ << "        { const T cy = " << v << " * y[" << J << "]; const T cb = " << v << " * db[" << J
-           << "];\n"
-           << "          gx" << X << "[" << I << "] = fma(cb, gzp[" << K << "], fma(cy, gzc[" << K << "], gx" << X
-           << "[" << I << "]));\n"
-           << "          gy[" << J << "] = fma(" << v << " * av[" << I << "], gzp[" << K << "], fma(" << v
-           << " * xv[" << I << "], gzc[" << K << "], gy[" << J << "]));\n"
-           << "          zx[" << K << "] = fma(cy, xv[" << I << "], zx[" << K << "]); za[" << K
-           << "] = fma(cy, av[" << I << "], za[" << K << "]); zb[" << K << "] = fma(cb, xv[" << I << "], zb[" << K
-           << "]); }\n";
+      if (need_gzc) {
+        l << " " << AX << "[" << I << "] = fma(cb, gzp[" << K << "], fma(cy, gzc[" << K << "], " << AX << "[" << I << "]));"
+          << " " << GY(e.j) << " = fma(" << v << " * av[" << I << "], gzp[" << K << "], fma(" << v << " * xv[" << I
+          << "], gzc[" << K << "], " << GY(e.j) << "));";
       }
+      l << " }\n";
+      o_ << l.str();
     }
-    // Weight application / weight gradients.
-    const std::string nw = std::to_string(p_.n_w);
-    if (cfg_.op == Op::Fwd) {
+    // ---- weight application (z-type outputs) ----
+    if (out_z()) {
+      const bool dz_mode = cfg_.comp != Comp::Fwd;  // dgz = W.(za+zb) + dC.zx
       if (s.kind == Kind::B) {
-        for (int k = 0; k < dz; ++k) o_ << "        pz" << zc << "[" << k << "] = fma(wt, zp[" << k << "], pz" << zc << "[" << k << "]);\n";
+        for (int k = 0; k < dz; ++k) {
+          if (dz_mode)
+            o_ << "        " << PZ << "[" << k << "] = fma(ct, zx[" << k << "], fma(wt, za[" << k << "] + zb[" << k << "], " << PZ << "[" << k << "]));\n";
+          else
+            o_ << "        " << PZ << "[" << k << "] = fma(wt, zx[" << k << "], " << PZ << "[" << k << "]);\n";
+        }
       } else {
         o_ << "        if (lane < " << s.bp << ") {";
-        for (int k = 0; k < dz; ++k) o_ << " zs[lane * " << dz << " + " << k << "] = zp[" << k << "];";
-        o_ << " }\n        { const T* wg = " << wsrc(s, "W") << ";\n"
-           << "#pragma unroll 4\n          for (int r = 0; r < " << s.b << "; ++r) if (lane < " << s.bp
-           << ") wts[r * 33 + lane] = __ldg(wg + r * " << s.w_stride << " + lane); }\n"
-           << "        __syncwarp();\n        if (lane < " << s.b << ") {\n#pragma unroll 4\n"
-           << "          for (int c = 0; c < " << s.bp << "; ++c) { const T wv = wts[lane * 33 + c];";
-        for (int k = 0; k < dz; ++k) o_ << " pz" << zc << "[" << k << "] = fma(wv, zs[c * " << dz << " + " << k << "], pz" << zc << "[" << k << "]);";
+        for (int k = 0; k < dz; ++k) {
+          if (dz_mode)
+            o_ << " zs[lane * " << dz << " + " << k << "] = za[" << k << "] + zb[" << k << "]; zs[" << 32 * dz << " + lane * " << dz << " + " << k << "] = zx[" << k << "];";
+          else
+            o_ << " zs[lane * " << dz << " + " << k << "] = zx[" << k << "];";
+        }
+        o_ << " }\n        { const T* wg = " << wsrc(s, "W") << ";" << (dz_mode ? " const T* cg = " + wsrc(s, "DC") + ";" : "") << "\n"
+           << "#pragma unroll 4\n          for (int r = 0; r < " << s.b << "; ++r) if (lane < " << s.bp << ") { wts[r * 33 + lane] = __ldg(wg + r * " << s.w_stride << " + lane);";
+        if (dz_mode) o_ << " cts[r * 33 + lane] = __ldg(cg + r * " << s.w_stride << " + lane);";
+        o_ << " } }\n        __syncwarp();\n        if (lane < " << s.b << ") {\n#pragma unroll 4\n"
+           << "          for (int c = 0; c < " << s.bp << "; ++c) { const T wv = wts[lane * 33 + c];" << (dz_mode ? " const T cv = cts[lane * 33 + c];" : "");
+        for (int k = 0; k < dz; ++k) {
+          if (dz_mode)
+            o_ << " " << PZ << "[" << k << "] = fma(cv, zs[" << 32 * dz << " + c * " << dz << " + " << k << "], fma(wv, zs[c * " << dz << " + " << k << "], " << PZ << "[" << k << "]));";
+          else
+            o_ << " " << PZ << "[" << k << "] = fma(wv, zs[c * " << dz << " + " << k << "], " << PZ << "[" << k << "]);";
+        }
         o_ << " }\n        }\n        __syncwarp();\n";
-      }
-    } else if (cfg_.op == Op::Bwd) {
-      if (s.kind == Kind::B) {
-        o_ << "        { T g = 0;";
-        for (int k = 0; k < dz; ++k) o_ << " g = fma(gz[" << k << "], zp[" << k << "], g);";
-        o_ << " if (lane < " << s.b << ") O2[row * (i64)" << nw << " + " << s.w_off << " + lane] = g; }\n";
-      } else {
-        o_ << "#pragma unroll 2\n        for (int r = 0; r < " << s.b << "; ++r) { T g = 0;";
-        for (int k = 0; k < dz; ++k) o_ << " g = fma(sl[" << gzs << " + r * " << dz << " + " << k << "], zp[" << k << "], g);";
-        o_ << " if (lane < " << s.bp << ") O2[row * (i64)" << nw << " + " << s.w_off << " + r * " << s.w_stride
-           << " + lane] = g; }\n";
-      }
-    } else {  // DBwd
-      if (s.kind == Kind::B) {
-        for (int k = 0; k < dz; ++k)
-          o_ << "        pz" << zc << "[" << k << "] = fma(ct, zx[" << k << "], fma(wt, za[" << k << "] + zb[" << k
-             << "], pz" << zc << "[" << k << "]));\n";
-        o_ << "        { T g = 0;";
-        for (int k = 0; k < dz; ++k) o_ << " g = fma(gz[" << k << "], za[" << k << "] + zb[" << k << "], g);";
-        o_ << " if (lane < " << s.b << ") O2[row * (i64)" << nw << " + " << s.w_off << " + lane] = g; }\n";
-      } else {
-        o_ << "        if (lane < " << s.bp << ") {";
-        for (int k = 0; k < dz; ++k)
-          o_ << " zs[lane * " << dz << " + " << k << "] = za[" << k << "] + zb[" << k << "]; zs[" << 32 * dz
-             << " + lane * " << dz << " + " << k << "] = zx[" << k << "];";
-        o_ << " }\n        { const T* wg = " << wsrc(s, "W") << "; const T* cg = " << wsrc(s, "DC") << ";\n"
-           << "#pragma unroll 4\n          for (int r = 0; r < " << s.b << "; ++r) if (lane < " << s.bp
-           << ") { wts[r * 33 + lane] = __ldg(wg + r * " << s.w_stride << " + lane); cts[r * 33 + lane] = __ldg(cg + r * "
-           << s.w_stride << " + lane); } }\n"
-           << "        __syncwarp();\n        if (lane < " << s.b << ") {\n#pragma unroll 4\n"
-           << "          for (int c = 0; c < " << s.bp << "; ++c) { const T wv = wts[lane * 33 + c]; const T cv = cts[lane * 33 + c];";
-        for (int k = 0; k < dz; ++k)
-          o_ << " pz" << zc << "[" << k << "] = fma(cv, zs[" << 32 * dz << " + c * " << dz << " + " << k
-             << "], fma(wv, zs[c * " << dz << " + " << k << "], pz" << zc << "[" << k << "]));";
-        o_ << " }\n        }\n        __syncwarp();\n";
-        o_ << "#pragma unroll 2\n        for (int r = 0; r < " << s.b << "; ++r) { T g = 0;";
-        for (int k = 0; k < dz; ++k)
-          o_ << " g = fma(sl[" << gzs << " + r * " << dz << " + " << k << "], za[" << k << "] + zb[" << k << "], g);";
-        o_ << " if (lane < " << s.bp << ") O2[row * (i64)" << nw << " + " << s.w_off << " + r * " << s.w_stride
-           << " + lane] = g; }\n";
       }
     }
+    // ---- weight gradients (per sub, written directly) ----
+    if (out_w()) {
+      const std::string zsum = cfg_.comp == Comp::Bwd ? "zx[K]" : "(za[K] + zb[K])";
+      auto zk = [&](int k) {
+        std::string t = zsum;
+        for (size_t pos; (pos = t.find("[K]")) != std::string::npos;) t.replace(pos, 3, "[" + S(k) + "]");
+        return t;
+      };
+      if (s.kind == Kind::B) {
+        o_ << "        { T g = 0;";
+        for (int k = 0; k < dz; ++k) o_ << " g = fma(gz[" << k << "], " << zk(k) << ", g);";
+        o_ << " if (lane < " << s.b << ") O2[" << wrow << " * (i64)" << nw << " + " << s.w_off << " + lane] = g; }\n";
+      } else {
+        o_ << "#pragma unroll 2\n        for (int r = 0; r < " << s.b << "; ++r) { T g = 0;";
+        for (int k = 0; k < dz; ++k) o_ << " g = fma(sl[" << gzs << " + r * " << dz << " + " << k << "], " << zk(k) << ", g);";
+        o_ << " if (lane < " << s.bp << ") O2[" << wrow << " * (i64)" << nw << " + " << s.w_off << " + r * " << s.w_stride << " + lane] = g; }\n";
+      }
+    }
+    if (gfl)
+      for (int j = 0; j < s.dy(); ++j)
+        o_ << "        { const T s_ = warp_sum(gyl[" << j << "]); if (lane == " << j % 32 << ") gya[" << s.y_off + j
+           << "] += s_; }\n";
     o_ << "      }\n";
+    if (post_sub) post_sub(static_cast<int>(q));
   }
-  // Stores of owned outputs.
-  if (bwd())
+}
+
+void Gen::emit_gy_flush_row(const std::string& rowexpr) {
+  o_ << "    __syncwarp();\n    for (int j = lane; j < " << p_.dim_y << "; j += 32) { O1[" << rowexpr << " * (i64)"
+     << p_.dim_y << " + j] = gya[j]; gya[j] = 0; }\n    __syncwarp();\n";
+}
+
+void Gen::emit_gy_reduce(const std::string& rowexpr) {
+  const int dy = p_.dim_y;
+  for (int j0 = 0; j0 < dy; j0 += 32) {
+    o_ << "    { T mine = 0;\n";
+    for (int j = j0; j < std::min(dy, j0 + 32); ++j)
+      o_ << "      { const T s_ = warp_sum(gy[" << j << "]); if (lane == " << j - j0 << ") mine = s_; }\n";
+    o_ << "      if (lane < " << std::min(dy - j0, 32) << ") O1[" << rowexpr << " * (i64)" << dy << " + " << j0 << " + lane] = mine; }\n";
+  }
+}
+
+std::string zero_init(const std::string& name, int n) { return "T " + name + "[" + S(n) + "] = {};"; }
+
+void Gen::emit_rows_loop() {
+  // Producer: items are (row ordinal, unit) in order; lane 0 issues item n + D.
+  o_ << "  i64 pn = 0;  // next item to issue (lane 0)\n"
+        "#define producer_next() do { if (pn < total) {\\\n"
+        "    const i64 rr_ = pn / NU; const int u_ = (int)(pn - rr_ * NU); const i64 r_ = gwarp + rr_ * nwarp;\\\n"
+        "    const int s_ = (int)(pn % D);\\\n"
+        "    issue_unit(u_, r_, r_, r_, rows, rows, wsm + s_ * SLOT_WORDS, &bars[s_], X, Y, W, GZ, DA, DB, DC);\\\n"
+        "    ++pn; } } while (0)\n"
+        "  if (lane == 0) for (int d = 0; d < D; ++d) producer_next();\n"
+        "  int slot = 0; u32 phase = 0;\n"
+        "  for (i64 rr = 0; rr < my_rows; ++rr) {\n    const i64 row = gwarp + rr * nwarp;\n"
+        "    const i64 nbr = row, eid = row; (void)nbr; (void)eid;\n";
+  if (out_y() && !gy_flush()) o_ << "    " << zero_init("gy", p_.dim_y) << "\n";
+  for (size_t ui = 0; ui < units_.size(); ++ui) {
+    const Unit& u = units_[ui];
+    o_ << "    { // ---- unit " << ui << ": " << u.subs.size() << " subkernels\n";
+    std::map<std::uint32_t, int> xdx, xb, zdz, zb;
+    for (int si : u.subs) {
+      const Sub& s = p_.subs[si];
+      xdx[s.x_off] = s.dx();
+      xb[s.x_off] = s.bp;
+      zdz[s.z_off] = s.dz();
+      zb[s.z_off] = s.b;
+    }
+    if (out_x())
+      for (size_t c = 0; c < u.x_chunks.size(); ++c) o_ << "      " << zero_init("ax" + S(c), xdx[u.x_chunks[c].off]) << "\n";
+    if (out_z())
+      for (size_t z = 0; z < u.z_pieces.size(); ++z)
+        o_ << "      " << zero_init("pz" + S(ui) + "_" + S(z), zdz[u.z_pieces[z].off]) << "\n";
+    emit_wait_and_sync(static_cast<int>(ui));
+    // Store every owned output right after the last subkernel that writes it
+    // (keeps accumulator live ranges short).
+    std::map<int, std::vector<int>> x_done, z_done;  // sub position -> chunks / pieces completed
     for (size_t c = 0; c < u.x_chunks.size(); ++c) {
-      const auto& xc = u.x_chunks[c];
-      emit_store("O0", p_.dim_x, xc.off, xc.words, std::to_string(xb[xc.off]), xdx[xc.off], "gx" + std::to_string(c));
+      int last = 0;
+      for (size_t q = 0; q < u.subs.size(); ++q)
+        if (p_.subs[u.subs[q]].x_off == u.x_chunks[c].off) last = static_cast<int>(q);
+      x_done[last].push_back(static_cast<int>(c));
     }
-  if (cfg_.op != Op::Bwd)
     for (size_t z = 0; z < u.z_pieces.size(); ++z) {
-      const auto& zp = u.z_pieces[z];
-      emit_store(cfg_.op == Op::Fwd ? "O0" : "O3", p_.dim_z, zp.off, zp.words, std::to_string(zb[zp.off]),
-                 zdz[zp.off], "pz" + std::to_string(z));
+      int last = 0;
+      for (size_t q = 0; q < u.subs.size(); ++q)
+        if (p_.subs[u.subs[q]].z_off == u.z_pieces[z].off) last = static_cast<int>(q);
+      z_done[last].push_back(static_cast<int>(z));
     }
-  // Release the slot: refill it with unit n + D.
-  o_ << "      if (lane == 0 && n + D < total) {\n"
-        "        const i64 m = n + D; const i64 rr2 = m / NU; const int u2 = (int)(m - rr2 * NU);\n"
-        "        issue_unit(u2, gwarp + rr2 * nwarp, sl, &bars[slot], X, W, GZ, DA, DC);\n      }\n"
-        "      ++n; if (++slot == D) { slot = 0; phase ^= 1u; }\n    }\n";
+    emit_unit_body(static_cast<int>(ui), "ax", [&](int q) {
+      if (out_x())
+        for (int c : x_done[q]) {
+          const auto& xc = u.x_chunks[c];
+          emit_store("O0", "row", p_.dim_x, xc.off, xc.words, xb[xc.off], xdx[xc.off], "ax" + S(c));
+        }
+      if (out_z())
+        for (int z : z_done[q]) {
+          const auto& zp = u.z_pieces[z];
+          emit_store(cfg_.comp == Comp::Fwd ? "O0" : "O3", "row", p_.dim_z, zp.off, zp.words, zb[zp.off], zdz[zp.off],
+                     "pz" + S(ui) + "_" + S(z));
+        }
+    });
+    emit_release();
+    o_ << "    }\n";
+  }
+  if (out_y()) {
+    if (gy_flush()) emit_gy_flush_row("row");
+    else emit_gy_reduce("row");
+  }
+  o_ << "  }\n";
+}
+
+void Gen::emit_conv_loop() {
+  // Producer cursor over (row, unit, edge) [ByOutput] or (row, edge, unit)
+  // [ByInput]; rows without edges yield no items.
+  const bool bi = by_input();
+  o_ << "  i64 pk = 0, pq = 0, pq1 = 0; int pu = 0;\n"
+        "#define prow(k) (gwarp + (k) * nwarp)\n"
+        "#define seek() do { while (pk < my_rows) { const i64 r_ = prow(pk); pq = RP[r_]; pq1 = RP[r_ + 1]; if (pq < pq1) break; ++pk; } } while (0)\n"
+        "  if (lane == 0) seek();\n"
+        "  int pslot = 0;\n"
+        "#define producer_next() do { if (pk < my_rows) {\\\n"
+        "    const i64 r_ = prow(pk);\\\n";
+  if (bi)
+    o_ << "    const i64 nb_ = NB[pq], e_ = EID[pq];\\\n";
+  else
+    o_ << "    const i64 nb_ = NB[pq], e_ = pq;\\\n";
+  o_ << "    issue_unit(pu, r_, nb_, e_, rows, edges_tot, wsm + pslot * SLOT_WORDS, &bars[pslot], X, Y, W, GZ, DA, DB, DC);\\\n"
+        "    if (++pslot == D) pslot = 0;\\\n";
+  if (bi)
+    o_ << "    if (++pu == NU) { pu = 0; if (++pq == pq1) { ++pk; seek(); } }\\\n";
+  else
+    o_ << "    if (++pq == pq1) { pq = RP[r_]; if (++pu == NU) { pu = 0; ++pk; seek(); } }\\\n";
+  o_ << "  } } while (0)\n"
+        "  if (lane == 0) for (int d = 0; d < D; ++d) producer_next();\n"
+        "  int slot = 0; u32 phase = 0;\n"
+        "  for (i64 k = 0; k < my_rows; ++k) {\n    const i64 row = prow(k);\n"
+        "    const i64 q0 = RP[row], q1 = RP[row + 1];\n";
+  if (!bi) {
+    for (size_t ui = 0; ui < units_.size(); ++ui) {
+      const Unit& u = units_[ui];
+      std::map<std::uint32_t, int> zdz, zb;
+      for (int si : u.subs) {
+        zdz[p_.subs[si].z_off] = p_.subs[si].dz();
+        zb[p_.subs[si].z_off] = p_.subs[si].b;
+      }
+      o_ << "    { // ---- unit " << ui << "\n";
+      for (size_t z = 0; z < u.z_pieces.size(); ++z)
+        o_ << "      " << zero_init("pz" + S(ui) + "_" + S(z), zdz[u.z_pieces[z].off]) << "\n";
+      o_ << "      for (i64 q = q0; q < q1; ++q) {\n      const i64 eid = q; const i64 nbr = NB[q]; (void)nbr;\n";
+      emit_wait_and_sync(static_cast<int>(ui));
+      emit_unit_body(static_cast<int>(ui), "ax");
+      emit_release();
+      o_ << "      }\n";
+      for (size_t z = 0; z < u.z_pieces.size(); ++z) {
+        const auto& zp = u.z_pieces[z];
+        emit_store(cfg_.comp == Comp::Fwd ? "O0" : "O3", "row", p_.dim_z, zp.off, zp.words, zb[zp.off], zdz[zp.off],
+                   "pz" + S(ui) + "_" + S(z));
+      }
+      o_ << "    }\n";
+    }
+  } else {
+    // gx-type accumulators for every unit's x chunks live across the edge loop.
+    for (size_t ui = 0; ui < units_.size(); ++ui) {
+      const Unit& u = units_[ui];
+      for (size_t c = 0; c < u.x_chunks.size(); ++c) {
+        int dx = 1;
+        for (int si : u.subs)
+          if (p_.subs[si].x_off == u.x_chunks[c].off) dx = p_.subs[si].dx();
+        o_ << "    " << zero_init("ax" + S(ui) + "_" + S(c), dx) << "\n";
+      }
+    }
+    o_ << "    for (i64 q = q0; q < q1; ++q) {\n      const i64 eid = EID[q]; const i64 nbr = NB[q]; (void)nbr;\n";
+    if (out_y() && !gy_flush()) o_ << "      " << zero_init("gy", p_.dim_y) << "\n";
+    for (size_t ui = 0; ui < units_.size(); ++ui) {
+      o_ << "      { // ---- unit " << ui << "\n";
+      emit_wait_and_sync(static_cast<int>(ui));
+      emit_unit_body(static_cast<int>(ui), "ax" + S(ui) + "_");
+      emit_release();
+      o_ << "      }\n";
+    }
+    if (out_y()) {
+      if (gy_flush()) emit_gy_flush_row("eid");
+      else emit_gy_reduce("eid");
+    }
+    o_ << "    }\n";
+    for (size_t ui = 0; ui < units_.size(); ++ui) {
+      const Unit& u = units_[ui];
+      for (size_t c = 0; c < u.x_chunks.size(); ++c) {
+        int dx = 1, bp = 1;
+        for (int si : u.subs)
+          if (p_.subs[si].x_off == u.x_chunks[c].off) {
+            dx = p_.subs[si].dx();
+            bp = p_.subs[si].bp;
+          }
+        emit_store("O0", "row", p_.dim_x, u.x_chunks[c].off, u.x_chunks[c].words, bp, dx,
+                   "ax" + S(ui) + "_" + S(c));
+      }
+    }
+  }
+  o_ << "  }\n";
 }
 
 KernelSource Gen::run() {
+  if (conv() && cfg_.w_shared) throw UnsupportedError("shared weights are not supported in the fused convolution");
+  if (cfg_.loop == Loop::ConvByOutput && !(cfg_.comp == Comp::Fwd || cfg_.comp == Comp::DBwdZ))
+    throw UnsupportedError("ConvByOutput computes z-type outputs only");
+  if (cfg_.loop == Loop::ConvByInput && !(cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwdX))
+    throw UnsupportedError("ConvByInput computes x-type outputs only");
+  if (!conv() && (cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX))
+    throw UnsupportedError("split double-backward passes are conv-only");
   layout();
   std::uint32_t slot_words = 0;
   int bulk = 0, sync = 0;
@@ -446,20 +669,19 @@ KernelSource Gen::run() {
     slot_words = std::max(slot_words, L.words);
     for (const auto& r : L.ranges) (r.bulk ? bulk : sync)++;
   }
-  // Fit the ring into shared memory: shrink depth, then warps.
   int depth = cfg_.depth, warps = cfg_.warps;
   auto warp_bytes = [&](int d) { return (static_cast<std::uint64_t>(d) * slot_words + scr_words_) * sz_; };
   const std::uint64_t budget = 200 * 1024;
   while (depth > 1 && warp_bytes(depth) * warps + 8ull * depth * warps > budget) --depth;
   while (warps > 1 && warp_bytes(depth) * warps + 8ull * depth * warps > budget) --warps;
   if (warp_bytes(depth) * warps + 8ull * depth * warps > 227 * 1024)
-    throw UnsupportedError("problem too large for one warp's shared-memory slot (" +
-                           std::to_string(warp_bytes(1)) + " bytes)");
+    throw UnsupportedError("problem too large for one warp's shared-memory slot (" + S(warp_bytes(1)) + " bytes)");
   const std::uint64_t wb = (warp_bytes(depth) + 127) / 128 * 128;
-  const char* opn[] = {"fwd", "bwd", "dbwd"};
+  static const char* compn[] = {"fwd", "bwd", "dbwd", "dbwdz", "dbwdx"};
+  static const char* loopn[] = {"tp", "convo", "convi"};
   KernelSource ks;
-  ks.name = std::string("cgf_tp_") + opn[static_cast<int>(cfg_.op)] + (cfg_.f64 ? "_f64" : "_f32") +
-            (cfg_.w_shared ? "_ws" : "") + (cfg_.aligned ? "" : "_u");
+  ks.name = std::string("cgf_") + loopn[static_cast<int>(cfg_.loop)] + "_" + compn[static_cast<int>(cfg_.comp)] +
+            (cfg_.f64 ? "_f64" : "_f32") + (cfg_.w_shared ? "_ws" : "") + (cfg_.aligned ? "" : "_u");
   ks.threads = warps * 32;
   ks.smem_bytes = static_cast<int>(wb * warps + 8ull * depth * warps);
   ks.units = static_cast<int>(units_.size());
@@ -468,75 +690,44 @@ KernelSource Gen::run() {
 
   o_ << device_runtime_source();
   o_ << "\n// Generated for: x = " << p_.x_ir.str() << " | y = " << p_.y_ir.str() << " | z = " << p_.z_ir.str()
-     << "\n// " << p_.subs.size() << " split subkernels in " << units_.size() << " units; op " << opn[static_cast<int>(cfg_.op)]
-     << "\n";
+     << "\n// " << p_.subs.size() << " split subkernels in " << units_.size() << " units; " << ks.name << "\n";
   o_ << "typedef " << (cfg_.f64 ? "double" : "float") << " T;\n";
-  o_ << "#define NW " << warps << "\n#define D " << depth << "\n#define NU " << units_.size()
-     << "\n#define SLOT_WORDS " << slot_words << "\n#define WARP_BYTES " << wb << "\n\n";
+  o_ << "#define NW " << warps << "\n#define D " << depth << "\n#define NU " << units_.size() << "\n#define SLOT_WORDS "
+     << slot_words << "\n#define WARP_BYTES " << wb << "\n\n";
   emit_issue();
   o_ << "extern \"C\" __global__ void __launch_bounds__(NW * 32) " << ks.name
      << "(const T* __restrict__ X, const T* __restrict__ Y, const T* __restrict__ W,"
         " const T* __restrict__ GZ, const T* __restrict__ DA, const T* __restrict__ DB,"
         " const T* __restrict__ DC, T* __restrict__ O0, T* __restrict__ O1, T* __restrict__ O2,"
-        " T* __restrict__ O3, i64 rows) {\n"
+        " T* __restrict__ O3, i64 rows, const i64* __restrict__ RP, const int* __restrict__ NB,"
+        " const int* __restrict__ EID, i64 edges_tot) {\n"
         "  extern __shared__ __align__(128) unsigned char smem_raw[];\n"
         "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
         "  T* wsm = (T*)(smem_raw + wid * WARP_BYTES);\n"
         "  T* scr = wsm + D * SLOT_WORDS;\n";
   if (has_c_)
-    o_ << "  T* zs = scr + " << off_zs_ << "; T* wts = scr + " << off_wt_ << ";" << (dbl() ? " T* cts = scr + " + std::to_string(off_ct_) + ";" : "")
-       << "\n";
+    o_ << "  T* zs = scr + " << off_zs_ << "; T* wts = scr + " << off_wt_ << ";"
+       << (dual() ? " T* cts = scr + " + S(off_ct_) + ";" : "") << " (void)zs; (void)wts;\n";
+  o_ << "  T* gya = scr + " << off_gya_ << "; (void)gya;\n"
+        "  for (int j = lane; j < " << p_.dim_y << "; j += 32) gya[j] = 0;\n";
   o_ << "  u64* bars = (u64*)(smem_raw + NW * WARP_BYTES) + wid * D;\n"
         "  if (lane == 0) { for (int d = 0; d < D; ++d) mbar_init(&bars[d], 1); mbar_fence_init(); }\n"
         "  __syncwarp();\n"
         "  const i64 gwarp = (i64)blockIdx.x * NW + wid, nwarp = (i64)gridDim.x * NW;\n"
         "  const i64 my_rows = gwarp < rows ? (rows - 1 - gwarp) / nwarp + 1 : 0;\n"
-        "  const i64 total = my_rows * NU;\n"
-        "  if (lane == 0)\n"
-        "    for (int d = 0; d < D && d < total; ++d) {\n"
-        "      const i64 rr = d / NU; const int u = (int)(d - rr * NU);\n"
-        "      issue_unit(u, gwarp + rr * nwarp, wsm + d * SLOT_WORDS, &bars[d], X, W, GZ, DA, DC);\n"
-        "    }\n"
-        "  i64 n = 0; int slot = 0; u32 phase = 0;\n";
-  const int dy = p_.dim_y;
-  o_ << "  T y[" << dy << "], yn[" << dy << "];\n";
-  if (dbl()) o_ << "  T db[" << dy << "], dbn[" << dy << "];\n";
-  o_ << "  if (my_rows > 0) {";
-  for (int j = 0; j < dy; ++j) {
-    o_ << " yn[" << j << "] = __ldg(Y + gwarp * " << dy << " + " << j << ");";
-    if (dbl()) o_ << " dbn[" << j << "] = __ldg(DB + gwarp * " << dy << " + " << j << ");";
-  }
-  o_ << " }\n";
-  o_ << "  for (i64 rr = 0; rr < my_rows; ++rr) {\n    const i64 row = gwarp + rr * nwarp;\n";
-  o_ << "   ";
-  for (int j = 0; j < dy; ++j) {
-    o_ << " y[" << j << "] = yn[" << j << "];";
-    if (dbl()) o_ << " db[" << j << "] = dbn[" << j << "];";
-  }
-  o_ << "\n    if (rr + 1 < my_rows) {";
-  for (int j = 0; j < dy; ++j) {
-    o_ << " yn[" << j << "] = __ldg(Y + (row + nwarp) * " << dy << " + " << j << ");";
-    if (dbl()) o_ << " dbn[" << j << "] = __ldg(DB + (row + nwarp) * " << dy << " + " << j << ");";
-  }
-  o_ << " }\n";
-  if (bwd()) o_ << "    T gy[" << dy << "] = {};\n";
-  for (size_t u = 0; u < units_.size(); ++u) emit_unit(static_cast<int>(u));
-  if (bwd()) {
-    for (int j0 = 0; j0 < dy; j0 += 32) {
-    o_ << "    { T mine = 0;\n";
-    for (int j = j0; j < std::min(dy, j0 + 32); ++j) o_ << "      { const T s = warp_sum(gy[" << j << "]); if (lane == " << j - j0 << ") mine = s; }\n";
-    o_ << "      if (lane < " << std::min(dy - j0, 32) << ") O1[row * (i64)" << dy << " + " << j0 << " + lane] = mine; }\n";
-    }
-  }
-  o_ << "  }\n}\n";
+        "  const i64 total = my_rows * NU; (void)total;\n";
+  if (conv())
+    emit_conv_loop();
+  else
+    emit_rows_loop();
+  o_ << "}\n";
   ks.source = o_.str();
   return ks;
 }
 
 }  // namespace
 
-KernelSource generate_tp_kernel(const Problem& p, const std::vector<Unit>& units,
-                                const KernelConfig& cfg) {
+KernelSource generate_kernel(const Problem& p, const std::vector<Unit>& units, const KernelConfig& cfg) {
   Gen g(p, units, cfg);
   return g.run();
 }

@@ -3,10 +3,19 @@
 // Replaces the reference's IR generator + interpreter (kernelgen::gen_forward /
 // gen_backward / interpret, kernelgen.cpp:135-251, 547-675): instead of an op
 // stream interpreted per row, every split subkernel becomes straight-line CUDA
-// with its CG coefficients as immediates, and the whole row is one warp's
-// program. Inputs are staged per unit into shared memory by the bulk-copy
-// engine (cp.async.bulk + mbarrier, a D-deep per-warp ring); outputs leave
-// through a per-warp staging buffer as coalesced 16-byte stores.
+// with its CG coefficients as immediates, and a row's units run back to back
+// in one warp. Inputs are staged per (unit, item) into shared memory by the
+// bulk-copy engine (cp.async.bulk + mbarrier, a D-deep ring per warp); outputs
+// leave through a per-warp staging buffer as coalesced 16-byte stores.
+//
+// The same per-subkernel code drives three loop structures:
+//   Rows          batched TP: item = (row, unit); every output row-owned.
+//   ConvByOutput  fused conv, row = output node s (CSR by s): for each unit,
+//                 stream the row's edges and accumulate z_s in registers
+//                 (conv.cpp:234-355, without the chunk fixup: rows are owned).
+//   ConvByInput   fused conv, row = neighbour node d (transposed CSR):
+//                 for each edge, all units; gx_d accumulated in registers,
+//                 per-edge gy / gW written directly (conv.cpp:357-528).
 #pragma once
 
 #include <string>
@@ -18,8 +27,20 @@ namespace cgf {
 
 enum class Op : int { Fwd = 0, Bwd = 1, DBwd = 2 };
 
+// What each generated kernel computes.
+enum class Comp : int {
+  Fwd = 0,    // z = W . cg(x, y)
+  Bwd = 1,    // gx, gy, gW
+  DBwd = 2,   // dx, dy, dW, dgz in one pass (unfused TP)
+  DBwdZ = 3,  // conv double-backward pass 1: dgz = W.(cg(da,y)+cg(x,db)) + dC.cg(x,y)
+  DBwdX = 4,  // conv double-backward pass 2: dx, dy, dW
+};
+
+enum class Loop : int { Rows = 0, ConvByOutput = 1, ConvByInput = 2 };
+
 struct KernelConfig {
-  Op op = Op::Fwd;
+  Comp comp = Comp::Fwd;
+  Loop loop = Loop::Rows;
   bool f64 = false;
   bool w_shared = false;  // one W row for every batch row (superset of the reference API)
   bool aligned = true;    // all base pointers 16-byte aligned -> bulk copies allowed
@@ -33,12 +54,23 @@ struct KernelSource {
   int threads = 0;
   int smem_bytes = 0;
   int units = 0;
-  int bulk_ranges = 0;  // ranges moved by cp.async.bulk per row
+  int bulk_ranges = 0;  // ranges moved by cp.async.bulk per item
   int sync_ranges = 0;  // ranges copied by the warp (unaligned)
 };
 
-KernelSource generate_tp_kernel(const Problem& p, const std::vector<Unit>& units,
-                                const KernelConfig& cfg);
+// Kernel parameters (all generated kernels share this signature):
+//   (const T* X, const T* Y, const T* W, const T* GZ, const T* DA, const T* DB,
+//    const T* DC, T* O0, T* O1, T* O2, T* O3, i64 rows,
+//    const i64* RP, const int* NB, const int* EID)
+// Rows: rows = batch rows; RP/NB/EID unused.
+// ConvByOutput: rows = nodes, RP = CSR row_ptr by output node, NB[e] = the
+//   neighbour read by edge e (reference `dst`); edge id = CSR position.
+// ConvByInput: rows = nodes, RP = transposed row_ptr, NB[q] = output node of
+//   transposed position q, EID[q] = its edge id.
+// Outputs: Fwd O0=z; Bwd O0=gx O1=gy O2=gW; DBwd O0=dx O1=dy O2=dW O3=dgz;
+//   DBwdZ O3=dgz; DBwdX O0=dx O1=dy O2=dW.
+KernelSource generate_kernel(const Problem& p, const std::vector<Unit>& units,
+                             const KernelConfig& cfg);
 
 // Shared device helpers (mbarrier, bulk copy, cooperative copies), prepended
 // to every generated translation unit.

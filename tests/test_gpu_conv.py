@@ -1,0 +1,173 @@
+"""GPU parity tests for the fused TP + graph convolution (deterministic,
+row-owned, no atomics) against the CPU oracle's conv (reference semantics,
+conv.cpp:234-528; double-backward composed per SURVEY.md §8c)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from problems import config, random_problem
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float32: 1e-5, np.float64: 1e-12}
+DTYPES = [np.float32, np.float64]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def P():
+    import paper_2501_13986_b200 as pkg
+    return pkg
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def check(got, want, dt, what):
+    err = O.rel_error(got, want)
+    assert err <= TOL[dt], f"{what}: rel err {err:.3e} > {TOL[dt]:.0e}"
+
+
+def conv_inputs(o, g, dt, seed=1234):
+    gen = O.NormalGen(seed)
+    nx = gen.normal_vec(g.nodes * o.dim_x, dt).reshape(g.nodes, -1)
+    ey = gen.normal_vec(g.edges * o.dim_y, dt).reshape(g.edges, -1)
+    ew = gen.normal_vec(g.edges * o.n_w, dt).reshape(g.edges, -1)
+    gnz = O.NormalGen(seed + 1).normal_vec(g.nodes * o.dim_z, dt).reshape(g.nodes, -1)
+    dgx = O.NormalGen(seed + 2).normal_vec(nx.size, dt).reshape(nx.shape)
+    dgy = O.NormalGen(seed + 3).normal_vec(ey.size, dt).reshape(ey.shape)
+    dgw = O.NormalGen(seed + 4).normal_vec(ew.size, dt).reshape(ew.shape)
+    return nx, ey, ew, gnz, dgx, dgy, dgw
+
+
+def graphs():
+    g1 = O.radius_graph(O.cubic_lattice(4), 1.5)
+    # ragged: a lattice with some nodes isolated (rows with no edges) and an
+    # isolated neighbour set (nodes never read)
+    g = O.radius_graph(O.cubic_lattice(5), 1.8)
+    keep = (g.src % 7 != 3) & (g.nbr % 11 != 5)
+    g2 = O.make_graph(g.nodes, g.src[keep], g.nbr[keep])
+    return {"lat4": g1, "ragged5": g2}
+
+
+CASES = [("paper", config("paper")), ("c1", config("c1")), ("c2", config("c2")),
+         ("rand311", random_problem(311)), ("rand2", random_problem(2)), ("rand5", random_problem(5))]
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f32", "f64"])
+@pytest.mark.parametrize("gname", ["lat4", "ragged5"])
+@pytest.mark.parametrize("name,js", CASES, ids=[c[0] for c in CASES])
+def test_conv_fwd_bwd_dbwd(name, js, gname, dt):
+    og = graphs()[gname]
+    o, pkg = O.Oracle(js), P()
+    plan = pkg.TpPlan(js)
+    cp = pkg.ConvPlan(plan)
+    g = pkg.Graph(og.nodes, og.src, og.nbr)
+    nx, ey, ew, gnz, dgx, dgy, dgw = conv_inputs(o, og, dt)
+    z = cp.forward(g, dev(nx), dev(ey), dev(ew))
+    check(host(z), o.conv_forward(og, nx, ey, ew), dt, "conv forward")
+    outs = cp.backward(g, dev(nx), dev(ey), dev(ew), dev(gnz))
+    for a, b, n in zip(outs, o.conv_backward(og, nx, ey, ew, gnz), ("g_node_x", "g_edge_y", "g_edge_w")):
+        check(host(a), b, dt, n)
+    outs = cp.double_backward(g, dev(nx), dev(ey), dev(ew), dev(gnz), (dev(dgx), dev(dgy), dev(dgw)))
+    want = o.conv_double_backward(og, nx, ey, ew, gnz, dgx, dgy, dgw)
+    for a, b, n in zip(outs, want, ("dnode_x", "dedge_y", "dedge_w", "dg_node_z")):
+        check(host(a), b, dt, n)
+
+
+def test_golden_conv_fixture():
+    d = np.load("tests/golden/conv_paper_float64.npz")
+    js = str(d["problem"])
+    o, pkg = O.Oracle(js), P()
+    og = O.make_graph(27, d["src"], d["nbr"])
+    cp = pkg.ConvPlan(pkg.TpPlan(js))
+    g = pkg.Graph(og.nodes, og.src, og.nbr)
+    nx, ey, ew, gnz, *_ = conv_inputs(o, og, np.float64)
+    check(host(cp.forward(g, dev(nx), dev(ey), dev(ew))), d["z"], np.float64, "golden z")
+    for a, k in zip(cp.backward(g, dev(nx), dev(ey), dev(ew), dev(gnz)), ("gx", "gy", "gw")):
+        check(host(a), d[k], np.float64, k)
+
+
+@pytest.mark.parametrize("name", ["paper", "c2"])
+def test_single_edge_conv_equals_tp_bitwise(name):
+    """A single-edge conv is one TP, bit for bit (test_conv.cpp:162-180, 308-333)."""
+    js = config(name)
+    o, pkg = O.Oracle(js), P()
+    plan = pkg.TpPlan(js)
+    cp = pkg.ConvPlan(plan)
+    g = pkg.Graph(2, [0], [1])
+    gen = O.NormalGen(7)
+    nx = gen.normal_vec(2 * o.dim_x).reshape(2, -1)
+    ey = gen.normal_vec(o.dim_y).reshape(1, -1)
+    ew = gen.normal_vec(o.n_w).reshape(1, -1)
+    z = cp.forward(g, dev(nx), dev(ey), dev(ew))
+    zt = plan.forward(dev(nx[1:2]), dev(ey), dev(ew))
+    assert torch.equal(z[0], zt[0])
+    assert not z[1].any()
+    gz = O.NormalGen(8).normal_vec(2 * o.dim_z).reshape(2, -1)
+    gx, gy, gw = cp.backward(g, dev(nx), dev(ey), dev(ew), dev(gz))
+    tx, ty, tw = plan.backward(dev(nx[1:2]), dev(ey), dev(ew), dev(gz[0:1]))
+    assert torch.equal(gx[1], tx[0]) and torch.equal(gy, ty) and torch.equal(gw, tw)
+    assert not gx[0].any()
+
+
+def test_conv_deterministic_bitwise():
+    js = config("c1")
+    o, pkg = O.Oracle(js), P()
+    og = O.radius_graph(O.cubic_lattice(6), 2.0)
+    cp = pkg.ConvPlan(pkg.TpPlan(js))
+    g = pkg.Graph(og.nodes, og.src, og.nbr)
+    nx, ey, ew, gnz, *_ = conv_inputs(o, og, np.float64)
+    a = cp.backward(g, dev(nx), dev(ey), dev(ew), dev(gnz))
+    b = cp.backward(g, dev(nx), dev(ey), dev(ew), dev(gnz))
+    for u, v in zip(a, b):
+        assert torch.equal(u, v)
+
+
+def test_unsorted_edges_rejected():
+    pkg = P()
+    with pytest.raises(pkg.InvalidArgument):
+        pkg.Graph(3, [1, 0], [0, 1])
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f32", "f64"])
+def test_c4_full_graph_sampled(dt):
+    """C4 at full size: C2 TP on radius_graph(cubic_lattice(29), 3.0) =
+    24,389 nodes / 2,634,962 edges. Output rows sampled against the oracle."""
+    js = config("c2")
+    o, pkg = O.Oracle(js), P()
+    og = O.radius_graph(O.cubic_lattice(29), 3.0)
+    assert (og.nodes, og.edges) == (24389, 2634962)
+    cp = pkg.ConvPlan(pkg.TpPlan(js))
+    g = pkg.Graph(og.nodes, og.src, og.nbr)
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    nx = torch.randn((og.nodes, o.dim_x), device="cuda", dtype=tdt, generator=gen)
+    ey = torch.randn((og.edges, o.dim_y), device="cuda", dtype=tdt, generator=gen)
+    ew = torch.randn((og.edges, o.n_w), device="cuda", dtype=tdt, generator=gen)
+    z = cp.forward(g, nx, ey, ew)
+    rows = np.array([0, 1, 12194, 24388])
+    keep = np.isin(og.src, rows)
+    sub = O.make_graph(og.nodes, og.src[keep], og.nbr[keep])
+    eidx = torch.from_numpy(np.nonzero(keep)[0]).cuda()
+    want = o.conv_forward(sub, host(nx), host(ey[eidx]), host(ew[eidx]))
+    check(host(z)[rows], want[rows], dt, "C4 sampled forward rows")
+    gz = torch.randn((og.nodes, o.dim_z), device="cuda", dtype=tdt, generator=gen)
+    gx, gy, gw = cp.backward(g, nx, ey, ew, gz)
+    keep = np.isin(og.nbr, rows)
+    sub = O.make_graph(og.nodes, og.src[keep], og.nbr[keep])
+    eidx = torch.from_numpy(np.nonzero(keep)[0]).cuda()
+    wx, wy, ww = o.conv_backward(sub, host(nx), host(ey[eidx]), host(ew[eidx]), host(gz))
+    check(host(gx)[rows], wx[rows], dt, "C4 sampled g_node_x")
+    check(host(gy[eidx]), wy, dt, "C4 sampled g_edge_y")
+    check(host(gw[eidx]), ww, dt, "C4 sampled g_edge_w")
