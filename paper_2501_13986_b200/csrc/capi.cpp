@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <nvrtc.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -24,7 +25,7 @@ struct cgf_plan {
   std::uint32_t budget = 4096;
   bool z_covered = true, x_covered = true;
   std::mutex mu;
-  std::map<std::tuple<int, int, int, int, int>, std::shared_ptr<cgf::KernelSource>> sources;
+  std::map<std::tuple<int, int, int, int, int, std::string>, std::shared_ptr<cgf::KernelSource>> sources;
 };
 
 namespace {
@@ -86,8 +87,10 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
                                               int w_shared, int aligned) {
   if (dtype != CGF_F32 && dtype != CGF_F64) throw std::invalid_argument("bad dtype");
   std::lock_guard<std::mutex> g(p->mu);
+  const char* env = std::getenv("CGF_GEN");
+  const std::string flags = env ? env : "";
   const auto key = std::make_tuple(static_cast<int>(comp), static_cast<int>(loop), dtype, w_shared ? 1 : 0,
-                                   aligned ? 1 : 0);
+                                   aligned ? 1 : 0, flags);
   auto it = p->sources.find(key);
   if (it != p->sources.end()) return it->second;
   if (w_shared && comp != cgf::Comp::Fwd)
@@ -98,6 +101,7 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   cfg.f64 = dtype == CGF_F64;
   cfg.w_shared = w_shared != 0;
   cfg.aligned = aligned != 0;
+  cgf::apply_gen_flags(cfg, flags);
   auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_kernel(p->problem, p->units, cfg));
   p->sources.emplace(key, ks);
   return ks;

@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <sstream>
@@ -112,6 +113,7 @@ class Gen {
   bool out_y() const { return out_x(); }
   bool out_w() const { return out_x(); }
   bool conv() const { return cfg_.loop != Loop::Rows; }
+  bool yreg() const { return cfg_.y_regs && cfg_.loop == Loop::Rows; }
   bool by_input() const { return cfg_.loop == Loop::ConvByInput; }
   Src x_src() const { return cfg_.loop == Loop::ConvByOutput ? Src::Nbr : Src::Row; }
   Src z_src() const { return cfg_.loop == Loop::ConvByInput ? Src::Nbr : Src::Row; }
@@ -175,11 +177,13 @@ void Gen::layout() {
   for (const auto& u : units_) {
     UnitLayout L;
     std::uint32_t so = 0;
-    add(L, "Y", p_.dim_y, e_src(), 0, p_.dim_y, so, true);
-    L.y_slot = so;
-    if (dual()) {
-      add(L, "DB", p_.dim_y, e_src(), 0, p_.dim_y, so, true);
-      L.db_slot = so;
+    if (!yreg()) {
+      add(L, "Y", p_.dim_y, e_src(), 0, p_.dim_y, so, true);
+      L.y_slot = so;
+      if (dual()) {
+        add(L, "DB", p_.dim_y, e_src(), 0, p_.dim_y, so, true);
+        L.db_slot = so;
+      }
     }
     for (const auto& xc : u.x_chunks) {
       add(L, "X", p_.dim_x, x_src(), xc.off, xc.words, so);
@@ -229,8 +233,8 @@ std::string Gen::wsrc(const Sub& s, const std::string& arr) const {
   return "(" + arr + " + " + idx(e_src()) + " * (i64)" + S(p_.n_w) + " + " + S(s.w_off) + ")";
 }
 
-std::string Gen::yv(int j) const { return "sl[ys + " + S(j) + "]"; }
-std::string Gen::dbv(int j) const { return "sl[dbs + " + S(j) + "]"; }
+std::string Gen::yv(int j) const { return yreg() ? "y[" + S(j) + "]" : "sl[ys + " + S(j) + "]"; }
+std::string Gen::dbv(int j) const { return yreg() ? "db[" + S(j) + "]" : "sl[dbs + " + S(j) + "]"; }
 
 // issue_unit: arm the slot's mbarrier with this item's byte count and start
 // its bulk copies. Window ranges (y-like rows that are not 16-byte aligned)
@@ -337,7 +341,7 @@ void Gen::emit_unit_body(int ui, const std::string& axp, const std::function<voi
     const int dx = s.dx(), dz = s.dz();
     const int xc = u.x_chunk_of(s), zc = u.z_piece_of(s);
     const std::string AX = axp + S(xc), PZ = "pz" + S(ui) + "_" + S(zc);
-    if (q) o_ << "      asm volatile(\"\" ::: \"memory\");\n";  // keep subkernels' live ranges apart
+    if (q && cfg_.sub_barrier) o_ << "      asm volatile(\"\" ::: \"memory\");\n";  // keep subkernels' live ranges apart
     o_ << "      { // sub " << si << ": " << (s.kind == Kind::B ? "B" : "C") << " l=(" << s.l1 << "," << s.l2 << ","
        << s.l3 << ") b=" << s.b << " b'=" << s.bp << " nnz=" << s.cg->entries.size() << "\n";
     const bool gfl = gy_flush();
@@ -497,6 +501,7 @@ std::string zero_init(const std::string& name, int n) { return "T " + name + "["
 
 void Gen::emit_rows_loop() {
   // Producer: items are (row ordinal, unit) in order; lane 0 issues item n + D.
+  if (yreg()) o_ << "  T y[" << p_.dim_y << "], yn[" << p_.dim_y << "];" << (dual() ? " T db[" + S(p_.dim_y) + "], dbn[" + S(p_.dim_y) + "];" : "") << "\n";
   o_ << "  i64 pn = 0;  // next item to issue (lane 0)\n"
         "#define producer_next() do { if (pn < total) {\\\n"
         "    const i64 rr_ = pn / NU; const int u_ = (int)(pn - rr_ * NU); const i64 r_ = gwarp + rr_ * nwarp;\\\n"
@@ -507,6 +512,22 @@ void Gen::emit_rows_loop() {
         "  int slot = 0; u32 phase = 0;\n"
         "  for (i64 rr = 0; rr < my_rows; ++rr) {\n    const i64 row = gwarp + rr * nwarp;\n"
         "    const i64 nbr = row, eid = row; (void)nbr; (void)eid;\n";
+  if (yreg()) {
+    const int dy = p_.dim_y;
+    o_ << "    if (rr == 0) {";
+    for (int j = 0; j < dy; ++j) {
+      o_ << " yn[" << j << "] = __ldg(Y + row * " << dy << " + " << j << ");";
+      if (dual()) o_ << " dbn[" << j << "] = __ldg(DB + row * " << dy << " + " << j << ");";
+    }
+    o_ << " }\n   ";
+    for (int j = 0; j < dy; ++j) o_ << " y[" << j << "] = yn[" << j << "];" << (dual() ? " db[" + S(j) + "] = dbn[" + S(j) + "];" : "");
+    o_ << "\n    if (rr + 1 < my_rows) {";
+    for (int j = 0; j < dy; ++j) {
+      o_ << " yn[" << j << "] = __ldg(Y + (row + nwarp) * " << dy << " + " << j << ");";
+      if (dual()) o_ << " dbn[" << j << "] = __ldg(DB + (row + nwarp) * " << dy << " + " << j << ");";
+    }
+    o_ << " }\n";
+  }
   if (out_y() && !gy_flush()) o_ << "    " << zero_init("gy", p_.dim_y) << "\n";
   for (size_t ui = 0; ui < units_.size(); ++ui) {
     const Unit& u = units_[ui];
@@ -695,7 +716,7 @@ KernelSource Gen::run() {
   o_ << "#define NW " << warps << "\n#define D " << depth << "\n#define NU " << units_.size() << "\n#define SLOT_WORDS "
      << slot_words << "\n#define WARP_BYTES " << wb << "\n\n";
   emit_issue();
-  o_ << "extern \"C\" __global__ void __launch_bounds__(NW * 32) " << ks.name
+  o_ << "extern \"C\" __global__ void __launch_bounds__(NW * 32" << (cfg_.min_blocks > 0 ? ", " + S(cfg_.min_blocks) : "") << ") " << ks.name
      << "(const T* __restrict__ X, const T* __restrict__ Y, const T* __restrict__ W,"
         " const T* __restrict__ GZ, const T* __restrict__ DA, const T* __restrict__ DB,"
         " const T* __restrict__ DC, T* __restrict__ O0, T* __restrict__ O1, T* __restrict__ O2,"
@@ -726,6 +747,24 @@ KernelSource Gen::run() {
 }
 
 }  // namespace
+
+void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
+  std::stringstream ss(flags);
+  std::string tok;
+  while (std::getline(ss, tok, ',')) {
+    if (tok.empty()) continue;
+    const auto eq = tok.find('=');
+    const std::string k = tok.substr(0, eq);
+    const int v = eq == std::string::npos ? 0 : std::atoi(tok.c_str() + eq + 1);
+    if (k == "depth") cfg.depth = std::max(1, v);
+    else if (k == "warps") cfg.warps = std::max(1, v);
+    else if (k == "minb") cfg.min_blocks = std::max(0, v);
+    else if (k == "nobarrier") cfg.sub_barrier = false;
+    else if (k == "barrier") cfg.sub_barrier = true;
+    else if (k == "yreg") cfg.y_regs = true;
+    else if (k == "yslot") cfg.y_regs = false;
+  }
+}
 
 KernelSource generate_kernel(const Problem& p, const std::vector<Unit>& units, const KernelConfig& cfg) {
   Gen g(p, units, cfg);

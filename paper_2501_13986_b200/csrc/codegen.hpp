@@ -46,7 +46,14 @@ struct KernelConfig {
   bool aligned = true;    // all base pointers 16-byte aligned -> bulk copies allowed
   int warps = 4;          // warps per CTA
   int depth = 3;          // staging ring depth per warp
+  int min_blocks = 0;     // __launch_bounds__ min blocks per SM (0: unset)
+  bool sub_barrier = true;  // compiler memory barrier between subkernels
+  bool y_regs = false;    // Rows loop: y / db in registers (prefetched) instead of the slot
 };
+
+// Applies "k=v,flag,..." overrides (env CGF_GEN) to a config: depth=N,
+// warps=N, minb=N, nobarrier, barrier, yreg, yslot.
+void apply_gen_flags(KernelConfig& cfg, const std::string& flags);
 
 struct KernelSource {
   std::string name;
