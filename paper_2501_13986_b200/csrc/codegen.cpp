@@ -69,22 +69,38 @@ std::string hexd(double v) {
 
 std::string S(long long v) { return std::to_string(v); }
 
+// base + kc * step, as source text (kc: the runtime chunk index of a class).
+std::string O(long long base, long long step) {
+  if (step == 0) return S(base);
+  return "(" + S(base) + " + kc * " + S(step) + ")";
+}
+
 enum class Src { Row, Nbr, Edge };
 
 struct SlotRange {
-  std::string arr;     // kernel parameter name
+  std::string arr;           // kernel parameter name
   std::uint32_t stride = 0;  // words per indexed row
   Src src = Src::Row;
-  std::uint32_t off = 0, words = 0, slot_off = 0;
+  long long off = 0, step = 0;  // word offset within the row (affine in kc)
+  std::uint32_t words = 0, slot_off = 0;
   bool bulk = false;
   bool window = false;  // y-like: copy the 16-byte aligned window around the row
 };
 
-struct UnitLayout {
+// A class is a run of units with identical code whose global offsets are
+// affine in a chunk index kc (the 32-lane chunks of the same instructions).
+// One code body per class keeps the per-row program small enough for the
+// instruction cache.
+struct UClass {
+  int u0 = 0, n = 1;
+  std::vector<long long> sx, sz, sw;    // per sub position: x_off, z_off, w_off steps
+  std::vector<long long> xstep, zstep;  // per x chunk / z piece
+};
+
+struct Layout {
   std::vector<SlotRange> ranges;
-  std::map<std::uint32_t, std::uint32_t> x_slot, a_slot, gz_slot;  // row offset -> slot offset
-  std::map<int, std::uint32_t> w_slot, c_slot;                      // sub index -> slot offset
-  std::uint32_t y_slot = 0, db_slot = 0;
+  std::map<std::uint32_t, std::uint32_t> x_slot, a_slot, gz_slot;  // u0 offset -> slot offset
+  std::map<int, std::uint32_t> w_slot, c_slot;                      // sub position -> slot offset
   std::uint32_t words = 0, fixed_bulk_bytes = 0;
 };
 
@@ -100,12 +116,12 @@ class Gen {
   KernelConfig cfg_;
   int sz_;
   std::ostringstream o_;
-  std::vector<UnitLayout> lay_;
+  std::vector<UClass> cls_;
+  std::vector<Layout> lay_;  // per class
   int max_dz_ = 1, max_dx_ = 1, max_piece_ = 1;
   bool has_c_ = false;
-  std::uint32_t scr_words_ = 0, off_zs_ = 0, off_wt_ = 0, off_ct_ = 0;
+  std::uint32_t scr_words_ = 0, off_zs_ = 0, off_wt_ = 0, off_ct_ = 0, off_gya_ = 0, off_gxs_ = 0;
 
-  // What the compute mode reads / writes.
   bool reads_gz() const { return cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdX; }
   bool dual() const { return cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX; }
   bool out_x() const { return cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdX; }
@@ -113,52 +129,127 @@ class Gen {
   bool out_y() const { return out_x(); }
   bool out_w() const { return out_x(); }
   bool conv() const { return cfg_.loop != Loop::Rows; }
-  bool yreg() const { return cfg_.y_regs && cfg_.loop == Loop::Rows; }
   bool by_input() const { return cfg_.loop == Loop::ConvByInput; }
+  bool yreg() const { return cfg_.y_regs && cfg_.loop == Loop::Rows; }
+  bool gy_flush() const { return out_y() && (dual() || cfg_.f64); }
   Src x_src() const { return cfg_.loop == Loop::ConvByOutput ? Src::Nbr : Src::Row; }
   Src z_src() const { return cfg_.loop == Loop::ConvByInput ? Src::Nbr : Src::Row; }
   Src e_src() const { return conv() ? Src::Edge : Src::Row; }
   const char* idx(Src s) const { return s == Src::Row ? "row" : s == Src::Nbr ? "nbr" : "eid"; }
-  std::uint32_t A() const { return 16u / sz_; }  // words per 16 bytes
+  std::uint32_t A() const { return 16u / sz_; }
   std::uint32_t up(std::uint32_t w) const { return (w + A() - 1) / A() * A(); }
-  bool al16(std::uint64_t words) const { return (words * sz_) % 16 == 0; }
+  bool al16(long long words) const { return (words * sz_) % 16 == 0; }
 
-  void add(UnitLayout& L, const std::string& arr, std::uint32_t stride, Src src, std::uint32_t off,
+  void classify();
+  void add(Layout& L, const std::string& arr, std::uint32_t stride, Src src, long long off, long long step,
            std::uint32_t words, std::uint32_t& so, bool window = false);
   void layout();
+  std::string range_src(const SlotRange& r) const;
   void emit_issue();
-  void emit_unit_body(int u, const std::string& accx_prefix, const std::function<void(int)>& post_sub = {});
-  bool gy_flush() const { return out_y() && (dual() || cfg_.f64); }
-  void emit_gy_flush_row(const std::string& rowexpr);
-  std::uint32_t off_gya_ = 0;
-  void emit_wait_and_sync(int u);
+  void emit_wait_and_sync(int k);
   void emit_release();
-  void emit_store(const std::string& dst, const std::string& rowexpr, std::uint32_t stride, std::uint32_t off,
-                  std::uint32_t words, int guard_rows, int width, const std::string& reg);
-  std::string wsrc(const Sub& s, const std::string& arr) const;
-  std::string yv(int j) const;
-  std::string dbv(int j) const;
-  void emit_gy_reduce(const std::string& dst_rowexpr);
+  void emit_store(const std::string& dst, const std::string& rowexpr, std::uint32_t stride, long long off,
+                  long long step, std::uint32_t words, int guard_rows, int width, const std::string& reg);
+  void emit_unit_body(int k, const std::function<void(int)>& post_sub = {});
+  std::string wsrc(const Sub& s, long long step, const std::string& arr) const;
+  std::string yv(int j) const { return yreg() ? "y[" + S(j) + "]" : "sl[ys + " + S(j) + "]"; }
+  std::string dbv(int j) const { return yreg() ? "db[" + S(j) + "]" : "sl[dbs + " + S(j) + "]"; }
+  void emit_gy_reduce(const std::string& rowexpr);
+  void emit_gy_flush_row(const std::string& rowexpr);
+  void emit_class_loop_open(int k);
+  void emit_class_loop_close(int k);
   void emit_rows_loop();
   void emit_conv_loop();
+  const Unit& U0(int k) const { return units_[cls_[k].u0]; }
 };
 
-void Gen::add(UnitLayout& L, const std::string& arr, std::uint32_t stride, Src src, std::uint32_t off,
+bool same_shape(const Problem& p, const Unit& a, const Unit& b) {
+  if (a.subs.size() != b.subs.size() || a.x_chunks.size() != b.x_chunks.size() ||
+      a.z_pieces.size() != b.z_pieces.size())
+    return false;
+  for (size_t q = 0; q < a.subs.size(); ++q) {
+    const Sub &s = p.subs[a.subs[q]], &t = p.subs[b.subs[q]];
+    if (s.kind != t.kind || s.l1 != t.l1 || s.l2 != t.l2 || s.l3 != t.l3 || s.b != t.b || s.bp != t.bp ||
+        s.y_off != t.y_off || s.w_stride != t.w_stride || a.x_chunk_of(s) != b.x_chunk_of(t) ||
+        a.z_piece_of(s) != b.z_piece_of(t))
+      return false;
+  }
+  for (size_t c = 0; c < a.x_chunks.size(); ++c)
+    if (a.x_chunks[c].words != b.x_chunks[c].words) return false;
+  for (size_t z = 0; z < a.z_pieces.size(); ++z)
+    if (a.z_pieces[z].words != b.z_pieces[z].words) return false;
+  return true;
+}
+
+void Gen::classify() {
+  const int nu = static_cast<int>(units_.size());
+  int u = 0;
+  while (u < nu) {
+    UClass c;
+    c.u0 = u;
+    c.n = 1;
+    const Unit& a = units_[u];
+    auto diff = [&](const Unit& b, std::vector<long long>& sx, std::vector<long long>& sz,
+                    std::vector<long long>& sw, std::vector<long long>& xs, std::vector<long long>& zs) {
+      for (size_t q = 0; q < a.subs.size(); ++q) {
+        const Sub &s = p_.subs[a.subs[q]], &t = p_.subs[b.subs[q]];
+        sx.push_back(static_cast<long long>(t.x_off) - s.x_off);
+        sz.push_back(static_cast<long long>(t.z_off) - s.z_off);
+        sw.push_back(static_cast<long long>(t.w_off) - s.w_off);
+      }
+      for (size_t q = 0; q < a.x_chunks.size(); ++q)
+        xs.push_back(static_cast<long long>(b.x_chunks[q].off) - a.x_chunks[q].off);
+      for (size_t q = 0; q < a.z_pieces.size(); ++q)
+        zs.push_back(static_cast<long long>(b.z_pieces[q].off) - a.z_pieces[q].off);
+    };
+    c.sx.assign(a.subs.size(), 0);
+    c.sz.assign(a.subs.size(), 0);
+    c.sw.assign(a.subs.size(), 0);
+    c.xstep.assign(a.x_chunks.size(), 0);
+    c.zstep.assign(a.z_pieces.size(), 0);
+    while (u + c.n < nu && same_shape(p_, a, units_[u + c.n])) {
+      std::vector<long long> sx, sz, sw, xs, zs;
+      diff(units_[u + c.n], sx, sz, sw, xs, zs);
+      if (c.n == 1) {
+        c.sx = sx; c.sz = sz; c.sw = sw; c.xstep = xs; c.zstep = zs;
+      } else {
+        bool ok = true;
+        for (size_t q = 0; q < sx.size() && ok; ++q)
+          ok = sx[q] == c.n * c.sx[q] && sz[q] == c.n * c.sz[q] && sw[q] == c.n * c.sw[q];
+        for (size_t q = 0; q < xs.size() && ok; ++q) ok = xs[q] == c.n * c.xstep[q];
+        for (size_t q = 0; q < zs.size() && ok; ++q) ok = zs[q] == c.n * c.zstep[q];
+        if (!ok) break;
+      }
+      ++c.n;
+    }
+    if (c.n == 1) {
+      c.sx.assign(a.subs.size(), 0);
+      c.sz.assign(a.subs.size(), 0);
+      c.sw.assign(a.subs.size(), 0);
+      c.xstep.assign(a.x_chunks.size(), 0);
+      c.zstep.assign(a.z_pieces.size(), 0);
+    }
+    cls_.push_back(c);
+    u += c.n;
+  }
+}
+
+void Gen::add(Layout& L, const std::string& arr, std::uint32_t stride, Src src, long long off, long long step,
               std::uint32_t words, std::uint32_t& so, bool window) {
   SlotRange r;
   r.arr = arr;
   r.stride = stride;
   r.src = src;
   r.off = off;
+  r.step = step;
   r.words = words;
   r.window = window;
   r.slot_off = L.words;
   if (window) {
-    // Row start is only A-word aligned up to a runtime shift of < A words.
     r.bulk = cfg_.aligned;
     L.words = up(L.words + words + 2 * A());
   } else {
-    r.bulk = cfg_.aligned && al16(stride) && al16(off) && al16(words);
+    r.bulk = cfg_.aligned && al16(stride) && al16(off) && al16(step) && al16(words);
     L.words = up(L.words + words);
     if (r.bulk) L.fixed_bulk_bytes += words * sz_;
   }
@@ -174,41 +265,40 @@ void Gen::layout() {
     if (s.kind == Kind::C) has_c_ = true;
   }
   const std::uint32_t nw = cfg_.w_shared ? 0 : p_.n_w;
-  for (const auto& u : units_) {
-    UnitLayout L;
+  for (size_t k = 0; k < cls_.size(); ++k) {
+    const UClass& C = cls_[k];
+    const Unit& u = units_[C.u0];
+    Layout L;
     std::uint32_t so = 0;
     if (!yreg()) {
-      add(L, "Y", p_.dim_y, e_src(), 0, p_.dim_y, so, true);
-      L.y_slot = so;
-      if (dual()) {
-        add(L, "DB", p_.dim_y, e_src(), 0, p_.dim_y, so, true);
-        L.db_slot = so;
-      }
+      add(L, "Y", p_.dim_y, e_src(), 0, 0, p_.dim_y, so, true);
+      if (dual()) add(L, "DB", p_.dim_y, e_src(), 0, 0, p_.dim_y, so, true);
     }
-    for (const auto& xc : u.x_chunks) {
-      add(L, "X", p_.dim_x, x_src(), xc.off, xc.words, so);
+    for (size_t c = 0; c < u.x_chunks.size(); ++c) {
+      const auto& xc = u.x_chunks[c];
+      add(L, "X", p_.dim_x, x_src(), xc.off, C.xstep[c], xc.words, so);
       L.x_slot[xc.off] = so;
       if (dual()) {
-        add(L, "DA", p_.dim_x, x_src(), xc.off, xc.words, so);
+        add(L, "DA", p_.dim_x, x_src(), xc.off, C.xstep[c], xc.words, so);
         L.a_slot[xc.off] = so;
       }
     }
     if (!cfg_.w_shared) {
-      for (int si : u.subs) {
-        const Sub& s = p_.subs[si];
+      for (size_t q = 0; q < u.subs.size(); ++q) {
+        const Sub& s = p_.subs[u.subs[q]];
         if (s.kind != Kind::B) continue;
-        add(L, "W", nw, e_src(), s.w_off, s.b, so);
-        L.w_slot[si] = so;
+        add(L, "W", nw, e_src(), s.w_off, C.sw[q], s.b, so);
+        L.w_slot[static_cast<int>(q)] = so;
         if (dual()) {
-          add(L, "DC", nw, e_src(), s.w_off, s.b, so);
-          L.c_slot[si] = so;
+          add(L, "DC", nw, e_src(), s.w_off, C.sw[q], s.b, so);
+          L.c_slot[static_cast<int>(q)] = so;
         }
       }
     }
     if (reads_gz()) {
-      for (const auto& zp : u.z_pieces) {
-        add(L, "GZ", p_.dim_z, z_src(), zp.off, zp.words, so);
-        L.gz_slot[zp.off] = so;
+      for (size_t z = 0; z < u.z_pieces.size(); ++z) {
+        add(L, "GZ", p_.dim_z, z_src(), u.z_pieces[z].off, C.zstep[z], u.z_pieces[z].words, so);
+        L.gz_slot[u.z_pieces[z].off] = so;
       }
     }
     L.words = std::max<std::uint32_t>(L.words, A());
@@ -218,6 +308,8 @@ void Gen::layout() {
   scr_words_ = stage;
   off_gya_ = scr_words_;
   scr_words_ += up(static_cast<std::uint32_t>(p_.dim_y));
+  off_gxs_ = scr_words_;
+  if (by_input()) scr_words_ += up(static_cast<std::uint32_t>(p_.dim_x));
   off_zs_ = scr_words_;
   if (has_c_) {
     scr_words_ += up(2u * 32u * max_dz_);
@@ -228,56 +320,54 @@ void Gen::layout() {
   }
 }
 
-std::string Gen::wsrc(const Sub& s, const std::string& arr) const {
-  if (cfg_.w_shared) return "(" + arr + " + " + S(s.w_off) + ")";
-  return "(" + arr + " + " + idx(e_src()) + " * (i64)" + S(p_.n_w) + " + " + S(s.w_off) + ")";
+std::string Gen::wsrc(const Sub& s, long long step, const std::string& arr) const {
+  if (cfg_.w_shared) return "(" + arr + " + " + O(s.w_off, step) + ")";
+  return "(" + arr + " + " + idx(e_src()) + " * (i64)" + S(p_.n_w) + " + " + O(s.w_off, step) + ")";
 }
 
-std::string Gen::yv(int j) const { return yreg() ? "y[" + S(j) + "]" : "sl[ys + " + S(j) + "]"; }
-std::string Gen::dbv(int j) const { return yreg() ? "db[" + S(j) + "]" : "sl[dbs + " + S(j) + "]"; }
+std::string Gen::range_src(const SlotRange& r) const {
+  const std::string I = (r.arr == "W" || r.arr == "DC") && cfg_.w_shared ? "0" : idx(r.src);
+  return r.arr + " + " + I + " * (i64)" + S(r.stride) + " + " + O(r.off, r.step);
+}
 
-// issue_unit: arm the slot's mbarrier with this item's byte count and start
-// its bulk copies. Window ranges (y-like rows that are not 16-byte aligned)
-// copy the aligned window around the row unless it would run past the array.
+// issue_unit(u, ...): arm the slot's mbarrier with the item's byte count and
+// start its bulk copies. u is the flat unit index -> (class, kc).
 void Gen::emit_issue() {
-  o_ << "__device__ __noinline__ void issue_unit(int u, i64 row, i64 nbr, i64 eid, i64 rows_tot, i64 edges_tot, T* sl, u64* bar,"
-        " const T* __restrict__ X, const T* __restrict__ Y, const T* __restrict__ W, const T* __restrict__ GZ,"
-        " const T* __restrict__ DA, const T* __restrict__ DB, const T* __restrict__ DC) {\n"
-        "  fence_proxy_async();\n  switch (u) {\n";
-  for (size_t u = 0; u < lay_.size(); ++u) {
-    const auto& L = lay_[u];
-    o_ << "  case " << u << ": {\n    u32 tx = " << L.fixed_bulk_bytes << "u;\n";
+  o_ << "__device__ __noinline__ void issue_unit(int u, i64 row, i64 nbr, i64 eid, i64 rows_tot, i64 edges_tot, T* sl,"
+        " u64* bar, const T* __restrict__ X, const T* __restrict__ Y, const T* __restrict__ W,"
+        " const T* __restrict__ GZ, const T* __restrict__ DA, const T* __restrict__ DB, const T* __restrict__ DC) {\n"
+        "  (void)nbr; (void)eid; (void)rows_tot; (void)edges_tot;\n  fence_proxy_async();\n";
+  for (size_t k = 0; k < cls_.size(); ++k) {
+    const UClass& C = cls_[k];
+    const Layout& L = lay_[k];
+    o_ << "  " << (k ? "else " : "") << "if (u < " << C.u0 + C.n << ") {\n    const int kc = u - " << C.u0
+       << "; (void)kc;\n    u32 tx = " << L.fixed_bulk_bytes << "u;\n";
     for (const auto& r : L.ranges)
       if (r.bulk && r.window) {
         const std::string I = r.src == Src::Edge ? "eid" : "row";
         const std::string tot = r.src == Src::Edge && conv() ? "edges_tot" : "rows_tot";
-        o_ << "    { const i64 b0 = " << I << " * " << r.stride << "; const i64 a0 = b0 & ~(i64)" << A() - 1
-           << "; const i64 a1 = (b0 + " << r.words << " + " << A() - 1 << ") & ~(i64)" << A() - 1 << ";\n"
-           << "      if (a1 <= " << tot << " * (i64)" << r.stride << ") { tx += (u32)((a1 - a0) * sizeof(T)); }\n    }\n";
+        o_ << "    const i64 b0_" << r.arr << " = " << I << " * " << r.stride << ", a0_" << r.arr << " = b0_" << r.arr
+           << " & ~(i64)" << A() - 1 << ", a1_" << r.arr << " = (b0_" << r.arr << " + " << r.words << " + " << A() - 1
+           << ") & ~(i64)" << A() - 1 << ";\n    const bool ok_" << r.arr << " = a1_" << r.arr << " <= " << tot
+           << " * (i64)" << r.stride << ";\n    if (ok_" << r.arr << ") tx += (u32)((a1_" << r.arr << " - a0_" << r.arr
+           << ") * sizeof(T));\n";
       }
     o_ << "    mbar_expect_tx(bar, tx);\n";
     for (const auto& r : L.ranges) {
       if (!r.bulk) continue;
-      if (r.window) {
-        const std::string I = r.src == Src::Edge ? "eid" : "row";
-        const std::string tot = r.src == Src::Edge && conv() ? "edges_tot" : "rows_tot";
-        o_ << "    { const i64 b0 = " << I << " * " << r.stride << "; const i64 a0 = b0 & ~(i64)" << A() - 1
-           << "; const i64 a1 = (b0 + " << r.words << " + " << A() - 1 << ") & ~(i64)" << A() - 1 << ";\n"
-           << "      if (a1 <= " << tot << " * (i64)" << r.stride << ") bulk_g2s(sl + " << r.slot_off << ", " << r.arr
-           << " + a0, (u32)((a1 - a0) * sizeof(T)), bar); }\n";
-      } else {
-        const std::string I = (r.arr == "W" || r.arr == "DC") && cfg_.w_shared ? "0" : idx(r.src);
-        o_ << "    bulk_g2s(sl + " << r.slot_off << ", " << r.arr << " + " << I << " * (i64)" << r.stride << " + "
-           << r.off << ", " << r.words * sz_ << "u, bar);\n";
-      }
+      if (r.window)
+        o_ << "    if (ok_" << r.arr << ") bulk_g2s(sl + " << r.slot_off << ", " << r.arr << " + a0_" << r.arr
+           << ", (u32)((a1_" << r.arr << " - a0_" << r.arr << ") * sizeof(T)), bar);\n";
+      else
+        o_ << "    bulk_g2s(sl + " << r.slot_off << ", " << range_src(r) << ", " << r.words * sz_ << "u, bar);\n";
     }
-    o_ << "    break; }\n";
+    o_ << "  }\n";
   }
-  o_ << "  default: break;\n  }\n}\n\n";
+  o_ << "}\n\n";
 }
 
-void Gen::emit_wait_and_sync(int ui) {
-  const UnitLayout& L = lay_[ui];
+void Gen::emit_wait_and_sync(int k) {
+  const Layout& L = lay_[k];
   o_ << "      T* sl = wsm + slot * SLOT_WORDS;\n      mbar_wait(&bars[slot], phase);\n";
   bool sync = false;
   for (const auto& r : L.ranges) {
@@ -285,7 +375,6 @@ void Gen::emit_wait_and_sync(int ui) {
       const std::string I = r.src == Src::Edge ? "eid" : "row";
       const std::string tot = r.src == Src::Edge && conv() ? "edges_tot" : "rows";
       const std::string var = r.arr == "Y" ? "ys" : "dbs";
-      // bulk path: data sits at (b0 - a0) inside the window; sync path: at 0.
       if (r.bulk) {
         o_ << "      int " << var << ";\n      { const i64 b0 = " << I << " * " << r.stride << "; const i64 a0 = b0 & ~(i64)"
            << A() - 1 << "; const i64 a1 = (b0 + " << r.words << " + " << A() - 1 << ") & ~(i64)" << A() - 1 << ";\n"
@@ -293,16 +382,14 @@ void Gen::emit_wait_and_sync(int ui) {
            << " + (int)(b0 - a0);\n        else { " << var << " = " << r.slot_off << "; coop_load(sl + "
            << r.slot_off << ", " << r.arr << " + b0, " << r.words << ", lane); __syncwarp(); } }\n";
       } else {
-        o_ << "      const int " << var << " = " << r.slot_off << ";\n      coop_load(sl + " << r.slot_off << ", " << r.arr
-           << " + " << I << " * (i64)" << r.stride << ", " << r.words << ", lane);\n";
+        o_ << "      const int " << var << " = " << r.slot_off << ";\n      coop_load(sl + " << r.slot_off << ", "
+           << r.arr << " + " << I << " * (i64)" << r.stride << ", " << r.words << ", lane);\n";
         sync = true;
       }
       continue;
     }
     if (r.bulk) continue;
-    const std::string I = (r.arr == "W" || r.arr == "DC") && cfg_.w_shared ? "0" : idx(r.src);
-    o_ << "      coop_load(sl + " << r.slot_off << ", " << r.arr << " + " << I << " * (i64)" << r.stride << " + "
-       << r.off << ", " << r.words << ", lane);\n";
+    o_ << "      coop_load(sl + " << r.slot_off << ", " << range_src(r) << ", " << r.words << ", lane);\n";
     sync = true;
   }
   if (sync) o_ << "      __syncwarp();\n";
@@ -313,45 +400,50 @@ void Gen::emit_release() {
         "      if (++slot == D) { slot = 0; phase ^= 1u; }\n";
 }
 
-void Gen::emit_store(const std::string& dst, const std::string& rowexpr, std::uint32_t stride, std::uint32_t off,
-                     std::uint32_t words, int guard_rows, int width, const std::string& reg) {
+void Gen::emit_store(const std::string& dst, const std::string& rowexpr, std::uint32_t stride, long long off,
+                     long long step, std::uint32_t words, int guard_rows, int width, const std::string& reg) {
   o_ << "      if (lane < " << guard_rows << ") {";
   for (int k = 0; k < width; ++k) o_ << " scr[lane * " << width << " + " << k << "] = " << reg << "[" << k << "];";
   o_ << " }\n      __syncwarp();\n";
-  const bool vec = cfg_.aligned && al16(stride) && al16(off) && al16(words);
+  const bool vec = cfg_.aligned && al16(stride) && al16(off) && al16(step) && al16(words);
   if (vec)
-    o_ << "      coop_store16(" << dst << " + " << rowexpr << " * (i64)" << stride << " + " << off << ", scr, "
-       << words * sz_ / 16 << ", lane);\n";
+    o_ << "      coop_store16(" << dst << " + " << rowexpr << " * (i64)" << stride << " + " << O(off, step)
+       << ", scr, " << words * sz_ / 16 << ", lane);\n";
   else
-    o_ << "      coop_store(" << dst << " + " << rowexpr << " * (i64)" << stride << " + " << off << ", scr, " << words
-       << ", lane);\n";
+    o_ << "      coop_store(" << dst << " + " << rowexpr << " * (i64)" << stride << " + " << O(off, step) << ", scr, "
+       << words << ", lane);\n";
   o_ << "      __syncwarp();\n";
 }
 
-// Compute of one unit on its staged slot. Accumulators (ax<prefix><c> for x
-// chunks, pz<u>_<z> for z pieces, gy) are declared by the caller.
-void Gen::emit_unit_body(int ui, const std::string& axp, const std::function<void(int)>& post_sub) {
-  const Unit& u = units_[ui];
-  const UnitLayout& L = lay_[ui];
+// Compute of one unit (class k, chunk kc) on its staged slot. The caller
+// declares x-chunk accumulators ax<c> (when the unit owns them) and z-piece
+// accumulators pz<c>.
+void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
+  const UClass& Cl = cls_[k];
+  const Unit& u = U0(k);
+  const Layout& L = lay_[k];
   const std::string nw = S(p_.n_w);
   const std::string wrow = cfg_.w_shared ? "0" : idx(e_src());
   for (size_t q = 0; q < u.subs.size(); ++q) {
-    const int si = u.subs[q];
-    const Sub& s = p_.subs[si];
+    const int qi = static_cast<int>(q);
+    const Sub& s = p_.subs[u.subs[q]];
     const int dx = s.dx(), dz = s.dz();
     const int xc = u.x_chunk_of(s), zc = u.z_piece_of(s);
-    const std::string AX = axp + S(xc), PZ = "pz" + S(ui) + "_" + S(zc);
-    if (q && cfg_.sub_barrier) o_ << "      asm volatile(\"\" ::: \"memory\");\n";  // keep subkernels' live ranges apart
-    o_ << "      { // sub " << si << ": " << (s.kind == Kind::B ? "B" : "C") << " l=(" << s.l1 << "," << s.l2 << ","
-       << s.l3 << ") b=" << s.b << " b'=" << s.bp << " nnz=" << s.cg->entries.size() << "\n";
+    const std::string AX = "ax" + S(xc), PZ = "pz" + S(zc);
+    const long long swq = Cl.sw[q];
+    if (q && cfg_.sub_barrier) o_ << "      asm volatile(\"\" ::: \"memory\");\n";
+    o_ << "      { // sub " << u.subs[q] << ": " << (s.kind == Kind::B ? "B" : "C") << " l=(" << s.l1 << "," << s.l2
+       << "," << s.l3 << ") b=" << s.b << " b'=" << s.bp << " nnz=" << s.cg->entries.size() << "\n";
     const bool gfl = gy_flush();
-    if (gfl) o_ << "        T gyl[" << s.dy() << "] = {};\n";
+    if (gfl && out_y()) o_ << "        T gyl[" << s.dy() << "] = {};\n";
     auto GY = [&](int j) { return gfl ? "gyl[" + S(j) + "]" : "gy[" + S(s.y_off + j) + "]"; };
     const std::uint32_t xs = L.x_slot.at(s.x_off);
-    o_ << "        T xv[" << dx << "];" << (dual() ? " T av[" + S(dx) + "];" : "") << "\n        if (lane < " << s.bp << ") {";
+    o_ << "        T xv[" << dx << "];" << (dual() ? " T av[" + S(dx) + "];" : "") << "\n        if (lane < " << s.bp
+       << ") {";
     for (int i = 0; i < dx; ++i) o_ << " xv[" << i << "] = sl[" << xs << " + lane * " << dx << " + " << i << "];";
     if (dual())
-      for (int i = 0; i < dx; ++i) o_ << " av[" << i << "] = sl[" << L.a_slot.at(s.x_off) << " + lane * " << dx << " + " << i << "];";
+      for (int i = 0; i < dx; ++i)
+        o_ << " av[" << i << "] = sl[" << L.a_slot.at(s.x_off) << " + lane * " << dx << " + " << i << "];";
     o_ << " } else {";
     for (int i = 0; i < dx; ++i) o_ << " xv[" << i << "] = 0;";
     if (dual())
@@ -362,16 +454,16 @@ void Gen::emit_unit_body(int ui, const std::string& axp, const std::function<voi
       gzs = S(L.gz_slot.at(s.z_off));
       if (s.kind == Kind::B) {
         o_ << "        T gz[" << dz << "];\n        if (lane < " << s.b << ") {";
-        for (int k = 0; k < dz; ++k) o_ << " gz[" << k << "] = sl[" << gzs << " + lane * " << dz << " + " << k << "];";
+        for (int kk = 0; kk < dz; ++kk) o_ << " gz[" << kk << "] = sl[" << gzs << " + lane * " << dz << " + " << kk << "];";
         o_ << " } else {";
-        for (int k = 0; k < dz; ++k) o_ << " gz[" << k << "] = 0;";
+        for (int kk = 0; kk < dz; ++kk) o_ << " gz[" << kk << "] = 0;";
         o_ << " }\n";
       }
     }
     if (s.kind == Kind::B) {
       auto wexpr = [&](const std::string& arr, const std::map<int, std::uint32_t>& slot) {
-        if (cfg_.w_shared) return "__ldg(" + wsrc(s, arr) + " + lane)";
-        return "sl[" + S(slot.at(si)) + " + lane]";
+        if (cfg_.w_shared) return "__ldg(" + wsrc(s, swq, arr) + " + lane)";
+        return "sl[" + S(slot.at(qi)) + " + lane]";
       };
       o_ << "        const T wt = (lane < " << s.b << ") ? " << wexpr("W", L.w_slot) << " : (T)0;\n";
       if (dual()) o_ << "        const T ct = (lane < " << s.b << ") ? " << wexpr("DC", L.c_slot) << " : (T)0;\n";
@@ -380,19 +472,22 @@ void Gen::emit_unit_body(int ui, const std::string& axp, const std::function<voi
     if (reads_gz()) {
       o_ << "        T gzp[" << dz << "];" << (need_gzc ? " T gzc[" + S(dz) + "];" : "") << "\n";
       if (s.kind == Kind::B) {
-        for (int k = 0; k < dz; ++k)
-          o_ << "        gzp[" << k << "] = wt * gz[" << k << "];" << (need_gzc ? " gzc[" + S(k) + "] = ct * gz[" + S(k) + "];" : "") << "\n";
+        for (int kk = 0; kk < dz; ++kk)
+          o_ << "        gzp[" << kk << "] = wt * gz[" << kk << "];"
+             << (need_gzc ? " gzc[" + S(kk) + "] = ct * gz[" + S(kk) + "];" : "") << "\n";
       } else {
         o_ << "        {";
-        for (int k = 0; k < dz; ++k) o_ << " gzp[" << k << "] = 0;" << (need_gzc ? " gzc[" + S(k) + "] = 0;" : "");
-        o_ << "\n          const T* wg = " << wsrc(s, "W") << ";\n";
-        if (need_gzc) o_ << "          const T* cg = " << wsrc(s, "DC") << ";\n";
+        for (int kk = 0; kk < dz; ++kk) o_ << " gzp[" << kk << "] = 0;" << (need_gzc ? " gzc[" + S(kk) + "] = 0;" : "");
+        o_ << "\n          const T* wg = " << wsrc(s, swq, "W") << ";\n";
+        if (need_gzc) o_ << "          const T* cg = " << wsrc(s, swq, "DC") << ";\n";
         o_ << "#pragma unroll 2\n          for (int r = 0; r < " << s.b << "; ++r) {\n"
            << "            const T wv = (lane < " << s.bp << ") ? __ldg(wg + r * " << s.w_stride << " + lane) : (T)0;\n";
-        if (need_gzc) o_ << "            const T cv = (lane < " << s.bp << ") ? __ldg(cg + r * " << s.w_stride << " + lane) : (T)0;\n";
-        for (int k = 0; k < dz; ++k) {
-          o_ << "            { const T g = sl[" << gzs << " + r * " << dz << " + " << k << "]; gzp[" << k << "] = fma(wv, g, gzp[" << k << "]);";
-          if (need_gzc) o_ << " gzc[" << k << "] = fma(cv, g, gzc[" << k << "]);";
+        if (need_gzc)
+          o_ << "            const T cv = (lane < " << s.bp << ") ? __ldg(cg + r * " << s.w_stride << " + lane) : (T)0;\n";
+        for (int kk = 0; kk < dz; ++kk) {
+          o_ << "            { const T g = sl[" << gzs << " + r * " << dz << " + " << kk << "]; gzp[" << kk
+             << "] = fma(wv, g, gzp[" << kk << "]);";
+          if (need_gzc) o_ << " gzc[" << kk << "] = fma(cv, g, gzc[" << kk << "]);";
           o_ << " }\n";
         }
         o_ << "          }\n        }\n";
@@ -410,81 +505,82 @@ void Gen::emit_unit_body(int ui, const std::string& axp, const std::function<voi
       l << "        { const T cy = " << v << " * " << yv(J) << ";";
       if (dual()) l << " const T cb = " << v << " * " << dbv(J) << ";";
       if (zx) l << " zx[" << K << "] = fma(cy, xv[" << I << "], zx[" << K << "]);";
-      if (zab) l << " za[" << K << "] = fma(cy, av[" << I << "], za[" << K << "]); zb[" << K << "] = fma(cb, xv[" << I << "], zb[" << K << "]);";
-      if (cfg_.comp == Comp::Bwd) {
+      if (zab)
+        l << " za[" << K << "] = fma(cy, av[" << I << "], za[" << K << "]); zb[" << K << "] = fma(cb, xv[" << I
+          << "], zb[" << K << "]);";
+      if (cfg_.comp == Comp::Bwd)
         l << " " << AX << "[" << I << "] = fma(cy, gzp[" << K << "], " << AX << "[" << I << "]);"
           << " " << GY(e.j) << " = fma(" << v << " * xv[" << I << "], gzp[" << K << "], " << GY(e.j) << ");";
-      }
-      if (need_gzc) {
-        l << " " << AX << "[" << I << "] = fma(cb, gzp[" << K << "], fma(cy, gzc[" << K << "], " << AX << "[" << I << "]));"
+      if (need_gzc)
+        l << " " << AX << "[" << I << "] = fma(cb, gzp[" << K << "], fma(cy, gzc[" << K << "], " << AX << "[" << I
+          << "]));"
           << " " << GY(e.j) << " = fma(" << v << " * av[" << I << "], gzp[" << K << "], fma(" << v << " * xv[" << I
           << "], gzc[" << K << "], " << GY(e.j) << "));";
-      }
       l << " }\n";
       o_ << l.str();
     }
     // ---- weight application (z-type outputs) ----
     if (out_z()) {
-      const bool dz_mode = cfg_.comp != Comp::Fwd;  // dgz = W.(za+zb) + dC.zx
+      const bool dzm = cfg_.comp != Comp::Fwd;  // dgz = W.(za+zb) + dC.zx
       if (s.kind == Kind::B) {
-        for (int k = 0; k < dz; ++k) {
-          if (dz_mode)
-            o_ << "        " << PZ << "[" << k << "] = fma(ct, zx[" << k << "], fma(wt, za[" << k << "] + zb[" << k << "], " << PZ << "[" << k << "]));\n";
+        for (int kk = 0; kk < dz; ++kk) {
+          if (dzm)
+            o_ << "        " << PZ << "[" << kk << "] = fma(ct, zx[" << kk << "], fma(wt, za[" << kk << "] + zb[" << kk
+               << "], " << PZ << "[" << kk << "]));\n";
           else
-            o_ << "        " << PZ << "[" << k << "] = fma(wt, zx[" << k << "], " << PZ << "[" << k << "]);\n";
+            o_ << "        " << PZ << "[" << kk << "] = fma(wt, zx[" << kk << "], " << PZ << "[" << kk << "]);\n";
         }
       } else {
         o_ << "        if (lane < " << s.bp << ") {";
-        for (int k = 0; k < dz; ++k) {
-          if (dz_mode)
-            o_ << " zs[lane * " << dz << " + " << k << "] = za[" << k << "] + zb[" << k << "]; zs[" << 32 * dz << " + lane * " << dz << " + " << k << "] = zx[" << k << "];";
+        for (int kk = 0; kk < dz; ++kk) {
+          if (dzm)
+            o_ << " zs[lane * " << dz << " + " << kk << "] = za[" << kk << "] + zb[" << kk << "]; zs[" << 32 * dz
+               << " + lane * " << dz << " + " << kk << "] = zx[" << kk << "];";
           else
-            o_ << " zs[lane * " << dz << " + " << k << "] = zx[" << k << "];";
+            o_ << " zs[lane * " << dz << " + " << kk << "] = zx[" << kk << "];";
         }
-        o_ << " }\n        { const T* wg = " << wsrc(s, "W") << ";" << (dz_mode ? " const T* cg = " + wsrc(s, "DC") + ";" : "") << "\n"
-           << "#pragma unroll 4\n          for (int r = 0; r < " << s.b << "; ++r) if (lane < " << s.bp << ") { wts[r * 33 + lane] = __ldg(wg + r * " << s.w_stride << " + lane);";
-        if (dz_mode) o_ << " cts[r * 33 + lane] = __ldg(cg + r * " << s.w_stride << " + lane);";
+        o_ << " }\n        { const T* wg = " << wsrc(s, swq, "W") << ";"
+           << (dzm ? " const T* cg = " + wsrc(s, swq, "DC") + ";" : "") << "\n"
+           << "#pragma unroll 4\n          for (int r = 0; r < " << s.b << "; ++r) if (lane < " << s.bp
+           << ") { wts[r * 33 + lane] = __ldg(wg + r * " << s.w_stride << " + lane);";
+        if (dzm) o_ << " cts[r * 33 + lane] = __ldg(cg + r * " << s.w_stride << " + lane);";
         o_ << " } }\n        __syncwarp();\n        if (lane < " << s.b << ") {\n#pragma unroll 4\n"
-           << "          for (int c = 0; c < " << s.bp << "; ++c) { const T wv = wts[lane * 33 + c];" << (dz_mode ? " const T cv = cts[lane * 33 + c];" : "");
-        for (int k = 0; k < dz; ++k) {
-          if (dz_mode)
-            o_ << " " << PZ << "[" << k << "] = fma(cv, zs[" << 32 * dz << " + c * " << dz << " + " << k << "], fma(wv, zs[c * " << dz << " + " << k << "], " << PZ << "[" << k << "]));";
+           << "          for (int c = 0; c < " << s.bp << "; ++c) { const T wv = wts[lane * 33 + c];"
+           << (dzm ? " const T cv = cts[lane * 33 + c];" : "");
+        for (int kk = 0; kk < dz; ++kk) {
+          if (dzm)
+            o_ << " " << PZ << "[" << kk << "] = fma(cv, zs[" << 32 * dz << " + c * " << dz << " + " << kk
+               << "], fma(wv, zs[c * " << dz << " + " << kk << "], " << PZ << "[" << kk << "]));";
           else
-            o_ << " " << PZ << "[" << k << "] = fma(wv, zs[c * " << dz << " + " << k << "], " << PZ << "[" << k << "]);";
+            o_ << " " << PZ << "[" << kk << "] = fma(wv, zs[c * " << dz << " + " << kk << "], " << PZ << "[" << kk << "]);";
         }
         o_ << " }\n        }\n        __syncwarp();\n";
       }
     }
     // ---- weight gradients (per sub, written directly) ----
     if (out_w()) {
-      const std::string zsum = cfg_.comp == Comp::Bwd ? "zx[K]" : "(za[K] + zb[K])";
-      auto zk = [&](int k) {
-        std::string t = zsum;
-        for (size_t pos; (pos = t.find("[K]")) != std::string::npos;) t.replace(pos, 3, "[" + S(k) + "]");
-        return t;
+      auto zk = [&](int kk) {
+        return cfg_.comp == Comp::Bwd ? "zx[" + S(kk) + "]" : "(za[" + S(kk) + "] + zb[" + S(kk) + "])";
       };
       if (s.kind == Kind::B) {
         o_ << "        { T g = 0;";
-        for (int k = 0; k < dz; ++k) o_ << " g = fma(gz[" << k << "], " << zk(k) << ", g);";
-        o_ << " if (lane < " << s.b << ") O2[" << wrow << " * (i64)" << nw << " + " << s.w_off << " + lane] = g; }\n";
+        for (int kk = 0; kk < dz; ++kk) o_ << " g = fma(gz[" << kk << "], " << zk(kk) << ", g);";
+        o_ << " if (lane < " << s.b << ") O2[" << wrow << " * (i64)" << nw << " + " << O(s.w_off, swq) << " + lane] = g; }\n";
       } else {
         o_ << "#pragma unroll 2\n        for (int r = 0; r < " << s.b << "; ++r) { T g = 0;";
-        for (int k = 0; k < dz; ++k) o_ << " g = fma(sl[" << gzs << " + r * " << dz << " + " << k << "], " << zk(k) << ", g);";
-        o_ << " if (lane < " << s.bp << ") O2[" << wrow << " * (i64)" << nw << " + " << s.w_off << " + r * " << s.w_stride << " + lane] = g; }\n";
+        for (int kk = 0; kk < dz; ++kk)
+          o_ << " g = fma(sl[" << gzs << " + r * " << dz << " + " << kk << "], " << zk(kk) << ", g);";
+        o_ << " if (lane < " << s.bp << ") O2[" << wrow << " * (i64)" << nw << " + " << O(s.w_off, swq) << " + r * "
+           << s.w_stride << " + lane] = g; }\n";
       }
     }
-    if (gfl)
+    if (gfl && out_y())
       for (int j = 0; j < s.dy(); ++j)
         o_ << "        { const T s_ = warp_sum(gyl[" << j << "]); if (lane == " << j % 32 << ") gya[" << s.y_off + j
            << "] += s_; }\n";
     o_ << "      }\n";
-    if (post_sub) post_sub(static_cast<int>(q));
+    if (post_sub) post_sub(qi);
   }
-}
-
-void Gen::emit_gy_flush_row(const std::string& rowexpr) {
-  o_ << "    __syncwarp();\n    for (int j = lane; j < " << p_.dim_y << "; j += 32) { O1[" << rowexpr << " * (i64)"
-     << p_.dim_y << " + j] = gya[j]; gya[j] = 0; }\n    __syncwarp();\n";
 }
 
 void Gen::emit_gy_reduce(const std::string& rowexpr) {
@@ -493,15 +589,33 @@ void Gen::emit_gy_reduce(const std::string& rowexpr) {
     o_ << "    { T mine = 0;\n";
     for (int j = j0; j < std::min(dy, j0 + 32); ++j)
       o_ << "      { const T s_ = warp_sum(gy[" << j << "]); if (lane == " << j - j0 << ") mine = s_; }\n";
-    o_ << "      if (lane < " << std::min(dy - j0, 32) << ") O1[" << rowexpr << " * (i64)" << dy << " + " << j0 << " + lane] = mine; }\n";
+    o_ << "      if (lane < " << std::min(dy - j0, 32) << ") O1[" << rowexpr << " * (i64)" << dy << " + " << j0
+       << " + lane] = mine; }\n";
   }
+}
+
+void Gen::emit_gy_flush_row(const std::string& rowexpr) {
+  o_ << "    __syncwarp();\n    for (int j = lane; j < " << p_.dim_y << "; j += 32) { O1[" << rowexpr << " * (i64)"
+     << p_.dim_y << " + j] = gya[j]; gya[j] = 0; }\n    __syncwarp();\n";
 }
 
 std::string zero_init(const std::string& name, int n) { return "T " + name + "[" + S(n) + "] = {};"; }
 
+void Gen::emit_class_loop_open(int k) {
+  const UClass& C = cls_[k];
+  if (C.n > 1)
+    o_ << "#pragma unroll 1\n    for (int kc = 0; kc < " << C.n << "; ++kc) { // ---- class " << k << ": units "
+       << C.u0 << ".." << C.u0 + C.n - 1 << "\n";
+  else
+    o_ << "    { const int kc = 0; (void)kc; // ---- class " << k << ": unit " << C.u0 << "\n";
+}
+
+void Gen::emit_class_loop_close(int) { o_ << "    }\n"; }
+
 void Gen::emit_rows_loop() {
-  // Producer: items are (row ordinal, unit) in order; lane 0 issues item n + D.
-  if (yreg()) o_ << "  T y[" << p_.dim_y << "], yn[" << p_.dim_y << "];" << (dual() ? " T db[" + S(p_.dim_y) + "], dbn[" + S(p_.dim_y) + "];" : "") << "\n";
+  if (yreg())
+    o_ << "  T y[" << p_.dim_y << "], yn[" << p_.dim_y << "];"
+       << (dual() ? " T db[" + S(p_.dim_y) + "], dbn[" + S(p_.dim_y) + "];" : "") << "\n";
   o_ << "  i64 pn = 0;  // next item to issue (lane 0)\n"
         "#define producer_next() do { if (pn < total) {\\\n"
         "    const i64 rr_ = pn / NU; const int u_ = (int)(pn - rr_ * NU); const i64 r_ = gwarp + rr_ * nwarp;\\\n"
@@ -520,7 +634,8 @@ void Gen::emit_rows_loop() {
       if (dual()) o_ << " dbn[" << j << "] = __ldg(DB + row * " << dy << " + " << j << ");";
     }
     o_ << " }\n   ";
-    for (int j = 0; j < dy; ++j) o_ << " y[" << j << "] = yn[" << j << "];" << (dual() ? " db[" + S(j) + "] = dbn[" + S(j) + "];" : "");
+    for (int j = 0; j < dy; ++j)
+      o_ << " y[" << j << "] = yn[" << j << "];" << (dual() ? " db[" + S(j) + "] = dbn[" + S(j) + "];" : "");
     o_ << "\n    if (rr + 1 < my_rows) {";
     for (int j = 0; j < dy; ++j) {
       o_ << " yn[" << j << "] = __ldg(Y + (row + nwarp) * " << dy << " + " << j << ");";
@@ -529,9 +644,10 @@ void Gen::emit_rows_loop() {
     o_ << " }\n";
   }
   if (out_y() && !gy_flush()) o_ << "    " << zero_init("gy", p_.dim_y) << "\n";
-  for (size_t ui = 0; ui < units_.size(); ++ui) {
-    const Unit& u = units_[ui];
-    o_ << "    { // ---- unit " << ui << ": " << u.subs.size() << " subkernels\n";
+  for (size_t k = 0; k < cls_.size(); ++k) {
+    const UClass& C = cls_[k];
+    const Unit& u = U0(static_cast<int>(k));
+    emit_class_loop_open(static_cast<int>(k));
     std::map<std::uint32_t, int> xdx, xb, zdz, zb;
     for (int si : u.subs) {
       const Sub& s = p_.subs[si];
@@ -543,12 +659,10 @@ void Gen::emit_rows_loop() {
     if (out_x())
       for (size_t c = 0; c < u.x_chunks.size(); ++c) o_ << "      " << zero_init("ax" + S(c), xdx[u.x_chunks[c].off]) << "\n";
     if (out_z())
-      for (size_t z = 0; z < u.z_pieces.size(); ++z)
-        o_ << "      " << zero_init("pz" + S(ui) + "_" + S(z), zdz[u.z_pieces[z].off]) << "\n";
-    emit_wait_and_sync(static_cast<int>(ui));
-    // Store every owned output right after the last subkernel that writes it
-    // (keeps accumulator live ranges short).
-    std::map<int, std::vector<int>> x_done, z_done;  // sub position -> chunks / pieces completed
+      for (size_t z = 0; z < u.z_pieces.size(); ++z) o_ << "      " << zero_init("pz" + S(z), zdz[u.z_pieces[z].off]) << "\n";
+    emit_wait_and_sync(static_cast<int>(k));
+    // Store every owned output right after the last subkernel that writes it.
+    std::map<int, std::vector<int>> x_done, z_done;
     for (size_t c = 0; c < u.x_chunks.size(); ++c) {
       int last = 0;
       for (size_t q = 0; q < u.subs.size(); ++q)
@@ -561,32 +675,32 @@ void Gen::emit_rows_loop() {
         if (p_.subs[u.subs[q]].z_off == u.z_pieces[z].off) last = static_cast<int>(q);
       z_done[last].push_back(static_cast<int>(z));
     }
-    emit_unit_body(static_cast<int>(ui), "ax", [&](int q) {
+    emit_unit_body(static_cast<int>(k), [&](int q) {
       if (out_x())
         for (int c : x_done[q]) {
           const auto& xc = u.x_chunks[c];
-          emit_store("O0", "row", p_.dim_x, xc.off, xc.words, xb[xc.off], xdx[xc.off], "ax" + S(c));
+          emit_store("O0", "row", p_.dim_x, xc.off, C.xstep[c], xc.words, xb[xc.off], xdx[xc.off], "ax" + S(c));
         }
       if (out_z())
         for (int z : z_done[q]) {
           const auto& zp = u.z_pieces[z];
-          emit_store(cfg_.comp == Comp::Fwd ? "O0" : "O3", "row", p_.dim_z, zp.off, zp.words, zb[zp.off], zdz[zp.off],
-                     "pz" + S(ui) + "_" + S(z));
+          emit_store(cfg_.comp == Comp::Fwd ? "O0" : "O3", "row", p_.dim_z, zp.off, C.zstep[z], zp.words, zb[zp.off],
+                     zdz[zp.off], "pz" + S(z));
         }
     });
     emit_release();
-    o_ << "    }\n";
+    emit_class_loop_close(static_cast<int>(k));
   }
   if (out_y()) {
-    if (gy_flush()) emit_gy_flush_row("row");
-    else emit_gy_reduce("row");
+    if (gy_flush())
+      emit_gy_flush_row("row");
+    else
+      emit_gy_reduce("row");
   }
   o_ << "  }\n";
 }
 
 void Gen::emit_conv_loop() {
-  // Producer cursor over (row, unit, edge) [ByOutput] or (row, edge, unit)
-  // [ByInput]; rows without edges yield no items.
   const bool bi = by_input();
   o_ << "  i64 pk = 0, pq = 0, pq1 = 0; int pu = 0;\n"
         "#define prow(k) (gwarp + (k) * nwarp)\n"
@@ -595,82 +709,81 @@ void Gen::emit_conv_loop() {
         "  int pslot = 0;\n"
         "#define producer_next() do { if (pk < my_rows) {\\\n"
         "    const i64 r_ = prow(pk);\\\n";
-  if (bi)
-    o_ << "    const i64 nb_ = NB[pq], e_ = EID[pq];\\\n";
-  else
-    o_ << "    const i64 nb_ = NB[pq], e_ = pq;\\\n";
+  o_ << (bi ? "    const i64 nb_ = NB[pq], e_ = EID[pq];\\\n" : "    const i64 nb_ = NB[pq], e_ = pq;\\\n");
   o_ << "    issue_unit(pu, r_, nb_, e_, rows, edges_tot, wsm + pslot * SLOT_WORDS, &bars[pslot], X, Y, W, GZ, DA, DB, DC);\\\n"
         "    if (++pslot == D) pslot = 0;\\\n";
-  if (bi)
-    o_ << "    if (++pu == NU) { pu = 0; if (++pq == pq1) { ++pk; seek(); } }\\\n";
-  else
-    o_ << "    if (++pq == pq1) { pq = RP[r_]; if (++pu == NU) { pu = 0; ++pk; seek(); } }\\\n";
+  o_ << (bi ? "    if (++pu == NU) { pu = 0; if (++pq == pq1) { ++pk; seek(); } }\\\n"
+            : "    if (++pq == pq1) { pq = RP[r_]; if (++pu == NU) { pu = 0; ++pk; seek(); } }\\\n");
   o_ << "  } } while (0)\n"
         "  if (lane == 0) for (int d = 0; d < D; ++d) producer_next();\n"
         "  int slot = 0; u32 phase = 0;\n"
         "  for (i64 k = 0; k < my_rows; ++k) {\n    const i64 row = prow(k);\n"
         "    const i64 q0 = RP[row], q1 = RP[row + 1];\n";
   if (!bi) {
-    for (size_t ui = 0; ui < units_.size(); ++ui) {
-      const Unit& u = units_[ui];
+    for (size_t k = 0; k < cls_.size(); ++k) {
+      const UClass& C = cls_[k];
+      const Unit& u = U0(static_cast<int>(k));
       std::map<std::uint32_t, int> zdz, zb;
       for (int si : u.subs) {
         zdz[p_.subs[si].z_off] = p_.subs[si].dz();
         zb[p_.subs[si].z_off] = p_.subs[si].b;
       }
-      o_ << "    { // ---- unit " << ui << "\n";
-      for (size_t z = 0; z < u.z_pieces.size(); ++z)
-        o_ << "      " << zero_init("pz" + S(ui) + "_" + S(z), zdz[u.z_pieces[z].off]) << "\n";
+      emit_class_loop_open(static_cast<int>(k));
+      for (size_t z = 0; z < u.z_pieces.size(); ++z) o_ << "      " << zero_init("pz" + S(z), zdz[u.z_pieces[z].off]) << "\n";
       o_ << "      for (i64 q = q0; q < q1; ++q) {\n      const i64 eid = q; const i64 nbr = NB[q]; (void)nbr;\n";
-      emit_wait_and_sync(static_cast<int>(ui));
-      emit_unit_body(static_cast<int>(ui), "ax");
+      emit_wait_and_sync(static_cast<int>(k));
+      emit_unit_body(static_cast<int>(k));
       emit_release();
       o_ << "      }\n";
       for (size_t z = 0; z < u.z_pieces.size(); ++z) {
         const auto& zp = u.z_pieces[z];
-        emit_store(cfg_.comp == Comp::Fwd ? "O0" : "O3", "row", p_.dim_z, zp.off, zp.words, zb[zp.off], zdz[zp.off],
-                   "pz" + S(ui) + "_" + S(z));
+        emit_store(cfg_.comp == Comp::Fwd ? "O0" : "O3", "row", p_.dim_z, zp.off, C.zstep[z], zp.words, zb[zp.off],
+                   zdz[zp.off], "pz" + S(z));
       }
-      o_ << "    }\n";
+      emit_class_loop_close(static_cast<int>(k));
     }
   } else {
-    // gx-type accumulators for every unit's x chunks live across the edge loop.
-    for (size_t ui = 0; ui < units_.size(); ++ui) {
-      const Unit& u = units_[ui];
-      for (size_t c = 0; c < u.x_chunks.size(); ++c) {
-        int dx = 1;
-        for (int si : u.subs)
-          if (p_.subs[si].x_off == u.x_chunks[c].off) dx = p_.subs[si].dx();
-        o_ << "    " << zero_init("ax" + S(ui) + "_" + S(c), dx) << "\n";
-      }
-    }
+    // gx-type outputs accumulate over the row's edges in the warp's shared
+    // gxs[dim_x]; each item adds its register partials (lane-owned, conflict-free).
     o_ << "    for (i64 q = q0; q < q1; ++q) {\n      const i64 eid = EID[q]; const i64 nbr = NB[q]; (void)nbr;\n";
     if (out_y() && !gy_flush()) o_ << "      " << zero_init("gy", p_.dim_y) << "\n";
-    for (size_t ui = 0; ui < units_.size(); ++ui) {
-      o_ << "      { // ---- unit " << ui << "\n";
-      emit_wait_and_sync(static_cast<int>(ui));
-      emit_unit_body(static_cast<int>(ui), "ax" + S(ui) + "_");
+    for (size_t k = 0; k < cls_.size(); ++k) {
+      const UClass& C = cls_[k];
+      const Unit& u = U0(static_cast<int>(k));
+      std::map<std::uint32_t, int> xdx, xb;
+      for (int si : u.subs) {
+        xdx[p_.subs[si].x_off] = p_.subs[si].dx();
+        xb[p_.subs[si].x_off] = p_.subs[si].bp;
+      }
+      emit_class_loop_open(static_cast<int>(k));
+      for (size_t c = 0; c < u.x_chunks.size(); ++c) o_ << "      " << zero_init("ax" + S(c), xdx[u.x_chunks[c].off]) << "\n";
+      emit_wait_and_sync(static_cast<int>(k));
+      emit_unit_body(static_cast<int>(k));
+      for (size_t c = 0; c < u.x_chunks.size(); ++c) {
+        const auto& xc = u.x_chunks[c];
+        const int dx = xdx[xc.off];
+        o_ << "      if (lane < " << xb[xc.off] << ") {";
+        for (int i = 0; i < dx; ++i)
+          o_ << " gxs[" << O(xc.off, C.xstep[c]) << " + lane * " << dx << " + " << i << "] += ax" << c << "[" << i << "];";
+        o_ << " }\n";
+      }
       emit_release();
-      o_ << "      }\n";
+      emit_class_loop_close(static_cast<int>(k));
     }
     if (out_y()) {
-      if (gy_flush()) emit_gy_flush_row("eid");
-      else emit_gy_reduce("eid");
+      if (gy_flush())
+        emit_gy_flush_row("eid");
+      else
+        emit_gy_reduce("eid");
     }
     o_ << "    }\n";
-    for (size_t ui = 0; ui < units_.size(); ++ui) {
-      const Unit& u = units_[ui];
-      for (size_t c = 0; c < u.x_chunks.size(); ++c) {
-        int dx = 1, bp = 1;
-        for (int si : u.subs)
-          if (p_.subs[si].x_off == u.x_chunks[c].off) {
-            dx = p_.subs[si].dx();
-            bp = p_.subs[si].bp;
-          }
-        emit_store("O0", "row", p_.dim_x, u.x_chunks[c].off, u.x_chunks[c].words, bp, dx,
-                   "ax" + S(ui) + "_" + S(c));
-      }
-    }
+    const bool vec = cfg_.aligned && al16(p_.dim_x);
+    o_ << "    __syncwarp();\n";
+    if (vec)
+      o_ << "    coop_store16(O0 + row * (i64)" << p_.dim_x << ", gxs, " << p_.dim_x * sz_ / 16 << ", lane);\n";
+    else
+      o_ << "    coop_store(O0 + row * (i64)" << p_.dim_x << ", gxs, " << p_.dim_x << ", lane);\n";
+    o_ << "    __syncwarp();\n    for (int j = lane; j < " << p_.dim_x << "; j += 32) gxs[j] = 0;\n    __syncwarp();\n";
   }
   o_ << "  }\n";
 }
@@ -683,6 +796,7 @@ KernelSource Gen::run() {
     throw UnsupportedError("ConvByInput computes x-type outputs only");
   if (!conv() && (cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX))
     throw UnsupportedError("split double-backward passes are conv-only");
+  classify();
   layout();
   std::uint32_t slot_words = 0;
   int bulk = 0, sync = 0;
@@ -711,12 +825,14 @@ KernelSource Gen::run() {
 
   o_ << device_runtime_source();
   o_ << "\n// Generated for: x = " << p_.x_ir.str() << " | y = " << p_.y_ir.str() << " | z = " << p_.z_ir.str()
-     << "\n// " << p_.subs.size() << " split subkernels in " << units_.size() << " units; " << ks.name << "\n";
+     << "\n// " << p_.subs.size() << " split subkernels in " << units_.size() << " units / " << cls_.size()
+     << " code classes; " << ks.name << "\n";
   o_ << "typedef " << (cfg_.f64 ? "double" : "float") << " T;\n";
   o_ << "#define NW " << warps << "\n#define D " << depth << "\n#define NU " << units_.size() << "\n#define SLOT_WORDS "
      << slot_words << "\n#define WARP_BYTES " << wb << "\n\n";
   emit_issue();
-  o_ << "extern \"C\" __global__ void __launch_bounds__(NW * 32" << (cfg_.min_blocks > 0 ? ", " + S(cfg_.min_blocks) : "") << ") " << ks.name
+  o_ << "extern \"C\" __global__ void __launch_bounds__(NW * 32"
+     << (cfg_.min_blocks > 0 ? ", " + S(cfg_.min_blocks) : "") << ") " << ks.name
      << "(const T* __restrict__ X, const T* __restrict__ Y, const T* __restrict__ W,"
         " const T* __restrict__ GZ, const T* __restrict__ DA, const T* __restrict__ DB,"
         " const T* __restrict__ DC, T* __restrict__ O0, T* __restrict__ O1, T* __restrict__ O2,"
@@ -730,7 +846,9 @@ KernelSource Gen::run() {
     o_ << "  T* zs = scr + " << off_zs_ << "; T* wts = scr + " << off_wt_ << ";"
        << (dual() ? " T* cts = scr + " + S(off_ct_) + ";" : "") << " (void)zs; (void)wts;\n";
   o_ << "  T* gya = scr + " << off_gya_ << "; (void)gya;\n"
-        "  for (int j = lane; j < " << p_.dim_y << "; j += 32) gya[j] = 0;\n";
+     << "  for (int j = lane; j < " << p_.dim_y << "; j += 32) gya[j] = 0;\n";
+  if (by_input())
+    o_ << "  T* gxs = scr + " << off_gxs_ << ";\n  for (int j = lane; j < " << p_.dim_x << "; j += 32) gxs[j] = 0;\n";
   o_ << "  u64* bars = (u64*)(smem_raw + NW * WARP_BYTES) + wid * D;\n"
         "  if (lane == 0) { for (int d = 0; d < D; ++d) mbar_init(&bars[d], 1); mbar_fence_init(); }\n"
         "  __syncwarp();\n"
