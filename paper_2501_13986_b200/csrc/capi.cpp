@@ -101,6 +101,9 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   cfg.f64 = dtype == CGF_F64;
   cfg.w_shared = w_shared != 0;
   cfg.aligned = aligned != 0;
+  // Batched fwd / bwd keep y in registers (prefetched a row ahead); the
+  // double-backward needs those registers for its three z' accumulators.
+  cfg.y_regs = loop == cgf::Loop::Rows && (comp == cgf::Comp::Fwd || comp == cgf::Comp::Bwd);
   cgf::apply_gen_flags(cfg, flags);
   auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_kernel(p->problem, p->units, cfg));
   p->sources.emplace(key, ks);

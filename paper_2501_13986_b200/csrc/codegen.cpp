@@ -702,18 +702,21 @@ void Gen::emit_rows_loop() {
 
 void Gen::emit_conv_loop() {
   const bool bi = by_input();
-  o_ << "  i64 pk = 0, pq = 0, pq1 = 0; int pu = 0;\n"
+  // The producer (lane 0) walks (row, unit, edge) [ByOutput] or (row, edge,
+  // unit) [ByInput]; the neighbour / edge-id of the NEXT edge is loaded one
+  // step ahead so the index fetch never sits on the critical path.
+  o_ << "  i64 pk = 0, pq = 0, pq1 = 0, pq0 = 0, pnb = 0, peid = 0; int pu = 0;\n"
         "#define prow(k) (gwarp + (k) * nwarp)\n"
-        "#define seek() do { while (pk < my_rows) { const i64 r_ = prow(pk); pq = RP[r_]; pq1 = RP[r_ + 1]; if (pq < pq1) break; ++pk; } } while (0)\n"
-        "  if (lane == 0) seek();\n"
+        "#define seek() do { while (pk < my_rows) { const i64 r_ = prow(pk); pq0 = pq = RP[r_]; pq1 = RP[r_ + 1]; if (pq < pq1) break; ++pk; } } while (0)\n"
+        "#define fetch_idx() do { if (pk < my_rows) { pnb = NB[pq]; peid = " << (bi ? "EID[pq]" : "pq") << "; } } while (0)\n"
+        "  if (lane == 0) { seek(); fetch_idx(); }\n"
         "  int pslot = 0;\n"
         "#define producer_next() do { if (pk < my_rows) {\\\n"
-        "    const i64 r_ = prow(pk);\\\n";
-  o_ << (bi ? "    const i64 nb_ = NB[pq], e_ = EID[pq];\\\n" : "    const i64 nb_ = NB[pq], e_ = pq;\\\n");
-  o_ << "    issue_unit(pu, r_, nb_, e_, rows, edges_tot, wsm + pslot * SLOT_WORDS, &bars[pslot], X, Y, W, GZ, DA, DB, DC);\\\n"
+        "    const i64 r_ = prow(pk);\\\n"
+        "    issue_unit(pu, r_, pnb, peid, rows, edges_tot, wsm + pslot * SLOT_WORDS, &bars[pslot], X, Y, W, GZ, DA, DB, DC);\\\n"
         "    if (++pslot == D) pslot = 0;\\\n";
-  o_ << (bi ? "    if (++pu == NU) { pu = 0; if (++pq == pq1) { ++pk; seek(); } }\\\n"
-            : "    if (++pq == pq1) { pq = RP[r_]; if (++pu == NU) { pu = 0; ++pk; seek(); } }\\\n");
+  o_ << (bi ? "    if (++pu == NU) { pu = 0; if (++pq == pq1) { ++pk; seek(); } fetch_idx(); }\\\n"
+            : "    if (++pq == pq1) { pq = pq0; if (++pu == NU) { pu = 0; ++pk; seek(); } } fetch_idx();\\\n");
   o_ << "  } } while (0)\n"
         "  if (lane == 0) for (int d = 0; d < D; ++d) producer_next();\n"
         "  int slot = 0; u32 phase = 0;\n"
@@ -804,7 +807,10 @@ KernelSource Gen::run() {
     slot_words = std::max(slot_words, L.words);
     for (const auto& r : L.ranges) (r.bulk ? bulk : sync)++;
   }
-  int depth = cfg_.depth, warps = cfg_.warps;
+  // Default ring depth: ~12 KB of staged inputs per warp, 2..4 slots.
+  int depth = cfg_.depth > 0 ? cfg_.depth
+                             : static_cast<int>(std::clamp<std::uint64_t>(12288 / std::max<std::uint64_t>(1, slot_words * sz_), 2, 4));
+  int warps = cfg_.warps;
   auto warp_bytes = [&](int d) { return (static_cast<std::uint64_t>(d) * slot_words + scr_words_) * sz_; };
   const std::uint64_t budget = 200 * 1024;
   while (depth > 1 && warp_bytes(depth) * warps + 8ull * depth * warps > budget) --depth;
@@ -874,7 +880,7 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     const auto eq = tok.find('=');
     const std::string k = tok.substr(0, eq);
     const int v = eq == std::string::npos ? 0 : std::atoi(tok.c_str() + eq + 1);
-    if (k == "depth") cfg.depth = std::max(1, v);
+    if (k == "depth") cfg.depth = std::max(0, v);
     else if (k == "warps") cfg.warps = std::max(1, v);
     else if (k == "minb") cfg.min_blocks = std::max(0, v);
     else if (k == "nobarrier") cfg.sub_barrier = false;

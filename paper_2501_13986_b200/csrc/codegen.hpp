@@ -45,7 +45,7 @@ struct KernelConfig {
   bool w_shared = false;  // one W row for every batch row (superset of the reference API)
   bool aligned = true;    // all base pointers 16-byte aligned -> bulk copies allowed
   int warps = 4;          // warps per CTA
-  int depth = 3;          // staging ring depth per warp
+  int depth = 0;          // staging ring depth per warp (0: from the slot size)
   int min_blocks = 0;     // __launch_bounds__ min blocks per SM (0: unset)
   bool sub_barrier = true;  // compiler memory barrier between subkernels
   bool y_regs = false;    // Rows loop: y / db in registers (prefetched) instead of the slot
