@@ -11,6 +11,12 @@ reference's flop rule (kernelgen::flop_count, kernelgen.cpp:253-276):
 1M-row batch (rows are independent — "replicas / batch split"),
 no data-path collective; time = max over ranks.
 
+The line also carries "conv": the fused graph convolution of config C5 (C1 TP
+on radius_graph(cubic_lattice(58^3), 3.0), 22.4M edges) as forward + backward
+per step, destination-partitioned over the N ranks with NCCL all-gather of
+node_x and reduce-scatter of g_node_x (paper_2501_13986_b200/dist.py);
+edges/s over the whole graph, max over ranks ("scaling": "strong").
+
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
 unmodified cgforge built from /root/reference) on this box's host cores, same
 metric, a bounded row sample per step.
@@ -42,6 +48,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-rows", type=int, default=50_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--conv-n", type=int, default=58, help="lattice side of the conv leg (58 = C5); 0 = skip")
+    ap.add_argument("--conv-config", default="c1", help="TP of the conv leg (C5 uses the C1 TP)")
+    ap.add_argument("--conv-steps", type=int, default=5)
     return ap.parse_args()
 
 
@@ -143,6 +152,100 @@ def run_reference(args, rank, world):
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def conv_leg(args, rank, world, dev, clk_index):
+    """C5: fused conv (C1 TP) on radius_graph(cubic_lattice(n^3), 3.0),
+    destination-partitioned over the ranks (dist.DistConvPlan: NCCL all-gather
+    of node_x, local fused conv, reduce-scatter of g_node_x). One step =
+    forward + backward, collectives included; strong scaling (|E| fixed)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_13986_b200 as cgf
+    from paper_2501_13986_b200 import dist as cdist
+    from oracle.oracle import config_json
+
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
+    es = 4 if args.dtype == "f32" else 8
+    plan = cgf.TpPlan(config_json(args.conv_config))
+    nodes, src, nbr = cdist.lattice_radius_graph(args.conv_n, 1.0, 3.0)
+    g = cgf.Graph(nodes, src, nbr)
+    del src, nbr
+    sh = cdist.GraphShard(g, world, rank)
+    dc = cdist.DistConvPlan(plan, sh, group=None)
+    gen = torch.Generator(device=dev).manual_seed(4321 + rank)
+    rnd = lambda *s: torch.randn(s, device=dev, dtype=tdt, generator=gen)
+    nx, ey, ew, gnz = rnd(sh.out_nodes, plan.dim_x), rnd(sh.edges, plan.dim_y), rnd(sh.edges, plan.n_w), \
+        rnd(sh.out_nodes, plan.dim_z)
+    stream = torch.cuda.current_stream(dev)
+    fwd_ms, bwd_ms, coll_ms = [], [], []
+
+    def step(record=False):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if record else None
+        if record:
+            evs[0].record(stream)
+        x_all = dc.gather_x(nx)
+        if record:
+            evs[1].record(stream)
+        z = dc.local.forward_shard(sh, x_all, ey, ew)
+        if record:
+            evs[2].record(stream)
+        gx_part, gy, gw = dc.local.backward_shard(sh, x_all, ey, ew, gnz)
+        if record:
+            evs[3].record(stream)
+        gx = dc._reduce_scatter(gx_part)
+        if record:
+            evs[4].record(stream)
+            fwd_ms.append((evs[1], evs[2]))
+            bwd_ms.append((evs[2], evs[3]))
+            coll_ms.append(((evs[0], evs[1]), (evs[3], evs[4])))
+        return z, gx, gy, gw
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.conv_steps):
+        step(record=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = torch.tensor([a.elapsed_time(b)], device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item()) / args.conv_steps
+    avg = lambda L: sum(x.elapsed_time(y) for x, y in L) / len(L)
+    f_ms, b_ms = avg(fwd_ms), avg(bwd_ms)
+    c_ms = sum(p.elapsed_time(q) + r.elapsed_time(t) for (p, q), (r, t) in coll_ms) / len(coll_ms)
+    # algorithmic bytes of this rank's kernels (SURVEY.md §8d conv rules; node
+    # terms over the rows each kernel owns)
+    E, Vo, Vi = sh.edges, sh.out_nodes, sh.in_nodes
+    fb = (E * (plan.dim_y + plan.n_w) + Vi * plan.dim_x + Vo * plan.dim_z) * es
+    bb = (2 * E * (plan.dim_y + plan.n_w) + Vi * 2 * plan.dim_x + Vo * plan.dim_z) * es
+    peak, _ = measured_peak()
+    per_rank = torch.tensor([f_ms, b_ms, c_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(per_rank, op=dist.ReduceOp.MAX)
+    return {
+        "workload": f"c5: {args.conv_config} TP on radius_graph(cubic_lattice({args.conv_n}^3), 3.0), "
+                    f"{nodes} nodes / {g.edges} edges, fwd+bwd, destination-partitioned",
+        "edges_per_s": g.edges / (ms / 1e3), "ms_per_step": ms, "steps": args.conv_steps, "n_gpus": world,
+        "scaling": "strong", "dtype": args.dtype,
+        "collectives": "NCCL all_gather_into_tensor(node_x) + reduce_scatter_tensor(g_node_x)" if world > 1
+        else "none (1 rank)",
+        "max_over_ranks_ms": {"forward_kernel": float(per_rank[0]), "backward_kernel": float(per_rank[1]),
+                              "collectives": float(per_rank[2])},
+        "rank0_roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
+                           "forward": {"GB/s": fb / (f_ms / 1e3) / 1e9, "frac": fb / (f_ms / 1e3) / 1e9 / peak},
+                           "backward": {"GB/s": bb / (b_ms / 1e3) / 1e9, "frac": bb / (b_ms / 1e3) / 1e9 / peak}},
+        "gpu_launches_per_step": 2,
+    }
 
 
 def main():
@@ -275,6 +378,16 @@ def main():
     h2d = (hx.numel() + hy.numel() + hw.numel() + hg.numel()) * es
     d2h = (oz.numel() + ogx.numel() + ogy.numel() + ogw.numel()) * es
 
+    del x, y, w, gz, z, hx, hy, hw, hg, oz, ogx, ogy, ogw
+    torch.cuda.empty_cache()
+    conv = None
+    if args.conv_n > 0:
+        try:
+            conv = conv_leg(args, rank, world, dev, local)
+        except Exception as exc:  # report, never sink the headline line
+            conv = {"error": repr(exc)}
+        torch.cuda.empty_cache()
+
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -297,6 +410,7 @@ def main():
             "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "rows_per_step": Re, "path": "pinned host -> TpPlan.forward/backward (C ABI) -> pinned host"},
             "gpu_launches": 2 * args.steps,
+            "conv": conv,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

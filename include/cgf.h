@@ -176,6 +176,32 @@ int cgf_conv_double_backward(cgf_plan* plan, int dtype, int64_t nodes, int64_t e
                              void* o_node_x, void* o_edge_y, void* o_edge_w, void* o_g_node_z, int mode,
                              void* stream);
 
+/* ---- sharded convolution (multi-GPU, destination-partitioned) ------------
+ * One rank owns a contiguous range of out_nodes output nodes and their edges
+ * (SURVEY.md §8e). Node-indexed inputs read through nbr (node_x, d_gx) and the
+ * x-type outputs (g_node_x, o_node_x) span in_nodes rows — the all-gathered
+ * neighbour space; output-node arrays (node_z, g_node_z, o_g_node_z) span
+ * out_nodes rows; edge arrays span the shard's edges. row_ptr[out_nodes + 1]
+ * is rebased to the shard; t_row_ptr[in_nodes + 1] / t_src / t_eid are the
+ * shard's transposed CSR (t_src local to the shard). The x-type outputs are
+ * the shard's PARTIAL sums; the caller reduce-scatters them across ranks.
+ * With out_nodes == in_nodes and a whole graph these are the calls above. */
+int cgf_conv_transpose_shard_host(int64_t out_nodes, int64_t in_nodes, int64_t edges, const int64_t* row_ptr,
+                                  const int32_t* nbr, int64_t* t_row_ptr, int32_t* t_src, int32_t* t_eid);
+int cgf_conv_forward_shard(cgf_plan* plan, int dtype, int64_t out_nodes, int64_t in_nodes, int64_t edges,
+                           const int64_t* row_ptr, const int32_t* nbr, const void* node_x, const void* edge_y,
+                           const void* edge_w, void* node_z, int mode, void* stream);
+int cgf_conv_backward_shard(cgf_plan* plan, int dtype, int64_t out_nodes, int64_t in_nodes, int64_t edges,
+                            const int64_t* t_row_ptr, const int32_t* t_src, const int32_t* t_eid,
+                            const void* node_x, const void* edge_y, const void* edge_w, const void* g_node_z,
+                            void* g_node_x, void* g_edge_y, void* g_edge_w, int mode, void* stream);
+int cgf_conv_double_backward_shard(cgf_plan* plan, int dtype, int64_t out_nodes, int64_t in_nodes, int64_t edges,
+                                   const int64_t* row_ptr, const int32_t* nbr, const int64_t* t_row_ptr,
+                                   const int32_t* t_src, const int32_t* t_eid, const void* node_x,
+                                   const void* edge_y, const void* edge_w, const void* g_node_z, const void* d_gx,
+                                   const void* d_gy, const void* d_gw, void* o_node_x, void* o_edge_y,
+                                   void* o_edge_w, void* o_g_node_z, int mode, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,6 +118,10 @@ def lib():
     L.cgf_conv_forward.argtypes = [P, I, I64, I64, P, P, P, P, P, P, I, P]
     L.cgf_conv_backward.argtypes = [P, I, I64, I64] + [P] * 12 + [I, P]
     L.cgf_conv_double_backward.argtypes = [P, I, I64, I64] + [P] * 16 + [I, P]
+    L.cgf_conv_transpose_shard_host.argtypes = [I64, I64, I64, P, P, P, P, P]
+    L.cgf_conv_forward_shard.argtypes = [P, I, I64, I64, I64, P, P, P, P, P, P, I, P]
+    L.cgf_conv_backward_shard.argtypes = [P, I, I64, I64, I64] + [P] * 10 + [I, P]
+    L.cgf_conv_double_backward_shard.argtypes = [P, I, I64, I64, I64] + [P] * 16 + [I, P]
     _lib = L
     return L
 
@@ -435,6 +439,57 @@ class ConvPlan:
             p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"], d["t_row_ptr"], d["t_src"],
             d["t_eid"], *(TpPlan._p(a) for a in (node_x, edge_y, edge_w, g_node_z, d_gx, d_gy, d_gw, ox, oy, ow,
                                                  ogz)), mode, TpPlan._stream(node_x)))
+        return ox, oy, ow, ogz
+
+
+    # -- sharded calls (one rank of a destination-partitioned graph) ---------
+    # ``sh`` is a dist.GraphShard: out_nodes owned output rows, in_nodes
+    # (padded, all-gathered) neighbour rows, local CSR + transposed CSR.
+    def _shard_ptrs(self, sh, ref):
+        d = sh.device(ref.device)
+        return {k: C.c_void_p(v.data_ptr()) for k, v in d.items()}
+
+    def forward_shard(self, sh, node_x_all, edge_y, edge_w, mode=DETERMINISTIC):
+        """Local output rows of the conv; node_x_all spans sh.in_nodes rows."""
+        p = self.plan
+        TpPlan._same(node_x_all, edge_y, edge_w)
+        z = TpPlan._empty_like(node_x_all, (sh.out_nodes, p.dim_z))
+        d = self._shard_ptrs(sh, node_x_all)
+        _check(lib().cgf_conv_forward_shard(p._h, _dtype_code(node_x_all), sh.out_nodes, sh.in_nodes, sh.edges,
+                                            d["row_ptr"], d["nbr"], TpPlan._p(node_x_all), TpPlan._p(edge_y),
+                                            TpPlan._p(edge_w), TpPlan._p(z), mode, TpPlan._stream(node_x_all)))
+        return z
+
+    def backward_shard(self, sh, node_x_all, edge_y, edge_w, g_node_z, mode=DETERMINISTIC):
+        """(partial g_node_x over sh.in_nodes rows, g_edge_y, g_edge_w)."""
+        p = self.plan
+        TpPlan._same(node_x_all, edge_y, edge_w, g_node_z)
+        gx = TpPlan._empty_like(node_x_all, (sh.in_nodes, p.dim_x))
+        gy = TpPlan._empty_like(node_x_all, (sh.edges, p.dim_y))
+        gw = TpPlan._empty_like(node_x_all, (sh.edges, p.n_w))
+        d = self._shard_ptrs(sh, node_x_all)
+        _check(lib().cgf_conv_backward_shard(p._h, _dtype_code(node_x_all), sh.out_nodes, sh.in_nodes, sh.edges,
+                                             d["t_row_ptr"], d["t_src"], d["t_eid"], TpPlan._p(node_x_all),
+                                             TpPlan._p(edge_y), TpPlan._p(edge_w), TpPlan._p(g_node_z),
+                                             TpPlan._p(gx), TpPlan._p(gy), TpPlan._p(gw), mode,
+                                             TpPlan._stream(node_x_all)))
+        return gx, gy, gw
+
+    def double_backward_shard(self, sh, node_x_all, edge_y, edge_w, g_node_z, d_gx_all, d_gy, d_gw,
+                              mode=DETERMINISTIC):
+        """(partial dL/dnode_x over sh.in_nodes rows, dL/dedge_y, dL/dedge_w, dL/dg_node_z local)."""
+        p = self.plan
+        TpPlan._same(node_x_all, edge_y, edge_w, g_node_z, d_gx_all, d_gy, d_gw)
+        ox = TpPlan._empty_like(node_x_all, (sh.in_nodes, p.dim_x))
+        oy = TpPlan._empty_like(node_x_all, (sh.edges, p.dim_y))
+        ow = TpPlan._empty_like(node_x_all, (sh.edges, p.n_w))
+        ogz = TpPlan._empty_like(node_x_all, (sh.out_nodes, p.dim_z))
+        d = self._shard_ptrs(sh, node_x_all)
+        _check(lib().cgf_conv_double_backward_shard(
+            p._h, _dtype_code(node_x_all), sh.out_nodes, sh.in_nodes, sh.edges, d["row_ptr"], d["nbr"],
+            d["t_row_ptr"], d["t_src"], d["t_eid"],
+            *(TpPlan._p(a) for a in (node_x_all, edge_y, edge_w, g_node_z, d_gx_all, d_gy, d_gw, ox, oy, ow, ogz)),
+            mode, TpPlan._stream(node_x_all)))
         return ox, oy, ow, ogz
 
 

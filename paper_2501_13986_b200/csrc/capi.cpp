@@ -470,24 +470,26 @@ int cgf_plan_kernel_compile(cgf_plan* p, int comp, int loop, int dtype, int w_sh
   });
 }
 
-int cgf_conv_transpose_host(int64_t nodes, int64_t edges, const int64_t* row_ptr, const int32_t* nbr,
-                            int64_t* t_row_ptr, int32_t* t_out, int32_t* t_eid) {
+int cgf_conv_transpose_shard_host(int64_t out_nodes, int64_t in_nodes, int64_t edges, const int64_t* row_ptr,
+                                  const int32_t* nbr, int64_t* t_row_ptr, int32_t* t_out, int32_t* t_eid) {
   return guarded([&] {
-    if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
-    if (edges > 0) {
-      need(row_ptr, "row_ptr"); need(nbr, "nbr"); need(t_row_ptr, "t_row_ptr"); need(t_out, "t_src"); need(t_eid, "t_eid");
-    }
-    if (row_ptr[0] != 0 || row_ptr[nodes] != edges) throw std::invalid_argument("row_ptr does not span the edge list");
+    if (out_nodes < 0 || in_nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    need(t_row_ptr, "t_row_ptr");
+    if (out_nodes > 0) need(row_ptr, "row_ptr");
+    if (edges > 0) { need(nbr, "nbr"); need(t_out, "t_src"); need(t_eid, "t_eid"); }
+    if (out_nodes > 0 && (row_ptr[0] != 0 || row_ptr[out_nodes] != edges))
+      throw std::invalid_argument("row_ptr does not span the edge list");
+    if (out_nodes == 0 && edges != 0) throw std::invalid_argument("row_ptr does not span the edge list");
     // Stable counting sort by neighbour (conv.cpp:135-151): within a bucket
     // edges keep CSR order, i.e. ascending output node.
-    std::vector<int64_t> cnt(static_cast<size_t>(nodes) + 1, 0);
+    std::vector<int64_t> cnt(static_cast<size_t>(in_nodes) + 1, 0);
     for (int64_t e = 0; e < edges; ++e) {
-      if (nbr[e] < 0 || nbr[e] >= nodes) throw std::invalid_argument("neighbour index out of range");
+      if (nbr[e] < 0 || nbr[e] >= in_nodes) throw std::invalid_argument("neighbour index out of range");
       ++cnt[static_cast<size_t>(nbr[e]) + 1];
     }
-    for (int64_t v = 0; v < nodes; ++v) cnt[v + 1] += cnt[v];
-    std::memcpy(t_row_ptr, cnt.data(), sizeof(int64_t) * (static_cast<size_t>(nodes) + 1));
-    for (int64_t s = 0; s < nodes; ++s)
+    for (int64_t v = 0; v < in_nodes; ++v) cnt[v + 1] += cnt[v];
+    std::memcpy(t_row_ptr, cnt.data(), sizeof(int64_t) * (static_cast<size_t>(in_nodes) + 1));
+    for (int64_t s = 0; s < out_nodes; ++s)
       for (int64_t e = row_ptr[s]; e < row_ptr[s + 1]; ++e) {
         const int64_t q = cnt[nbr[e]]++;
         t_out[q] = static_cast<int32_t>(s);
@@ -496,20 +498,57 @@ int cgf_conv_transpose_host(int64_t nodes, int64_t edges, const int64_t* row_ptr
   });
 }
 
-int cgf_conv_forward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr, const int32_t* nbr,
-                     const void* node_x, const void* edge_y, const void* edge_w, void* node_z, int mode, void* stream) {
+int cgf_conv_transpose_host(int64_t nodes, int64_t edges, const int64_t* row_ptr, const int32_t* nbr,
+                            int64_t* t_row_ptr, int32_t* t_out, int32_t* t_eid) {
+  return cgf_conv_transpose_shard_host(nodes, nodes, edges, row_ptr, nbr, t_row_ptr, t_out, t_eid);
+}
+
+int cgf_conv_forward_shard(cgf_plan* p, int dtype, int64_t out_nodes, int64_t in_nodes, int64_t edges,
+                           const int64_t* row_ptr, const int32_t* nbr, const void* node_x, const void* edge_y,
+                           const void* edge_w, void* node_z, int mode, void* stream) {
   return guarded([&] {
     need(p, "plan");
     if (mode != CGF_CONV_DETERMINISTIC) throw cgf::UnsupportedError("only the deterministic conv mode is built");
-    if (nodes <= 0) return;
-    need(row_ptr, "row_ptr"); need(node_x, "node_x"); need(node_z, "node_z");
-    if (edges > 0) { need(nbr, "nbr"); need(edge_y, "edge_y"); need(edge_w, "edge_w"); }
+    if (out_nodes < 0 || in_nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (out_nodes == 0) return;
+    need(row_ptr, "row_ptr"); need(node_z, "node_z");
+    if (edges > 0) { need(node_x, "node_x"); need(nbr, "nbr"); need(edge_y, "edge_y"); need(edge_w, "edge_w"); }
     const std::size_t es = dtype == CGF_F64 ? 8 : 4;
-    if (!p->z_covered) memzero(node_z, es * nodes * p->problem.dim_z, stream);
+    if (!p->z_covered) memzero(node_z, es * out_nodes * p->problem.dim_z, stream);
     Args a;
-    a.x = node_x; a.y = edge_y; a.w = edge_w; a.o0 = node_z; a.rows = nodes;
+    a.x = node_x; a.y = edge_y; a.w = edge_w; a.o0 = node_z; a.rows = out_nodes;
     a.rp = row_ptr; a.nb = nbr; a.edges = edges;
     run_kernel(p, cgf::Comp::Fwd, cgf::Loop::ConvByOutput, dtype, 0, a, stream);
+  });
+}
+
+int cgf_conv_forward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr, const int32_t* nbr,
+                     const void* node_x, const void* edge_y, const void* edge_w, void* node_z, int mode, void* stream) {
+  return cgf_conv_forward_shard(p, dtype, nodes, nodes, edges, row_ptr, nbr, node_x, edge_y, edge_w, node_z, mode,
+                                stream);
+}
+
+int cgf_conv_backward_shard(cgf_plan* p, int dtype, int64_t out_nodes, int64_t in_nodes, int64_t edges,
+                            const int64_t* t_row_ptr, const int32_t* t_out, const int32_t* t_eid, const void* node_x,
+                            const void* edge_y, const void* edge_w, const void* g_node_z, void* g_node_x,
+                            void* g_edge_y, void* g_edge_w, int mode, void* stream) {
+  return guarded([&] {
+    need(p, "plan");
+    if (mode != CGF_CONV_DETERMINISTIC) throw cgf::UnsupportedError("only the deterministic conv mode is built");
+    if (out_nodes < 0 || in_nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (in_nodes == 0) return;
+    need(t_row_ptr, "t_row_ptr"); need(node_x, "node_x"); need(g_node_x, "g_node_x");
+    if (edges > 0) {
+      need(g_node_z, "g_node_z"); need(t_out, "t_src"); need(t_eid, "t_eid"); need(edge_y, "edge_y");
+      need(edge_w, "edge_w"); need(g_edge_y, "g_edge_y"); need(g_edge_w, "g_edge_w");
+    }
+    const std::size_t es = dtype == CGF_F64 ? 8 : 4;
+    if (!p->x_covered) memzero(g_node_x, es * in_nodes * p->problem.dim_x, stream);
+    Args a;
+    a.x = node_x; a.y = edge_y; a.w = edge_w; a.gz = g_node_z;
+    a.o0 = g_node_x; a.o1 = g_edge_y; a.o2 = g_edge_w; a.rows = in_nodes;
+    a.rp = t_row_ptr; a.nb = t_out; a.eid = t_eid; a.edges = edges;
+    run_kernel(p, cgf::Comp::Bwd, cgf::Loop::ConvByInput, dtype, 0, a, stream);
   });
 }
 
@@ -517,23 +556,42 @@ int cgf_conv_backward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, cons
                       const int32_t* nbr, const int64_t* t_row_ptr, const int32_t* t_out, const int32_t* t_eid,
                       const void* node_x, const void* edge_y, const void* edge_w, const void* g_node_z,
                       void* g_node_x, void* g_edge_y, void* g_edge_w, int mode, void* stream) {
+  (void)row_ptr; (void)nbr;
+  return cgf_conv_backward_shard(p, dtype, nodes, nodes, edges, t_row_ptr, t_out, t_eid, node_x, edge_y, edge_w,
+                                 g_node_z, g_node_x, g_edge_y, g_edge_w, mode, stream);
+}
+
+int cgf_conv_double_backward_shard(cgf_plan* p, int dtype, int64_t out_nodes, int64_t in_nodes, int64_t edges,
+                                   const int64_t* row_ptr, const int32_t* nbr, const int64_t* t_row_ptr,
+                                   const int32_t* t_out, const int32_t* t_eid, const void* node_x,
+                                   const void* edge_y, const void* edge_w, const void* g_node_z, const void* d_gx,
+                                   const void* d_gy, const void* d_gw, void* o_node_x, void* o_edge_y,
+                                   void* o_edge_w, void* o_g_node_z, int mode, void* stream) {
   return guarded([&] {
     need(p, "plan");
     if (mode != CGF_CONV_DETERMINISTIC) throw cgf::UnsupportedError("only the deterministic conv mode is built");
-    (void)row_ptr; (void)nbr;
-    if (nodes <= 0) return;
-    need(t_row_ptr, "t_row_ptr"); need(node_x, "node_x"); need(g_node_z, "g_node_z"); need(g_node_x, "g_node_x");
-    if (edges > 0) {
-      need(t_out, "t_src"); need(t_eid, "t_eid"); need(edge_y, "edge_y"); need(edge_w, "edge_w");
-      need(g_edge_y, "g_edge_y"); need(g_edge_w, "g_edge_w");
-    }
+    if (out_nodes < 0 || in_nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
     const std::size_t es = dtype == CGF_F64 ? 8 : 4;
-    if (!p->x_covered) memzero(g_node_x, es * nodes * p->problem.dim_x, stream);
-    Args a;
-    a.x = node_x; a.y = edge_y; a.w = edge_w; a.gz = g_node_z;
-    a.o0 = g_node_x; a.o1 = g_edge_y; a.o2 = g_edge_w; a.rows = nodes;
-    a.rp = t_row_ptr; a.nb = t_out; a.eid = t_eid; a.edges = edges;
-    run_kernel(p, cgf::Comp::Bwd, cgf::Loop::ConvByInput, dtype, 0, a, stream);
+    // Pass 1, by output node: dL/dg_node_z = sum_e op3 + op6 + op7 (PAPER.md:1001-1032).
+    if (out_nodes > 0) {
+      need(row_ptr, "row_ptr"); need(o_g_node_z, "o_g_node_z");
+      if (!p->z_covered) memzero(o_g_node_z, es * out_nodes * p->problem.dim_z, stream);
+      Args a;
+      a.x = node_x; a.y = edge_y; a.w = edge_w; a.da = d_gx; a.db = d_gy; a.dc = d_gw;
+      a.o3 = o_g_node_z; a.rows = out_nodes; a.rp = row_ptr; a.nb = nbr; a.edges = edges;
+      run_kernel(p, cgf::Comp::DBwdZ, cgf::Loop::ConvByOutput, dtype, 0, a, stream);
+    }
+    // Pass 2, by neighbour node (transposed CSR): dL/dnode_x = sum_e op1.gx + op2.gx,
+    // per edge dL/dy = op1.gy + op2.gy and dL/dW = op4.gw + op5.gw.
+    if (in_nodes > 0) {
+      need(t_row_ptr, "t_row_ptr"); need(o_node_x, "o_node_x");
+      if (!p->x_covered) memzero(o_node_x, es * in_nodes * p->problem.dim_x, stream);
+      Args b;
+      b.x = node_x; b.y = edge_y; b.w = edge_w; b.gz = g_node_z; b.da = d_gx; b.db = d_gy; b.dc = d_gw;
+      b.o0 = o_node_x; b.o1 = o_edge_y; b.o2 = o_edge_w; b.rows = in_nodes;
+      b.rp = t_row_ptr; b.nb = t_out; b.eid = t_eid; b.edges = edges;
+      run_kernel(p, cgf::Comp::DBwdX, cgf::Loop::ConvByInput, dtype, 0, b, stream);
+    }
   });
 }
 
@@ -543,26 +601,9 @@ int cgf_conv_double_backward(cgf_plan* p, int dtype, int64_t nodes, int64_t edge
                              const void* g_node_z, const void* d_gx, const void* d_gy, const void* d_gw,
                              void* o_node_x, void* o_edge_y, void* o_edge_w, void* o_g_node_z, int mode,
                              void* stream) {
-  return guarded([&] {
-    need(p, "plan");
-    if (mode != CGF_CONV_DETERMINISTIC) throw cgf::UnsupportedError("only the deterministic conv mode is built");
-    if (nodes <= 0) return;
-    const std::size_t es = dtype == CGF_F64 ? 8 : 4;
-    if (!p->z_covered) memzero(o_g_node_z, es * nodes * p->problem.dim_z, stream);
-    if (!p->x_covered) memzero(o_node_x, es * nodes * p->problem.dim_x, stream);
-    // Pass 1, by output node: dL/dg_node_z = sum_e op3 + op6 + op7 (PAPER.md:1001-1032).
-    Args a;
-    a.x = node_x; a.y = edge_y; a.w = edge_w; a.da = d_gx; a.db = d_gy; a.dc = d_gw;
-    a.o3 = o_g_node_z; a.rows = nodes; a.rp = row_ptr; a.nb = nbr; a.edges = edges;
-    run_kernel(p, cgf::Comp::DBwdZ, cgf::Loop::ConvByOutput, dtype, 0, a, stream);
-    // Pass 2, by neighbour node (transposed CSR): dL/dnode_x = sum_e op1.gx + op2.gx,
-    // per edge dL/dy = op1.gy + op2.gy and dL/dW = op4.gw + op5.gw.
-    Args b;
-    b.x = node_x; b.y = edge_y; b.w = edge_w; b.gz = g_node_z; b.da = d_gx; b.db = d_gy; b.dc = d_gw;
-    b.o0 = o_node_x; b.o1 = o_edge_y; b.o2 = o_edge_w; b.rows = nodes;
-    b.rp = t_row_ptr; b.nb = t_out; b.eid = t_eid; b.edges = edges;
-    run_kernel(p, cgf::Comp::DBwdX, cgf::Loop::ConvByInput, dtype, 0, b, stream);
-  });
+  return cgf_conv_double_backward_shard(p, dtype, nodes, nodes, edges, row_ptr, nbr, t_row_ptr, t_out, t_eid,
+                                        node_x, edge_y, edge_w, g_node_z, d_gx, d_gy, d_gw, o_node_x, o_edge_y,
+                                        o_edge_w, o_g_node_z, mode, stream);
 }
 
 }  // extern "C"

@@ -1,0 +1,184 @@
+"""Multi-GPU fused convolution: destination-partitioned graph, one rank per GPU.
+
+SURVEY.md §8e. The reference runs the fused conv on one host (``ConvPlan``,
+conv.hpp:93-115, conv.cpp:234-528); here the OUTPUT nodes (the reference's
+``src``, the CSR row) are split into P contiguous ranges holding ~|E|/P edges
+each, and each rank owns its range's node features and its edges' y / W (and
+their gradients). Per direction there is exactly one exchange step:
+
+* forward:          all-gather node_x (each rank reads neighbours anywhere),
+                    then the local fused conv writes its own node_z rows;
+* backward:         local conv backward over the shard's transposed CSR gives
+                    PARTIAL g_node_x for every neighbour row, reduce-scattered
+                    back to the owners (the adjoint of the all-gather);
+                    g_edge_y / g_edge_w are local;
+* double-backward:  all-gather node_x and dL/dg_node_x, reduce-scatter
+                    dL/dnode_x; dL/dg_node_z and per-edge terms are local.
+
+There is no weight all-reduce: the reference's conv weights are per edge. The
+all-gathered layout is padded: rank r's rows sit at [r*chunk, r*chunk + n_r)
+of a P*chunk buffer (``chunk`` = the largest range), so every collective is a
+plain equal-split NCCL all_gather_into_tensor / reduce_scatter_tensor, and
+``GraphShard.nbr`` is pre-remapped into that padded index space on the host.
+
+The local compute is ``ConvPlan.*_shard`` (the generated sm_100a kernels via
+the C ABI). ``DistConvPlan`` takes it as ``local`` so the partition and
+collective logic can be exercised on CPU ranks (gloo) with a test double.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import ShapeError, lib, _check
+
+__all__ = ["partition_bounds", "GraphShard", "DistConvPlan", "lattice_radius_graph"]
+
+
+def partition_bounds(row_ptr: np.ndarray, world: int) -> np.ndarray:
+    """Output-node boundaries b[0..P] with ~|E|/P edges per range (contiguous,
+    monotone; ranges may be empty on tiny graphs)."""
+    row_ptr = np.asarray(row_ptr, np.int64)
+    nodes = row_ptr.size - 1
+    edges = int(row_ptr[-1])
+    targets = (np.arange(world + 1, dtype=np.float64) * edges / world).round().astype(np.int64)
+    b = np.searchsorted(row_ptr, targets, side="left").astype(np.int64)
+    b[0], b[-1] = 0, nodes
+    if edges == 0:  # nothing to balance: split nodes evenly
+        b = (np.arange(world + 1, dtype=np.int64) * nodes) // world
+    return np.maximum.accumulate(np.minimum(b, nodes))
+
+
+class GraphShard:
+    """Rank ``rank``'s part of a destination-partitioned CSR graph.
+
+    ``graph`` is the global ``Graph`` (host CSR, reference GraphCSR layout).
+    Fields: out_nodes (owned output rows), node0 (first owned global node),
+    chunk (padded rows per rank), in_nodes = world * chunk, edges, edge0
+    (first owned global edge), row_ptr (rebased), nbr (padded index space),
+    t_row_ptr / t_src / t_eid (transposed shard CSR)."""
+
+    def __init__(self, graph, world: int, rank: int, bounds: np.ndarray | None = None):
+        if not 0 <= rank < world:
+            raise ShapeError(f"rank {rank} outside world {world}")
+        b = partition_bounds(graph.row_ptr, world) if bounds is None else np.asarray(bounds, np.int64)
+        self.world, self.rank, self.bounds = world, rank, b
+        self.chunk = max(int(np.max(np.diff(b))), 1)
+        self.in_nodes = world * self.chunk
+        s0, s1 = int(b[rank]), int(b[rank + 1])
+        e0, e1 = int(graph.row_ptr[s0]), int(graph.row_ptr[s1])
+        self.node0, self.out_nodes, self.edge0, self.edges = s0, s1 - s0, e0, e1 - e0
+        self.row_ptr = np.ascontiguousarray(graph.row_ptr[s0:s1 + 1] - e0)
+        gnbr = np.asarray(graph.nbr[e0:e1], np.int64)
+        owner = np.searchsorted(b, gnbr, side="right") - 1
+        self.nbr = np.ascontiguousarray((owner * self.chunk + gnbr - b[owner]).astype(np.int32))
+        self.t_row_ptr = np.zeros(self.in_nodes + 1, np.int64)
+        self.t_src = np.zeros(max(self.edges, 1), np.int32)
+        self.t_eid = np.zeros(max(self.edges, 1), np.int32)
+        _check(lib().cgf_conv_transpose_shard_host(
+            self.out_nodes, self.in_nodes, self.edges, self.row_ptr.ctypes.data,
+            self.nbr.ctypes.data if self.edges else None, self.t_row_ptr.ctypes.data, self.t_src.ctypes.data,
+            self.t_eid.ctypes.data))
+        self._dev = {}
+
+    def padded_index(self, nodes: np.ndarray) -> np.ndarray:
+        """Global node ids -> rows of the padded all-gathered buffer."""
+        nodes = np.asarray(nodes, np.int64)
+        owner = np.searchsorted(self.bounds, nodes, side="right") - 1
+        return owner * self.chunk + nodes - self.bounds[owner]
+
+    def device(self, dev):
+        import torch
+        key = str(dev)
+        if key not in self._dev:
+            t = lambda a: torch.from_numpy(a).to(dev)
+            self._dev[key] = {k: t(getattr(self, k)) for k in ("row_ptr", "nbr", "t_row_ptr", "t_src", "t_eid")}
+        return self._dev[key]
+
+
+class DistConvPlan:
+    """ConvPlan over a destination-partitioned graph (one rank per GPU).
+
+    Inputs / outputs of each call are the rank's own slices: node-indexed
+    arrays have ``shard.out_nodes`` rows (the rank's node range), edge arrays
+    ``shard.edges`` rows. ``local`` computes the shard (default: the CUDA
+    ``ConvPlan``); ``group`` is the torch.distributed process group."""
+
+    def __init__(self, plan, shard: GraphShard, group=None, local=None):
+        from . import ConvPlan
+        self.plan, self.shard, self.group = plan, shard, group
+        self.local = local if local is not None else ConvPlan(plan)
+        self._gather_cache = {}
+
+    # -- collectives -----------------------------------------------------------
+    def _all_gather(self, a, key=None):
+        """[out_nodes, d] per rank -> [world * chunk, d] padded, on every rank."""
+        import torch
+        import torch.distributed as dist
+        sh = self.shard
+        if a.shape[0] != sh.out_nodes:
+            raise ShapeError(f"expected {sh.out_nodes} local node rows, got {a.shape[0]}")
+        if sh.world == 1 and sh.chunk == sh.out_nodes:
+            return a
+        buf = a.new_zeros((sh.chunk, a.shape[1]))
+        buf[:sh.out_nodes] = a
+        out = a.new_empty((sh.in_nodes, a.shape[1]))
+        dist.all_gather_into_tensor(out, buf, group=self.group)
+        return out
+
+    def _reduce_scatter(self, partial):
+        """[world * chunk, d] partial sums -> this rank's [out_nodes, d] totals."""
+        import torch.distributed as dist
+        sh = self.shard
+        if sh.world == 1:
+            return partial[:sh.out_nodes]
+        out = partial.new_empty((sh.chunk, partial.shape[1]))
+        dist.reduce_scatter_tensor(out, partial, group=self.group)
+        return out[:sh.out_nodes]
+
+    # -- the three entry points -------------------------------------------------
+    def forward(self, node_x, edge_y, edge_w):
+        x_all = self._all_gather(node_x)
+        return self.local.forward_shard(self.shard, x_all, edge_y, edge_w)
+
+    def backward(self, node_x, edge_y, edge_w, g_node_z, node_x_all=None):
+        x_all = self._all_gather(node_x) if node_x_all is None else node_x_all
+        gx_part, gy, gw = self.local.backward_shard(self.shard, x_all, edge_y, edge_w, g_node_z)
+        return self._reduce_scatter(gx_part), gy, gw
+
+    def double_backward(self, node_x, edge_y, edge_w, g_node_z, upstream):
+        d_gx, d_gy, d_gw = upstream
+        x_all = self._all_gather(node_x)
+        dgx_all = self._all_gather(d_gx)
+        ox_part, oy, ow, ogz = self.local.double_backward_shard(self.shard, x_all, edge_y, edge_w, g_node_z,
+                                                                dgx_all, d_gy, d_gw)
+        return self._reduce_scatter(ox_part), oy, ow, ogz
+
+    def gather_x(self, node_x):
+        """The padded all-gathered node features (reusable across fwd / bwd)."""
+        return self._all_gather(node_x)
+
+
+def lattice_radius_graph(n: int, spacing: float = 1.0, r_cut: float = 3.0):
+    """``conv::radius_graph(conv::cubic_lattice(n, n, n, spacing), r_cut)``
+    (conv.cpp:89-133, 153-164) for the benchmark graphs C4 / C5, built directly
+    from the lattice's neighbour offsets: node id = (i * n + j) * n + k, edges
+    (s, d) for every d != s within r_cut, sorted by (s, d). Returns (nodes,
+    src int64, nbr int64)."""
+    R = int(np.floor(r_cut / spacing + 1e-9))
+    offs = [(a, b, c) for a in range(-R, R + 1) for b in range(-R, R + 1) for c in range(-R, R + 1)
+            if (a, b, c) != (0, 0, 0) and (a * a + b * b + c * c) * spacing * spacing <= r_cut * r_cut + 1e-9]
+    # neighbour id delta is monotone in the (a, b, c) lexicographic order, so
+    # emitting offsets in that order per source keeps (s, d) sorted.
+    offs.sort()
+    idx = np.arange(n, dtype=np.int64)
+    ii, jj, kk = np.meshgrid(idx, idx, idx, indexing="ij")
+    ii, jj, kk = ii.ravel(), jj.ravel(), kk.ravel()
+    nodes = n ** 3
+    valid = np.zeros((nodes, len(offs)), dtype=bool)
+    for t, (a, b, c) in enumerate(offs):
+        valid[:, t] = ((ii + a >= 0) & (ii + a < n) & (jj + b >= 0) & (jj + b < n) & (kk + c >= 0) & (kk + c < n))
+    delta = np.array([(a * n + b) * n + c for a, b, c in offs], dtype=np.int64)
+    s_idx, t_idx = np.nonzero(valid)  # row-major: by source, then offset order
+    src = s_idx.astype(np.int64)
+    nbr = src + delta[t_idx]
+    return nodes, src, nbr
