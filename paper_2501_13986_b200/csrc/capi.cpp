@@ -18,6 +18,7 @@
 #include "cuda_api.hpp"
 #include "jit.hpp"
 #include "problem.hpp"
+#include "uvw.hpp"
 
 struct cgf_plan {
   cgf::Problem problem;
@@ -26,6 +27,17 @@ struct cgf_plan {
   bool z_covered = true, x_covered = true;
   std::mutex mu;
   std::map<std::tuple<int, int, int, int, int, std::string>, std::shared_ptr<cgf::KernelSource>> sources;
+  // uvw tensor-core path (all-C problems, shared W): generated source and the
+  // per-context device buffer of swizzled tf32 W images.
+  std::shared_ptr<cgf::UvwSource> uvw;
+  std::map<CUcontext, CUdeviceptr> wimg;
+  ~cgf_plan() {
+    for (auto& [ctx, ptr] : wimg) {
+      CUcontext cur = nullptr;
+      cgf::drv::cuCtxGetCurrent(&cur);
+      if (cur == ctx) cgf::drv::cuMemFree(ptr);
+    }
+  }
 };
 
 namespace {
@@ -110,7 +122,21 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   return ks;
 }
 
+bool use_uvw(cgf_plan* p, int op, int dtype, int w_shared) {
+  if (op != CGF_OP_FORWARD || dtype != CGF_F32 || !w_shared) return false;
+  const char* env = std::getenv("CGF_UVW");
+  if (env && env[0] == '0') return false;
+  return cgf::uvw_eligible(p->problem);
+}
+
+std::shared_ptr<cgf::UvwSource> uvw_source(cgf_plan* p) {
+  std::lock_guard<std::mutex> g(p->mu);
+  if (!p->uvw) p->uvw = std::make_shared<cgf::UvwSource>(cgf::generate_uvw_forward(p->problem));
+  return p->uvw;
+}
+
 std::shared_ptr<cgf::KernelSource> source_for_op(cgf_plan* p, int op, int dtype, int w_shared, int aligned) {
+  if (use_uvw(p, op, dtype, w_shared)) return std::make_shared<cgf::KernelSource>(uvw_source(p)->main);
   if (op < 0 || op > 2) throw std::invalid_argument("bad op");
   return source_for(p, static_cast<cgf::Comp>(op), cgf::Loop::Rows, dtype, w_shared, aligned);
 }
@@ -144,6 +170,38 @@ void run_kernel(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype, int w_sh
                                     reinterpret_cast<CUstream>(stream), args, nullptr));
 }
 
+// uvw forward on the tensor cores: W -> swizzled tf32 hi / lo images (one
+// small kernel), then the warp-specialised tcgen05 kernel over 128-row tiles.
+void run_uvw_forward(cgf_plan* p, const Args& a, void* stream) {
+  const auto us = uvw_source(p);
+  const cgf::Kernel prep = cgf::load_kernel(us->prep);
+  const cgf::Kernel main = cgf::load_kernel(us->main);
+  CUcontext ctx = cgf::ensure_context();
+  CUdeviceptr img = 0;
+  {
+    std::lock_guard<std::mutex> g(p->mu);
+    auto it = p->wimg.find(ctx);
+    if (it == p->wimg.end()) {
+      CU_CHECK(cgf::drv::cuMemAlloc(&img, us->wimg_bytes));
+      p->wimg.emplace(ctx, img);
+    } else {
+      img = it->second;
+    }
+  }
+  CUstream st = reinterpret_cast<CUstream>(stream);
+  const void* w = a.w;
+  void* pargs[] = {&w, &img};
+  const unsigned pgrid = static_cast<unsigned>((p->problem.n_w + 255) / 256);
+  CU_CHECK(cgf::drv::cuLaunchKernel(prep.fn, pgrid, 1, 1, 256, 1, 1, 0, st, pargs, nullptr));
+  Args c = a;
+  c.w = reinterpret_cast<const void*>(img);
+  const std::int64_t tiles = (a.rows + us->tile_rows - 1) / us->tile_rows;
+  const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(tiles, main.max_grid));
+  void* args[] = {&c.x, &c.y, &c.w, &c.gz, &c.da, &c.db, &c.dc, &c.o0, &c.o1, &c.o2, &c.o3, &c.rows,
+                  &c.rp, &c.nb, &c.eid, &c.edges};
+  CU_CHECK(cgf::drv::cuLaunchKernel(main.fn, grid, 1, 1, main.threads, 1, 1, main.smem_bytes, st, args, nullptr));
+}
+
 void memzero(void* ptr, std::size_t bytes, void* stream) {
   if (bytes) CU_CHECK(cgf::drv::cuMemsetD8Async(reinterpret_cast<CUdeviceptr>(ptr), 0, bytes, reinterpret_cast<CUstream>(stream)));
 }
@@ -162,6 +220,10 @@ void launch(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, con
   Args a;
   a.x = x; a.y = y; a.w = w; a.gz = gz; a.da = da; a.db = db; a.dc = dc;
   a.o0 = o0; a.o1 = o1; a.o2 = o2; a.o3 = o3; a.rows = rows;
+  if (use_uvw(p, op, dtype, w_shared)) {
+    run_uvw_forward(p, a, stream);
+    return;
+  }
   run_kernel(p, static_cast<cgf::Comp>(op), cgf::Loop::Rows, dtype, w_shared, a, stream);
 }
 

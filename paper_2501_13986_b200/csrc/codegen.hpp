@@ -56,7 +56,8 @@ struct KernelConfig {
 void apply_gen_flags(KernelConfig& cfg, const std::string& flags);
 
 struct KernelSource {
-  std::string name;
+  std::string name;    // entry point
+  std::string module;  // cubin cache name when several entry points share one source (default: name)
   std::string source;
   int threads = 0;
   int smem_bytes = 0;

@@ -139,7 +139,7 @@ Kernel load_kernel(const KernelSource& ks) {
   std::lock_guard<std::mutex> g(mu);
   auto it = loaded.find({ctx, key});
   if (it != loaded.end()) return it->second;
-  const std::string cubin = compile_cubin(ks.source, ks.name);
+  const std::string cubin = compile_cubin(ks.source, ks.module.empty() ? ks.name : ks.module);
   CUmodule mod;
   CU_CHECK(drv::cuModuleLoadData(&mod, cubin.data()));
   Kernel k;

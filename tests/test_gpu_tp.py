@@ -167,3 +167,38 @@ def test_full_size_c2_sampled_rows_and_linearity(dt):
     z2 = plan.forward(x * 2.5, y, w)
     err = (z2 - 2.5 * z).norm() / (2.5 * z).norm()
     assert err.item() <= TOL[dt] * 10
+
+
+@pytest.mark.parametrize("rows", [1, 127, 128, 1000, 128 * 150 + 37])
+def test_c3_shared_w_tensor_core_forward(rows):
+    """uvw (kind C) with shared W on tcgen05 (3xTF32): one-tile, tail tile and
+    more tiles than SMs (persistent loop) against the FP32 oracle."""
+    js = config("c3")
+    o, plan = O.Oracle(js), P().TpPlan(js)
+    assert "tcgen05.mma" in plan.source(op=0, dtype=0, w_shared=True)
+    x, y, w, *_ = inputs(o, rows, np.float32, seed=77, w_shared=True)
+    z = plan.forward(dev(x), dev(y), dev(w), w_shared=True)
+    torch.cuda.synchronize()
+    if rows > 4000:  # the oracle on a row sample (rows are independent)
+        idx = np.r_[0:64, rows // 2:rows // 2 + 64, rows - 100:rows]
+        check(host(z)[idx], o.forward(x[idx], y[idx], w, w_shared=True), np.float32, "c3 tcgen05 fwd (sampled)")
+    else:
+        check(host(z), o.forward(x, y, w, w_shared=True), np.float32, "c3 tcgen05 fwd")
+
+
+def test_c3_tensor_core_matches_simt_path(monkeypatch):
+    """The tcgen05 path and the SIMT generator agree on 64K rows; both deterministic."""
+    js = config("c3")
+    plan = P().TpPlan(js)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    rows = 65_536
+    x = torch.randn((rows, plan.dim_x), device="cuda", generator=g)
+    y = torch.randn((rows, plan.dim_y), device="cuda", generator=g)
+    w = torch.randn((1, plan.n_w), device="cuda", generator=g)
+    a = plan.forward(x, y, w, w_shared=True)
+    b = plan.forward(x, y, w, w_shared=True)
+    assert torch.equal(a, b)
+    monkeypatch.setenv("CGF_UVW", "0")
+    c = plan.forward(x, y, w, w_shared=True)
+    err = ((a - c).norm() / c.norm()).item()
+    assert err <= 1e-5, err
