@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <nvrtc.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -193,13 +194,48 @@ void run_uvw_forward(cgf_plan* p, const Args& a, void* stream) {
   void* pargs[] = {&w, &img};
   const unsigned pgrid = static_cast<unsigned>((p->problem.n_w + 255) / 256);
   CU_CHECK(cgf::drv::cuLaunchKernel(prep.fn, pgrid, 1, 1, 256, 1, 1, 0, st, pargs, nullptr));
-  Args c = a;
-  c.w = reinterpret_cast<const void*>(img);
+  // x viewed as [rows][dim_x / 16][16] fp32; one tile = 128 rows x dx lines of
+  // 16 channels' worth of one x segment, 64-byte swizzled (conflict-free
+  // per-row 16-byte reads). Rows past the batch are zero-filled by the TMA.
+  if (reinterpret_cast<std::uintptr_t>(a.x) & 15u) throw cgf::ShapeError("uvw path: x must be 16-byte aligned");
+  CUtensorMap maps[4];
+  const int dxs[4] = {1, 3, 5, 7};
+  for (int i = 0; i < 4; ++i) {
+    const cuuint64_t gdim[3] = {16, static_cast<cuuint64_t>(p->problem.dim_x / 16), static_cast<cuuint64_t>(a.rows)};
+    const cuuint64_t gstride[2] = {64, static_cast<cuuint64_t>(p->problem.dim_x) * 4};
+    const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(std::min(dxs[i], p->problem.dim_x / 16)), 128};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CU_CHECK(cgf::drv::cuTensorMapEncodeTiled(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(a.x), gdim,
+                                              gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+  }
+  const void* y = a.y;
+  void* z = a.o0;
+  std::int64_t rows = a.rows;
+  const void* wi = reinterpret_cast<const void*>(img);
   const std::int64_t tiles = (a.rows + us->tile_rows - 1) / us->tile_rows;
   const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(tiles, main.max_grid));
-  void* args[] = {&c.x, &c.y, &c.w, &c.gz, &c.da, &c.db, &c.dc, &c.o0, &c.o1, &c.o2, &c.o3, &c.rows,
-                  &c.rp, &c.nb, &c.eid, &c.edges};
+  // CGF_UVW_PROF: per-role mbarrier wait cycles (summed over CTAs), printed per call.
+  CUdeviceptr prof = 0;
+  if (std::getenv("CGF_UVW_PROF")) {
+    CU_CHECK(cgf::drv::cuMemAlloc(&prof, 16 * 8));
+    CU_CHECK(cgf::drv::cuMemsetD8Async(prof, 0, 16 * 8, st));
+  }
+  void* args[] = {&maps[0], &maps[1], &maps[2], &maps[3], &y, &wi, &z, &rows, &prof};
   CU_CHECK(cgf::drv::cuLaunchKernel(main.fn, grid, 1, 1, main.threads, 1, 1, main.smem_bytes, st, args, nullptr));
+  if (prof) {
+    unsigned long long h[16];
+    CU_CHECK(cgf::drv::cuStreamSynchronize(st));
+    CU_CHECK(cgf::drv::cuMemcpyDtoH(h, prof, sizeof h));
+    cgf::drv::cuMemFree(prof);
+    static const char* names[16] = {"-", "prod:aempty", "wload:wempty", "mma:sdrained(cur)", "mma:sdrained(prev)",
+                                    "mma:wfull", "mma:afull", "epi:sfull", "prod:xfull", "", "", "", "xload:xempty",
+                                    "", "", "kernel(cta0 cycles x ctas)"};
+    std::fprintf(stderr, "cgf_uvw prof (cycles summed over CTAs, lane-0 per warp) grid=%u:\n", grid);
+    for (int i = 0; i < 16; ++i)
+      if (h[i]) std::fprintf(stderr, "  %-28s %14llu  (%.1f per CTA)\n", names[i], h[i], double(h[i]) / grid);
+  }
 }
 
 void memzero(void* ptr, std::size_t bytes, void* stream) {

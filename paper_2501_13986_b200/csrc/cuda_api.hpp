@@ -13,7 +13,8 @@ namespace cgf::drv {
   X(cuFuncSetAttribute) X(cuOccupancyMaxActiveBlocksPerMultiprocessor) X(cuCtxGetDevice)   \
   X(cuDeviceGetAttribute) X(cuLaunchKernel) X(cuMemsetD8Async) X(cuMemAlloc) X(cuMemFree)  \
   X(cuMemcpyHtoD) X(cuMemcpyDtoH) X(cuCtxSynchronize) X(cuMemcpyHtoDAsync)                 \
-  X(cuMemcpyDtoHAsync) X(cuStreamSynchronize) X(cuLaunchKernelEx) X(cuFuncGetAttribute)
+  X(cuMemcpyDtoHAsync) X(cuStreamSynchronize) X(cuLaunchKernelEx) X(cuFuncGetAttribute)    \
+  X(cuTensorMapEncodeTiled)
 
 #define CGF_DRV_DECL(fn) extern decltype(&::fn) fn;
 CGF_DRV_FUNCS(CGF_DRV_DECL)

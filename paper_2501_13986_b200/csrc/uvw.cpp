@@ -11,12 +11,14 @@ namespace cgf {
 namespace {
 
 constexpr int kTileRows = 128;
-constexpr int kProdWarps = 8;     // 2 per SM sub-partition: thread = (row, 16 channels)
-constexpr int kMmaWarp = 8;
-constexpr int kEpiWarp0 = 9;      // warps 9..12: one per TMEM lane quadrant (warp % 4)
-constexpr int kWarps = 13;
+constexpr int kProdWarps = 16;    // producer warps (default); MMA warp, 4 epilogue warps, TMA warp follow
+
+
+
+
 constexpr int kTmemCols = 512;
-constexpr int kASlotBytes = 2 * kTileRows * 128;  // hi + lo, 128 rows x 32 fp32, SW128 K-major
+constexpr int kCh = 16;           // channels per unit = K of one A block (64 B rows, SW64)
+constexpr int kASlotBytes = 2 * kTileRows * kCh * 4;  // hi + lo, 128 rows x 16 fp32
 
 std::string S(long long v) { return std::to_string(v); }
 
@@ -43,13 +45,13 @@ bool uvw_eligible(const Problem& p, std::string* why) {
   for (const auto& s : p.resolved) {
     if (s.kind != Kind::C) return no("not all instructions are uvw (kind C)");
     if (s.b % 16 || s.b > 256) return no("z multiplicity must be a multiple of 16 and <= 256");
-    if (s.bp % 32) return no("x multiplicity must be a multiple of 32");
-    if (s.dz() * s.b > kTmemCols) return no("z segment accumulator exceeds TMEM");
+    if (s.bp % kCh) return no("x multiplicity must be a multiple of 16");
+    if (s.dz() * s.b > kTmemCols - 64) return no("z segment accumulator exceeds TMEM");
     if (s.dx() > 7 || s.dz() > 7) return no("l > 3 not supported by the tensor-core path");
   }
-  if (p.dim_z % 4 || p.dim_x % 4) return no("dim_x / dim_z must be multiples of 4");
+  if (p.dim_z % 4 || p.dim_x % kCh) return no("dim_x must be a multiple of 16 and dim_z of 4");
   for (const auto& s : p.resolved)
-    if (s.z_off % 4 || s.x_off % 4) return no("segment offsets must be multiples of 4");
+    if (s.z_off % 4 || s.x_off % kCh) return no("x segment offsets must be multiples of 16, z of 4");
   return true;
 }
 
@@ -78,14 +80,50 @@ UvwSource generate_uvw_forward(const Problem& p) {
         segs[it->second].ins.push_back(q);
       }
     }
-    std::stable_sort(segs.begin(), segs.end(), [](const Seg& a, const Seg& b) { return a.dz * a.n > b.dz * b.n; });
-    int cur = 0;
-    for (auto& s : segs) {
-      const int cols = s.dz * s.n;
-      if (cur + cols > kTmemCols) cur = 0;
-      s.col = cur;
-      cur += cols;
+  }
+  // TMEM plan: the A ring (na blocks of hi + lo, 32 columns each) sits at the
+  // top, accumulators below it. Segments are allocated around the accumulator
+  // ring in processing order; pick the order (and the deepest A ring) whose
+  // accumulator reuse leaves the fewest back-to-back waits on an epilogue drain.
+  int na = 0;
+  {
+    std::vector<int> perm(segs.size());
+    for (size_t i = 0; i < perm.size(); ++i) perm[i] = static_cast<int>(i);
+    int best_score = 1 << 30;
+    std::vector<Seg> best;
+    for (int cand = 4; cand >= 2 && best.empty(); --cand) {
+      const int cap = kTmemCols - 32 * cand;
+      bool fits = true;
+      for (const auto& sg : segs) fits = fits && sg.dz * sg.n <= cap;
+      if (!fits) continue;
+      std::sort(perm.begin(), perm.end());
+      int iters = 0;
+      do {
+        std::vector<Seg> o2;
+        for (int i : perm) o2.push_back(segs[i]);
+        int cur = 0;
+        for (auto& sg : o2) {
+          const int cols = sg.dz * sg.n;
+          if (cur + cols > cap) cur = 0;
+          sg.col = cur;
+          cur += cols;
+        }
+        auto ov = [&](const Seg& a, const Seg& b) {
+          return a.col < b.col + b.dz * b.n && b.col < a.col + a.dz * a.n;
+        };
+        int score = 0;
+        const int k = static_cast<int>(o2.size());
+        for (int i = 1; i < k; ++i) score += ov(o2[i], o2[i - 1]);
+        if (k > 1) score += ov(o2[0], o2[k - 1]);
+        if (score < best_score) {
+          best_score = score;
+          best = o2;
+        }
+      } while (++iters < 5040 && std::next_permutation(perm.begin(), perm.end()));
+      if (!best.empty()) na = cand;
     }
+    if (best.empty()) throw UnsupportedError("uvw tensor-core path: z segment accumulators exceed TMEM");
+    segs = best;
   }
   const int ns = static_cast<int>(segs.size());
   auto overlap = [&](int a, int b) {
@@ -101,47 +139,69 @@ UvwSource generate_uvw_forward(const Problem& p) {
     for (int o = 0; o < ns; ++o)
       if (overlap(s, o)) (o < s ? wait_cur[s] : wait_prev[s]) |= 1u << o;
 
-  // ---- units: (instruction, 32-channel block) in segment order
+  // ---- units: (instruction, 16-channel block) in segment order
   struct U {
-    int ins, cb, seg, dz, n;
+    int ins, cb, seg, dz, n, dx;
     bool first, last;
     std::size_t wimg;
   };
   std::vector<U> units;
-  int max_n = 16;
+  int max_n = 16, max_dx = 1;
   for (const auto& s : segs) max_n = std::max(max_n, s.n);
-  const int wslot = 2 * max_n * 128;  // hi + lo, N rows x 32 fp32
+  for (const auto& s : R) max_dx = std::max(max_dx, s.dx());
+  const int wslot = 2 * max_n * kCh * 4;                           // hi + lo images, N rows x 16 fp32
+  const int xslot = (kTileRows * kCh * max_dx * 4 + 1023) / 1024 * 1024;  // 128 rows x 16 channels x dx
   std::size_t wimg = 0;
   std::vector<std::size_t> wimg_of(np, 0);
   for (int q = 0; q < np; ++q) {
     wimg_of[q] = wimg;
-    wimg += static_cast<std::size_t>(R[q].bp / 32) * wslot;
+    wimg += static_cast<std::size_t>(R[q].bp / kCh) * wslot;
   }
   for (int si = 0; si < ns; ++si) {
     const auto& s = segs[si];
     for (size_t t = 0; t < s.ins.size(); ++t) {
       const int q = s.ins[t];
-      const int nb = R[q].bp / 32;
+      const int nb = R[q].bp / kCh;
       for (int cb = 0; cb < nb; ++cb)
-        units.push_back({q, cb, si, s.dz, s.n, t == 0 && cb == 0, t + 1 == s.ins.size() && cb + 1 == nb,
+        units.push_back({q, cb, si, s.dz, s.n, R[q].dx(), t == 0 && cb == 0, t + 1 == s.ins.size() && cb + 1 == nb,
                          wimg_of[q] + static_cast<std::size_t>(cb) * wslot});
     }
   }
   const int nu = static_cast<int>(units.size());
-  const int a_slots = std::min(6, (227 * 1024 - 3 * wslot - 1536) / kASlotBytes);
-  if (a_slots < 2) throw UnsupportedError("uvw tensor-core path: shared memory too small");
-  const int smem = 1024 /*align*/ + a_slots * kASlotBytes + 3 * wslot + 512 /*barriers*/;
+  // producer warps (2 or 4 per SM sub-partition; thread = (row, 16 * 4 / pw
+  // channels)) and x-tile ring depth; env overrides for A/B runs.
+  const int pw = std::getenv("CGF_UVW_PW") ? std::atoi(std::getenv("CGF_UVW_PW")) : kProdWarps;
+  const int nx = std::getenv("CGF_UVW_NX") ? std::atoi(std::getenv("CGF_UVW_NX")) : 3;
+  if (pw != 8 && pw != 16) throw UnsupportedError("CGF_UVW_PW must be 8 or 16");
+  const int cpt = kCh * 4 / pw;  // channels per producer thread
+  const int nwr = std::getenv("CGF_UVW_NW") ? std::atoi(std::getenv("CGF_UVW_NW")) : 6;  // W ring depth
+  // warps: producers | MMA | 4 epilogue | W loader | x loader
+  const int mma_warp = pw, wload_warp = pw + 5, xload_warp = pw + 6, nwarps = pw + 7;
+  const int smem = 1024 /*align*/ + nx * xslot + nwr * wslot + 1024 /*barriers*/;
+  if (smem > 227 * 1024) throw UnsupportedError("uvw tensor-core path: shared memory too small");
+  const int acol0 = kTmemCols - 32 * na;  // A ring columns [acol0, 512)
 
   std::ostringstream o;
   if (std::getenv("CGF_UVW_DEBUG")) o << "#define CGF_UVW_DEBUG 1\n";
+  if (std::getenv("CGF_UVW_PROF")) o << "#define CGF_UVW_PROF 1\n";
   o << device_runtime_source();
   o << R"(
-// ---- tcgen05 / TMEM helpers (sm_100a) ----
+// ---- tcgen05 / TMEM / TMA helpers (sm_100a) ----
+struct __align__(64) TMap { unsigned long long v[16]; };  // CUtensorMap
+DEVI u64 gtimer() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
 // Bounded wait: a barrier that never completes traps after ~4 s with its tag
 // instead of hanging the device.
-DEVI u64 gtimer() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
+#ifdef CGF_UVW_PROF
+__shared__ unsigned long long prof_s[16];
+#endif
 DEVI void mbar_wait_t(u64* b, u32 parity, int tag) {
   if (mbar_try(b, parity)) return;
+#ifdef CGF_UVW_PROF
+  const long long c0 = clock64();
+  while (!mbar_try(b, parity)) { }
+  if ((threadIdx.x & 31) == 0) atomicAdd(&prof_s[tag], (unsigned long long)(clock64() - c0));
+  return;
+#endif
   const u64 t0 = gtimer();
   for (u32 it = 1;; ++it) {
     if (mbar_try(b, parity)) return;
@@ -172,70 +232,107 @@ DEVI void tc_ld8(u32 taddr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 DEVI void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups
-// 1024 B apart (SBO), version 1 (sm_100).
-DEVI u64 sdesc(u32 saddr) {
-  return (u64)((saddr & 0x3FFFFu) >> 4) | ((u64)1 << 16) | ((u64)(1024 >> 4) << 32) | ((u64)1 << 46) | ((u64)2 << 61);
+DEVI void tc_st8(u32 taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                  "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                  "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])) : "memory");
+}
+DEVI void tc_st4(u32 taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+               :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                  "r"(__float_as_uint(v[3])) : "memory");
+}
+DEVI u32 elect_one() {
+  u32 p;
+  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n selp.u32 %0, 1, 0, e;\n}" : "=r"(p));
+  return p;
+}
+DEVI void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// D[tmem] (+)= A[tmem] * B[smem]^T (A: 128 lanes x 8 tf32 columns)
+DEVI void tc_mma_ts(u32 d, u32 a, u64 b, u32 idesc, u32 acc) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}"
+               :: "r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+// 3-D TMA tile load global -> shared, completion on an mbarrier (bytes).
+DEVI void tma_load3(void* dst, const TMap* map, int c0, int c1, int c2, u64* bar) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+               :: "r"(smem_addr(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)) : "memory");
+}
+// Shared-memory matrix descriptor: K-major, 64-byte swizzle (rows of 16 fp32),
+// 8-row groups 512 B apart (SBO), version 1 (sm_100).
+DEVI u64 sdesc64(u32 saddr) {
+  return (u64)((saddr & 0x3FFFFu) >> 4) | ((u64)1 << 16) | ((u64)(512 >> 4) << 32) | ((u64)1 << 46) | ((u64)4 << 61);
 }
 // Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M = 128, N.
 DEVI constexpr u32 idesc_tf32(int n) { return (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(n >> 3) << 17) | ((u32)(128 >> 4) << 24); }
 // tf32 split: hi keeps the top 19 bits (exactly representable), lo the rest.
 DEVI float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
-// Byte offset of element (m, c) of a 128 x 32 fp32 K-major SW128 tile.
-DEVI u32 sw128(int m, int chunk) { return (u32)((m >> 3) * 1024 + (m & 7) * 128 + ((chunk ^ (m & 7)) << 4)); }
+// Byte offset of 16-byte chunk `chunk` of row m in a K-major SW64 tile (64 B rows).
+DEVI u32 sw64(int m, int chunk) { return (u32)((m >> 3) * 512 + (m & 7) * 64 + ((chunk ^ ((m >> 1) & 3)) << 4)); }
 )";
   o << "\n// uvw forward: x = " << p.x_ir.str() << " | y = " << p.y_ir.str() << " | z = " << p.z_ir.str() << "\n";
-  o << "// " << np << " instructions, " << ns << " z segments, " << nu << " units / 128-row tile, " << a_slots
-    << " A slots\n";
-  o << "#define DIMX " << p.dim_x << "\n#define DIMY " << p.dim_y << "\n#define DIMZ " << p.dim_z << "\n#define NW_ "
-    << p.n_w << "\n#define NS " << a_slots << "\n#define WSLOT " << wslot << "\n#define NSEG " << ns << "\n";
+  o << "// " << np << " instructions, " << ns << " z segments, " << nu << " units / 128-row tile, " << na
+    << " TMEM A blocks\n";
+  o << "#define DIMX " << p.dim_x << "\n#define DIMY " << p.dim_y << "\n#define DIMZ " << p.dim_z << "\n#define NS "
+    << na << "\n#define ACOL0 " << acol0 << "\n#define NX " << nx << "\n#define NWR " << nwr << "\n#define WSLOT " << wslot << "\n#define XSLOT " << xslot << "\n#define NSEG " << ns
+    << "\n";
 
-  // ---- prep kernel: shared W -> per-(instruction, channel block) images
+  // ---- prep kernel: shared W -> per-(instruction, 16-channel block) images
   o << "extern \"C\" __global__ void cgf_uvw_prep_f32(const float* __restrict__ W, float* __restrict__ img) {\n"
        "  const int t = blockIdx.x * blockDim.x + threadIdx.x;\n  int e = t;\n";
   for (int q = 0; q < np; ++q) {
     const auto& s = R[q];
     const int cnt = s.b * s.bp;
-    o << "  if (e < " << cnt << ") { const int r = e / " << s.bp << ", c = e % " << s.bp << ", cb = c >> 5, cl = c & 31;\n"
+    o << "  if (e < " << cnt << ") { const int r = e / " << s.bp << ", c = e % " << s.bp << ", cb = c >> 4, cl = c & 15;\n"
       << "    const float v = W[" << s.w_off << " + r * " << s.w_stride << " + c]; const float h = tf32_hi(v);\n"
       << "    char* base = (char*)img + " << wimg_of[q] << " + (size_t)cb * WSLOT;\n"
-      << "    const u32 off = (u32)((r >> 3) * 1024 + (r & 7) * 128 + (((cl >> 2) ^ (r & 7)) << 4) + (cl & 3) * 4);\n"
-      << "    *(float*)(base + off) = h; *(float*)(base + " << s.b * 128 << " + off) = v - h; return; }\n"
+      << "    const u32 off = sw64(r, cl >> 2) + (cl & 3) * 4;\n"
+      << "    *(float*)(base + off) = h; *(float*)(base + " << s.b * kCh * 4 << " + off) = v - h; return; }\n"
       << "  e -= " << cnt << ";\n";
   }
   o << "}\n\n";
 
-  // ---- producer: one function per instruction (CG coefficients as immediates)
+  // ---- producer: one function per instruction (CG coefficients as immediates).
+  // Thread (row m, sub) owns channels [8 sub, 8 sub + 8) of the unit's 16.
   for (int q = 0; q < np; ++q) {
     const auto& s = R[q];
     const int dx = s.dx(), dz = s.dz();
     o << "// instruction " << q << ": l=(" << s.l1 << "," << s.l2 << "," << s.l3 << ") b=" << s.b << " b'=" << s.bp
       << " nnz=" << s.cg->entries.size() << "\n";
-    o << "DEVI void produce_" << q << "(const float* __restrict__ xr, const float* yv, bool valid, int m, int sub,"
-         " unsigned char* abase, u64* afull, u64* aempty, u32& seq) {\n";
+    o << "DEVI void produce_" << q << "(const unsigned char* xs, const float* yv, int m, int sub,"
+         " u32 tq, u64* afull, u64* aempty, u64* xempty, u32& slot, u32& ph) {\n";
+    // x: cpt channels x dx floats = cpt * dx / 4 float4 chunks of the staged SW64 tile
+    const int nch = cpt * dx / 4;
+    o << "  float xv[" << cpt * dx << "];\n#pragma unroll\n  for (int t = 0; t < " << nch
+      << "; ++t) {\n    const int g = " << nch << " * sub + t, L = m * " << dx
+      << " + (g >> 2), j = g & 3;\n    const float4 v = *(const float4*)(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4));\n"
+         "    xv[4 * t] = v.x; xv[4 * t + 1] = v.y; xv[4 * t + 2] = v.z; xv[4 * t + 3] = v.w;\n  }\n"
+         // generic-proxy reads of the slot must be ordered before the next
+         // TMA (async proxy) write into it: without this fence the refill
+         // raced the reads (measured: corrupted rows).
+         "  fence_proxy_async();\n"
+         "  __syncwarp();\n  if ((threadIdx.x & 31) == 0) mbar_arrive(xempty);\n";
     o << "  float q[" << dz << "][" << dx << "];\n#pragma unroll\n  for (int k = 0; k < " << dz
       << "; ++k)\n#pragma unroll\n    for (int i = 0; i < " << dx << "; ++i) q[k][i] = 0.f;\n";
     for (const auto& e : s.cg->entries)
       o << "  q[" << e.k << "][" << e.i << "] = fmaf((float)" << hexd(e.v) << ", yv[" << s.y_off + e.j << "], q[" << e.k
         << "][" << e.i << "]);\n";
-    o << "  float xv[" << 16 * dx << "];\n"
-      << "  if (valid) {\n#pragma unroll\n    for (int t = 0; t < " << 4 * dx
-      << "; ++t) { const float4 v = __ldg((const float4*)xr + t); xv[4*t] = v.x; xv[4*t+1] = v.y; xv[4*t+2] = v.z; xv[4*t+3] = v.w; }\n"
-      << "  } else {\n#pragma unroll\n    for (int t = 0; t < " << 16 * dx << "; ++t) xv[t] = 0.f;\n  }\n";
+    // A block k -> TMEM columns [ACOL0 + 32 slot, +32): hi in the first 16, lo in
+    // the next 16; this thread's row is its TMEM lane, its channels its columns.
     o << "#pragma unroll\n  for (int k = 0; k < " << dz << "; ++k) {\n"
-      << "    const u32 slot = seq % NS, ph = (seq / NS) & 1u;\n"
       << "    mbar_wait_t(&aempty[slot], ph ^ 1u, 1);\n"
-      << "    unsigned char* hi = abase + slot * " << kASlotBytes << "; unsigned char* lo = hi + " << kASlotBytes / 2 << ";\n"
-      << "#pragma unroll\n    for (int g = 0; g < 4; ++g) {\n"
-      << "      float h[4], l[4];\n#pragma unroll\n      for (int cc = 0; cc < 4; ++cc) {\n"
-      << "        const int c = 4 * g + cc; float z = 0.f;\n#pragma unroll\n        for (int i = 0; i < " << dx
+      << "    tc_fence_after();\n"
+      << "    float h[" << cpt << "], l[" << cpt << "];\n"
+      << "#pragma unroll\n    for (int c = 0; c < " << cpt << "; ++c) {\n"
+      << "      float z = 0.f;\n#pragma unroll\n      for (int i = 0; i < " << dx
       << "; ++i) z = fmaf(q[k][i], xv[c * " << dx << " + i], z);\n"
-      << "        h[cc] = tf32_hi(z); l[cc] = z - h[cc];\n      }\n"
-      << "      const u32 off = sw128(m, 4 * sub + g);\n"
-      << "      *(float4*)(hi + off) = make_float4(h[0], h[1], h[2], h[3]);\n"
-      << "      *(float4*)(lo + off) = make_float4(l[0], l[1], l[2], l[3]);\n    }\n"
-      << "    fence_proxy_async();\n    __syncwarp();\n    if ((threadIdx.x & 31) == 0) mbar_arrive(&afull[slot]);\n"
-      << "    ++seq;\n  }\n}\n\n";
+      << "      h[c] = tf32_hi(z); l[c] = z - h[c];\n    }\n"
+      << "    const u32 ta = tq + ACOL0 + 32 * slot + " << cpt << " * sub;\n"
+      << "    tc_st" << cpt << "(ta, h); tc_st" << cpt << "(ta + 16, l);\n"
+      << "    tc_wait_st();\n    tc_fence_before();\n"
+      << "    __syncwarp();\n    if ((threadIdx.x & 31) == 0) mbar_arrive(&afull[slot]);\n"
+      << "    if (++slot == NS) { slot = 0; ph ^= 1u; }\n  }\n}\n\n";
   }
 
   // ---- unit / segment tables
@@ -246,8 +343,9 @@ DEVI u32 sw128(int m, int chunk) { return (u32)((m >> 3) * 1024 + (m & 7) * 128 
     o << "};\n";
   };
   {
-    std::vector<long long> udz, ucol, un, ufirst, ulast, useg, uw;
+    std::vector<long long> udz, ucol, un, ufirst, ulast, useg, uw, udx, uxc, uins;
     for (const auto& u : units) {
+      uins.push_back(u.ins);
       udz.push_back(u.dz);
       ucol.push_back(segs[u.seg].col);
       un.push_back(u.n);
@@ -255,6 +353,8 @@ DEVI u32 sw128(int m, int chunk) { return (u32)((m >> 3) * 1024 + (m & 7) * 128 
       ulast.push_back(u.last);
       useg.push_back(u.seg);
       uw.push_back(static_cast<long long>(u.wimg));
+      udx.push_back(u.dx);
+      uxc.push_back((R[u.ins].x_off + static_cast<long long>(u.cb) * kCh * u.dx) / kCh);  // TMA coordinate 1
     }
     arr("U_DZ", udz);
     arr("U_COL", ucol);
@@ -263,97 +363,93 @@ DEVI u32 sw128(int m, int chunk) { return (u32)((m >> 3) * 1024 + (m & 7) * 128 
     arr("U_LAST", ulast);
     arr("U_SEG", useg);
     arr("U_WIMG", uw);
-    std::vector<long long> sz, sdz, sn, scol, swc, swp;
+    arr("U_DX", udx);
+    arr("U_XC", uxc);
+    arr("U_INS", uins);
+    std::vector<long long> swc, swp;
     for (int si = 0; si < ns; ++si) {
-      sz.push_back(segs[si].z_off);
-      sdz.push_back(segs[si].dz);
-      sn.push_back(segs[si].n);
-      scol.push_back(segs[si].col);
       swc.push_back(wait_cur[si]);
       swp.push_back(wait_prev[si]);
     }
-    arr("S_ZOFF", sz);
-    arr("S_DZ", sdz);
-    arr("S_N", sn);
-    arr("S_COL", scol);
     arr("S_WAITCUR", swc);
     arr("S_WAITPREV", swp);
   }
   o << "#define NU " << nu << "\n\n";
 
   // ---- the main kernel
-  o << "extern \"C\" __global__ void __launch_bounds__(" << kWarps * 32 << ", 1) cgf_uvw_fwd_f32("
-       "const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ WIMG, "
-       "const float* __restrict__ GZ, const float* __restrict__ DA, const float* __restrict__ DB, "
-       "const float* __restrict__ DC, float* __restrict__ Z, float* __restrict__ O1, float* __restrict__ O2, "
-       "float* __restrict__ O3, i64 rows, const i64* __restrict__ RP, const int* __restrict__ NB, "
-       "const int* __restrict__ EID, i64 edges_tot) {\n"
+  o << "extern \"C\" __global__ void __launch_bounds__(" << nwarps * 32 << ", 1) cgf_uvw_fwd_f32("
+       "const __grid_constant__ TMap tx1, const __grid_constant__ TMap tx3, const __grid_constant__ TMap tx5, "
+       "const __grid_constant__ TMap tx7, const float* __restrict__ Y, const float* __restrict__ WIMG, "
+       "float* __restrict__ Z, i64 rows, unsigned long long* __restrict__ prof) {\n"
+       "#ifdef CGF_UVW_PROF\n  if (threadIdx.x < 16) prof_s[threadIdx.x] = 0;\n  const long long kc0 = clock64();\n#endif\n"
        "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n"
        "  unsigned char* sm = (unsigned char*)(((unsigned long long)smem_raw + 1023) & ~1023ull);\n"
-       "  unsigned char* abase = sm;\n"
-       "  unsigned char* wbase = sm + NS * "
-    << kASlotBytes << ";\n"
-       "  u64* bars = (u64*)(wbase + 3 * WSLOT);\n"
-       "  u64* afull = bars; u64* aempty = afull + NS; u64* wfull = aempty + NS; u64* wempty = wfull + 3;\n"
-       "  u64* sfull = wempty + 3; u64* sdrained = sfull + NSEG;\n"
+       "  unsigned char* xbase = sm;\n"
+       "  unsigned char* wbase = xbase + NX * XSLOT;\n"
+       "  u64* bars = (u64*)(wbase + NWR * WSLOT);\n"
+       "  u64* afull = bars; u64* aempty = afull + NS; u64* wfull = aempty + NS; u64* wempty = wfull + NWR;\n"
+       "  u64* xfull = wempty + NWR; u64* xempty = xfull + NX;\n"
+       "  u64* sfull = xempty + NX; u64* sdrained = sfull + NSEG;\n"
        "  u32* tmem_slot = (u32*)(sdrained + NSEG);\n"
        "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n"
        "  const i64 ntiles = (rows + 127) / 128;\n"
+       "  const i64 my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;\n"
        "  if (threadIdx.x == 0) {\n"
        "    for (int i = 0; i < NS; ++i) { mbar_init(&afull[i], "
-    << kProdWarps
+    << pw
     << "); mbar_init(&aempty[i], 1); }\n"
-       "    for (int i = 0; i < 3; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }\n"
+       "    for (int i = 0; i < NWR; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }\n"
+       "    for (int i = 0; i < NX; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], "
+    << pw
+    << "); }\n"
        "    for (int i = 0; i < NSEG; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sdrained[i], 4); }\n"
        "    mbar_fence_init();\n  }\n"
        "  if (warp == "
-    << kMmaWarp
+    << mma_warp
     << ") {\n"
        "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" :: \"r\"(smem_addr(tmem_slot)));\n"
        "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\");\n"
        "  }\n"
        "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n"
-       "  const u32 tmem = *tmem_slot;\n\n";
+       "  const u32 tmem = 0;  // all 512 columns are ours: the allocation starts at lane 0, column 0\n"
+       "  if (threadIdx.x == 0 && *tmem_slot != 0) { printf(\"cgf_uvw: unexpected TMEM base %u\\n\", *tmem_slot); __trap(); }\n\n";
 
   // producers
-  o << "  if (warp < " << kProdWarps
+  o << "  if (warp < " << pw
     << ") {\n"
        "    const int m = 32 * (warp & 3) + lane, sub = warp >> 2;\n"
-       "    u32 seq = 0;\n"
+       "    const u32 tq = tmem + ((u32)(32 * (warp & 3)) << 16);\n"
+       "    u32 slot = 0, ph = 0, gx = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
        "      const i64 row = tile * 128 + m;\n"
        "      const bool valid = row < rows;\n"
-       "      { const i64 nrow = row + (i64)gridDim.x * 128;  // warm L2 with the next tile's x row\n"
-       "        if (nrow < rows) { const char* px = (const char*)(X + nrow * DIMX);\n"
-       "          for (int b = sub * 128; b < DIMX * 4; b += 256) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(px + b)); } }\n"
        "      float yv[DIMY];\n"
-       "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) yv[j] = valid ? __ldg(Y + row * DIMY + j) : 0.f;\n"
-       "      const float* xrow = X + (valid ? row : 0) * DIMX;\n";
-  for (const auto& u : units) {
-    const auto& s = R[u.ins];
-    const long long c0 = static_cast<long long>(u.cb) * 32;
-    o << "      produce_" << u.ins << "(xrow + " << s.x_off << " + (" << c0 << " + 16 * sub) * " << s.dx()
-      << ", yv, valid, m, sub, abase, afull, aempty, seq);\n";
-  }
+       "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) yv[j] = valid ? __ldg(Y + row * DIMY + j) : 0.f;\n";
+  // runtime unit loop, one switch arm per instruction: the body stays
+  // instruction-cache resident (the unrolled unit sequence was i-cache bound)
+  o << "#pragma unroll 1\n      for (int u = 0; u < NU; ++u) {\n"
+       "        const u32 xs_ = gx % NX; mbar_wait_t(&xfull[xs_], (gx / NX) & 1u, 8); ++gx;\n"
+       "        const unsigned char* xsl = xbase + xs_ * XSLOT;\n"
+       "        switch (U_INS[u]) {\n";
+  for (int q = 0; q < np; ++q)
+    o << "          case " << q << ": produce_" << q << "(xsl, yv, m, sub, tq, afull, aempty, &xempty[xs_], slot, ph); break;\n";
+  o << "        }\n      }\n";
   o << "    }\n  }\n";
 
   // MMA issuer
-  o << "  else if (warp == " << kMmaWarp
+  o << "  else if (warp == " << mma_warp
     << ") {\n"
-       "    if (lane == 0) {\n"
-       "      u32 seq = 0, gu = 0; i64 lt = 0;\n"
-       "      const i64 my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;\n"
-       "      const i64 total_units = my_tiles * NU;\n"
-       "      auto load_w = [&](u32 g) {  // W ring of 3, loaded two units ahead\n"
-       "        const int u = (int)(g % NU); const u32 sl = g % 3u;\n"
-       "        if (g >= 3) mbar_wait_t(&wempty[sl], (g / 3u - 1u) & 1u, 2);\n"
-       "        mbar_expect_tx(&wfull[sl], WSLOT);\n"
-       "        bulk_g2s(wbase + sl * WSLOT, (const char*)WIMG + U_WIMG[u], WSLOT, &wfull[sl]);\n"
-       "      };\n"
-       "      if (total_units > 0) load_w(0);\n"
-       "      if (total_units > 1) load_w(1);\n"
+       // The whole warp walks the schedule (so every loop value is warp-uniform
+       // and lives in uniform registers) and one elected lane issues each
+       // tcgen05.mma / commit. TMEM addresses are compile-time: the kernel owns
+       // all 512 columns, so the allocation base is column 0 (checked below).
+       // The naive lane-0 loop with per-MMA descriptor rebuilds measured
+       // ~150 cycles per MMA (tools/tc_bench.cu); this form is tensor-bound.
+       "    {\n"
+       "      const u64 wd0 = sdesc64(smem_addr(wbase));\n"
+       "      u32 slot = 0, ph = 0, wsl = 0, wph = 0; i64 lt = 0;\n"
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {\n"
-       "        for (int u = 0; u < NU; ++u, ++gu) {\n"
+       "        for (int u = 0; u < NU; ++u) {\n"
        "          if (U_FIRST[u]) {\n"
        "            const int s = U_SEG[u];\n"
        "            for (int o = 0; o < NSEG; ++o) {\n"
@@ -362,41 +458,72 @@ DEVI u32 sw128(int m, int chunk) { return (u32)((m >> 3) * 1024 + (m & 7) * 128 
        "            }\n"
        "            tc_fence_after();\n"
        "          }\n"
-       "          const u32 wsl = gu % 3u;\n"
-       "          mbar_wait_t(&wfull[wsl], (gu / 3u) & 1u, 5);\n"
+       "          mbar_wait_t(&wfull[wsl], wph, 5);\n"
        "          tc_fence_after();\n"
-       "          const u32 wad = smem_addr(wbase + wsl * WSLOT);\n"
        "          const int n = U_N[u];\n"
-       "          const u32 idesc = idesc_tf32(n);\n"
+       "          const u32 idesc = idesc_tf32(n), first = U_FIRST[u];\n"
+       "          const u64 bh = wd0 + (u64)(wsl * (WSLOT >> 4)), bl = bh + (u64)((n * 64) >> 4);\n"
+       "          const u32 dbase = (u32)U_COL[u];\n"
        "          for (int k = 0; k < U_DZ[u]; ++k) {\n"
-       "            const u32 slot = seq % NS, ph = (seq / NS) & 1u;\n"
        "            mbar_wait_t(&afull[slot], ph, 6);\n"
        "            tc_fence_after();\n"
-       "            const u32 aad = smem_addr(abase + slot * "
-    << kASlotBytes
-    << ");\n"
-       "            const u32 d = tmem + (u32)(U_COL[u] + k * n);\n"
-       "#pragma unroll\n"
-       "            for (int ps = 0; ps < 3; ++ps) {  // 3xTF32: hi*hi + hi*lo + lo*hi\n"
-       "              const u32 ao = ps == 2 ? "
-    << kASlotBytes / 2
-    << "u : 0u, bo = ps == 1 ? (u32)(n * 128) : 0u;\n"
-       "#pragma unroll\n"
-       "              for (int ks = 0; ks < 4; ++ks)\n"
-       "                tc_mma(d, sdesc(aad + ao + ks * 32), sdesc(wad + bo + ks * 32), idesc,\n"
-       "                       (U_FIRST[u] && ps == 0 && ks == 0) ? 0u : 1u);\n"
+       "            const u32 ah = ACOL0 + 32 * slot, al = ah + 16;\n"
+       "            const u32 d = dbase + (u32)(k * n);\n"
+       "            if (elect_one()) {\n"
+       // 3xTF32: hi*hi + hi*lo + lo*hi, two K=8 steps (A: +8 columns, B: +32 B) each
+       "              tc_mma_ts(d, ah, bh, idesc, first ? 0u : 1u);\n"
+       "              tc_mma_ts(d, ah + 8, bh + 2, idesc, 1u);\n"
+       "              tc_mma_ts(d, ah, bl, idesc, 1u);\n"
+       "              tc_mma_ts(d, ah + 8, bl + 2, idesc, 1u);\n"
+       "              tc_mma_ts(d, al, bh, idesc, 1u);\n"
+       "              tc_mma_ts(d, al + 8, bh + 2, idesc, 1u);\n"
+       "              tc_commit(&aempty[slot]);\n"
        "            }\n"
-       "            tc_commit(&aempty[slot]);\n"
-       "            ++seq;\n"
+       "            __syncwarp();\n"
+       "            if (++slot == NS) { slot = 0; ph ^= 1u; }\n"
        "          }\n"
-       "          tc_commit(&wempty[wsl]);\n"
-       "#ifdef CGF_UVW_DEBUG\n"
-       "          if (gu == 0) { mbar_wait_t(&aempty[0], 0, 9); printf(\"cgf_uvw dbg: unit 0 aempty[0] done\\n\");\n"
-       "            mbar_wait_t(&aempty[4], 0, 10); printf(\"cgf_uvw dbg: unit 0 aempty[4] done\\n\");\n"
-       "            mbar_wait_t(&wempty[0], 0, 11); printf(\"cgf_uvw dbg: unit 0 wempty[0] done\\n\"); }\n"
-       "#endif\n"
-       "          if (U_LAST[u]) tc_commit(&sfull[U_SEG[u]]);\n"
-       "          if (gu + 2 < total_units) load_w(gu + 2);  // waits for unit gu-1 only\n"
+       "          if (elect_one()) {\n"
+       "            tc_commit(&wempty[wsl]);\n"
+       "            if (U_LAST[u]) tc_commit(&sfull[U_SEG[u]]);\n"
+       "          }\n"
+       "          __syncwarp();\n"
+       "          if (++wsl == NWR) { wsl = 0; wph ^= 1u; }\n"
+       "        }\n"
+       "      }\n"
+       "    }\n"
+       "  }\n";
+
+  // TMA loaders, one warp each so neither ring's wait blocks the other:
+  // W images (ring of NWR, 1-D bulk copies) and x tiles (ring of NX, 3-D
+  // tensor copies), both in unit order.
+  o << "  else if (warp == " << wload_warp
+    << ") {\n"
+       "    if (lane == 0) {\n"
+       "      u32 gu = 0;\n"
+       "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
+       "        for (int u = 0; u < NU; ++u, ++gu) {\n"
+       "          const u32 ws = gu % NWR;\n"
+       "          mbar_wait_t(&wempty[ws], ((gu / NWR) & 1u) ^ 1u, 2);\n"
+       "          mbar_expect_tx(&wfull[ws], WSLOT);\n"
+       "          bulk_g2s(wbase + ws * WSLOT, (const char*)WIMG + U_WIMG[u], WSLOT, &wfull[ws]);\n"
+       "        }\n"
+       "      }\n"
+       "    }\n"
+       "    __syncwarp();\n"
+       "  }\n"
+       "  else if (warp == "
+    << xload_warp
+    << ") {\n"
+       "    if (lane == 0) {\n"
+       "      u32 gu = 0;\n"
+       "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
+       "        for (int u = 0; u < NU; ++u, ++gu) {\n"
+       "          const u32 xs = gu % NX;\n"
+       "          mbar_wait_t(&xempty[xs], ((gu / NX) & 1u) ^ 1u, 12);\n"
+       "          const int dx = U_DX[u];\n"
+       "          mbar_expect_tx(&xfull[xs], 128 * 64 * dx);\n"
+       "          const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
+       "          tma_load3(xbase + xs * XSLOT, mp, 0, U_XC[u], (int)(tile * 128), &xfull[xs]);\n"
        "        }\n"
        "      }\n"
        "    }\n"
@@ -434,20 +561,22 @@ DEVI u32 sw128(int m, int chunk) { return (u32)((m >> 3) * 1024 + (m & 7) * 128 
       << "        if (lane == 0) mbar_arrive(&sdrained[" << si << "]);\n      }\n";
   }
   o << "    }\n  }\n";
-  o <<        "  tc_fence_before();\n"
+  o << "  tc_fence_before();\n"
        "  __syncthreads();\n"
+       "#ifdef CGF_UVW_PROF\n  if (threadIdx.x < 16) atomicAdd(&prof[threadIdx.x], prof_s[threadIdx.x]);\n"
+       "  if (threadIdx.x == 0) atomicAdd(&prof[15], (unsigned long long)(clock64() - kc0));\n#endif\n"
        "  if (warp == "
-    << kMmaWarp
+    << mma_warp
     << ") {\n"
        "    tc_fence_after();\n"
-       "    asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\" :: \"r\"(tmem));\n"
+       "    asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\" :: \"r\"(*tmem_slot));\n"
        "  }\n"
        "}\n";
 
   UvwSource out;
   out.main.name = "cgf_uvw_fwd_f32";
   out.main.source = o.str();
-  out.main.threads = kWarps * 32;
+  out.main.threads = nwarps * 32;
   out.main.smem_bytes = smem;
   out.main.units = nu;
   out.prep = out.main;
@@ -456,6 +585,7 @@ DEVI u32 sw128(int m, int chunk) { return (u32)((m >> 3) * 1024 + (m & 7) * 128 
   out.prep.smem_bytes = 0;
   out.main.module = out.prep.module = "cgf_uvw_fwd_f32";
   out.wimg_bytes = wimg;
+  out.dims_x = p.dim_x;
   return out;
 }
 

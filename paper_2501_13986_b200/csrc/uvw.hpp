@@ -21,7 +21,7 @@
 namespace cgf {
 
 // True when every instruction is kind C with b % 16 == 0, b <= 256,
-// b' % 32 == 0 and each z segment's accumulator (dz * b columns) fits TMEM.
+// b' % 16 == 0, 16-aligned x segments and each z segment's accumulator (dz * b columns) fits TMEM.
 bool uvw_eligible(const Problem& p, std::string* why = nullptr);
 
 struct UvwSource {
@@ -29,6 +29,7 @@ struct UvwSource {
   KernelSource prep;      // cgf_uvw_prep_f32: W -> swizzled hi / lo tf32 images
   std::size_t wimg_bytes = 0;
   int tile_rows = 128;
+  int dims_x = 0;
 };
 
 UvwSource generate_uvw_forward(const Problem& p);

@@ -24,3 +24,18 @@ torch.cuda.synchronize()
 err = ((z - ref).norm() / ref.norm()).item()
 print("rows", rows, "rel err vs SIMT", err, flush=True)
 print("z[0,:8]", z[0, :8].tolist(), "\nref", ref[0, :8].tolist())
+d = (z - ref).abs()
+rowerr = d.max(dim=1).values / ref.abs().max()
+bad_rows = torch.nonzero(rowerr > 1e-4).flatten()
+print("bad rows:", bad_rows.numel(), "of", rows, "first:", bad_rows[:140].tolist())
+if rows >= 128:
+    m = torch.arange(rows, device=z.device) % 128
+    per_m = torch.zeros(128, device=z.device).index_reduce_(0, m, rowerr, "amax")
+    print("bad m (row % 128):", torch.nonzero(per_m > 1e-4).flatten().tolist())
+colerr = d.max(dim=0).values / ref.abs().max()
+bc = torch.nonzero(colerr > 1e-4).flatten().tolist()
+print("bad cols:", len(bc), "segments (0-63 | 64-255 | 256-575):", sum(c < 64 for c in bc), sum(64 <= c < 256 for c in bc), sum(c >= 256 for c in bc))
+if bad_rows.numel():
+    r0 = bad_rows[0].item()
+    e = (d[r0] / ref.abs().max()).tolist()
+    print("row", r0, "err by col group of 8:", [round(max(e[i:i+8]), 4) for i in range(0, len(e), 8)])
