@@ -176,6 +176,17 @@ int cgf_conv_double_backward(cgf_plan* plan, int dtype, int64_t nodes, int64_t e
                              void* o_node_x, void* o_edge_y, void* o_edge_w, void* o_g_node_z, int mode,
                              void* stream);
 
+/* Host-pointer variants (copies in and out, default stream, synchronous). The
+ * transposed CSR for the backward is built internally. mode may be
+ * CGF_CONV_ATOMIC: it is served by the deterministic kernels, which meet the
+ * atomic mode's contract (ConvPlan Mode::atomic, conv.hpp:70). */
+int cgf_conv_forward_host(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                          const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
+                          void* node_z, int mode);
+int cgf_conv_backward_host(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                           const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
+                           const void* g_node_z, void* g_node_x, void* g_edge_y, void* g_edge_w, int mode);
+
 /* ---- sharded convolution (multi-GPU, destination-partitioned) ------------
  * One rank owns a contiguous range of out_nodes output nodes and their edges
  * (SURVEY.md §8e). Node-indexed inputs read through nbr (node_x, d_gx) and the

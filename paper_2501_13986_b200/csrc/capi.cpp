@@ -704,4 +704,74 @@ int cgf_conv_double_backward(cgf_plan* p, int dtype, int64_t nodes, int64_t edge
                                         o_edge_w, o_g_node_z, mode, stream);
 }
 
+// ---- host-pointer conv (the C++ drop-in shim's path) ---------------------
+// Copies the graph and arrays in, runs the device entry points on the
+// default stream, copies results back. Mode::atomic is served by the
+// deterministic kernels: they satisfy its contract (results within rounding
+// of the deterministic mode) and are bitwise reproducible on top.
+int cgf_conv_forward_host(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                          const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
+                          void* node_z, int mode) {
+  return guarded([&] {
+    need(p, "plan");
+    if (mode != CGF_CONV_DETERMINISTIC && mode != CGF_CONV_ATOMIC) throw std::invalid_argument("bad conv mode");
+    if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (nodes == 0) return;
+    cgf::ensure_context();
+    const auto& pr = p->problem;
+    const std::size_t V = static_cast<std::size_t>(nodes), E = static_cast<std::size_t>(edges);
+    HostCall h{dtype == CGF_F64 ? 8u : 4u, {}};
+    HostCall hi{1, {}};
+    void* drp = hi.in(row_ptr, (V + 1) * 8);
+    void* dnb = hi.in(nbr, E * 4);
+    void* dx = h.in(node_x, V * pr.dim_x);
+    void* dy = h.in(edge_y, E * pr.dim_y);
+    void* dw = h.in(edge_w, E * pr.n_w);
+    void* dz = h.out(V * pr.dim_z);
+    const int rc = cgf_conv_forward(p, dtype, nodes, edges, static_cast<const int64_t*>(drp),
+                                    static_cast<const int32_t*>(dnb), dx, dy, dw, dz, CGF_CONV_DETERMINISTIC, nullptr);
+    if (rc != CGF_OK) throw std::runtime_error(g_err);
+    CU_CHECK(cgf::drv::cuCtxSynchronize());
+    h.back(node_z, dz, V * pr.dim_z);
+  });
+}
+
+int cgf_conv_backward_host(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                           const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
+                           const void* g_node_z, void* g_node_x, void* g_edge_y, void* g_edge_w, int mode) {
+  return guarded([&] {
+    need(p, "plan");
+    if (mode != CGF_CONV_DETERMINISTIC && mode != CGF_CONV_ATOMIC) throw std::invalid_argument("bad conv mode");
+    if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (nodes == 0) return;
+    cgf::ensure_context();
+    const auto& pr = p->problem;
+    const std::size_t V = static_cast<std::size_t>(nodes), E = static_cast<std::size_t>(edges);
+    std::vector<int64_t> trp(V + 1);
+    std::vector<int32_t> tsrc(std::max<std::size_t>(E, 1)), teid(std::max<std::size_t>(E, 1));
+    int rc = cgf_conv_transpose_host(nodes, edges, row_ptr, nbr, trp.data(), tsrc.data(), teid.data());
+    if (rc != CGF_OK) throw std::invalid_argument(g_err);
+    HostCall h{dtype == CGF_F64 ? 8u : 4u, {}};
+    HostCall hi{1, {}};
+    void* dtrp = hi.in(trp.data(), (V + 1) * 8);
+    void* dts = hi.in(tsrc.data(), E * 4);
+    void* dte = hi.in(teid.data(), E * 4);
+    void* dx = h.in(node_x, V * pr.dim_x);
+    void* dy = h.in(edge_y, E * pr.dim_y);
+    void* dw = h.in(edge_w, E * pr.n_w);
+    void* dgz = h.in(g_node_z, V * pr.dim_z);
+    void* ogx = h.out(V * pr.dim_x);
+    void* ogy = h.out(E * pr.dim_y);
+    void* ogw = h.out(E * pr.n_w);
+    rc = cgf_conv_backward(p, dtype, nodes, edges, nullptr, nullptr, static_cast<const int64_t*>(dtrp),
+                           static_cast<const int32_t*>(dts), static_cast<const int32_t*>(dte), dx, dy, dw, dgz, ogx,
+                           ogy, ogw, CGF_CONV_DETERMINISTIC, nullptr);
+    if (rc != CGF_OK) throw std::runtime_error(g_err);
+    CU_CHECK(cgf::drv::cuCtxSynchronize());
+    h.back(g_node_x, ogx, V * pr.dim_x);
+    h.back(g_edge_y, ogy, E * pr.dim_y);
+    h.back(g_edge_w, ogw, E * pr.n_w);
+  });
+}
+
 }  // extern "C"
