@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--conv-n", type=int, default=58, help="lattice side of the conv leg (58 = C5); 0 = skip")
     ap.add_argument("--conv-config", default="c1", help="TP of the conv leg (C5 uses the C1 TP)")
     ap.add_argument("--conv-steps", type=int, default=5)
+    ap.add_argument("--c3-rows", type=int, default=1_000_000, help="rows of the C3 (uvw, shared W) leg; 0 = skip")
     return ap.parse_args()
 
 
@@ -248,6 +249,48 @@ def conv_leg(args, rank, world, dev, clk_index):
     }
 
 
+def c3_leg(args, rank, world, dev):
+    """C3: e3nn FullyConnectedTP-style uvw TP with one shared W (64x0e+64x1o+64x2e
+    x 0e+1o+2e, 11 kind-C paths), FP32 forward on the tcgen05 kernel
+    (3xTF32, A operand in TMEM). Per rank its own batch (replicas)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_13986_b200 as cgf
+    from oracle.oracle import config_json
+
+    plan = cgf.TpPlan(config_json("c3"))
+    R = args.c3_rows
+    g = torch.Generator(device=dev).manual_seed(99 + rank)
+    x = torch.randn((R, plan.dim_x), device=dev, generator=g)
+    y = torch.randn((R, plan.dim_y), device=dev, generator=g)
+    w = torch.randn((1, plan.n_w), device=dev, generator=g)
+    z = torch.empty((R, plan.dim_z), device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(3, args.warmup)):
+        plan.forward(x, y, w, z=z, w_shared=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, args.steps)
+    a.record(stream)
+    for _ in range(steps):
+        plan.forward(x, y, w, z=z, w_shared=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([a.elapsed_time(b) / steps], device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    byts = (plan.dim_x + plan.dim_y + plan.dim_z) * 4 * R + plan.n_w * 4
+    peak, _ = measured_peak()
+    return {"workload": "c3: 64x0e+64x1o+64x2e x 0e+1o+2e -> 64x0e+64x1o+64x2e, 11 uvw paths, shared W, fwd",
+            "kernel": "cgf_uvw_fwd_f32 (tcgen05 kind::tf32, 3xTF32, A in TMEM)", "rows_per_gpu": R,
+            "ms": ms, "rows_per_s": R * world / (ms / 1e3), "GFLOP/s": plan.flops_fwd * R * world / (ms / 1e3) / 1e9,
+            "GB/s": byts / (ms / 1e3) / 1e9, "hbm_frac": byts / (ms / 1e3) / 1e9 / peak, "dtype": "f32"}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -332,8 +375,9 @@ def main():
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
-        try:
-            traffic = json.load(open(tfile)).get(f"{CONFIG}_{args.dtype}_{dom}")
+        try:  # per-launch DRAM bytes of this kernel from one ncu --set full capture (tools/ncu_traffic.py)
+            rec = json.load(open(tfile)).get(f"{CONFIG}_{args.dtype}_{dom}")
+            traffic = None if rec is None else rec["traffic_bytes"] * R / 1_000_000
         except Exception:
             traffic = None
     roof = {"bound": "hbm", "kernel": f"cgf_tp_{'fwd' if dom == 'forward' else 'bwd'}_{args.dtype}",
@@ -380,6 +424,13 @@ def main():
 
     del x, y, w, gz, z, hx, hy, hw, hg, oz, ogx, ogy, ogw
     torch.cuda.empty_cache()
+    c3 = None
+    if args.c3_rows > 0:
+        try:
+            c3 = c3_leg(args, rank, world, dev)
+        except Exception as exc:
+            c3 = {"error": repr(exc)}
+        torch.cuda.empty_cache()
     conv = None
     if args.conv_n > 0:
         try:
@@ -409,8 +460,9 @@ def main():
             "cpu_baseline": cb,
             "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "rows_per_step": Re, "path": "pinned host -> TpPlan.forward/backward (C ABI) -> pinned host"},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 2 * args.steps,  # TP leg: one forward + one backward kernel per step
             "conv": conv,
+            "c3": c3,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
