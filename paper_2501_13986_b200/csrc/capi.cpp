@@ -30,13 +30,13 @@ struct cgf_plan {
   std::map<std::tuple<int, int, int, int, int, std::string>, std::shared_ptr<cgf::KernelSource>> sources;
   // uvw tensor-core path (all-C problems, shared W): generated source and the
   // per-context device buffer of swizzled tf32 W images.
-  std::shared_ptr<cgf::UvwSource> uvw;
-  std::map<CUcontext, CUdeviceptr> wimg;
+  std::map<std::string, std::shared_ptr<cgf::UvwSource>> uvw;  // by kernel tag
+  std::map<std::pair<CUcontext, std::string>, CUdeviceptr> wimg;
   ~cgf_plan() {
-    for (auto& [ctx, ptr] : wimg) {
+    for (auto& [key, ptr] : wimg) {
       CUcontext cur = nullptr;
       cgf::drv::cuCtxGetCurrent(&cur);
-      if (cur == ctx) cgf::drv::cuMemFree(ptr);
+      if (cur == key.first) cgf::drv::cuMemFree(ptr);
     }
   }
 };
@@ -106,8 +106,8 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
                                    aligned ? 1 : 0, flags);
   auto it = p->sources.find(key);
   if (it != p->sources.end()) return it->second;
-  if (w_shared && comp != cgf::Comp::Fwd)
-    throw cgf::UnsupportedError("shared-weight backward / double-backward needs the uvw tensor-core path");
+  if (w_shared && comp != cgf::Comp::Fwd && !(comp == cgf::Comp::Bwd && cgf::uvw_eligible(p->problem) && dtype == CGF_F32))
+    throw cgf::UnsupportedError("shared-weight backward / double-backward: only the FP32 uvw tensor-core path");
   cgf::KernelConfig cfg;
   cfg.comp = comp;
   cfg.loop = loop;
@@ -124,20 +124,32 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
 }
 
 bool use_uvw(cgf_plan* p, int op, int dtype, int w_shared) {
-  if (op != CGF_OP_FORWARD || dtype != CGF_F32 || !w_shared) return false;
+  if ((op != CGF_OP_FORWARD && op != CGF_OP_BACKWARD) || dtype != CGF_F32 || !w_shared) return false;
   const char* env = std::getenv("CGF_UVW");
   if (env && env[0] == '0') return false;
   return cgf::uvw_eligible(p->problem);
 }
 
-std::shared_ptr<cgf::UvwSource> uvw_source(cgf_plan* p) {
+std::shared_ptr<cgf::UvwSource> uvw_source(cgf_plan* p, const std::string& tag) {
   std::lock_guard<std::mutex> g(p->mu);
-  if (!p->uvw) p->uvw = std::make_shared<cgf::UvwSource>(cgf::generate_uvw_forward(p->problem));
-  return p->uvw;
+  auto& slot = p->uvw[tag];
+  if (!slot) {
+    if (tag == "fwd") slot = std::make_shared<cgf::UvwSource>(cgf::generate_uvw_forward(p->problem));
+    else if (tag == "bwdx") slot = std::make_shared<cgf::UvwSource>(cgf::generate_uvw_backward_x(p->problem));
+    else if (tag == "bwdy") slot = std::make_shared<cgf::UvwSource>(cgf::generate_uvw_backward_y(p->problem));
+    else if (tag.rfind("bwdw", 0) == 0) {
+      const int first = std::atoi(tag.c_str() + 4);
+      const int count = std::min<int>(6, static_cast<int>(p->problem.resolved.size()) - first);
+      slot = std::make_shared<cgf::UvwSource>(cgf::generate_uvw_backward_w(p->problem, first, count));
+    }
+    else throw std::logic_error("unknown uvw kernel " + tag);
+  }
+  return slot;
 }
 
 std::shared_ptr<cgf::KernelSource> source_for_op(cgf_plan* p, int op, int dtype, int w_shared, int aligned) {
-  if (use_uvw(p, op, dtype, w_shared)) return std::make_shared<cgf::KernelSource>(uvw_source(p)->main);
+  if (use_uvw(p, op, dtype, w_shared))
+    return std::make_shared<cgf::KernelSource>(uvw_source(p, op == CGF_OP_FORWARD ? "fwd" : "bwdx")->main);
   if (op < 0 || op > 2) throw std::invalid_argument("bad op");
   return source_for(p, static_cast<cgf::Comp>(op), cgf::Loop::Rows, dtype, w_shared, aligned);
 }
@@ -173,46 +185,52 @@ void run_kernel(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype, int w_sh
 
 // uvw forward on the tensor cores: W -> swizzled tf32 hi / lo images (one
 // small kernel), then the warp-specialised tcgen05 kernel over 128-row tiles.
-void run_uvw_forward(cgf_plan* p, const Args& a, void* stream) {
-  const auto us = uvw_source(p);
+// One tcgen05 uvw kernel: `in` ([rows x in_dim], TMA-staged A source: x for
+// the forward, gz for the gx backward), y, the shared W (re-imaged per call),
+// `out` ([rows x out_dim]).
+void run_uvw(cgf_plan* p, const std::string& tag, const void* in, int in_dim, const void* y, const void* w, void* out,
+             std::int64_t rows, void* stream) {
+  const auto us = uvw_source(p, tag);
   const cgf::Kernel prep = cgf::load_kernel(us->prep);
   const cgf::Kernel main = cgf::load_kernel(us->main);
   CUcontext ctx = cgf::ensure_context();
   CUdeviceptr img = 0;
   {
     std::lock_guard<std::mutex> g(p->mu);
-    auto it = p->wimg.find(ctx);
+    auto it = p->wimg.find({ctx, tag});
     if (it == p->wimg.end()) {
       CU_CHECK(cgf::drv::cuMemAlloc(&img, us->wimg_bytes));
-      p->wimg.emplace(ctx, img);
+      p->wimg.emplace(std::make_pair(ctx, tag), img);
     } else {
       img = it->second;
     }
   }
+  Args a;
+  a.x = in; a.y = y; a.w = w; a.o0 = out; a.rows = rows;
   CUstream st = reinterpret_cast<CUstream>(stream);
-  const void* w = a.w;
-  void* pargs[] = {&w, &img};
+  const void* wsrc = a.w;
+  void* pargs[] = {&wsrc, &img};
   const unsigned pgrid = static_cast<unsigned>((p->problem.n_w + 255) / 256);
   CU_CHECK(cgf::drv::cuLaunchKernel(prep.fn, pgrid, 1, 1, 256, 1, 1, 0, st, pargs, nullptr));
   // x viewed as [rows][dim_x / 16][16] fp32; one tile = 128 rows x dx lines of
   // 16 channels' worth of one x segment, 64-byte swizzled (conflict-free
   // per-row 16-byte reads). Rows past the batch are zero-filled by the TMA.
-  if (reinterpret_cast<std::uintptr_t>(a.x) & 15u) throw cgf::ShapeError("uvw path: x must be 16-byte aligned");
+  if (reinterpret_cast<std::uintptr_t>(a.x) & 15u) throw cgf::ShapeError("uvw path: inputs must be 16-byte aligned");
   CUtensorMap maps[4];
   const int dxs[4] = {1, 3, 5, 7};
   for (int i = 0; i < 4; ++i) {
-    const cuuint64_t gdim[3] = {16, static_cast<cuuint64_t>(p->problem.dim_x / 16), static_cast<cuuint64_t>(a.rows)};
-    const cuuint64_t gstride[2] = {64, static_cast<cuuint64_t>(p->problem.dim_x) * 4};
-    const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(std::min(dxs[i], p->problem.dim_x / 16)), 128};
+    const cuuint64_t gdim[3] = {16, static_cast<cuuint64_t>(in_dim / 16), static_cast<cuuint64_t>(a.rows)};
+    const cuuint64_t gstride[2] = {64, static_cast<cuuint64_t>(in_dim) * 4};
+    const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(std::min(dxs[i], in_dim / 16)), 128};
     const cuuint32_t estr[3] = {1, 1, 1};
     CU_CHECK(cgf::drv::cuTensorMapEncodeTiled(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(a.x), gdim,
                                               gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                               CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
   }
-  const void* y = a.y;
+  const void* ya = a.y;
   void* z = a.o0;
-  std::int64_t rows = a.rows;
+  std::int64_t nrows = a.rows;
   const void* wi = reinterpret_cast<const void*>(img);
   const std::int64_t tiles = (a.rows + us->tile_rows - 1) / us->tile_rows;
   const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(tiles, main.max_grid));
@@ -222,7 +240,7 @@ void run_uvw_forward(cgf_plan* p, const Args& a, void* stream) {
     CU_CHECK(cgf::drv::cuMemAlloc(&prof, 16 * 8));
     CU_CHECK(cgf::drv::cuMemsetD8Async(prof, 0, 16 * 8, st));
   }
-  void* args[] = {&maps[0], &maps[1], &maps[2], &maps[3], &y, &wi, &z, &rows, &prof};
+  void* args[] = {&maps[0], &maps[1], &maps[2], &maps[3], &ya, &wi, &z, &nrows, &prof};
   CU_CHECK(cgf::drv::cuLaunchKernel(main.fn, grid, 1, 1, main.threads, 1, 1, main.smem_bytes, st, args, nullptr));
   if (prof) {
     unsigned long long h[16];
@@ -238,8 +256,89 @@ void run_uvw_forward(cgf_plan* p, const Args& a, void* stream) {
   }
 }
 
+// dL/dy and the shared dL/dW of a uvw backward: the tcgen05 gradient kernel
+// (per-CTA gW partials) + a fixed-order reduction over CTAs.
+void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, const void* gz, void* gy, void* gw,
+                     std::int64_t rows, void* stream);
+
 void memzero(void* ptr, std::size_t bytes, void* stream) {
   if (bytes) CU_CHECK(cgf::drv::cuMemsetD8Async(reinterpret_cast<CUdeviceptr>(ptr), 0, bytes, reinterpret_cast<CUstream>(stream)));
+}
+
+// Tensor maps over a [rows][dim] fp32 array viewed as [rows][dim / 16][16]:
+// boxes of 128 rows x dx lines (dx = 1, 3, 5, 7), 64-byte swizzle.
+void uvw_tmaps(CUtensorMap maps[4], const void* base, int dim, std::int64_t rows) {
+  if (reinterpret_cast<std::uintptr_t>(base) & 15u) throw cgf::ShapeError("uvw path: inputs must be 16-byte aligned");
+  const int dxs[4] = {1, 3, 5, 7};
+  for (int i = 0; i < 4; ++i) {
+    const cuuint64_t gdim[3] = {16, static_cast<cuuint64_t>(dim / 16), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t gstride[2] = {64, static_cast<cuuint64_t>(dim) * 4};
+    const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(std::min(dxs[i], dim / 16)), 128};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CU_CHECK(cgf::drv::cuTensorMapEncodeTiled(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), gdim,
+                                              gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+  }
+}
+
+void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, const void* gz, void* gy, void* gw,
+                     std::int64_t rows, void* stream) {
+  (void)w;  // the W^T images were just written by the gx kernel's prep (same call, same stream)
+  CUcontext ctx = cgf::ensure_context();
+  CUstream st = reinterpret_cast<CUstream>(stream);
+  CUtensorMap maps[4];
+  uvw_tmaps(maps, x, p->problem.dim_x, rows);
+  const std::int64_t tiles = (rows + 127) / 128;
+  std::int64_t nrows = rows;
+  const void* ya = y;
+  const void* gza = gz;
+  // dL/dy
+  {
+    const auto us = uvw_source(p, "bwdy");
+    const cgf::Kernel k = cgf::load_kernel(us->main);
+    CUdeviceptr img;
+    {
+      std::lock_guard<std::mutex> g(p->mu);
+      img = p->wimg.at({ctx, "bwdx"});
+    }
+    const void* wi = reinterpret_cast<const void*>(img);
+    void* gya = gy;
+    void* args[] = {&maps[0], &maps[1], &maps[2], &maps[3], &ya, &wi, &gza, &gya, &nrows};
+    const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(tiles, k.max_grid));
+    CU_CHECK(cgf::drv::cuLaunchKernel(k.fn, grid, 1, 1, k.threads, 1, 1, k.smem_bytes, st, args, nullptr));
+  }
+  // shared dL/dW: <= 6 instructions per pass (TMEM), per-CTA partials, then a
+  // fixed-order reduction of each pass's weight range
+  const int np = static_cast<int>(p->problem.resolved.size());
+  for (int first = 0; first < np; first += 6) {
+    const auto us = uvw_source(p, "bwdw" + std::to_string(first));
+    const cgf::Kernel k = cgf::load_kernel(us->main);
+    const cgf::Kernel red = cgf::load_kernel(us->prep);
+    CUdeviceptr part;
+    {
+      std::lock_guard<std::mutex> g(p->mu);
+      auto it = p->wimg.find({ctx, "gw_part"});
+      if (it == p->wimg.end()) {
+        CU_CHECK(cgf::drv::cuMemAlloc(&part, 4ull * k.max_grid * p->problem.n_w));
+        p->wimg.emplace(std::make_pair(ctx, std::string("gw_part")), part);
+      } else {
+        part = it->second;
+      }
+    }
+    void* pa = reinterpret_cast<void*>(part);
+    void* args[] = {&maps[0], &maps[1], &maps[2], &maps[3], &ya, &gza, &pa, &nrows};
+    const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(tiles, k.max_grid));
+    CU_CHECK(cgf::drv::cuLaunchKernel(k.fn, grid, 1, 1, k.threads, 1, 1, k.smem_bytes, st, args, nullptr));
+    const int last = std::min(np, first + 6) - 1;
+    int w0 = static_cast<int>(p->problem.resolved[first].w_off);
+    int w1 = static_cast<int>(p->problem.resolved[last].w_off + p->problem.resolved[last].b * p->problem.resolved[last].bp);
+    int nparts = static_cast<int>(grid);
+    void* gwa = gw;
+    void* rargs[] = {&pa, &nparts, &gwa, &w0, &w1};
+    const unsigned rgrid = static_cast<unsigned>((w1 - w0 + 255) / 256);
+    CU_CHECK(cgf::drv::cuLaunchKernel(red.fn, rgrid, 1, 1, 256, 1, 1, 0, st, rargs, nullptr));
+  }
 }
 
 void launch(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, const void* x,
@@ -257,7 +356,14 @@ void launch(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, con
   a.x = x; a.y = y; a.w = w; a.gz = gz; a.da = da; a.db = db; a.dc = dc;
   a.o0 = o0; a.o1 = o1; a.o2 = o2; a.o3 = o3; a.rows = rows;
   if (use_uvw(p, op, dtype, w_shared)) {
-    run_uvw_forward(p, a, stream);
+    if (op == CGF_OP_FORWARD) {
+      run_uvw(p, "fwd", x, pr.dim_x, y, w, o0, rows, stream);
+    } else {
+      // backward, shared W: gx on the tensor cores (transposed forward);
+      // gy and gW by the uvw gradient kernel.
+      run_uvw(p, "bwdx", gz, pr.dim_z, y, w, o0, rows, stream);
+      run_uvw_grad_yw(p, x, y, w, gz, o1, o2, rows, stream);
+    }
     return;
   }
   run_kernel(p, static_cast<cgf::Comp>(op), cgf::Loop::Rows, dtype, w_shared, a, stream);
@@ -379,8 +485,17 @@ int cgf_plan_source(cgf_plan* p, int op, int dtype, int w_shared, int aligned, c
 int cgf_plan_compile(cgf_plan* p, int op, int dtype, int w_shared, int aligned) {
   return guarded([&] {
     need(p, "plan");
+    if (use_uvw(p, op, dtype, w_shared) && op == CGF_OP_BACKWARD) {
+      std::vector<std::string> tags = {"bwdx", "bwdy"};
+      for (std::size_t f = 0; f < p->problem.resolved.size(); f += 6) tags.push_back("bwdw" + std::to_string(f));
+      for (const auto& tag : tags) {
+        const auto us = uvw_source(p, tag);
+        cgf::compile_cubin(us->main.source, us->main.module.empty() ? us->main.name : us->main.module);
+      }
+      return;
+    }
     const auto ks = source_for_op(p, op, dtype, w_shared, aligned);
-    cgf::compile_cubin(ks->source, ks->name);
+    cgf::compile_cubin(ks->source, ks->module.empty() ? ks->name : ks->module);
   });
 }
 

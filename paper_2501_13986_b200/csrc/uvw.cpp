@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <set>
 #include <sstream>
 
 namespace cgf {
@@ -55,9 +56,599 @@ bool uvw_eligible(const Problem& p, std::string* why) {
   return true;
 }
 
+namespace {
+UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_transposed);
+
+// Device helpers shared by the uvw kernels (tcgen05 / TMEM / TMA / mbarrier).
+const char* uvw_helpers() {
+  return R"(
+// ---- tcgen05 / TMEM / TMA helpers (sm_100a) ----
+struct __align__(64) TMap { unsigned long long v[16]; };  // CUtensorMap
+DEVI u64 gtimer() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
+// Bounded wait: a barrier that never completes traps after ~4 s with its tag
+// instead of hanging the device.
+#ifdef CGF_UVW_PROF
+__shared__ unsigned long long prof_s[16];
+#endif
+DEVI void mbar_wait_t(u64* b, u32 parity, int tag) {
+  if (mbar_try(b, parity)) return;
+#ifdef CGF_UVW_PROF
+  const long long c0 = clock64();
+  while (!mbar_try(b, parity)) { }
+  if ((threadIdx.x & 31) == 0) atomicAdd(&prof_s[tag], (unsigned long long)(clock64() - c0));
+  return;
+#endif
+  const u64 t0 = gtimer();
+  for (u32 it = 1;; ++it) {
+    if (mbar_try(b, parity)) return;
+    if ((it & 1023u) == 0 && gtimer() - t0 > 4000000000ull) {
+      printf("cgf_uvw: mbarrier timeout tag=%d block=%d thread=%d parity=%u\n", tag, blockIdx.x, threadIdx.x, parity);
+      __trap();
+    }
+  }
+}
+DEVI void mbar_arrive(u64* b) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_addr(b)) : "memory"); }
+DEVI void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+DEVI void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// D[tmem] (+)= A[smem] * B[smem]^T, tf32 inputs, fp32 accumulate, single CTA.
+DEVI void tc_mma(u32 d, u64 a, u64 b, u32 idesc, u32 acc) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}"
+               :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+// Arrive on an mbarrier once every previously issued tcgen05.mma completed.
+DEVI void tc_commit(u64* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_addr(b)) : "memory");
+}
+DEVI void tc_ld8(u32 taddr, float* v) {
+  u32 r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+DEVI void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+DEVI void tc_st8(u32 taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                  "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                  "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])) : "memory");
+}
+DEVI void tc_st4(u32 taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+               :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                  "r"(__float_as_uint(v[3])) : "memory");
+}
+DEVI u32 elect_one() {
+  u32 p;
+  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n selp.u32 %0, 1, 0, e;\n}" : "=r"(p));
+  return p;
+}
+DEVI void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// D[tmem] (+)= A[tmem] * B[smem]^T (A: 128 lanes x 8 tf32 columns)
+DEVI void tc_mma_ts(u32 d, u32 a, u64 b, u32 idesc, u32 acc) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}"
+               :: "r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+// 3-D TMA tile load global -> shared, completion on an mbarrier (bytes).
+DEVI void tma_load3(void* dst, const TMap* map, int c0, int c1, int c2, u64* bar) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+               :: "r"(smem_addr(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)) : "memory");
+}
+// Shared-memory matrix descriptor: K-major, 64-byte swizzle (rows of 16 fp32),
+// 8-row groups 512 B apart (SBO), version 1 (sm_100).
+DEVI u64 sdesc64(u32 saddr) {
+  return (u64)((saddr & 0x3FFFFu) >> 4) | ((u64)1 << 16) | ((u64)(512 >> 4) << 32) | ((u64)1 << 46) | ((u64)4 << 61);
+}
+// Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M = 128, N.
+DEVI constexpr u32 idesc_tf32(int n) { return (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(n >> 3) << 17) | ((u32)(128 >> 4) << 24); }
+// tf32 split: hi keeps the top 19 bits (exactly representable), lo the rest.
+DEVI float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
+// Byte offset of 16-byte chunk `chunk` of row m in a K-major SW64 tile (64 B rows).
+DEVI u32 sw64(int m, int chunk) { return (u32)((m >> 3) * 512 + (m & 7) * 64 + ((chunk ^ ((m >> 1) & 3)) << 4)); }
+)";
+}
+}  // namespace
+
 UvwSource generate_uvw_forward(const Problem& p) {
   std::string why;
   if (!uvw_eligible(p, &why)) throw UnsupportedError("uvw tensor-core path: " + why);
+  return generate_uvw_impl(p, "fwd", false);
+}
+
+// gx = dL/dx is the forward contraction of the TRANSPOSED problem: for each
+// instruction, gx[l1 seg][c][i] += sum_r W[r][c] sum_{(i,j,k)} v y[j] gz[l3 seg][r][k]
+// (kernelgen.cpp:222-226 with gzp = W^T gz), i.e. x <-> gz, l1 <-> l3,
+// b <-> b', CG entries (i,j,k) -> (k,j,i) and W read transposed. The same
+// generator then emits the tcgen05 kernel (A = CG(gz, y) in TMEM, B = W^T).
+UvwSource generate_uvw_backward_x(const Problem& p) {
+  std::string why;
+  if (!uvw_eligible(p, &why)) throw UnsupportedError("uvw tensor-core path: " + why);
+  Problem t = p;
+  std::swap(t.x_ir, t.z_ir);
+  std::swap(t.dim_x, t.dim_z);
+  for (auto& s : t.resolved) {
+    std::swap(s.x_off, s.z_off);
+    std::swap(s.l1, s.l3);
+    std::swap(s.b, s.bp);
+    auto cg = std::make_shared<CGBlock>(*s.cg);
+    std::swap(cg->l1, cg->l3);
+    for (auto& e : cg->entries) std::swap(e.i, e.k);
+    std::stable_sort(cg->entries.begin(), cg->entries.end(), [](const CGEntry& a, const CGEntry& b) {
+      return a.k != b.k ? a.k < b.k : a.i != b.i ? a.i < b.i : a.j < b.j;
+    });
+    s.cg = cg;
+  }
+  if (!uvw_eligible(t, &why)) throw UnsupportedError("uvw tensor-core backward: " + why);
+  return generate_uvw_impl(t, "bwdx", true);
+}
+
+
+// Shared pieces of the two uvw gradient kernels (gy, shared gW).
+namespace {
+
+struct GradInfo {
+  int np = 0, max_dx = 1, wslot = 0, xslot = 0;
+  std::vector<std::size_t> wimg_of;
+};
+
+GradInfo grad_info(const Problem& p) {
+  std::string why;
+  if (!uvw_eligible(p, &why)) throw UnsupportedError("uvw tensor-core path: " + why);
+  GradInfo g;
+  const auto& R = p.resolved;
+  g.np = static_cast<int>(R.size());
+  int max_bp = 16;
+  for (const auto& s : R) {
+    if (s.b != 64 || s.bp != 64) throw UnsupportedError("uvw gradient kernels: multiplicities must be 64");
+    g.max_dx = std::max(g.max_dx, s.dx());
+    max_bp = std::max(max_bp, s.bp);
+  }
+  // W^T images of the gx kernel's prep: per instruction, b / 16 images of
+  // [b' rows][16 fp32] hi + lo (same offsets as generate_uvw_backward_x).
+  g.wslot = 2 * max_bp * kCh * 4;
+  std::size_t w = 0;
+  for (const auto& s : R) {
+    g.wimg_of.push_back(w);
+    w += static_cast<std::size_t>(s.b / kCh) * g.wslot;
+  }
+  g.xslot = (kTileRows * kCh * g.max_dx * 4 + 1023) / 1024 * 1024;
+  return g;
+}
+
+void emit_grad_tables(std::ostringstream& o, const Problem& p) {
+  const auto& R = p.resolved;
+  auto arr = [&](const char* name, const std::vector<long long>& v) {
+    o << "__constant__ int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
+    for (size_t i = 0; i < v.size(); ++i) o << (i ? "," : "") << v[i];
+    o << "};\n";
+  };
+  std::vector<long long> dz, dx, zoff, xc, woff;
+  for (const auto& s : R) {
+    dz.push_back(s.dz());
+    dx.push_back(s.dx());
+    zoff.push_back(s.z_off);
+    xc.push_back(s.x_off / kCh);
+    woff.push_back(s.w_off);
+  }
+  arr("P_DZ", dz);
+  arr("P_DX", dx);
+  arr("P_ZOFF", zoff);
+  arr("P_XC", xc);
+  arr("P_WOFF", woff);
+}
+
+const char* grad_helpers() {
+  return R"(
+DEVI void tc_ld32(u32 taddr, float* v) {
+  u32 r[32];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+               "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                 "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+                 "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+DEVI void prod_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// element (row r of the operand, K index k) of a K-major SW64 tile whose K
+// runs over the 128 batch rows: 16-row K blocks 4 KB apart (64 operand rows)
+DEVI u32 kmaj_rows(int r, int k) { return (u32)((k >> 4) * 4096 + sw64(r, (k & 15) >> 2) + (k & 3) * 4); }
+)";
+}
+
+// x tile -> this thread's 8 channels x dx floats (the forward producer's read)
+void emit_x_read(std::ostringstream& o, int dx) {
+  o << "  float xv[" << 8 * dx << "];\n#pragma unroll\n  for (int t = 0; t < " << 2 * dx << "; ++t) {\n"
+    << "    const int g = " << 2 * dx << " * sub + t, L = m * " << dx << " + (g >> 2), j = g & 3;\n"
+    << "    const float4 v = *(const float4*)(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4));\n"
+    << "    xv[4 * t] = v.x; xv[4 * t + 1] = v.y; xv[4 * t + 2] = v.z; xv[4 * t + 3] = v.w;\n  }\n"
+    << "  fence_proxy_async();\n  __syncwarp();\n  if ((threadIdx.x & 31) == 0) mbar_arrive(xempty);\n";
+}
+
+const char* grad_kernel_head() {
+  return
+       "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n"
+       "  unsigned char* sm = (unsigned char*)(((unsigned long long)smem_raw + 1023) & ~1023ull);\n"
+       "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n"
+       "  const i64 ntiles = (rows + 127) / 128;\n";
+}
+
+// x loader warp: x tiles (q, cb) of every unit in order, ring of one slot
+std::string grad_x_loader(const std::string& q_range) {
+  return "  else if (warp == 9) {\n"
+         "    if (lane == 0) {\n"
+         "      u32 gx = 0;\n"
+         "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
+         "        for (int q = " + q_range + "; ++q)\n"
+         "          for (int k = 0; k < P_DZ[q]; ++k)\n"
+         "            for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
+         "              mbar_wait_t(x_empty, (gx & 1u) ^ 1u, 29);\n"
+         "              const int dx = P_DX[q];\n"
+         "              mbar_expect_tx(x_full, 128 * 64 * dx);\n"
+         "              const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
+         "              tma_load3(xs, mp, 0, P_XC[q] + cb * dx, (int)(tile * 128), x_full);\n"
+         "            }\n"
+         "    }\n"
+         "    __syncwarp();\n"
+         "  }\n";
+}
+
+}  // namespace
+
+// dL/dy of a uvw backward with shared W (kernel "cgf_uvw_bwdy_f32"). Per
+// 128-row tile and unit (instruction q, component k):
+//   gzp_k[row, c] = sum_r gz[row][q.z][r][k] W_q[r][c]     tcgen05: M=128 rows, N=64 (c), K=64 (r), 3xTF32
+//   gy[row, j]   += sum_{(i,j,k)} v sum_c x[row][q.x][c][i] gzp_k[row, c]          SIMT (producers)
+// (kernelgen.cpp:222-226: gy accumulates v x[i] gzp[k]). The gz_k tile is the
+// K-major A operand; B is the gx kernel's W^T image; gzp is read back from
+// TMEM by the producers, which hold x for the same 8 channels.
+UvwSource generate_uvw_backward_y(const Problem& p) {
+  const GradInfo g = grad_info(p);
+  const auto& R = p.resolved;
+  const int np = g.np;
+  const int gz_bytes = 2 * kTileRows * 64 * 4;
+  const int smem = 1024 + gz_bytes + g.xslot + 4 * g.wslot + 1024 + 128 * p.dim_y * 4;
+  if (smem > 227 * 1024) throw UnsupportedError("uvw gy kernel: shared memory too small");
+  std::ostringstream o;
+  if (std::getenv("CGF_UVW_DEBUG")) o << "#define CGF_UVW_DEBUG 1\n";
+  o << device_runtime_source() << uvw_helpers() << grad_helpers();
+  o << "// uvw gy: " << np << " instructions\n#define DIMX " << p.dim_x << "\n#define DIMY " << p.dim_y
+    << "\n#define DIMZ " << p.dim_z << "\n#define NP " << np << "\n#define WSLOT " << g.wslot << "\n#define XSLOT "
+    << g.xslot << "\n#define GZB " << gz_bytes << "\n";
+  emit_grad_tables(o, p);
+  {
+    std::vector<long long> wi(g.wimg_of.begin(), g.wimg_of.end());
+    o << "__constant__ int P_WIMG[" << np << "] = {";
+    for (int q = 0; q < np; ++q) o << (q ? "," : "") << wi[q];
+    o << "};\n";
+  }
+  for (int q = 0; q < np; ++q) {
+    const auto& sq = R[q];
+    const int dx = sq.dx(), dz = sq.dz();
+    o << "DEVI void gyk_" << q << "(int k, int cb, const unsigned char* xs, int m, int sub, u32 tgzp, float* gy,"
+      << " u64* xempty) {\n";
+    emit_x_read(o, dx);
+    o << "  float gp[8];\n  tc_ld8(tgzp + cb * 16 + 8 * sub, gp);\n  tc_wait_ld();\n  switch (k) {\n";
+    for (int k = 0; k < dz; ++k) {
+      std::set<int> is;
+      for (const auto& e : sq.cg->entries)
+        if (e.k == k) is.insert(e.i);
+      o << "  case " << k << ": {\n";
+      for (int i : is) o << "    float xg" << i << " = 0.f;\n";
+      o << "#pragma unroll\n    for (int c = 0; c < 8; ++c) {\n";
+      for (int i : is) o << "      xg" << i << " = fmaf(xv[c * " << dx << " + " << i << "], gp[c], xg" << i << ");\n";
+      o << "    }\n";
+      for (const auto& e : sq.cg->entries)
+        if (e.k == k)
+          o << "    gy[" << sq.y_off + e.j << "] = fmaf((float)" << hexd(e.v) << ", xg" << e.i << ", gy[" << sq.y_off + e.j
+            << "]);\n";
+      o << "    break; }\n";
+    }
+    o << "  }\n}\n\n";
+  }
+  o << "extern \"C\" __global__ void __launch_bounds__(352, 1) cgf_uvw_bwdy_f32("
+       "const __grid_constant__ TMap tx1, const __grid_constant__ TMap tx3, const __grid_constant__ TMap tx5, "
+       "const __grid_constant__ TMap tx7, const float* __restrict__ Y, const float* __restrict__ WIMG, "
+       "const float* __restrict__ GZ, float* __restrict__ GY, i64 rows) {\n"
+    << grad_kernel_head()
+    << "  unsigned char* gzt = sm;                 // gz_k tile [rows][r]: hi [4][128][16], lo after GZB/2\n"
+       "  unsigned char* xs = gzt + GZB;           // x tile (TMA, SW64)\n"
+       "  unsigned char* ws = xs + XSLOT;          // W^T images of one instruction (4 r-blocks)\n"
+       "  u64* bars = (u64*)(ws + 4 * WSLOT);\n"
+       "  u64* gz_full = bars; u64* gz_empty = bars + 1;\n"
+       "  u64* gzp_full = bars + 4; u64* gzp_empty = bars + 6; u64* x_full = bars + 8; u64* x_empty = bars + 9;\n"
+       "  u64* w_full = bars + 10; u64* w_empty = bars + 11;\n"
+       "  u32* tmem_slot = (u32*)(bars + 13);\n"
+       "  float* gys = (float*)(bars + 16);\n"
+       "  if (threadIdx.x == 0) {\n"
+       "    mbar_init(gz_full, 8); mbar_init(gz_empty, 1);\n"
+       "    for (int i = 0; i < 2; ++i) { mbar_init(&gzp_full[i], 1); mbar_init(&gzp_empty[i], 8); }\n"
+       "    mbar_init(x_full, 1); mbar_init(x_empty, 8); mbar_init(w_full, 1); mbar_init(w_empty, 1);\n"
+       "    mbar_fence_init();\n  }\n"
+       "  if (warp == 8) {\n"
+       "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\" :: \"r\"(smem_addr(tmem_slot)));\n"
+       "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\");\n"
+       "  }\n"
+       "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n"
+       "  const u32 tmem = *tmem_slot;\n"
+       "  if (warp < 8) {\n"
+       "    const int m = 32 * (warp & 3) + lane, sub = warp >> 2;\n"
+       "    const u32 tq = tmem + ((u32)(32 * (warp & 3)) << 16);\n"
+       "    u32 ug = 0, gx = 0;\n"
+       "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
+       "      const i64 row = tile * 128 + m;\n"
+       "      const bool valid = row < rows;\n"
+       "      float gy[DIMY];\n"
+       "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) gy[j] = 0.f;\n"
+       "      const float* gzr = GZ + (valid ? row : 0) * DIMZ;\n"
+       "#pragma unroll 1\n      for (int q = 0; q < NP; ++q) {\n"
+       "        const int dz = P_DZ[q];\n"
+       "#pragma unroll 1\n        for (int k = 0; k < dz; ++k, ++ug) {\n"
+       "          mbar_wait_t(gz_empty, (ug & 1u) ^ 1u, 20);\n"
+       "#pragma unroll\n          for (int g = 0; g < 8; ++g) {\n"
+       "            float h[4], l[4];\n"
+       "#pragma unroll\n            for (int a = 0; a < 4; ++a) {\n"
+       "              const float v = valid ? __ldg(gzr + P_ZOFF[q] + (32 * sub + 4 * g + a) * dz + k) : 0.f;\n"
+       "              h[a] = tf32_hi(v); l[a] = v - h[a];\n            }\n"
+       "            const int c4 = 8 * sub + g;\n"
+       "            const u32 off = (c4 >> 2) * 8192 + sw64(m, c4 & 3);\n"
+       "            *(float4*)(gzt + off) = make_float4(h[0], h[1], h[2], h[3]);\n"
+       "            *(float4*)(gzt + GZB / 2 + off) = make_float4(l[0], l[1], l[2], l[3]);\n          }\n"
+       "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(gz_full);\n"
+       "          const u32 buf = ug & 1u;\n"
+       "          mbar_wait_t(&gzp_full[buf], (ug >> 1) & 1u, 22);\n"
+       "          tc_fence_after();\n"
+       "          const u32 tgzp = tq + 64 * buf;\n"
+       "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
+       "            mbar_wait_t(x_full, gx & 1u, 23);\n"
+       "            switch (q) {\n";
+  for (int q = 0; q < np; ++q)
+    o << "              case " << q << ": gyk_" << q << "(k, cb, xs, m, sub, tgzp, gy, x_empty); break;\n";
+  o << "            }\n"
+       "          }\n"
+       "          tc_fence_before();\n          __syncwarp();\n"
+       "          if (lane == 0) mbar_arrive(&gzp_empty[buf]);\n"
+       "        }\n"
+       "      }\n"
+       "      if (sub == 1) {\n#pragma unroll\n        for (int j = 0; j < DIMY; ++j) gys[m * DIMY + j] = gy[j];\n      }\n"
+       "      prod_sync();\n"
+       "      if (sub == 0 && valid) {\n#pragma unroll\n        for (int j = 0; j < DIMY; ++j) GY[row * DIMY + j] = gy[j] + gys[m * DIMY + j];\n      }\n"
+       "      prod_sync();\n"
+       "    }\n"
+       "  }\n"
+       "  else if (warp == 8) {\n"
+       "    const u64 gzh = sdesc64(smem_addr(gzt)), gzl = gzh + (u64)((GZB / 2) >> 4);\n"
+       "    const u64 wd = sdesc64(smem_addr(ws));\n"
+       "    const u32 id_gzp = idesc_tf32(64);\n"
+       "    u32 ug = 0, wg = 0;\n"
+       "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
+       "      for (int q = 0; q < NP; ++q, ++wg) {\n"
+       "        mbar_wait_t(w_full, wg & 1u, 25);\n        tc_fence_after();\n"
+       "        const int dz = P_DZ[q];\n"
+       "        for (int k = 0; k < dz; ++k, ++ug) {\n"
+       "          const u32 buf = ug & 1u;\n"
+       "          mbar_wait_t(gz_full, ug & 1u, 26);\n"
+       "          mbar_wait_t(&gzp_empty[buf], ((ug >> 1) & 1u) ^ 1u, 27);\n"
+       "          tc_fence_after();\n"
+       "          const u32 dg = tmem + 64 * buf;\n"
+       "          if (elect_one()) {\n"
+       "#pragma unroll\n            for (int s = 0; s < 8; ++s) {\n"
+       "              const u64 ao = (u64)(((s >> 1) * 8192 + (s & 1) * 32) >> 4);\n"
+       "              const u64 bo = (u64)(((s >> 1) * WSLOT + (s & 1) * 32) >> 4);\n"
+       "              tc_mma(dg, gzh + ao, wd + bo, id_gzp, s ? 1u : 0u);\n"
+       "              tc_mma(dg, gzh + ao, wd + bo + (u64)((64 * 64) >> 4), id_gzp, 1u);\n"
+       "              tc_mma(dg, gzl + ao, wd + bo, id_gzp, 1u);\n"
+       "            }\n"
+       "            tc_commit(&gzp_full[buf]);\n"
+       "            tc_commit(gz_empty);\n"
+       "            if (k == dz - 1) tc_commit(w_empty);\n"
+       "          }\n"
+       "          __syncwarp();\n"
+       "        }\n"
+       "      }\n"
+       "    }\n"
+       "  }\n"
+    << grad_x_loader("0; q < NP")
+    << "  else if (warp == 10) {\n"
+       "    if (lane == 0) {\n"
+       "      u32 wg = 0;\n"
+       "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
+       "        for (int q = 0; q < NP; ++q, ++wg) {\n"
+       "          mbar_wait_t(w_empty, (wg & 1u) ^ 1u, 30);\n"
+       "          mbar_expect_tx(w_full, 4 * WSLOT);\n"
+       "          bulk_g2s(ws, (const char*)WIMG + P_WIMG[q], 4 * WSLOT, w_full);\n"
+       "        }\n"
+       "    }\n"
+       "    __syncwarp();\n"
+       "  }\n"
+       "  tc_fence_before();\n  __syncthreads();\n"
+       "  if (warp == 8) { tc_fence_after(); asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\" :: \"r\"(tmem)); }\n"
+       "}\n";
+  UvwSource out;
+  out.main.name = out.main.module = "cgf_uvw_bwdy_f32";
+  out.main.source = o.str();
+  out.main.threads = 352;
+  out.main.smem_bytes = smem;
+  out.prep = out.main;
+  out.wimg_bytes = 0;
+  return out;
+}
+
+// The shared-W gradient dL/dW of a uvw backward (kernel "cgf_uvw_bwdw<first>_f32")
+// for instructions [first, first + count) (count <= 6: one 64-column TMEM
+// accumulator each):
+//   gW_q[r][c] += sum_row sum_k gz[row][q.z][r][k] z'_k[row][c],  z'_k = CG(x, y)[.., k]
+// (kernelgen.cpp:639-650 summed over rows): tcgen05 M=64 (c), N=64 (r), K=128
+// rows per tile, both operands K-major over the batch rows (written by the
+// producers transposed), 3xTF32. Accumulators live in TMEM across all tiles of
+// the CTA and are written once as this CTA's partial; `prep` sums the
+// partials over CTAs in a fixed order (deterministic).
+UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
+  const GradInfo g = grad_info(p);
+  const auto& R = p.resolved;
+  if (count < 1 || count > 6 || first < 0 || first + count > g.np) throw std::logic_error("bad gW instruction range");
+  const int tb = 2 * 64 * kTileRows * 4;  // hi + lo of a [64][128 rows] K-major tile
+  const int smem = 1024 + 2 * tb + g.xslot + 1024;
+  if (smem > 227 * 1024) throw UnsupportedError("uvw gW kernel: shared memory too small");
+  const std::string kname = "cgf_uvw_bwdw" + S(first) + "_f32";
+  std::ostringstream o;
+  if (std::getenv("CGF_UVW_DEBUG")) o << "#define CGF_UVW_DEBUG 1\n";
+  o << device_runtime_source() << uvw_helpers() << grad_helpers();
+  o << "// uvw gW: instructions [" << first << ", " << first + count << ")\n#define DIMX " << p.dim_x
+    << "\n#define DIMY " << p.dim_y << "\n#define DIMZ " << p.dim_z << "\n#define NW_ " << p.n_w << "\n#define Q0 "
+    << first << "\n#define Q1 " << first + count << "\n#define XSLOT " << g.xslot << "\n#define TB " << tb << "\n";
+  emit_grad_tables(o, p);
+  for (int q = first; q < first + count; ++q) {
+    const auto& sq = R[q];
+    const int dx = sq.dx(), dz = sq.dz();
+    o << "DEVI void zw_" << q << "(int k, int cb, const unsigned char* xs, const float* yv, int m, int sub,"
+      << " unsigned char* zt, u64* xempty) {\n";
+    emit_x_read(o, dx);
+    o << "  float zc[8];\n#pragma unroll\n  for (int c = 0; c < 8; ++c) zc[c] = 0.f;\n  switch (k) {\n";
+    for (int k = 0; k < dz; ++k) {
+      std::map<int, std::string> qk;
+      for (const auto& e : sq.cg->entries) {
+        if (e.k != k) continue;
+        std::string& t = qk[e.i];
+        t += (t.empty() ? "" : " + ") + std::string("(float)") + hexd(e.v) + " * yv[" + S(sq.y_off + e.j) + "]";
+      }
+      o << "  case " << k << ": {\n";
+      for (const auto& [i, ex] : qk) o << "    const float q" << i << " = " << ex << ";\n";
+      o << "#pragma unroll\n    for (int c = 0; c < 8; ++c) {\n";
+      for (const auto& kv : qk) o << "      zc[c] = fmaf(q" << kv.first << ", xv[c * " << dx << " + " << kv.first << "], zc[c]);\n";
+      o << "    }\n    break; }\n";
+    }
+    o << "  }\n"
+      << "#pragma unroll\n  for (int c = 0; c < 8; ++c) {\n"
+      << "    const float h = tf32_hi(zc[c]);\n    const u32 off = kmaj_rows(16 * cb + 8 * sub + c, m);\n"
+      << "    *(float*)(zt + off) = h; *(float*)(zt + TB / 2 + off) = zc[c] - h;\n  }\n}\n\n";
+  }
+  o << "extern \"C\" __global__ void " << kname << "_reduce(const float* __restrict__ part, int nparts, "
+       "float* __restrict__ gw, int w0, int w1) {\n"
+       "  const int e = w0 + blockIdx.x * blockDim.x + threadIdx.x;\n  if (e >= w1) return;\n"
+       "  float s = 0.f;\n  for (int c = 0; c < nparts; ++c) s += part[(size_t)c * NW_ + e];\n  gw[e] = s;\n}\n\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(320, 1) " << kname << "("
+       "const __grid_constant__ TMap tx1, const __grid_constant__ TMap tx3, const __grid_constant__ TMap tx5, "
+       "const __grid_constant__ TMap tx7, const float* __restrict__ Y, const float* __restrict__ GZ, "
+       "float* __restrict__ PART, i64 rows) {\n"
+    << grad_kernel_head()
+    << "  unsigned char* gzt = sm;                 // gz_k tile [r][rows] K-major: hi, lo after TB/2\n"
+       "  unsigned char* zt = sm + TB;             // z'_k tile [c][rows] K-major\n"
+       "  unsigned char* xs = zt + TB;             // x tile (TMA, SW64)\n"
+       "  u64* bars = (u64*)(xs + XSLOT);\n"
+       "  u64* gz_full = bars; u64* gz_empty = bars + 1; u64* z_full = bars + 2; u64* z_empty = bars + 3;\n"
+       "  u64* x_full = bars + 8; u64* x_empty = bars + 9; u64* done = bars + 12;\n"
+       "  u32* tmem_slot = (u32*)(bars + 13);\n"
+       "  if (threadIdx.x == 0) {\n"
+       "    mbar_init(gz_full, 8); mbar_init(gz_empty, 1); mbar_init(z_full, 8); mbar_init(z_empty, 1);\n"
+       "    mbar_init(x_full, 1); mbar_init(x_empty, 8); mbar_init(done, 1);\n"
+       "    mbar_fence_init();\n  }\n"
+       "  if (warp == 8) {\n"
+       "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" :: \"r\"(smem_addr(tmem_slot)));\n"
+       "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\");\n"
+       "  }\n"
+       "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n"
+       "  const u32 tmem = *tmem_slot;\n"
+       "  if (warp < 8) {\n"
+       "    const int m = 32 * (warp & 3) + lane, sub = warp >> 2;\n"
+       "    u32 ug = 0, gx = 0;\n"
+       "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
+       "      const i64 row = tile * 128 + m;\n"
+       "      const bool valid = row < rows;\n"
+       "      float yv[DIMY];\n"
+       "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) yv[j] = valid ? __ldg(Y + row * DIMY + j) : 0.f;\n"
+       "      const float* gzr = GZ + (valid ? row : 0) * DIMZ;\n"
+       "#pragma unroll 1\n      for (int q = Q0; q < Q1; ++q) {\n"
+       "        const int dz = P_DZ[q];\n"
+       "#pragma unroll 1\n        for (int k = 0; k < dz; ++k, ++ug) {\n"
+       "          mbar_wait_t(gz_empty, (ug & 1u) ^ 1u, 20);\n"
+       "#pragma unroll 4\n          for (int t = 0; t < 32; ++t) {\n"
+       "            const int r = 32 * sub + t;\n"
+       "            const float v = valid ? __ldg(gzr + P_ZOFF[q] + r * dz + k) : 0.f;\n"
+       "            const float h = tf32_hi(v);\n            const u32 off = kmaj_rows(r, m);\n"
+       "            *(float*)(gzt + off) = h; *(float*)(gzt + TB / 2 + off) = v - h;\n          }\n"
+       "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(gz_full);\n"
+       "          mbar_wait_t(z_empty, (ug & 1u) ^ 1u, 21);\n"
+       "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
+       "            mbar_wait_t(x_full, gx & 1u, 23);\n"
+       "            switch (q) {\n";
+  for (int q = first; q < first + count; ++q)
+    o << "              case " << q << ": zw_" << q << "(k, cb, xs, yv, m, sub, zt, x_empty); break;\n";
+  o << "            }\n"
+       "          }\n"
+       "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(z_full);\n"
+       "        }\n"
+       "      }\n"
+       "    }\n"
+       // this CTA's partial: M=64 accumulators use lanes 0-15 of each 32-lane
+       // quadrant: quadrant w holds c in [16 w, 16 w + 16), all 64 r columns
+       "    mbar_wait_t(done, 0, 24);\n    tc_fence_after();\n"
+       "    if (sub == 0) {\n"
+       "      const u32 tq = tmem + ((u32)(32 * warp) << 16);\n"
+       "      const int c = 16 * warp + lane;\n"
+       "      float* pr = PART + (size_t)blockIdx.x * NW_;\n"
+       "      for (int q = Q0; q < Q1; ++q) {\n"
+       "        float v[32];\n"
+       "        for (int h = 0; h < 2; ++h) {\n"
+       "          tc_ld32(tq + 64 * (q - Q0) + 32 * h, v);\n          tc_wait_ld();\n"
+       "          if (lane < 16) {\n"
+       "#pragma unroll\n            for (int j = 0; j < 32; ++j) pr[P_WOFF[q] + (32 * h + j) * 64 + c] = v[j];\n"
+       "          }\n"
+       "        }\n"
+       "      }\n"
+       "    }\n"
+       "  }\n"
+       "  else if (warp == 8) {\n"
+       "    const u64 gh = sdesc64(smem_addr(gzt)), gl = gh + (u64)((TB / 2) >> 4);\n"
+       "    const u64 zh = sdesc64(smem_addr(zt)), zl = zh + (u64)((TB / 2) >> 4);\n"
+       "    const u32 id_w = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(64 >> 3) << 17) | ((u32)(64 >> 4) << 24);\n"
+       "    u32 ug = 0; i64 lt = 0;\n"
+       "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {\n"
+       "      for (int q = Q0; q < Q1; ++q) {\n"
+       "        const int dz = P_DZ[q];\n"
+       "        for (int k = 0; k < dz; ++k, ++ug) {\n"
+       "          mbar_wait_t(gz_full, ug & 1u, 26);\n"
+       "          mbar_wait_t(z_full, ug & 1u, 28);\n"
+       "          tc_fence_after();\n"
+       "          if (elect_one()) {\n"
+       "            const u32 dw = tmem + 64 * (q - Q0);\n"
+       "            const u32 first = (lt == 0 && k == 0) ? 1u : 0u;\n"
+       "#pragma unroll\n            for (int s = 0; s < 16; ++s) {\n"
+       "              const u64 o = (u64)(((s >> 1) * 4096 + (s & 1) * 32) >> 4);\n"
+       "              tc_mma(dw, zh + o, gh + o, id_w, (first && s == 0) ? 0u : 1u);\n"
+       "              tc_mma(dw, zh + o, gl + o, id_w, 1u);\n"
+       "              tc_mma(dw, zl + o, gh + o, id_w, 1u);\n"
+       "            }\n"
+       "            tc_commit(gz_empty);\n            tc_commit(z_empty);\n"
+       "          }\n"
+       "          __syncwarp();\n"
+       "        }\n"
+       "      }\n"
+       "    }\n"
+       "    if (elect_one()) tc_commit(done);\n    __syncwarp();\n"
+       "  }\n"
+    << grad_x_loader("Q0; q < Q1")
+    << "  tc_fence_before();\n  __syncthreads();\n"
+       "  if (warp == 8) { tc_fence_after(); asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\" :: \"r\"(tmem)); }\n"
+       "}\n";
+  UvwSource out;
+  out.main.name = out.main.module = kname;
+  out.main.source = o.str();
+  out.main.threads = 320;
+  out.main.smem_bytes = smem;
+  out.prep = out.main;
+  out.prep.name = kname + "_reduce";
+  out.prep.threads = 256;
+  out.prep.smem_bytes = 0;
+  return out;
+}
+
+namespace {
+
+UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_transposed) {
   const auto& R = p.resolved;
   const int np = static_cast<int>(R.size());
 
@@ -185,92 +776,7 @@ UvwSource generate_uvw_forward(const Problem& p) {
   if (std::getenv("CGF_UVW_DEBUG")) o << "#define CGF_UVW_DEBUG 1\n";
   if (std::getenv("CGF_UVW_PROF")) o << "#define CGF_UVW_PROF 1\n";
   o << device_runtime_source();
-  o << R"(
-// ---- tcgen05 / TMEM / TMA helpers (sm_100a) ----
-struct __align__(64) TMap { unsigned long long v[16]; };  // CUtensorMap
-DEVI u64 gtimer() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
-// Bounded wait: a barrier that never completes traps after ~4 s with its tag
-// instead of hanging the device.
-#ifdef CGF_UVW_PROF
-__shared__ unsigned long long prof_s[16];
-#endif
-DEVI void mbar_wait_t(u64* b, u32 parity, int tag) {
-  if (mbar_try(b, parity)) return;
-#ifdef CGF_UVW_PROF
-  const long long c0 = clock64();
-  while (!mbar_try(b, parity)) { }
-  if ((threadIdx.x & 31) == 0) atomicAdd(&prof_s[tag], (unsigned long long)(clock64() - c0));
-  return;
-#endif
-  const u64 t0 = gtimer();
-  for (u32 it = 1;; ++it) {
-    if (mbar_try(b, parity)) return;
-    if ((it & 1023u) == 0 && gtimer() - t0 > 4000000000ull) {
-      printf("cgf_uvw: mbarrier timeout tag=%d block=%d thread=%d parity=%u\n", tag, blockIdx.x, threadIdx.x, parity);
-      __trap();
-    }
-  }
-}
-DEVI void mbar_arrive(u64* b) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_addr(b)) : "memory"); }
-DEVI void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-DEVI void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-// D[tmem] (+)= A[smem] * B[smem]^T, tf32 inputs, fp32 accumulate, single CTA.
-DEVI void tc_mma(u32 d, u64 a, u64 b, u32 idesc, u32 acc) {
-  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}"
-               :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
-}
-// Arrive on an mbarrier once every previously issued tcgen05.mma completed.
-DEVI void tc_commit(u64* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_addr(b)) : "memory");
-}
-DEVI void tc_ld8(u32 taddr, float* v) {
-  u32 r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
-}
-DEVI void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-DEVI void tc_st8(u32 taddr, const float* v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
-               :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-                  "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-                  "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])) : "memory");
-}
-DEVI void tc_st4(u32 taddr, const float* v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
-               :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-                  "r"(__float_as_uint(v[3])) : "memory");
-}
-DEVI u32 elect_one() {
-  u32 p;
-  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n selp.u32 %0, 1, 0, e;\n}" : "=r"(p));
-  return p;
-}
-DEVI void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-// D[tmem] (+)= A[tmem] * B[smem]^T (A: 128 lanes x 8 tf32 columns)
-DEVI void tc_mma_ts(u32 d, u32 a, u64 b, u32 idesc, u32 acc) {
-  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}"
-               :: "r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
-}
-// 3-D TMA tile load global -> shared, completion on an mbarrier (bytes).
-DEVI void tma_load3(void* dst, const TMap* map, int c0, int c1, int c2, u64* bar) {
-  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-               :: "r"(smem_addr(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)) : "memory");
-}
-// Shared-memory matrix descriptor: K-major, 64-byte swizzle (rows of 16 fp32),
-// 8-row groups 512 B apart (SBO), version 1 (sm_100).
-DEVI u64 sdesc64(u32 saddr) {
-  return (u64)((saddr & 0x3FFFFu) >> 4) | ((u64)1 << 16) | ((u64)(512 >> 4) << 32) | ((u64)1 << 46) | ((u64)4 << 61);
-}
-// Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M = 128, N.
-DEVI constexpr u32 idesc_tf32(int n) { return (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(n >> 3) << 17) | ((u32)(128 >> 4) << 24); }
-// tf32 split: hi keeps the top 19 bits (exactly representable), lo the rest.
-DEVI float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
-// Byte offset of 16-byte chunk `chunk` of row m in a K-major SW64 tile (64 B rows).
-DEVI u32 sw64(int m, int chunk) { return (u32)((m >> 3) * 512 + (m & 7) * 64 + ((chunk ^ ((m >> 1) & 3)) << 4)); }
-)";
+  o << uvw_helpers();
   o << "\n// uvw forward: x = " << p.x_ir.str() << " | y = " << p.y_ir.str() << " | z = " << p.z_ir.str() << "\n";
   o << "// " << np << " instructions, " << ns << " z segments, " << nu << " units / 128-row tile, " << na
     << " TMEM A blocks\n";
@@ -279,13 +785,15 @@ DEVI u32 sw64(int m, int chunk) { return (u32)((m >> 3) * 512 + (m & 7) * 64 + (
     << "\n";
 
   // ---- prep kernel: shared W -> per-(instruction, 16-channel block) images
-  o << "extern \"C\" __global__ void cgf_uvw_prep_f32(const float* __restrict__ W, float* __restrict__ img) {\n"
+  const std::string kname = "cgf_uvw_" + tag + "_f32", pname = "cgf_uvw_" + tag + "_prep_f32";
+  o << "extern \"C\" __global__ void " << pname << "(const float* __restrict__ W, float* __restrict__ img) {\n"
        "  const int t = blockIdx.x * blockDim.x + threadIdx.x;\n  int e = t;\n";
   for (int q = 0; q < np; ++q) {
     const auto& s = R[q];
     const int cnt = s.b * s.bp;
     o << "  if (e < " << cnt << ") { const int r = e / " << s.bp << ", c = e % " << s.bp << ", cb = c >> 4, cl = c & 15;\n"
-      << "    const float v = W[" << s.w_off << " + r * " << s.w_stride << " + c]; const float h = tf32_hi(v);\n"
+      << "    const float v = W[" << s.w_off << " + "
+      << (w_transposed ? "c * " + S(s.w_stride) + " + r" : "r * " + S(s.w_stride) + " + c") << "]; const float h = tf32_hi(v);\n"
       << "    char* base = (char*)img + " << wimg_of[q] << " + (size_t)cb * WSLOT;\n"
       << "    const u32 off = sw64(r, cl >> 2) + (cl & 3) * 4;\n"
       << "    *(float*)(base + off) = h; *(float*)(base + " << s.b * kCh * 4 << " + off) = v - h; return; }\n"
@@ -377,7 +885,7 @@ DEVI u32 sw64(int m, int chunk) { return (u32)((m >> 3) * 512 + (m & 7) * 64 + (
   o << "#define NU " << nu << "\n\n";
 
   // ---- the main kernel
-  o << "extern \"C\" __global__ void __launch_bounds__(" << nwarps * 32 << ", 1) cgf_uvw_fwd_f32("
+  o << "extern \"C\" __global__ void __launch_bounds__(" << nwarps * 32 << ", 1) " << kname << "("
        "const __grid_constant__ TMap tx1, const __grid_constant__ TMap tx3, const __grid_constant__ TMap tx5, "
        "const __grid_constant__ TMap tx7, const float* __restrict__ Y, const float* __restrict__ WIMG, "
        "float* __restrict__ Z, i64 rows, unsigned long long* __restrict__ prof) {\n"
@@ -574,19 +1082,21 @@ DEVI u32 sw64(int m, int chunk) { return (u32)((m >> 3) * 512 + (m & 7) * 64 + (
        "}\n";
 
   UvwSource out;
-  out.main.name = "cgf_uvw_fwd_f32";
+  out.main.name = kname;
   out.main.source = o.str();
   out.main.threads = nwarps * 32;
   out.main.smem_bytes = smem;
   out.main.units = nu;
   out.prep = out.main;
-  out.prep.name = "cgf_uvw_prep_f32";
+  out.prep.name = pname;
   out.prep.threads = 256;
   out.prep.smem_bytes = 0;
-  out.main.module = out.prep.module = "cgf_uvw_fwd_f32";
+  out.main.module = out.prep.module = kname;
   out.wimg_bytes = wimg;
   out.dims_x = p.dim_x;
   return out;
 }
+
+}  // namespace
 
 }  // namespace cgf

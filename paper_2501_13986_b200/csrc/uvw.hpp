@@ -33,5 +33,12 @@ struct UvwSource {
 };
 
 UvwSource generate_uvw_forward(const Problem& p);
+// gx of the backward as the forward of the transposed problem (x <-> gz).
+UvwSource generate_uvw_backward_x(const Problem& p);
+// dL/dy of the backward (shared W).
+UvwSource generate_uvw_backward_y(const Problem& p);
+// Shared dL/dW for instructions [first, first + count), count <= 6: per-CTA
+// partials; `prep` is the fixed-order reduction over CTAs.
+UvwSource generate_uvw_backward_w(const Problem& p, int first, int count);
 
 }  // namespace cgf

@@ -202,3 +202,20 @@ def test_c3_tensor_core_matches_simt_path(monkeypatch):
     c = plan.forward(x, y, w, w_shared=True)
     err = ((a - c).norm() / c.norm()).item()
     assert err <= 1e-5, err
+
+
+@pytest.mark.parametrize("rows", [1, 127, 1000, 128 * 150 + 37])
+def test_c3_shared_w_tensor_core_backward(rows):
+    """uvw backward with shared W on tcgen05: gx (transposed forward), gy
+    (gzp = W^T gz on the tensor cores + SIMT contraction) and the shared gW
+    (rows contracted on the tensor cores, per-CTA partials, fixed-order sum)."""
+    js = config("c3")
+    o, plan = O.Oracle(js), P().TpPlan(js)
+    x, y, w, gz, *_ = inputs(o, rows, np.float32, seed=91, w_shared=True)
+    gx, gy, gw = plan.backward(dev(x), dev(y), dev(w), dev(gz), w_shared=True)
+    a, b, c = plan.backward(dev(x), dev(y), dev(w), dev(gz), w_shared=True)
+    assert torch.equal(gx, a) and torch.equal(gy, b) and torch.equal(gw, c)  # deterministic
+    wx, wy, ww = o.backward(x, y, w, gz, w_shared=True)
+    check(host(gx), wx, np.float32, "c3 gx")
+    check(host(gy), wy, np.float32, "c3 gy")
+    check(host(gw).reshape(ww.shape), ww, np.float32, "c3 shared gW")
