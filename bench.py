@@ -386,8 +386,10 @@ def main():
             "algorithmic_bytes_per_launch": kern[dom]["bytes"],
             "per_kernel": {k: {"ms": v["ms"], "GB/s": v["gbs"], "frac": v["gbs"] / peak} for k, v in kern.items()}}
 
-    # End to end through the public API with host buffers: pinned inputs
-    # H2D, forward + backward, all outputs D2H, every step.
+    # End to end through the public API with HOST buffers: the C ABI host
+    # entry points (cgf_tp_forward_host / cgf_tp_backward_host via TpPlan on
+    # numpy arrays) copy each call's inputs in and outputs back, pipelined in
+    # row chunks on two streams; host wall clock around the synchronous calls.
     Re = min(args.e2e_rows, R)
     hx = x[:Re].cpu().pin_memory()
     hy = y[:Re].cpu().pin_memory()
@@ -397,29 +399,27 @@ def main():
     ogx = torch.empty((Re, plan.dim_x), dtype=tdt).pin_memory()
     ogy = torch.empty((Re, plan.dim_y), dtype=tdt).pin_memory()
     ogw = torch.empty((Re, plan.n_w), dtype=tdt).pin_memory()
+    nx_, ny_, nw_, ng_ = hx.numpy(), hy.numpy(), hw.numpy(), hg.numpy()
+    noz, ngx, ngy, ngw = oz.numpy(), ogx.numpy(), ogy.numpy(), ogw.numpy()
 
     def e2e_step():
-        dx, dy, dw, dg = (h.to(dev, non_blocking=True) for h in (hx, hy, hw, hg))
-        zz = plan.forward(dx, dy, dw)
-        a, b, c = plan.backward(dx, dy, dw, dg)
-        for o_, d_ in ((oz, zz), (ogx, a), (ogy, b), (ogw, c)):
-            o_.copy_(d_, non_blocking=True)
+        plan.forward(nx_, ny_, nw_, z=noz)
+        plan.backward(nx_, ny_, nw_, ng_, out=(ngx, ngy, ngw))
 
     for _ in range(2):
         e2e_step()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
     ke = max(3, args.steps // 2)
-    e0.record(stream)
+    t0 = time.perf_counter()
     for _ in range(ke):
         e2e_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ems = torch.tensor([e0.elapsed_time(e1) / ke], device=dev)
+    ems = torch.tensor([(time.perf_counter() - t0) * 1e3 / ke], device=dev)
     if world > 1:
         dist.all_reduce(ems, op=dist.ReduceOp.MAX)
     e2e_val = flops_row * Re * world / (float(ems.item()) / 1e3) / 1e9
-    h2d = (hx.numel() + hy.numel() + hw.numel() + hg.numel()) * es
+    # bytes actually copied: forward (x, y, W in; z out) + backward (x, y, W, gz in; gx, gy, gW out)
+    h2d = (2 * (hx.numel() + hy.numel() + hw.numel()) + hg.numel()) * es
     d2h = (oz.numel() + ogx.numel() + ogy.numel() + ogw.numel()) * es
 
     del x, y, w, gz, z, hx, hy, hw, hg, oz, ogx, ogy, ogw
@@ -459,7 +459,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cb,
             "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "rows_per_step": Re, "path": "pinned host -> TpPlan.forward/backward (C ABI) -> pinned host"},
+                    "rows_per_step": Re, "path": "pinned host arrays -> TpPlan.forward/backward -> cgf_tp_*_host (C ABI; chunked, 2 streams) -> pinned host", "timer": "host wall clock"},
             "gpu_launches": 2 * args.steps,  # TP leg: one forward + one backward kernel per step
             "conv": conv,
             "c3": c3,

@@ -265,17 +265,26 @@ class TpPlan:
                                              rows, int(w_shared)))
         return z
 
-    def backward(self, x, y, w, gz, w_shared=False):
-        """(gx, gy, gw) from gz (TpPlan::backward, engine.cpp:285-295)."""
+    def backward(self, x, y, w, gz, w_shared=False, out=None):
+        """(gx, gy, gw) from gz (TpPlan::backward, engine.cpp:285-295). ``out``:
+        optional preallocated (gx, gy, gw) (e.g. pinned host arrays)."""
         if not _is_torch(x):
             x, y, w, gz = (self._host(a) for a in (x, y, w, gz))
         self._same(x, y, w, gz)
         rows = self._rows(x, y, w, w_shared)
         if tuple(gz.shape) != (rows, self.dim_z):
             raise ShapeError(f"shape mismatch for g_z: expected ({rows}, {self.dim_z}), got {tuple(gz.shape)}")
-        gx = self._empty_like(x, (rows, self.dim_x))
-        gy = self._empty_like(x, (rows, self.dim_y))
-        gw = self._empty_like(x, (1 if w_shared else rows, self.n_w))
+        if out is not None:
+            gx, gy, gw = out
+            for name, a, shp in (("gx", gx, (rows, self.dim_x)), ("gy", gy, (rows, self.dim_y)),
+                                 ("gw", gw, (1 if w_shared else rows, self.n_w))):
+                if tuple(a.shape) != shp:
+                    raise ShapeError(f"shape mismatch for {name}: expected {shp}, got {tuple(a.shape)}")
+            self._same(x, gx, gy, gw)
+        else:
+            gx = self._empty_like(x, (rows, self.dim_x))
+            gy = self._empty_like(x, (rows, self.dim_y))
+            gw = self._empty_like(x, (1 if w_shared else rows, self.n_w))
         dt = _dtype_code(x)
         args = [self._p(a) for a in (x, y, w, gz, gx, gy, gw)]
         if _is_torch(x):

@@ -32,12 +32,26 @@ struct cgf_plan {
   // per-context device buffer of swizzled tf32 W images.
   std::map<std::string, std::shared_ptr<cgf::UvwSource>> uvw;  // by kernel tag
   std::map<std::pair<CUcontext, std::string>, CUdeviceptr> wimg;
+  // host-pointer path: two streams + double-buffered device staging per context
+  struct HostPipe {
+    CUstream s[2] = {nullptr, nullptr};
+    CUdeviceptr buf[2] = {0, 0};
+    std::size_t cap = 0;
+  };
+  std::map<CUcontext, HostPipe> pipes;
+  std::mutex host_mu;
   ~cgf_plan() {
-    for (auto& [key, ptr] : wimg) {
-      CUcontext cur = nullptr;
-      cgf::drv::cuCtxGetCurrent(&cur);
+    CUcontext cur = nullptr;
+    if (cgf::drv::cuCtxGetCurrent) cgf::drv::cuCtxGetCurrent(&cur);
+    for (auto& [key, ptr] : wimg)
       if (cur == key.first) cgf::drv::cuMemFree(ptr);
-    }
+    for (auto& [ctx, pp] : pipes)
+      if (cur == ctx) {
+        for (int k = 0; k < 2; ++k) {
+          if (pp.buf[k]) cgf::drv::cuMemFree(pp.buf[k]);
+          if (pp.s[k]) cgf::drv::cuStreamDestroy(pp.s[k]);
+        }
+      }
   }
 };
 
@@ -559,23 +573,113 @@ struct HostCall {
 
 }  // namespace
 
+}  // extern "C"
+
+namespace {
+
+// Host-pointer path: rows stream through the GPU in chunks on two streams, so
+// one chunk's host->device copy, the previous chunk's kernel and the one
+// before's device->host copy overlap (PCIe is full duplex). Device staging is
+// cached per plan and context. A shared-W backward reduces over all rows, so
+// it runs as one chunk.
+void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, const void* const in[7],
+              void* const out[4]) {
+  const auto& pr = p->problem;
+  const std::size_t es = dtype == CGF_F64 ? 8 : 4;
+  const bool ws = w_shared != 0;
+  const std::size_t iw[7] = {static_cast<std::size_t>(pr.dim_x), static_cast<std::size_t>(pr.dim_y), pr.n_w,
+                             static_cast<std::size_t>(pr.dim_z), static_cast<std::size_t>(pr.dim_x),
+                             static_cast<std::size_t>(pr.dim_y), pr.n_w};
+  const bool irow[7] = {true, true, !ws, true, true, true, !ws};
+  std::size_t ow[4] = {0, 0, 0, 0};
+  bool orow[4] = {true, true, true, true};
+  if (op == CGF_OP_FORWARD) {
+    ow[0] = pr.dim_z;
+  } else {
+    ow[0] = pr.dim_x; ow[1] = pr.dim_y; ow[2] = pr.n_w; orow[2] = !ws;
+    if (op == CGF_OP_DOUBLE_BACKWARD) ow[3] = pr.dim_z;
+  }
+  std::size_t row_words = 0, fixed_words = 0;
+  for (int i = 0; i < 7; ++i)
+    if (in[i]) (irow[i] ? row_words : fixed_words) += iw[i];
+  for (int i = 0; i < 4; ++i)
+    if (out[i]) (orow[i] ? row_words : fixed_words) += ow[i];
+  const bool one_chunk = ws && op != CGF_OP_FORWARD;
+  std::int64_t chunk = rows;
+  if (!one_chunk) {
+    const std::int64_t target = static_cast<std::int64_t>((256ull << 20) / std::max<std::size_t>(1, row_words * es));
+    chunk = std::min<std::int64_t>(rows, std::max<std::int64_t>(4096, target / 128 * 128));
+  }
+  const std::size_t need = (fixed_words + static_cast<std::size_t>(chunk) * row_words) * es + 11 * 256;
+  CUcontext ctx = cgf::ensure_context();
+  std::lock_guard<std::mutex> call_lock(p->host_mu);  // one host call per plan at a time (shared staging)
+  cgf_plan::HostPipe* pipe;
+  {
+    std::lock_guard<std::mutex> g(p->mu);
+    pipe = &p->pipes[ctx];
+  }
+  if (!pipe->s[0]) {
+    CU_CHECK(cgf::drv::cuStreamCreate(&pipe->s[0], CU_STREAM_NON_BLOCKING));
+    CU_CHECK(cgf::drv::cuStreamCreate(&pipe->s[1], CU_STREAM_NON_BLOCKING));
+  }
+  if (pipe->cap < need) {
+    for (int k = 0; k < 2; ++k) {
+      if (pipe->buf[k]) cgf::drv::cuMemFree(pipe->buf[k]);
+      pipe->buf[k] = 0;
+      CU_CHECK(cgf::drv::cuMemAlloc(&pipe->buf[k], need));
+    }
+    pipe->cap = need;
+  }
+  const std::int64_t nchunks = (rows + chunk - 1) / chunk;
+  for (std::int64_t c = 0; c < nchunks; ++c) {
+    const int k = static_cast<int>(c & 1);
+    CUstream st = pipe->s[k];
+    const std::int64_t r0 = c * chunk, n = std::min(chunk, rows - r0);
+    std::size_t off = 0;
+    auto carve = [&](std::size_t words) {
+      const CUdeviceptr d = pipe->buf[k] + off;
+      off += (words * es + 255) / 256 * 256;
+      return d;
+    };
+    void* din[7] = {};
+    for (int i = 0; i < 7; ++i) {
+      if (!in[i]) continue;
+      const std::size_t words = irow[i] ? iw[i] * static_cast<std::size_t>(n) : iw[i];
+      const CUdeviceptr d = carve(irow[i] ? iw[i] * static_cast<std::size_t>(chunk) : iw[i]);
+      din[i] = reinterpret_cast<void*>(d);
+      if (irow[i] || c < 2) {
+        const char* h = static_cast<const char*>(in[i]) + (irow[i] ? es * iw[i] * static_cast<std::size_t>(r0) : 0);
+        CU_CHECK(cgf::drv::cuMemcpyHtoDAsync(d, h, words * es, st));
+      }
+    }
+    void* dout[4] = {};
+    for (int i = 0; i < 4; ++i)
+      if (out[i]) dout[i] = reinterpret_cast<void*>(carve(orow[i] ? ow[i] * static_cast<std::size_t>(chunk) : ow[i]));
+    launch(p, op, dtype, w_shared, n, din[0], din[1], din[2], din[3], din[4], din[5], din[6], dout[0], dout[1], dout[2],
+           dout[3], st);
+    for (int i = 0; i < 4; ++i) {
+      if (!out[i]) continue;
+      const std::size_t words = orow[i] ? ow[i] * static_cast<std::size_t>(n) : ow[i];
+      char* h = static_cast<char*>(out[i]) + (orow[i] ? es * ow[i] * static_cast<std::size_t>(r0) : 0);
+      CU_CHECK(cgf::drv::cuMemcpyDtoHAsync(h, reinterpret_cast<CUdeviceptr>(dout[i]), words * es, st));
+    }
+  }
+  CU_CHECK(cgf::drv::cuStreamSynchronize(pipe->s[0]));
+  CU_CHECK(cgf::drv::cuStreamSynchronize(pipe->s[1]));
+}
+
+}  // namespace
+
+extern "C" {
+
 int cgf_tp_forward_host(cgf_plan* p, int dtype, const void* x, const void* y, const void* w, void* z,
                         int64_t rows, int w_shared) {
   return guarded([&] {
     need(p, "plan");
     if (rows <= 0) return;
-    cgf::ensure_context();
-    const auto& pr = p->problem;
-    HostCall h{dtype == CGF_F64 ? 8u : 4u, {}};
-    const std::size_t R = static_cast<std::size_t>(rows);
-    void* dx = h.in(x, R * pr.dim_x);
-    void* dy = h.in(y, R * pr.dim_y);
-    void* dw = h.in(w, (w_shared ? 1 : R) * pr.n_w);
-    void* dz = h.out(R * pr.dim_z);
-    launch(p, CGF_OP_FORWARD, dtype, w_shared, rows, dx, dy, dw, nullptr, nullptr, nullptr, nullptr, dz,
-           nullptr, nullptr, nullptr, nullptr);
-    CU_CHECK(cgf::drv::cuCtxSynchronize());
-    h.back(z, dz, R * pr.dim_z);
+    const void* in[7] = {x, y, w, nullptr, nullptr, nullptr, nullptr};
+    void* out[4] = {z, nullptr, nullptr, nullptr};
+    run_host(p, CGF_OP_FORWARD, dtype, w_shared, rows, in, out);
   });
 }
 
@@ -584,23 +688,9 @@ int cgf_tp_backward_host(cgf_plan* p, int dtype, const void* x, const void* y, c
   return guarded([&] {
     need(p, "plan");
     if (rows <= 0) return;
-    cgf::ensure_context();
-    const auto& pr = p->problem;
-    HostCall h{dtype == CGF_F64 ? 8u : 4u, {}};
-    const std::size_t R = static_cast<std::size_t>(rows), RW = w_shared ? 1 : R;
-    void* dx = h.in(x, R * pr.dim_x);
-    void* dy = h.in(y, R * pr.dim_y);
-    void* dw = h.in(w, RW * pr.n_w);
-    void* dg = h.in(gz, R * pr.dim_z);
-    void* ox = h.out(R * pr.dim_x);
-    void* oy = h.out(R * pr.dim_y);
-    void* ow = h.out(RW * pr.n_w);
-    launch(p, CGF_OP_BACKWARD, dtype, w_shared, rows, dx, dy, dw, dg, nullptr, nullptr, nullptr, ox, oy, ow,
-           nullptr, nullptr);
-    CU_CHECK(cgf::drv::cuCtxSynchronize());
-    h.back(gx, ox, R * pr.dim_x);
-    h.back(gy, oy, R * pr.dim_y);
-    h.back(gw, ow, RW * pr.n_w);
+    const void* in[7] = {x, y, w, gz, nullptr, nullptr, nullptr};
+    void* out[4] = {gx, gy, gw, nullptr};
+    run_host(p, CGF_OP_BACKWARD, dtype, w_shared, rows, in, out);
   });
 }
 
@@ -610,27 +700,9 @@ int cgf_tp_double_backward_host(cgf_plan* p, int dtype, const void* x, const voi
   return guarded([&] {
     need(p, "plan");
     if (rows <= 0) return;
-    cgf::ensure_context();
-    const auto& pr = p->problem;
-    HostCall h{dtype == CGF_F64 ? 8u : 4u, {}};
-    const std::size_t R = static_cast<std::size_t>(rows), RW = w_shared ? 1 : R;
-    void* dx = h.in(x, R * pr.dim_x);
-    void* dy = h.in(y, R * pr.dim_y);
-    void* dw = h.in(w, RW * pr.n_w);
-    void* dg = h.in(gz, R * pr.dim_z);
-    void* a = h.in(da, R * pr.dim_x);
-    void* b = h.in(db, R * pr.dim_y);
-    void* c = h.in(dc, RW * pr.n_w);
-    void* o0 = h.out(R * pr.dim_x);
-    void* o1 = h.out(R * pr.dim_y);
-    void* o2 = h.out(RW * pr.n_w);
-    void* o3 = h.out(R * pr.dim_z);
-    launch(p, CGF_OP_DOUBLE_BACKWARD, dtype, w_shared, rows, dx, dy, dw, dg, a, b, c, o0, o1, o2, o3, nullptr);
-    CU_CHECK(cgf::drv::cuCtxSynchronize());
-    h.back(ox, o0, R * pr.dim_x);
-    h.back(oy, o1, R * pr.dim_y);
-    h.back(ow, o2, RW * pr.n_w);
-    h.back(ogz, o3, R * pr.dim_z);
+    const void* in[7] = {x, y, w, gz, da, db, dc};
+    void* out[4] = {ox, oy, ow, ogz};
+    run_host(p, CGF_OP_DOUBLE_BACKWARD, dtype, w_shared, rows, in, out);
   });
 }
 

@@ -207,7 +207,7 @@ void Gen::classify() {
     c.sw.assign(a.subs.size(), 0);
     c.xstep.assign(a.x_chunks.size(), 0);
     c.zstep.assign(a.z_pieces.size(), 0);
-    while (u + c.n < nu && same_shape(p_, a, units_[u + c.n])) {
+    while (u + c.n < nu && c.n < cfg_.max_class && same_shape(p_, a, units_[u + c.n])) {
       std::vector<long long> sx, sz, sw, xs, zs;
       diff(units_[u + c.n], sx, sz, sw, xs, zs);
       if (c.n == 1) {
@@ -887,6 +887,7 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "barrier") cfg.sub_barrier = true;
     else if (k == "yreg") cfg.y_regs = true;
     else if (k == "yslot") cfg.y_regs = false;
+    else if (k == "class") cfg.max_class = std::max(1, v);
   }
 }
 

@@ -49,10 +49,11 @@ struct KernelConfig {
   int min_blocks = 0;     // __launch_bounds__ min blocks per SM (0: unset)
   bool sub_barrier = true;  // compiler memory barrier between subkernels
   bool y_regs = false;    // Rows loop: y / db in registers (prefetched) instead of the slot
+  int max_class = 1 << 20;  // max units folded into one code body (1 = fully unrolled units)
 };
 
 // Applies "k=v,flag,..." overrides (env CGF_GEN) to a config: depth=N,
-// warps=N, minb=N, nobarrier, barrier, yreg, yslot.
+// warps=N, minb=N, nobarrier, barrier, yreg, yslot, class=N.
 void apply_gen_flags(KernelConfig& cfg, const std::string& flags);
 
 struct KernelSource {

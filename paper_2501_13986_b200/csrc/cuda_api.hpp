@@ -14,7 +14,7 @@ namespace cgf::drv {
   X(cuDeviceGetAttribute) X(cuLaunchKernel) X(cuMemsetD8Async) X(cuMemAlloc) X(cuMemFree)  \
   X(cuMemcpyHtoD) X(cuMemcpyDtoH) X(cuCtxSynchronize) X(cuMemcpyHtoDAsync)                 \
   X(cuMemcpyDtoHAsync) X(cuStreamSynchronize) X(cuLaunchKernelEx) X(cuFuncGetAttribute)    \
-  X(cuTensorMapEncodeTiled)
+  X(cuTensorMapEncodeTiled) X(cuStreamCreate) X(cuStreamDestroy)
 
 #define CGF_DRV_DECL(fn) extern decltype(&::fn) fn;
 CGF_DRV_FUNCS(CGF_DRV_DECL)
