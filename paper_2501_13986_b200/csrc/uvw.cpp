@@ -276,26 +276,6 @@ const char* grad_kernel_head() {
        "  const i64 ntiles = (rows + 127) / 128;\n";
 }
 
-// x loader warp: x tiles (q, cb) of every unit in order, ring of one slot
-std::string grad_x_loader(const std::string& q_range) {
-  return "  else if (warp == 9) {\n"
-         "    if (lane == 0) {\n"
-         "      u32 gx = 0;\n"
-         "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
-         "        for (int q = " + q_range + "; ++q)\n"
-         "          for (int k = 0; k < P_DZ[q]; ++k)\n"
-         "            for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
-         "              mbar_wait_t(x_empty, (gx & 1u) ^ 1u, 29);\n"
-         "              const int dx = P_DX[q];\n"
-         "              mbar_expect_tx(x_full, 128 * 64 * dx);\n"
-         "              const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
-         "              tma_load3(xs, mp, 0, P_XC[q] + cb * dx, (int)(tile * 128), x_full);\n"
-         "            }\n"
-         "    }\n"
-         "    __syncwarp();\n"
-         "  }\n";
-}
-
 }  // namespace
 
 // dL/dy of a uvw backward with shared W (kernel "cgf_uvw_bwdy_f32"). Per
@@ -309,34 +289,39 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
   const GradInfo g = grad_info(p);
   const auto& R = p.resolved;
   const int np = g.np;
+  int max_dz = 1;
+  for (const auto& sq : R) max_dz = std::max(max_dz, sq.dz());
+  if (64 * max_dz > 512) throw UnsupportedError("uvw gy kernel: l3 too large");
   const int gz_bytes = 2 * kTileRows * 64 * 4;
-  const int smem = 1024 + gz_bytes + g.xslot + 4 * g.wslot + 1024 + 128 * p.dim_y * 4;
+  const int nx = 2;
+  const int smem = 1024 + gz_bytes + nx * g.xslot + 4 * g.wslot + 1024 + 128 * p.dim_y * 4;
   if (smem > 227 * 1024) throw UnsupportedError("uvw gy kernel: shared memory too small");
   std::ostringstream o;
   if (std::getenv("CGF_UVW_DEBUG")) o << "#define CGF_UVW_DEBUG 1\n";
   o << device_runtime_source() << uvw_helpers() << grad_helpers();
   o << "// uvw gy: " << np << " instructions\n#define DIMX " << p.dim_x << "\n#define DIMY " << p.dim_y
     << "\n#define DIMZ " << p.dim_z << "\n#define NP " << np << "\n#define WSLOT " << g.wslot << "\n#define XSLOT "
-    << g.xslot << "\n#define GZB " << gz_bytes << "\n";
+    << g.xslot << "\n#define GZB " << gz_bytes << "\n#define NX " << nx << "\n";
   emit_grad_tables(o, p);
   {
-    std::vector<long long> wi(g.wimg_of.begin(), g.wimg_of.end());
     o << "__constant__ int P_WIMG[" << np << "] = {";
-    for (int q = 0; q < np; ++q) o << (q ? "," : "") << wi[q];
+    for (int q = 0; q < np; ++q) o << (q ? "," : "") << g.wimg_of[q];
     o << "};\n";
   }
+  // per instruction: x once per 16-channel block, then every component k
+  // against gzp_k (TMEM columns 64 k of this thread's lane)
   for (int q = 0; q < np; ++q) {
     const auto& sq = R[q];
     const int dx = sq.dx(), dz = sq.dz();
-    o << "DEVI void gyk_" << q << "(int k, int cb, const unsigned char* xs, int m, int sub, u32 tgzp, float* gy,"
-      << " u64* xempty) {\n";
+    o << "DEVI void gyq_" << q << "(int cb, const unsigned char* xs, int m, int sub, u32 tq, float* gy, u64* xempty) {\n";
     emit_x_read(o, dx);
-    o << "  float gp[8];\n  tc_ld8(tgzp + cb * 16 + 8 * sub, gp);\n  tc_wait_ld();\n  switch (k) {\n";
     for (int k = 0; k < dz; ++k) {
       std::set<int> is;
       for (const auto& e : sq.cg->entries)
         if (e.k == k) is.insert(e.i);
-      o << "  case " << k << ": {\n";
+      if (is.empty()) continue;
+      o << "  { // k = " << k << "\n    float gp[8];\n    tc_ld8(tq + " << 64 * k << " + cb * 16 + 8 * sub, gp);\n"
+        << "    tc_wait_ld();\n";
       for (int i : is) o << "    float xg" << i << " = 0.f;\n";
       o << "#pragma unroll\n    for (int c = 0; c < 8; ++c) {\n";
       for (int i : is) o << "      xg" << i << " = fmaf(xv[c * " << dx << " + " << i << "], gp[c], xg" << i << ");\n";
@@ -345,9 +330,9 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
         if (e.k == k)
           o << "    gy[" << sq.y_off + e.j << "] = fmaf((float)" << hexd(e.v) << ", xg" << e.i << ", gy[" << sq.y_off + e.j
             << "]);\n";
-      o << "    break; }\n";
+      o << "  }\n";
     }
-    o << "  }\n}\n\n";
+    o << "}\n\n";
   }
   o << "extern \"C\" __global__ void __launch_bounds__(352, 1) cgf_uvw_bwdy_f32("
        "const __grid_constant__ TMap tx1, const __grid_constant__ TMap tx3, const __grid_constant__ TMap tx5, "
@@ -355,21 +340,20 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "const float* __restrict__ GZ, float* __restrict__ GY, i64 rows) {\n"
     << grad_kernel_head()
     << "  unsigned char* gzt = sm;                 // gz_k tile [rows][r]: hi [4][128][16], lo after GZB/2\n"
-       "  unsigned char* xs = gzt + GZB;           // x tile (TMA, SW64)\n"
-       "  unsigned char* ws = xs + XSLOT;          // W^T images of one instruction (4 r-blocks)\n"
+       "  unsigned char* xs0 = gzt + GZB;          // x tile ring (TMA, SW64)\n"
+       "  unsigned char* ws = xs0 + NX * XSLOT;    // W^T images of one instruction (4 r-blocks)\n"
        "  u64* bars = (u64*)(ws + 4 * WSLOT);\n"
-       "  u64* gz_full = bars; u64* gz_empty = bars + 1;\n"
-       "  u64* gzp_full = bars + 4; u64* gzp_empty = bars + 6; u64* x_full = bars + 8; u64* x_empty = bars + 9;\n"
-       "  u64* w_full = bars + 10; u64* w_empty = bars + 11;\n"
-       "  u32* tmem_slot = (u32*)(bars + 13);\n"
+       "  u64* gz_full = bars; u64* gz_empty = bars + 1; u64* gzp_full = bars + 2; u64* gzp_empty = bars + 3;\n"
+       "  u64* w_full = bars + 4; u64* w_empty = bars + 5; u64* x_full = bars + 6; u64* x_empty = bars + 6 + NX;\n"
+       "  u32* tmem_slot = (u32*)(bars + 6 + 2 * NX);\n"
        "  float* gys = (float*)(bars + 16);\n"
        "  if (threadIdx.x == 0) {\n"
-       "    mbar_init(gz_full, 8); mbar_init(gz_empty, 1);\n"
-       "    for (int i = 0; i < 2; ++i) { mbar_init(&gzp_full[i], 1); mbar_init(&gzp_empty[i], 8); }\n"
-       "    mbar_init(x_full, 1); mbar_init(x_empty, 8); mbar_init(w_full, 1); mbar_init(w_empty, 1);\n"
+       "    mbar_init(gz_full, 8); mbar_init(gz_empty, 1); mbar_init(gzp_full, 1); mbar_init(gzp_empty, 8);\n"
+       "    mbar_init(w_full, 1); mbar_init(w_empty, 1);\n"
+       "    for (int i = 0; i < NX; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n"
        "    mbar_fence_init();\n  }\n"
        "  if (warp == 8) {\n"
-       "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\" :: \"r\"(smem_addr(tmem_slot)));\n"
+       "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" :: \"r\"(smem_addr(tmem_slot)));\n"
        "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\");\n"
        "  }\n"
        "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n"
@@ -377,14 +361,14 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "  if (warp < 8) {\n"
        "    const int m = 32 * (warp & 3) + lane, sub = warp >> 2;\n"
        "    const u32 tq = tmem + ((u32)(32 * (warp & 3)) << 16);\n"
-       "    u32 ug = 0, gx = 0;\n"
+       "    u32 ug = 0, uq = 0, gx = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
        "      const i64 row = tile * 128 + m;\n"
        "      const bool valid = row < rows;\n"
        "      float gy[DIMY];\n"
        "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) gy[j] = 0.f;\n"
        "      const float* gzr = GZ + (valid ? row : 0) * DIMZ;\n"
-       "#pragma unroll 1\n      for (int q = 0; q < NP; ++q) {\n"
+       "#pragma unroll 1\n      for (int q = 0; q < NP; ++q, ++uq) {\n"
        "        const int dz = P_DZ[q];\n"
        "#pragma unroll 1\n        for (int k = 0; k < dz; ++k, ++ug) {\n"
        "          mbar_wait_t(gz_empty, (ug & 1u) ^ 1u, 20);\n"
@@ -398,20 +382,20 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "            *(float4*)(gzt + off) = make_float4(h[0], h[1], h[2], h[3]);\n"
        "            *(float4*)(gzt + GZB / 2 + off) = make_float4(l[0], l[1], l[2], l[3]);\n          }\n"
        "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(gz_full);\n"
-       "          const u32 buf = ug & 1u;\n"
-       "          mbar_wait_t(&gzp_full[buf], (ug >> 1) & 1u, 22);\n"
-       "          tc_fence_after();\n"
-       "          const u32 tgzp = tq + 64 * buf;\n"
-       "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
-       "            mbar_wait_t(x_full, gx & 1u, 23);\n"
-       "            switch (q) {\n";
-  for (int q = 0; q < np; ++q)
-    o << "              case " << q << ": gyk_" << q << "(k, cb, xs, m, sub, tgzp, gy, x_empty); break;\n";
-  o << "            }\n"
-       "          }\n"
-       "          tc_fence_before();\n          __syncwarp();\n"
-       "          if (lane == 0) mbar_arrive(&gzp_empty[buf]);\n"
        "        }\n"
+       "        mbar_wait_t(gzp_full, uq & 1u, 22);\n"
+       "        tc_fence_after();\n"
+       "#pragma unroll 1\n        for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
+       "          const u32 xsl = gx % NX;\n"
+       "          mbar_wait_t(&x_full[xsl], (gx / NX) & 1u, 23);\n"
+       "          const unsigned char* xs = xs0 + xsl * XSLOT;\n"
+       "          switch (q) {\n";
+  for (int q = 0; q < np; ++q)
+    o << "            case " << q << ": gyq_" << q << "(cb, xs, m, sub, tq, gy, &x_empty[xsl]); break;\n";
+  o << "          }\n"
+       "        }\n"
+       "        tc_fence_before();\n        __syncwarp();\n"
+       "        if (lane == 0) mbar_arrive(gzp_empty);\n"
        "      }\n"
        "      if (sub == 1) {\n#pragma unroll\n        for (int j = 0; j < DIMY; ++j) gys[m * DIMY + j] = gy[j];\n      }\n"
        "      prod_sync();\n"
@@ -423,17 +407,17 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "    const u64 gzh = sdesc64(smem_addr(gzt)), gzl = gzh + (u64)((GZB / 2) >> 4);\n"
        "    const u64 wd = sdesc64(smem_addr(ws));\n"
        "    const u32 id_gzp = idesc_tf32(64);\n"
-       "    u32 ug = 0, wg = 0;\n"
+       "    u32 ug = 0, uq = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
-       "      for (int q = 0; q < NP; ++q, ++wg) {\n"
-       "        mbar_wait_t(w_full, wg & 1u, 25);\n        tc_fence_after();\n"
+       "      for (int q = 0; q < NP; ++q, ++uq) {\n"
+       "        mbar_wait_t(w_full, uq & 1u, 25);\n"
+       "        mbar_wait_t(gzp_empty, (uq & 1u) ^ 1u, 27);\n"
+       "        tc_fence_after();\n"
        "        const int dz = P_DZ[q];\n"
        "        for (int k = 0; k < dz; ++k, ++ug) {\n"
-       "          const u32 buf = ug & 1u;\n"
        "          mbar_wait_t(gz_full, ug & 1u, 26);\n"
-       "          mbar_wait_t(&gzp_empty[buf], ((ug >> 1) & 1u) ^ 1u, 27);\n"
        "          tc_fence_after();\n"
-       "          const u32 dg = tmem + 64 * buf;\n"
+       "          const u32 dg = tmem + 64 * k;\n"
        "          if (elect_one()) {\n"
        "#pragma unroll\n            for (int s = 0; s < 8; ++s) {\n"
        "              const u64 ao = (u64)(((s >> 1) * 8192 + (s & 1) * 32) >> 4);\n"
@@ -442,17 +426,31 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "              tc_mma(dg, gzh + ao, wd + bo + (u64)((64 * 64) >> 4), id_gzp, 1u);\n"
        "              tc_mma(dg, gzl + ao, wd + bo, id_gzp, 1u);\n"
        "            }\n"
-       "            tc_commit(&gzp_full[buf]);\n"
        "            tc_commit(gz_empty);\n"
-       "            if (k == dz - 1) tc_commit(w_empty);\n"
+       "            if (k == dz - 1) { tc_commit(gzp_full); tc_commit(w_empty); }\n"
        "          }\n"
        "          __syncwarp();\n"
        "        }\n"
        "      }\n"
        "    }\n"
        "  }\n"
-    << grad_x_loader("0; q < NP")
-    << "  else if (warp == 10) {\n"
+       "  else if (warp == 9) {\n"
+       "    if (lane == 0) {\n"
+       "      u32 gx = 0;\n"
+       "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
+       "        for (int q = 0; q < NP; ++q)\n"
+       "          for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
+       "            const u32 xsl = gx % NX;\n"
+       "            mbar_wait_t(&x_empty[xsl], ((gx / NX) & 1u) ^ 1u, 29);\n"
+       "            const int dx = P_DX[q];\n"
+       "            mbar_expect_tx(&x_full[xsl], 128 * 64 * dx);\n"
+       "            const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
+       "            tma_load3(xs0 + xsl * XSLOT, mp, 0, P_XC[q] + cb * dx, (int)(tile * 128), &x_full[xsl]);\n"
+       "          }\n"
+       "    }\n"
+       "    __syncwarp();\n"
+       "  }\n"
+       "  else if (warp == 10) {\n"
        "    if (lane == 0) {\n"
        "      u32 wg = 0;\n"
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
@@ -465,7 +463,7 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "    __syncwarp();\n"
        "  }\n"
        "  tc_fence_before();\n  __syncthreads();\n"
-       "  if (warp == 8) { tc_fence_after(); asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\" :: \"r\"(tmem)); }\n"
+       "  if (warp == 8) { tc_fence_after(); asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\" :: \"r\"(tmem)); }\n"
        "}\n";
   UvwSource out;
   out.main.name = out.main.module = "cgf_uvw_bwdy_f32";
@@ -491,7 +489,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   const auto& R = p.resolved;
   if (count < 1 || count > 6 || first < 0 || first + count > g.np) throw std::logic_error("bad gW instruction range");
   const int tb = 2 * 64 * kTileRows * 4;  // hi + lo of a [64][128 rows] K-major tile
-  const int smem = 1024 + 2 * tb + g.xslot + 1024;
+  const int smem = 1024 + 2 * tb + 2 * g.xslot + 1024;
   if (smem > 227 * 1024) throw UnsupportedError("uvw gW kernel: shared memory too small");
   const std::string kname = "cgf_uvw_bwdw" + S(first) + "_f32";
   std::ostringstream o;
@@ -537,14 +535,14 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
     << grad_kernel_head()
     << "  unsigned char* gzt = sm;                 // gz_k tile [r][rows] K-major: hi, lo after TB/2\n"
        "  unsigned char* zt = sm + TB;             // z'_k tile [c][rows] K-major\n"
-       "  unsigned char* xs = zt + TB;             // x tile (TMA, SW64)\n"
-       "  u64* bars = (u64*)(xs + XSLOT);\n"
+       "  unsigned char* xs0 = zt + TB;            // x tile ring of 2 (TMA, SW64)\n"
+       "  u64* bars = (u64*)(xs0 + 2 * XSLOT);\n"
        "  u64* gz_full = bars; u64* gz_empty = bars + 1; u64* z_full = bars + 2; u64* z_empty = bars + 3;\n"
-       "  u64* x_full = bars + 8; u64* x_empty = bars + 9; u64* done = bars + 12;\n"
+       "  u64* x_full = bars + 8; u64* x_empty = bars + 10; u64* done = bars + 12;\n"
        "  u32* tmem_slot = (u32*)(bars + 13);\n"
        "  if (threadIdx.x == 0) {\n"
        "    mbar_init(gz_full, 8); mbar_init(gz_empty, 1); mbar_init(z_full, 8); mbar_init(z_empty, 1);\n"
-       "    mbar_init(x_full, 1); mbar_init(x_empty, 8); mbar_init(done, 1);\n"
+       "    for (int i = 0; i < 2; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n    mbar_init(done, 1);\n"
        "    mbar_fence_init();\n  }\n"
        "  if (warp == 8) {\n"
        "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" :: \"r\"(smem_addr(tmem_slot)));\n"
@@ -573,10 +571,12 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(gz_full);\n"
        "          mbar_wait_t(z_empty, (ug & 1u) ^ 1u, 21);\n"
        "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
-       "            mbar_wait_t(x_full, gx & 1u, 23);\n"
+       "            const u32 xsl = gx & 1u;\n"
+       "            mbar_wait_t(&x_full[xsl], (gx >> 1) & 1u, 23);\n"
+       "            const unsigned char* xs = xs0 + xsl * XSLOT;\n"
        "            switch (q) {\n";
   for (int q = first; q < first + count; ++q)
-    o << "              case " << q << ": zw_" << q << "(k, cb, xs, yv, m, sub, zt, x_empty); break;\n";
+    o << "              case " << q << ": zw_" << q << "(k, cb, xs, yv, m, sub, zt, &x_empty[xsl]); break;\n";
   o << "            }\n"
        "          }\n"
        "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(z_full);\n"
@@ -630,7 +630,23 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "    }\n"
        "    if (elect_one()) tc_commit(done);\n    __syncwarp();\n"
        "  }\n"
-    << grad_x_loader("Q0; q < Q1")
+    << "  else if (warp == 9) {\n"
+       "    if (lane == 0) {\n"
+       "      u32 gx = 0;\n"
+       "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
+       "        for (int q = Q0; q < Q1; ++q)\n"
+       "          for (int k = 0; k < P_DZ[q]; ++k)\n"
+       "            for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
+       "              const u32 xsl = gx & 1u;\n"
+       "              mbar_wait_t(&x_empty[xsl], ((gx >> 1) & 1u) ^ 1u, 29);\n"
+       "              const int dx = P_DX[q];\n"
+       "              mbar_expect_tx(&x_full[xsl], 128 * 64 * dx);\n"
+       "              const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
+       "              tma_load3(xs0 + xsl * XSLOT, mp, 0, P_XC[q] + cb * dx, (int)(tile * 128), &x_full[xsl]);\n"
+       "            }\n"
+       "    }\n"
+       "    __syncwarp();\n"
+       "  }\n"
     << "  tc_fence_before();\n  __syncthreads();\n"
        "  if (warp == 8) { tc_fence_after(); asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\" :: \"r\"(tmem)); }\n"
        "}\n";
@@ -775,6 +791,9 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
   std::ostringstream o;
   if (std::getenv("CGF_UVW_DEBUG")) o << "#define CGF_UVW_DEBUG 1\n";
   if (std::getenv("CGF_UVW_PROF")) o << "#define CGF_UVW_PROF 1\n";
+  // experiment knobs (A/B only): 1 = epilogue skips stores, 2 = one MMA pass
+  // instead of three, 4 = producers skip the TMEM stores
+  o << "#define UVW_EXP " << (std::getenv("CGF_UVW_EXP") ? std::atoi(std::getenv("CGF_UVW_EXP")) : 0) << "\n";
   o << device_runtime_source();
   o << uvw_helpers();
   o << "\n// uvw forward: x = " << p.x_ir.str() << " | y = " << p.y_ir.str() << " | z = " << p.z_ir.str() << "\n";
@@ -837,7 +856,7 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
       << "; ++i) z = fmaf(q[k][i], xv[c * " << dx << " + i], z);\n"
       << "      h[c] = tf32_hi(z); l[c] = z - h[c];\n    }\n"
       << "    const u32 ta = tq + ACOL0 + 32 * slot + " << cpt << " * sub;\n"
-      << "    tc_st" << cpt << "(ta, h); tc_st" << cpt << "(ta + 16, l);\n"
+      << "    if (!(UVW_EXP & 4)) { tc_st" << cpt << "(ta, h); tc_st" << cpt << "(ta + 16, l); }\n"
       << "    tc_wait_st();\n    tc_fence_before();\n"
       << "    __syncwarp();\n    if ((threadIdx.x & 31) == 0) mbar_arrive(&afull[slot]);\n"
       << "    if (++slot == NS) { slot = 0; ph ^= 1u; }\n  }\n}\n\n";
@@ -981,10 +1000,12 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
        // 3xTF32: hi*hi + hi*lo + lo*hi, two K=8 steps (A: +8 columns, B: +32 B) each
        "              tc_mma_ts(d, ah, bh, idesc, first ? 0u : 1u);\n"
        "              tc_mma_ts(d, ah + 8, bh + 2, idesc, 1u);\n"
+       "              if (!(UVW_EXP & 2)) {\n"
        "              tc_mma_ts(d, ah, bl, idesc, 1u);\n"
        "              tc_mma_ts(d, ah + 8, bl + 2, idesc, 1u);\n"
        "              tc_mma_ts(d, al, bh, idesc, 1u);\n"
        "              tc_mma_ts(d, al + 8, bh + 2, idesc, 1u);\n"
+       "              }\n"
        "              tc_commit(&aempty[slot]);\n"
        "            }\n"
        "            __syncwarp();\n"
@@ -1056,7 +1077,7 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
       << "          float v[" << sg.dz << "][8];\n";
     for (int k = 0; k < sg.dz; ++k)
       o << "          tc_ld8(tq + (u32)(" << sg.col + k * sg.n << " + r0), v[" << k << "]);\n";
-    o << "          tc_wait_ld();\n          if (valid) {\n            float4* dst = (float4*)(zr + r0 * " << sg.dz << ");\n";
+    o << "          tc_wait_ld();\n          if (valid && !(UVW_EXP & 1)) {\n            float4* dst = (float4*)(zr + r0 * " << sg.dz << ");\n";
     for (int t = 0; t < 2 * sg.dz; ++t) {
       o << "            __stcs(dst + " << t << ", make_float4(";
       for (int a = 0; a < 4; ++a) {
