@@ -38,6 +38,15 @@ DEVI void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
 }
+// 16-byte async copy global -> shared by one thread (LDGSTS, L2 only).
+DEVI void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_addr(dst)), "l"(src) : "memory");
+}
+// Arrive on the mbarrier once all of this thread's prior cp.async completed
+// (the barrier counts one arrival per lane).
+DEVI void cp_async_arrive(u64* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(smem_addr(b)) : "memory");
+}
 template <class T> DEVI void coop_load(T* dst, const T* __restrict__ src, int n, int lane) {
   for (int i = lane; i < n; i += 32) dst[i] = __ldg(src + i);
 }
@@ -333,15 +342,18 @@ std::string Gen::range_src(const SlotRange& r) const {
 // issue_unit(u, ...): arm the slot's mbarrier with the item's byte count and
 // start its bulk copies. u is the flat unit index -> (class, kc).
 void Gen::emit_issue() {
+  const bool lc = cfg_.lane_copy;
   o_ << "__device__ __noinline__ void issue_unit(int u, i64 row, i64 nbr, i64 eid, i64 rows_tot, i64 edges_tot, T* sl,"
         " u64* bar, const T* __restrict__ X, const T* __restrict__ Y, const T* __restrict__ W,"
-        " const T* __restrict__ GZ, const T* __restrict__ DA, const T* __restrict__ DB, const T* __restrict__ DC) {\n"
-        "  (void)nbr; (void)eid; (void)rows_tot; (void)edges_tot;\n  fence_proxy_async();\n";
+        " const T* __restrict__ GZ, const T* __restrict__ DA, const T* __restrict__ DB, const T* __restrict__ DC"
+     << (lc ? ", int lane" : "") << ") {\n"
+        "  (void)nbr; (void)eid; (void)rows_tot; (void)edges_tot;\n"
+     << (lc ? "" : "  fence_proxy_async();\n");
   for (size_t k = 0; k < cls_.size(); ++k) {
     const UClass& C = cls_[k];
     const Layout& L = lay_[k];
     o_ << "  " << (k ? "else " : "") << "if (u < " << C.u0 + C.n << ") {\n    const int kc = u - " << C.u0
-       << "; (void)kc;\n    u32 tx = " << L.fixed_bulk_bytes << "u;\n";
+       << "; (void)kc;\n    u32 tx = " << L.fixed_bulk_bytes << "u; (void)tx;\n";
     for (const auto& r : L.ranges)
       if (r.bulk && r.window) {
         const std::string I = r.src == Src::Edge ? "eid" : "row";
@@ -352,17 +364,53 @@ void Gen::emit_issue() {
            << " * (i64)" << r.stride << ";\n    if (ok_" << r.arr << ") tx += (u32)((a1_" << r.arr << " - a0_" << r.arr
            << ") * sizeof(T));\n";
       }
-    o_ << "    mbar_expect_tx(bar, tx);\n";
+    if (!lc) o_ << "    mbar_expect_tx(bar, tx);\n";
     for (const auto& r : L.ranges) {
       if (!r.bulk) continue;
+      if (lc) {
+        // window ranges (y): the lanes copy the 16-byte aligned window
+        if (r.window)
+          o_ << "    if (ok_" << r.arr << ") { const int n16 = (int)((a1_" << r.arr << " - a0_" << r.arr
+             << ") * sizeof(T) / 16); for (int c = lane; c < n16; c += 32) cp_async16((char*)(sl + " << r.slot_off
+             << ") + 16 * c, (const char*)(" << r.arr << " + a0_" << r.arr << ") + 16 * c); }\n";
+        continue;  // fixed ranges: packed 32 pieces per pass below
+      }
       if (r.window)
         o_ << "    if (ok_" << r.arr << ") bulk_g2s(sl + " << r.slot_off << ", " << r.arr << " + a0_" << r.arr
            << ", (u32)((a1_" << r.arr << " - a0_" << r.arr << ") * sizeof(T)), bar);\n";
       else
         o_ << "    bulk_g2s(sl + " << r.slot_off << ", " << range_src(r) << ", " << r.words * sz_ << "u, bar);\n";
     }
+    if (lc) {
+      // every fixed range's 16-byte pieces, packed across the warp: pass t
+      // gives lane l piece 32 t + l of the concatenated list
+      std::vector<std::pair<int, int>> pieces;  // (range, piece)
+      for (size_t ri = 0; ri < L.ranges.size(); ++ri) {
+        const auto& r = L.ranges[ri];
+        if (!r.bulk || r.window) continue;
+        for (std::uint32_t c = 0; c < r.words * sz_ / 16; ++c) pieces.emplace_back(static_cast<int>(ri), static_cast<int>(c));
+      }
+      for (size_t t0 = 0; t0 < pieces.size(); t0 += 32) {
+        const size_t t1 = std::min(pieces.size(), t0 + 32);
+        o_ << "    { const char* s_ = nullptr; char* d_ = nullptr; int c_ = 0;\n";
+        size_t a = t0;
+        bool first = true;
+        while (a < t1) {
+          size_t b = a;
+          while (b < t1 && pieces[b].first == pieces[a].first) ++b;
+          const auto& r = L.ranges[pieces[a].first];
+          o_ << "      " << (first ? "" : "else ") << "if (lane < " << b - t0 << ") { s_ = (const char*)(" << range_src(r)
+             << "); d_ = (char*)(sl + " << r.slot_off << "); c_ = lane - " << static_cast<long long>(a - t0) + 0 << " + "
+             << pieces[a].second << "; }\n";
+          first = false;
+          a = b;
+        }
+        o_ << "      if (lane < " << t1 - t0 << ") cp_async16(d_ + 16 * c_, s_ + 16 * c_); }\n";
+      }
+    }
     o_ << "  }\n";
   }
+  if (lc) o_ << "  cp_async_arrive(bar);\n";
   o_ << "}\n\n";
 }
 
@@ -396,7 +444,7 @@ void Gen::emit_wait_and_sync(int k) {
 }
 
 void Gen::emit_release() {
-  o_ << "      __syncwarp();\n      if (lane == 0) producer_next();\n"
+  o_ << "      __syncwarp();\n      " << (cfg_.lane_copy ? "" : "if (lane == 0) ") << "producer_next();\n"
         "      if (++slot == D) { slot = 0; phase ^= 1u; }\n";
 }
 
@@ -620,9 +668,9 @@ void Gen::emit_rows_loop() {
         "#define producer_next() do { if (pn < total) {\\\n"
         "    const i64 rr_ = pn / NU; const int u_ = (int)(pn - rr_ * NU); const i64 r_ = gwarp + rr_ * nwarp;\\\n"
         "    const int s_ = (int)(pn % D);\\\n"
-        "    issue_unit(u_, r_, r_, r_, rows, rows, wsm + s_ * SLOT_WORDS, &bars[s_], X, Y, W, GZ, DA, DB, DC);\\\n"
+        "    issue_unit(u_, r_, r_, r_, rows, rows, wsm + s_ * SLOT_WORDS, &bars[s_], X, Y, W, GZ, DA, DB, DC" << (cfg_.lane_copy ? ", lane" : "") << ");\\\n"
         "    ++pn; } } while (0)\n"
-        "  if (lane == 0) for (int d = 0; d < D; ++d) producer_next();\n"
+        "  " << (cfg_.lane_copy ? "" : "if (lane == 0) ") << "for (int d = 0; d < D; ++d) producer_next();\n"
         "  int slot = 0; u32 phase = 0;\n"
         "  for (i64 rr = 0; rr < my_rows; ++rr) {\n    const i64 row = gwarp + rr * nwarp;\n"
         "    const i64 nbr = row, eid = row; (void)nbr; (void)eid;\n";
@@ -709,16 +757,16 @@ void Gen::emit_conv_loop() {
         "#define prow(k) (gwarp + (k) * nwarp)\n"
         "#define seek() do { while (pk < my_rows) { const i64 r_ = prow(pk); pq0 = pq = RP[r_]; pq1 = RP[r_ + 1]; if (pq < pq1) break; ++pk; } } while (0)\n"
         "#define fetch_idx() do { if (pk < my_rows) { pnb = NB[pq]; peid = " << (bi ? "EID[pq]" : "pq") << "; } } while (0)\n"
-        "  if (lane == 0) { seek(); fetch_idx(); }\n"
+        "  " << (cfg_.lane_copy ? "" : "if (lane == 0) ") << "{ seek(); fetch_idx(); }\n"
         "  int pslot = 0;\n"
         "#define producer_next() do { if (pk < my_rows) {\\\n"
         "    const i64 r_ = prow(pk);\\\n"
-        "    issue_unit(pu, r_, pnb, peid, rows, edges_tot, wsm + pslot * SLOT_WORDS, &bars[pslot], X, Y, W, GZ, DA, DB, DC);\\\n"
+        "    issue_unit(pu, r_, pnb, peid, rows, edges_tot, wsm + pslot * SLOT_WORDS, &bars[pslot], X, Y, W, GZ, DA, DB, DC" << (cfg_.lane_copy ? ", lane" : "") << ");\\\n"
         "    if (++pslot == D) pslot = 0;\\\n";
   o_ << (bi ? "    if (++pu == NU) { pu = 0; if (++pq == pq1) { ++pk; seek(); } fetch_idx(); }\\\n"
             : "    if (++pq == pq1) { pq = pq0; if (++pu == NU) { pu = 0; ++pk; seek(); } } fetch_idx();\\\n");
   o_ << "  } } while (0)\n"
-        "  if (lane == 0) for (int d = 0; d < D; ++d) producer_next();\n"
+        "  " << (cfg_.lane_copy ? "" : "if (lane == 0) ") << "for (int d = 0; d < D; ++d) producer_next();\n"
         "  int slot = 0; u32 phase = 0;\n"
         "  for (i64 k = 0; k < my_rows; ++k) {\n    const i64 row = prow(k);\n"
         "    const i64 q0 = RP[row], q1 = RP[row + 1];\n";
@@ -856,7 +904,7 @@ KernelSource Gen::run() {
   if (by_input())
     o_ << "  T* gxs = scr + " << off_gxs_ << ";\n  for (int j = lane; j < " << p_.dim_x << "; j += 32) gxs[j] = 0;\n";
   o_ << "  u64* bars = (u64*)(smem_raw + NW * WARP_BYTES) + wid * D;\n"
-        "  if (lane == 0) { for (int d = 0; d < D; ++d) mbar_init(&bars[d], 1); mbar_fence_init(); }\n"
+        "  if (lane == 0) { for (int d = 0; d < D; ++d) mbar_init(&bars[d], " << (cfg_.lane_copy ? 32 : 1) << "); mbar_fence_init(); }\n"
         "  __syncwarp();\n"
         "  const i64 gwarp = (i64)blockIdx.x * NW + wid, nwarp = (i64)gridDim.x * NW;\n"
         "  const i64 my_rows = gwarp < rows ? (rows - 1 - gwarp) / nwarp + 1 : 0;\n"
@@ -888,6 +936,8 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "yreg") cfg.y_regs = true;
     else if (k == "yslot") cfg.y_regs = false;
     else if (k == "class") cfg.max_class = std::max(1, v);
+    else if (k == "bulk") cfg.lane_copy = false;
+    else if (k == "lanecopy") cfg.lane_copy = true;
   }
 }
 
