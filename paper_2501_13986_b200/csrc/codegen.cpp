@@ -937,12 +937,48 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "yslot") cfg.y_regs = false;
     else if (k == "class") cfg.max_class = std::max(1, v);
     else if (k == "bulk") cfg.lane_copy = false;
+    else if (k == "merge") cfg.merge = std::max(1, v);
     else if (k == "lanecopy") cfg.lane_copy = true;
   }
 }
 
+namespace {
+// Merges runs of up to `m` consecutive same-shape units (the 32-lane chunks of
+// the same instructions) into one unit: one staging item and one code body
+// then cover m chunks, so the per-item bookkeeping and the lane-uniform CG
+// products (v * y[j], shared by every chunk) are paid once per m chunks.
+std::vector<Unit> merge_units(const Problem& p, const std::vector<Unit>& units, int m) {
+  if (m <= 1) return units;
+  std::vector<Unit> out;
+  size_t i = 0;
+  while (i < units.size()) {
+    size_t j = i + 1;
+    while (j < units.size() && static_cast<int>(j - i) < m && same_shape(p, units[i], units[j])) ++j;
+    Unit u = units[i];
+    for (size_t k = i + 1; k < j; ++k) {
+      const Unit& v = units[k];
+      u.subs.insert(u.subs.end(), v.subs.begin(), v.subs.end());
+      for (const auto& c : v.x_chunks) {
+        bool have = false;
+        for (const auto& e : u.x_chunks) have = have || e.off == c.off;
+        if (!have) u.x_chunks.push_back(c);
+      }
+      for (const auto& z : v.z_pieces) {
+        bool have = false;
+        for (const auto& e : u.z_pieces) have = have || e.off == z.off;
+        if (!have) u.z_pieces.push_back(z);
+      }
+    }
+    out.push_back(std::move(u));
+    i = j;
+  }
+  return out;
+}
+}  // namespace
+
 KernelSource generate_kernel(const Problem& p, const std::vector<Unit>& units, const KernelConfig& cfg) {
-  Gen g(p, units, cfg);
+  const std::vector<Unit> merged = merge_units(p, units, cfg.merge);
+  Gen g(p, merged, cfg);
   return g.run();
 }
 

@@ -50,12 +50,14 @@ struct KernelConfig {
   bool sub_barrier = true;  // compiler memory barrier between subkernels
   bool y_regs = false;    // Rows loop: y / db in registers (prefetched) instead of the slot
   int max_class = 1 << 20;  // max units folded into one code body (1 = fully unrolled units)
+  int merge = 1;            // chunks (same-shape units) per staged item and code body
   bool lane_copy = true;    // stage inputs with per-lane 16-byte cp.async (whole warp) instead of
                             // one lane's cp.async.bulk: no single-lane issue loop per range
 };
 
 // Applies "k=v,flag,..." overrides (env CGF_GEN) to a config: depth=N,
-// warps=N, minb=N, nobarrier, barrier, yreg, yslot, class=N, bulk (one-lane bulk copies), lanecopy.
+// warps=N, minb=N, nobarrier, barrier, yreg, yslot, class=N, bulk (one-lane bulk copies), lanecopy,
+// merge=N.
 void apply_gen_flags(KernelConfig& cfg, const std::string& flags);
 
 struct KernelSource {
