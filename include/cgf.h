@@ -176,16 +176,86 @@ int cgf_conv_double_backward(cgf_plan* plan, int dtype, int64_t nodes, int64_t e
                              void* o_node_x, void* o_edge_y, void* o_edge_w, void* o_g_node_z, int mode,
                              void* stream);
 
+/* ---- atomic-mode convolution (ConvPlan Mode::atomic, conv.hpp:70,
+ * conv.cpp:311-324 and 470-486) -------------------------------------------
+ * The graph is an edge list in ANY order: edge e = (src[e], dst[e]), int32.
+ * No sorting, CSR or transposed permutation. One warp item per (edge, unit);
+ * node_z[src] and g_node_x[dst] accumulate with float atomics (16-byte vector
+ * reductions in FP32), so results vary in the last bits between runs; per-edge
+ * gradients are written directly. The double-backward runs in one pass.
+ * The CSR entry points above also accept mode = CGF_CONV_ATOMIC: they expand
+ * row_ptr to per-edge sources on the device and call these. */
+int cgf_conv_forward_atomic(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                            const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                            void* node_z, void* stream);
+int cgf_conv_backward_atomic(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                             const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                             const void* g_node_z, void* g_node_x, void* g_edge_y, void* g_edge_w, void* stream);
+int cgf_conv_double_backward_atomic(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                                    const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                                    const void* g_node_z, const void* d_gx, const void* d_gy, const void* d_gw,
+                                    void* o_node_x, void* o_edge_y, void* o_edge_w, void* o_g_node_z, void* stream);
+
 /* Host-pointer variants (copies in and out, default stream, synchronous). The
- * transposed CSR for the backward is built internally. mode may be
- * CGF_CONV_ATOMIC: it is served by the deterministic kernels, which meet the
- * atomic mode's contract (ConvPlan Mode::atomic, conv.hpp:70). */
+ * transposed CSR for the backward is built internally. With mode =
+ * CGF_CONV_ATOMIC the CSR variants run the atomic kernels. */
 int cgf_conv_forward_host(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
                           const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
                           void* node_z, int mode);
 int cgf_conv_backward_host(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
                            const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
                            const void* g_node_z, void* g_node_x, void* g_edge_y, void* g_edge_w, int mode);
+/* Host-pointer atomic mode over an edge list in any order (the shim's
+ * ConvPlan Mode::atomic path: no sortedness requirement, conv.cpp:240). */
+int cgf_conv_forward_atomic_host(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                                 const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                                 void* node_z);
+int cgf_conv_backward_atomic_host(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                                  const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                                  const void* g_node_z, void* g_node_x, void* g_edge_y, void* g_edge_w);
+
+/* ---- unfused comparator (conv::unfused_forward / unfused_backward,
+ * conv.cpp:530-616) on the GPU -----------------------------------------------
+ * Gathers node rows per edge (|E| x dim_x, and |E| x dim_z of g_node_z for the
+ * backward), runs the batched TP kernels over |E| rows, and sums the per-edge
+ * rows into the nodes in edge order (deterministic segmented sums over the
+ * CSR / transposed CSR). Stream-ordered device scratch of |E| (dim_x + dim_z)
+ * words (backward: |E| (2 dim_x + dim_z)); it exists to quantify what the
+ * fused kernels save. */
+int cgf_conv_unfused_forward(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                             const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
+                             void* node_z, void* stream);
+int cgf_conv_unfused_backward(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                              const int32_t* nbr, const int64_t* t_row_ptr, const int32_t* t_eid, const void* node_x,
+                              const void* edge_y, const void* edge_w, const void* g_node_z, void* g_node_x,
+                              void* g_edge_y, void* g_edge_w, void* stream);
+/* Host-pointer variants over an edge list in any order (the reference's
+ * unfused_forward / unfused_backward take any GraphCSR edge order). */
+int cgf_conv_unfused_forward_host(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                                  const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                                  void* node_z);
+int cgf_conv_unfused_backward_host(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                                   const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                                   const void* g_node_z, void* g_node_x, void* g_edge_y, void* g_edge_w);
+
+/* ---- graph construction on the device (conv.cpp:64-151) ------------------
+ * Device pointers; the calls returning a count synchronise `stream`.
+ * cgf_graph_make = conv::make_graph (conv.cpp:64-87): validates (the first
+ * offending edge decides: "make_graph: edge endpoint out of range" /
+ * "make_graph: self-loop (s)", CGF_E_INVALID), sorts by (src, dst), removes
+ * duplicates. row_ptr[nodes + 1]; nbr / out_src (nullable) need room for
+ * `edges` entries; *out_edges = the deduplicated count.
+ * cgf_graph_transpose = transpose_permutation (conv.cpp:135-151) as a
+ * transposed CSR (see cgf_conv_transpose_shard_host).
+ * cgf_graph_radius = conv::radius_graph (conv.cpp:89-133) over pos[n][3]
+ * (FP64): *out_edges = |E|; with nbr == NULL it only counts, else nbr needs
+ * cap >= |E| entries and row_ptr[n + 1] is written. */
+int cgf_graph_make(int64_t nodes, int64_t edges, const int32_t* src, const int32_t* dst, int allow_self_loops,
+                   int64_t* row_ptr, int32_t* nbr, int32_t* out_src, int64_t* out_edges, void* stream);
+int cgf_graph_transpose(int64_t out_nodes, int64_t in_nodes, int64_t edges, const int64_t* row_ptr,
+                        const int32_t* nbr, int64_t* t_row_ptr, int32_t* t_src, int32_t* t_eid, void* stream);
+int cgf_graph_radius(int64_t n, const double* pos, double r_cut, int64_t* row_ptr, int32_t* nbr, int64_t cap,
+                     int64_t* out_edges, void* stream);
 
 /* ---- sharded convolution (multi-GPU, destination-partitioned) ------------
  * One rank owns a contiguous range of out_nodes output nodes and their edges

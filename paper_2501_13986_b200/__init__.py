@@ -27,9 +27,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcgf.so")
 
 __all__ = [
-    "TpPlan", "ConvPlan", "Graph", "cg_block", "lib", "CgfError", "ParseError", "ValidationError", "ShapeError",
+    "TpPlan", "ConvPlan", "Graph", "DeviceGraph", "make_graph_device", "radius_graph_device", "cg_block", "lib", "CgfError", "ParseError", "ValidationError", "ShapeError",
     "BudgetError", "TriangleError", "InvalidArgument", "CudaError", "JitError",
-    "UnsupportedError", "F32", "F64", "OP_FORWARD", "OP_BACKWARD", "OP_DOUBLE_BACKWARD",
+    "UnsupportedError", "F32", "F64", "OP_FORWARD", "OP_BACKWARD", "OP_DOUBLE_BACKWARD", "DETERMINISTIC", "ATOMIC",
 ]
 
 F32, F64 = 0, 1
@@ -122,6 +122,18 @@ def lib():
     L.cgf_conv_forward_shard.argtypes = [P, I, I64, I64, I64, P, P, P, P, P, P, I, P]
     L.cgf_conv_backward_shard.argtypes = [P, I, I64, I64, I64] + [P] * 10 + [I, P]
     L.cgf_conv_double_backward_shard.argtypes = [P, I, I64, I64, I64] + [P] * 16 + [I, P]
+    L.cgf_conv_forward_atomic.argtypes = [P, I, I64, I64] + [P] * 6 + [P]
+    L.cgf_conv_backward_atomic.argtypes = [P, I, I64, I64] + [P] * 9 + [P]
+    L.cgf_conv_double_backward_atomic.argtypes = [P, I, I64, I64] + [P] * 13 + [P]
+    L.cgf_conv_forward_atomic_host.argtypes = [P, I, I64, I64] + [P] * 6
+    L.cgf_conv_backward_atomic_host.argtypes = [P, I, I64, I64] + [P] * 9
+    L.cgf_conv_unfused_forward.argtypes = [P, I, I64, I64] + [P] * 6 + [P]
+    L.cgf_conv_unfused_backward.argtypes = [P, I, I64, I64] + [P] * 11 + [P]
+    L.cgf_conv_unfused_forward_host.argtypes = [P, I, I64, I64] + [P] * 6
+    L.cgf_conv_unfused_backward_host.argtypes = [P, I, I64, I64] + [P] * 9
+    L.cgf_graph_make.argtypes = [I64, I64, P, P, I, P, P, P, P, P]
+    L.cgf_graph_transpose.argtypes = [I64, I64, I64, P, P, P, P, P, P]
+    L.cgf_graph_radius.argtypes = [I64, P, C.c_double, P, P, I64, P, P]
     _lib = L
     return L
 
@@ -322,15 +334,17 @@ class TpPlan:
 # ------------------------------------------------------------ convolution --
 
 COMP_FWD, COMP_BWD, COMP_DBWD, COMP_DBWD_Z, COMP_DBWD_X = range(5)
-LOOP_ROWS, LOOP_CONV_BY_OUTPUT, LOOP_CONV_BY_INPUT = range(3)
+LOOP_ROWS, LOOP_CONV_BY_OUTPUT, LOOP_CONV_BY_INPUT, LOOP_CONV_EDGES = range(4)
 DETERMINISTIC, ATOMIC = 0, 1
 
 
 class Graph:
-    """The reference's GraphCSR (conv.hpp:44-50): edges sorted strictly by
-    (src, dst); ``src`` is the output node of an edge, ``nbr`` (reference
-    ``dst``) the node whose features it reads. Holds host arrays and uploads
-    CSR + transposed CSR to a device on first use."""
+    """The reference's GraphCSR (conv.hpp:44-50): ``src`` is the output node of
+    an edge, ``nbr`` (reference ``dst``) the node whose features it reads.
+    The deterministic mode needs edges sorted strictly by (src, dst) and gets
+    the CSR + transposed CSR; the atomic mode takes the edges in any order
+    (conv.cpp:240, 371-374). Holds host arrays and uploads them to a device on
+    first use."""
 
     def __init__(self, nodes: int, src, nbr):
         src = np.ascontiguousarray(np.asarray(src, dtype=np.int64))
@@ -340,11 +354,13 @@ class Graph:
         if src.size and (src.min() < 0 or nbr.min() < 0 or src.max() >= nodes or nbr.max() >= nodes):
             raise InvalidArgument("edge endpoint out of range")
         key = src * max(nodes, 1) + nbr
-        if src.size > 1 and not np.all(np.diff(key) > 0):
-            raise InvalidArgument("conv: deterministic mode requires edges sorted by first coordinate")
+        self.sorted = bool(src.size <= 1 or np.all(np.diff(key) > 0))
         self.nodes = int(nodes)
         self.src = src.astype(np.int32)
         self.nbr = nbr.astype(np.int32)
+        self._dev = {}
+        if not self.sorted:
+            return
         counts = np.bincount(src, minlength=nodes) if src.size else np.zeros(nodes, np.int64)
         self.row_ptr = np.zeros(nodes + 1, np.int64)
         np.cumsum(counts, out=self.row_ptr[1:])
@@ -355,7 +371,6 @@ class Graph:
                                              self.nbr.ctypes.data if self.edges else None,
                                              self.t_row_ptr.ctypes.data, self.t_src.ctypes.data,
                                              self.t_eid.ctypes.data))
-        self._dev = {}
 
     @property
     def edges(self) -> int:
@@ -367,19 +382,113 @@ class Graph:
         perm[self.t_eid[:self.edges]] = np.arange(self.edges)
         return perm
 
+    def require_sorted(self):
+        if not self.sorted:
+            raise InvalidArgument("conv: deterministic mode requires edges sorted by first coordinate")
+
     def device(self, dev):
         import torch
         key = str(dev)
         if key not in self._dev:
             t = lambda a: torch.from_numpy(a).to(dev)
-            self._dev[key] = {k: t(getattr(self, k)) for k in ("row_ptr", "nbr", "t_row_ptr", "t_src", "t_eid")}
+            names = ("src", "nbr") + (("row_ptr", "t_row_ptr", "t_src", "t_eid") if self.sorted else ())
+            self._dev[key] = {k: t(getattr(self, k)) for k in names}
         return self._dev[key]
+
+
+class DeviceGraph:
+    """A GraphCSR built and held on the device (conv.cpp:64-151 on the GPU):
+    ``row_ptr`` / ``nbr`` / ``src`` (CSR by output node) and, built on first
+    use, the transposed CSR. Accepted wherever ConvPlan takes a Graph."""
+
+    sorted = True
+
+    def __init__(self, nodes: int, row_ptr, nbr, src):
+        self.nodes = int(nodes)
+        self.row_ptr, self.nbr, self.src = row_ptr, nbr, src
+        self._t = None
+
+    @property
+    def edges(self) -> int:
+        return int(self.nbr.numel())
+
+    def _transpose(self):
+        import torch
+        if self._t is None:
+            dev = self.nbr.device
+            E = max(self.edges, 1)
+            t_row_ptr = torch.empty(self.nodes + 1, dtype=torch.int64, device=dev)
+            t_src = torch.empty(E, dtype=torch.int32, device=dev)
+            t_eid = torch.empty(E, dtype=torch.int32, device=dev)
+            _check(lib().cgf_graph_transpose(self.nodes, self.nodes, self.edges, self.row_ptr.data_ptr(),
+                                             self.nbr.data_ptr(), t_row_ptr.data_ptr(), t_src.data_ptr(),
+                                             t_eid.data_ptr(), _stream_of(dev)))
+            self._t = (t_row_ptr, t_src, t_eid)
+        return self._t
+
+    def require_sorted(self):
+        pass
+
+    def device(self, dev):
+        t_row_ptr, t_src, t_eid = self._transpose()
+        return {"row_ptr": self.row_ptr, "nbr": self.nbr, "src": self.src, "t_row_ptr": t_row_ptr,
+                "t_src": t_src, "t_eid": t_eid}
+
+    def to_host(self) -> "Graph":
+        return Graph(self.nodes, self.src.cpu().numpy(), self.nbr.cpu().numpy())
+
+
+def _stream_of(dev):
+    import torch
+    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def make_graph_device(nodes: int, src, dst, allow_self_loops=False) -> DeviceGraph:
+    """conv::make_graph (conv.cpp:64-87) on the device: int32 CUDA tensors of
+    edges in any order -> sorted, deduplicated CSR."""
+    import torch
+    src = src.to(torch.int32).contiguous()
+    dst = dst.to(torch.int32).contiguous()
+    if src.shape != dst.shape or src.dim() != 1:
+        raise ShapeError("src / dst must be 1-D arrays of equal length")
+    dev = src.device
+    E = src.numel()
+    row_ptr = torch.empty(nodes + 1, dtype=torch.int64, device=dev)
+    nbr = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+    osrc = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+    m = C.c_int64(0)
+    _check(lib().cgf_graph_make(nodes, E, src.data_ptr() if E else None, dst.data_ptr() if E else None,
+                                int(allow_self_loops), row_ptr.data_ptr(), nbr.data_ptr(), osrc.data_ptr(),
+                                C.byref(m), _stream_of(dev)))
+    return DeviceGraph(nodes, row_ptr, nbr[:m.value], osrc[:m.value])
+
+
+def radius_graph_device(pos, r_cut: float) -> DeviceGraph:
+    """conv::radius_graph (conv.cpp:89-133) on the device: pos is an (n, 3)
+    float64 CUDA tensor."""
+    import torch
+    pos = pos.to(torch.float64).contiguous()
+    if pos.dim() != 2 or pos.shape[1] != 3:
+        raise ShapeError("pos must be (n, 3)")
+    n, dev = pos.shape[0], pos.device
+    row_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    m = C.c_int64(0)
+    _check(lib().cgf_graph_radius(n, pos.data_ptr() if n else None, float(r_cut), row_ptr.data_ptr(), None, 0,
+                                  C.byref(m), _stream_of(dev)))
+    nbr = torch.empty(max(m.value, 1), dtype=torch.int32, device=dev)
+    _check(lib().cgf_graph_radius(n, pos.data_ptr() if n else None, float(r_cut), row_ptr.data_ptr(),
+                                  nbr.data_ptr(), m.value, C.byref(m), _stream_of(dev)))
+    nbr = nbr[:m.value]
+    src = torch.repeat_interleave(torch.arange(n, dtype=torch.int32, device=dev), row_ptr.diff())
+    return DeviceGraph(n, row_ptr, nbr, src)
 
 
 class ConvPlan:
     """Fused tensor product + graph convolution over a TpPlan (conv.hpp:93-115).
-    Deterministic: each output row is owned by one warp and summed in edge
-    order (no atomics, no fixup pass)."""
+    DETERMINISTIC: each output row is owned by one warp and summed in edge
+    order (no atomics, no fixup pass). ATOMIC (Mode::atomic): one warp item
+    per (edge, unit), node outputs accumulated with float atomics; edges in
+    any order."""
 
     def __init__(self, plan: TpPlan):
         self.plan = plan
@@ -406,6 +515,12 @@ class ConvPlan:
         p = self.plan
         z = TpPlan._empty_like(node_x, (g.nodes, p.dim_z))
         d = self._ptrs(g, node_x)
+        if mode == ATOMIC:
+            _check(lib().cgf_conv_forward_atomic(p._h, _dtype_code(node_x), g.nodes, g.edges, d["src"], d["nbr"],
+                                                 TpPlan._p(node_x), TpPlan._p(edge_y), TpPlan._p(edge_w),
+                                                 TpPlan._p(z), TpPlan._stream(node_x)))
+            return z
+        g.require_sorted()
         _check(lib().cgf_conv_forward(p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"],
                                       TpPlan._p(node_x), TpPlan._p(edge_y), TpPlan._p(edge_w), TpPlan._p(z), mode,
                                       TpPlan._stream(node_x)))
@@ -422,6 +537,12 @@ class ConvPlan:
         gy = TpPlan._empty_like(node_x, (g.edges, p.dim_y))
         gw = TpPlan._empty_like(node_x, (g.edges, p.n_w))
         d = self._ptrs(g, node_x)
+        if mode == ATOMIC:
+            _check(lib().cgf_conv_backward_atomic(
+                p._h, _dtype_code(node_x), g.nodes, g.edges, d["src"], d["nbr"],
+                *(TpPlan._p(a) for a in (node_x, edge_y, edge_w, g_node_z, gx, gy, gw)), TpPlan._stream(node_x)))
+            return gx, gy, gw
+        g.require_sorted()
         _check(lib().cgf_conv_backward(p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"],
                                        d["t_row_ptr"], d["t_src"], d["t_eid"], TpPlan._p(node_x), TpPlan._p(edge_y),
                                        TpPlan._p(edge_w), TpPlan._p(g_node_z), TpPlan._p(gx), TpPlan._p(gy),
@@ -444,12 +565,45 @@ class ConvPlan:
         ow = TpPlan._empty_like(node_x, (g.edges, p.n_w))
         ogz = TpPlan._empty_like(node_x, (g.nodes, p.dim_z))
         d = self._ptrs(g, node_x)
+        if mode == ATOMIC:
+            _check(lib().cgf_conv_double_backward_atomic(
+                p._h, _dtype_code(node_x), g.nodes, g.edges, d["src"], d["nbr"],
+                *(TpPlan._p(a) for a in (node_x, edge_y, edge_w, g_node_z, d_gx, d_gy, d_gw, ox, oy, ow, ogz)),
+                TpPlan._stream(node_x)))
+            return ox, oy, ow, ogz
+        g.require_sorted()
         _check(lib().cgf_conv_double_backward(
             p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"], d["t_row_ptr"], d["t_src"],
             d["t_eid"], *(TpPlan._p(a) for a in (node_x, edge_y, edge_w, g_node_z, d_gx, d_gy, d_gw, ox, oy, ow,
                                                  ogz)), mode, TpPlan._stream(node_x)))
         return ox, oy, ow, ogz
 
+
+    # -- unfused comparator (conv.cpp:530-616) on the GPU ----------------------
+    def unfused_forward(self, g, node_x, edge_y, edge_w):
+        """Gather x per edge -> batched TP over |E| rows -> per-node sums in edge order."""
+        self._check_shapes(g, node_x, edge_y, edge_w)
+        g.require_sorted()
+        p = self.plan
+        z = TpPlan._empty_like(node_x, (g.nodes, p.dim_z))
+        d = self._ptrs(g, node_x)
+        _check(lib().cgf_conv_unfused_forward(p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"],
+                                              TpPlan._p(node_x), TpPlan._p(edge_y), TpPlan._p(edge_w), TpPlan._p(z),
+                                              TpPlan._stream(node_x)))
+        return z
+
+    def unfused_backward(self, g, node_x, edge_y, edge_w, g_node_z):
+        self._check_shapes(g, node_x, edge_y, edge_w)
+        g.require_sorted()
+        p = self.plan
+        gx = TpPlan._empty_like(node_x, (g.nodes, p.dim_x))
+        gy = TpPlan._empty_like(node_x, (g.edges, p.dim_y))
+        gw = TpPlan._empty_like(node_x, (g.edges, p.n_w))
+        d = self._ptrs(g, node_x)
+        _check(lib().cgf_conv_unfused_backward(
+            p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"], d["t_row_ptr"], d["t_eid"],
+            *(TpPlan._p(a) for a in (node_x, edge_y, edge_w, g_node_z, gx, gy, gw)), TpPlan._stream(node_x)))
+        return gx, gy, gw
 
     # -- sharded calls (one rank of a destination-partitioned graph) ---------
     # ``sh`` is a dist.GraphShard: out_nodes owned output rows, in_nodes

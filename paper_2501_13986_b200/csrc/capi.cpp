@@ -19,6 +19,7 @@
 #include "cuda_api.hpp"
 #include "jit.hpp"
 #include "problem.hpp"
+#include "graph_ops.hpp"
 #include "uvw.hpp"
 
 struct cgf_plan {
@@ -130,7 +131,8 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   cfg.aligned = aligned != 0;
   // Batched fwd / bwd keep y in registers (prefetched a row ahead); the
   // double-backward needs those registers for its three z' accumulators.
-  cfg.y_regs = loop == cgf::Loop::Rows && (comp == cgf::Comp::Fwd || comp == cgf::Comp::Bwd);
+  cfg.y_regs = (loop == cgf::Loop::Rows || loop == cgf::Loop::ConvEdges) &&
+               (comp == cgf::Comp::Fwd || comp == cgf::Comp::Bwd);
   // Two 32-lane chunks per staged item / code body: measured -4 % fwd, -11 %
   // bwd (TP) and -13 % (conv) in FP32; FP64 runs out of registers (keep 1).
   cfg.merge = (dtype == CGF_F32 && (comp == cgf::Comp::Fwd || comp == cgf::Comp::Bwd)) ? 2 : 1;
@@ -186,12 +188,13 @@ struct Args {
 };
 
 void run_kernel(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype, int w_shared, const Args& a, void* stream) {
-  if (a.rows <= 0) return;
+  const std::int64_t items = loop == cgf::Loop::ConvEdges ? a.edges : a.rows;
+  if (items <= 0) return;
   const bool al = aligned16({a.x, a.y, a.w, a.gz, a.da, a.db, a.dc, a.o0, a.o1, a.o2, a.o3});
   const auto ks = source_for(p, comp, loop, dtype, w_shared, al);
   const cgf::Kernel k = cgf::load_kernel(*ks);
   const int warps = k.threads / 32;
-  const std::int64_t need = (a.rows + warps - 1) / warps;
+  const std::int64_t need = (items + warps - 1) / warps;
   const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(need, k.max_grid));
   Args c = a;
   void* args[] = {&c.x, &c.y, &c.w, &c.gz, &c.da, &c.db, &c.dc, &c.o0, &c.o1, &c.o2, &c.o3, &c.rows,
@@ -279,6 +282,7 @@ void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, c
                      std::int64_t rows, void* stream);
 
 void memzero(void* ptr, std::size_t bytes, void* stream) {
+  if (bytes) cgf::ensure_context();  // the driver entry points resolve on first use
   if (bytes) CU_CHECK(cgf::drv::cuMemsetD8Async(reinterpret_cast<CUdeviceptr>(ptr), 0, bytes, reinterpret_cast<CUstream>(stream)));
 }
 
@@ -400,6 +404,134 @@ struct DevBuf {
   }
   void* get() const { return reinterpret_cast<void*>(p); }
 };
+
+// Per-edge output node of a CSR (row_ptr by output node), on the host.
+std::vector<std::int32_t> csr_sources(std::int64_t nodes, std::int64_t edges, const std::int64_t* row_ptr) {
+  need(row_ptr, "row_ptr");
+  if (row_ptr[0] != 0 || row_ptr[nodes] != edges) throw std::invalid_argument("row_ptr does not span the edge list");
+  std::vector<std::int32_t> src(static_cast<std::size_t>(std::max<std::int64_t>(edges, 1)));
+  for (std::int64_t v = 0; v < nodes; ++v) {
+    if (row_ptr[v + 1] < row_ptr[v]) throw std::invalid_argument("row_ptr is not monotone");
+    for (std::int64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) src[e] = static_cast<std::int32_t>(v);
+  }
+  return src;
+}
+
+// Host-side validation of an edge list (atomic mode needs no order).
+void check_edge_list(std::int64_t nodes, std::int64_t edges, const std::int32_t* src, const std::int32_t* dst) {
+  if (edges == 0) return;
+  need(src, "src");
+  need(dst, "dst");
+  for (std::int64_t e = 0; e < edges; ++e)
+    if (src[e] < 0 || src[e] >= nodes || dst[e] < 0 || dst[e] >= nodes)
+      throw std::invalid_argument("edge endpoint out of range");
+}
+
+// Atomic-mode conv (Mode::atomic, conv.cpp:311-324 / 470-486) over an edge
+// list: one item per (edge, unit); z / gx contributions accumulate at the
+// edge's src / dst nodes with float atomics into zeroed node arrays.
+void conv_atomic(cgf_plan* p, int dtype, cgf::Comp comp, std::int64_t nodes, std::int64_t edges, const std::int32_t* src,
+                 const std::int32_t* dst, Args a, void* stream) {
+  if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+  if (edges > 0 && nodes == 0) throw cgf::ShapeError("edges without nodes");
+  const std::size_t es = dtype == CGF_F64 ? 8 : 4;
+  const auto& pr = p->problem;
+  if (a.o3 || comp == cgf::Comp::Fwd) memzero(comp == cgf::Comp::Fwd ? a.o0 : a.o3, es * nodes * pr.dim_z, stream);
+  if (comp != cgf::Comp::Fwd) memzero(a.o0, es * nodes * pr.dim_x, stream);
+  if (edges == 0) return;
+  need(src, "src"); need(dst, "dst");
+  a.rows = nodes;
+  a.edges = edges;
+  a.eid = src;
+  a.nb = dst;
+  run_kernel(p, comp, cgf::Loop::ConvEdges, dtype, 0, a, stream);
+}
+
+// Stream-ordered device scratch.
+struct Scratch {
+  void* ptr = nullptr;
+  void* st = nullptr;
+  Scratch(std::size_t bytes, void* stream) : st(stream) { ptr = cgf::gops::scratch_alloc(bytes, stream); }
+  ~Scratch() { cgf::gops::scratch_free(ptr, st); }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+// Per-edge output node of a device CSR, for the CSR entry points called with
+// CGF_CONV_ATOMIC and for the unfused backward's g_node_z gather.
+struct CsrSrc : Scratch {
+  CsrSrc(const std::int64_t* row_ptr, std::int64_t nodes, std::int64_t edges, void* stream)
+      : Scratch(edges > 0 ? 4ull * edges : 0, stream) {
+    if (edges <= 0) return;
+    need(row_ptr, "row_ptr");
+    cgf::gops::rowptr_expand(row_ptr, nodes, as<std::int32_t>(), stream);
+  }
+  const std::int32_t* get() const { return as<const std::int32_t>(); }
+};
+
+// Unfused comparator (conv.cpp:530-616): gather x per edge, batched TP over
+// |E| rows, then per-node sums in edge order. The output node's edges are
+// positions [rp[v], rp[v+1]) of the edge list, through ridx when the list is
+// not in CSR order.
+void unfused_fwd(cgf_plan* p, int dtype, std::int64_t nodes, std::int64_t edges, const std::int64_t* rp,
+                 const std::int32_t* ridx, const std::int32_t* nbr, const void* node_x, const void* edge_y,
+                 const void* edge_w, void* node_z, void* stream) {
+  if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+  if (nodes == 0) return;
+  need(node_z, "node_z");
+  const auto& pr = p->problem;
+  const bool f64 = dtype == CGF_F64;
+  const std::size_t es = f64 ? 8 : 4;
+  if (edges == 0) {
+    memzero(node_z, es * nodes * pr.dim_z, stream);
+    return;
+  }
+  need(rp, "row_ptr"); need(nbr, "nbr"); need(node_x, "node_x"); need(edge_y, "edge_y"); need(edge_w, "edge_w");
+  Scratch xg(es * edges * pr.dim_x, stream), ze(es * edges * pr.dim_z, stream);
+  cgf::gops::gather_rows(f64, node_x, nbr, xg.ptr, edges, pr.dim_x, stream);
+  launch(p, CGF_OP_FORWARD, dtype, 0, edges, xg.ptr, edge_y, edge_w, nullptr, nullptr, nullptr, nullptr, ze.ptr,
+         nullptr, nullptr, nullptr, stream);
+  cgf::gops::segment_sum(f64, ze.ptr, rp, ridx, node_z, nodes, pr.dim_z, stream);
+}
+
+// src / nbr per edge (any order); (t_rp, t_idx) buckets the edges by nbr in
+// edge order.
+void unfused_bwd(cgf_plan* p, int dtype, std::int64_t nodes, std::int64_t edges, const std::int32_t* src,
+                 const std::int32_t* nbr, const std::int64_t* t_rp, const std::int32_t* t_idx, const void* node_x,
+                 const void* edge_y, const void* edge_w, const void* g_node_z, void* g_node_x, void* g_edge_y,
+                 void* g_edge_w, void* stream) {
+  if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+  if (nodes == 0) return;
+  need(g_node_x, "g_node_x");
+  const auto& pr = p->problem;
+  const bool f64 = dtype == CGF_F64;
+  const std::size_t es = f64 ? 8 : 4;
+  if (edges == 0) {
+    memzero(g_node_x, es * nodes * pr.dim_x, stream);
+    return;
+  }
+  need(src, "src"); need(nbr, "nbr"); need(t_rp, "t_row_ptr"); need(t_idx, "t_eid");
+  need(node_x, "node_x"); need(edge_y, "edge_y"); need(edge_w, "edge_w"); need(g_node_z, "g_node_z");
+  need(g_edge_y, "g_edge_y"); need(g_edge_w, "g_edge_w");
+  Scratch xg(es * edges * pr.dim_x, stream), gzg(es * edges * pr.dim_z, stream), gxe(es * edges * pr.dim_x, stream);
+  cgf::gops::gather_rows(f64, node_x, nbr, xg.ptr, edges, pr.dim_x, stream);
+  cgf::gops::gather_rows(f64, g_node_z, src, gzg.ptr, edges, pr.dim_z, stream);
+  launch(p, CGF_OP_BACKWARD, dtype, 0, edges, xg.ptr, edge_y, edge_w, gzg.ptr, nullptr, nullptr, nullptr, gxe.ptr,
+         g_edge_y, g_edge_w, nullptr, stream);
+  cgf::gops::segment_sum(f64, gxe.ptr, t_rp, t_idx, g_node_x, nodes, pr.dim_x, stream);
+}
+
+// Stable bucket of an edge list by key on the host: rp[nodes + 1], idx.
+void host_bucket(std::int64_t nodes, std::int64_t edges, const std::int32_t* key, std::vector<std::int64_t>& rp,
+                 std::vector<std::int32_t>& idx) {
+  rp.assign(static_cast<std::size_t>(nodes) + 1, 0);
+  for (std::int64_t e = 0; e < edges; ++e) ++rp[static_cast<std::size_t>(key[e]) + 1];
+  for (std::int64_t v = 0; v < nodes; ++v) rp[v + 1] += rp[v];
+  std::vector<std::int64_t> next(rp.begin(), rp.end() - 1);
+  idx.assign(static_cast<std::size_t>(std::max<std::int64_t>(edges, 1)), 0);
+  for (std::int64_t e = 0; e < edges; ++e) idx[next[key[e]]++] = static_cast<std::int32_t>(e);
+}
 
 }  // namespace
 
@@ -737,7 +869,7 @@ int cgf_plan_kernel_source(cgf_plan* p, int comp, int loop, int dtype, int w_sha
   int n = 0;
   const int rc = guarded([&] {
     need(p, "plan");
-    if (comp < 0 || comp > 4 || loop < 0 || loop > 2) throw std::invalid_argument("bad comp / loop");
+    if (comp < 0 || comp > 4 || loop < 0 || loop > 3) throw std::invalid_argument("bad comp / loop");
     const auto ks = source_for(p, static_cast<cgf::Comp>(comp), static_cast<cgf::Loop>(loop), dtype, w_shared, aligned);
     n = static_cast<int>(ks->source.size());
     if (buf && cap > 0) {
@@ -752,7 +884,7 @@ int cgf_plan_kernel_source(cgf_plan* p, int comp, int loop, int dtype, int w_sha
 int cgf_plan_kernel_compile(cgf_plan* p, int comp, int loop, int dtype, int w_shared, int aligned) {
   return guarded([&] {
     need(p, "plan");
-    if (comp < 0 || comp > 4 || loop < 0 || loop > 2) throw std::invalid_argument("bad comp / loop");
+    if (comp < 0 || comp > 4 || loop < 0 || loop > 3) throw std::invalid_argument("bad comp / loop");
     const auto ks = source_for(p, static_cast<cgf::Comp>(comp), static_cast<cgf::Loop>(loop), dtype, w_shared, aligned);
     cgf::compile_cubin(ks->source, ks->name);
   });
@@ -812,6 +944,13 @@ int cgf_conv_forward_shard(cgf_plan* p, int dtype, int64_t out_nodes, int64_t in
 
 int cgf_conv_forward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr, const int32_t* nbr,
                      const void* node_x, const void* edge_y, const void* edge_w, void* node_z, int mode, void* stream) {
+  if (mode == CGF_CONV_ATOMIC)
+    return guarded([&] {
+      need(p, "plan");
+      const CsrSrc src(row_ptr, nodes, edges, stream);
+      if (cgf_conv_forward_atomic(p, dtype, nodes, edges, src.get(), nbr, node_x, edge_y, edge_w, node_z, stream) != CGF_OK)
+        throw std::runtime_error(g_err);
+    });
   return cgf_conv_forward_shard(p, dtype, nodes, nodes, edges, row_ptr, nbr, node_x, edge_y, edge_w, node_z, mode,
                                 stream);
 }
@@ -844,7 +983,14 @@ int cgf_conv_backward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, cons
                       const int32_t* nbr, const int64_t* t_row_ptr, const int32_t* t_out, const int32_t* t_eid,
                       const void* node_x, const void* edge_y, const void* edge_w, const void* g_node_z,
                       void* g_node_x, void* g_edge_y, void* g_edge_w, int mode, void* stream) {
-  (void)row_ptr; (void)nbr;
+  if (mode == CGF_CONV_ATOMIC)
+    return guarded([&] {
+      need(p, "plan");
+      const CsrSrc src(row_ptr, nodes, edges, stream);
+      if (cgf_conv_backward_atomic(p, dtype, nodes, edges, src.get(), nbr, node_x, edge_y, edge_w, g_node_z, g_node_x,
+                                   g_edge_y, g_edge_w, stream) != CGF_OK)
+        throw std::runtime_error(g_err);
+    });
   return cgf_conv_backward_shard(p, dtype, nodes, nodes, edges, t_row_ptr, t_out, t_eid, node_x, edge_y, edge_w,
                                  g_node_z, g_node_x, g_edge_y, g_edge_w, mode, stream);
 }
@@ -889,9 +1035,123 @@ int cgf_conv_double_backward(cgf_plan* p, int dtype, int64_t nodes, int64_t edge
                              const void* g_node_z, const void* d_gx, const void* d_gy, const void* d_gw,
                              void* o_node_x, void* o_edge_y, void* o_edge_w, void* o_g_node_z, int mode,
                              void* stream) {
+  if (mode == CGF_CONV_ATOMIC)
+    return guarded([&] {
+      need(p, "plan");
+      const CsrSrc src(row_ptr, nodes, edges, stream);
+      if (cgf_conv_double_backward_atomic(p, dtype, nodes, edges, src.get(), nbr, node_x, edge_y, edge_w, g_node_z, d_gx,
+                                          d_gy, d_gw, o_node_x, o_edge_y, o_edge_w, o_g_node_z, stream) != CGF_OK)
+        throw std::runtime_error(g_err);
+    });
   return cgf_conv_double_backward_shard(p, dtype, nodes, nodes, edges, row_ptr, nbr, t_row_ptr, t_out, t_eid,
                                         node_x, edge_y, edge_w, g_node_z, d_gx, d_gy, d_gw, o_node_x, o_edge_y,
                                         o_edge_w, o_g_node_z, mode, stream);
+}
+
+// ---- atomic-mode conv over an edge list ----------------------------------
+
+int cgf_conv_forward_atomic(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int32_t* src, const int32_t* dst,
+                            const void* node_x, const void* edge_y, const void* edge_w, void* node_z, void* stream) {
+  return guarded([&] {
+    need(p, "plan");
+    if (nodes > 0) need(node_z, "node_z");
+    if (edges > 0) { need(node_x, "node_x"); need(edge_y, "edge_y"); need(edge_w, "edge_w"); }
+    Args a;
+    a.x = node_x; a.y = edge_y; a.w = edge_w; a.o0 = node_z;
+    conv_atomic(p, dtype, cgf::Comp::Fwd, nodes, edges, src, dst, a, stream);
+  });
+}
+
+int cgf_conv_backward_atomic(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                             const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                             const void* g_node_z, void* g_node_x, void* g_edge_y, void* g_edge_w, void* stream) {
+  return guarded([&] {
+    need(p, "plan");
+    if (nodes > 0) need(g_node_x, "g_node_x");
+    if (edges > 0) {
+      need(node_x, "node_x"); need(edge_y, "edge_y"); need(edge_w, "edge_w"); need(g_node_z, "g_node_z");
+      need(g_edge_y, "g_edge_y"); need(g_edge_w, "g_edge_w");
+    }
+    Args a;
+    a.x = node_x; a.y = edge_y; a.w = edge_w; a.gz = g_node_z;
+    a.o0 = g_node_x; a.o1 = g_edge_y; a.o2 = g_edge_w;
+    conv_atomic(p, dtype, cgf::Comp::Bwd, nodes, edges, src, dst, a, stream);
+  });
+}
+
+int cgf_conv_double_backward_atomic(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                                    const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                                    const void* g_node_z, const void* d_gx, const void* d_gy, const void* d_gw,
+                                    void* o_node_x, void* o_edge_y, void* o_edge_w, void* o_g_node_z, void* stream) {
+  return guarded([&] {
+    need(p, "plan");
+    if (nodes > 0) { need(o_node_x, "o_node_x"); need(o_g_node_z, "o_g_node_z"); }
+    if (edges > 0) {
+      need(node_x, "node_x"); need(edge_y, "edge_y"); need(edge_w, "edge_w"); need(g_node_z, "g_node_z");
+      need(d_gx, "d_gx"); need(d_gy, "d_gy"); need(d_gw, "d_gw"); need(o_edge_y, "o_edge_y"); need(o_edge_w, "o_edge_w");
+    }
+    Args a;
+    a.x = node_x; a.y = edge_y; a.w = edge_w; a.gz = g_node_z; a.da = d_gx; a.db = d_gy; a.dc = d_gw;
+    a.o0 = o_node_x; a.o1 = o_edge_y; a.o2 = o_edge_w; a.o3 = o_g_node_z;
+    conv_atomic(p, dtype, cgf::Comp::DBwd, nodes, edges, src, dst, a, stream);
+  });
+}
+
+// ---- unfused gather -> batched TP -> scatter (conv.cpp:530-616) ---------
+
+int cgf_conv_unfused_forward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                             const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
+                             void* node_z, void* stream) {
+  return guarded([&] {
+    need(p, "plan");
+    unfused_fwd(p, dtype, nodes, edges, row_ptr, nullptr, nbr, node_x, edge_y, edge_w, node_z, stream);
+  });
+}
+
+int cgf_conv_unfused_backward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
+                              const int32_t* nbr, const int64_t* t_row_ptr, const int32_t* t_eid, const void* node_x,
+                              const void* edge_y, const void* edge_w, const void* g_node_z, void* g_node_x,
+                              void* g_edge_y, void* g_edge_w, void* stream) {
+  return guarded([&] {
+    need(p, "plan");
+    if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    const CsrSrc src(edges > 0 ? row_ptr : nullptr, nodes, nodes > 0 ? edges : 0, stream);
+    unfused_bwd(p, dtype, nodes, edges, src.get(), nbr, t_row_ptr, t_eid, node_x, edge_y, edge_w, g_node_z, g_node_x,
+                g_edge_y, g_edge_w, stream);
+  });
+}
+
+// ---- graph construction on the device (conv.cpp:64-151) -----------------
+
+int cgf_graph_make(int64_t nodes, int64_t edges, const int32_t* src, const int32_t* dst, int allow_self_loops,
+                   int64_t* row_ptr, int32_t* nbr, int32_t* out_src, int64_t* out_edges, void* stream) {
+  return guarded([&] {
+    need(row_ptr, "row_ptr"); need(out_edges, "out_edges");
+    if (edges > 0) { need(src, "src"); need(dst, "dst"); need(nbr, "nbr"); }
+    cgf::ensure_context();
+    *out_edges = cgf::gops::make_graph(nodes, edges, src, dst, allow_self_loops != 0, row_ptr, nbr, out_src, stream);
+  });
+}
+
+int cgf_graph_transpose(int64_t out_nodes, int64_t in_nodes, int64_t edges, const int64_t* row_ptr,
+                        const int32_t* nbr, int64_t* t_row_ptr, int32_t* t_src, int32_t* t_eid, void* stream) {
+  return guarded([&] {
+    if (out_nodes < 0 || in_nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    need(t_row_ptr, "t_row_ptr");
+    if (edges > 0) { need(row_ptr, "row_ptr"); need(nbr, "nbr"); need(t_src, "t_src"); need(t_eid, "t_eid"); }
+    cgf::ensure_context();
+    cgf::gops::transpose(out_nodes, in_nodes, edges, row_ptr, nbr, t_row_ptr, t_src, t_eid, stream);
+  });
+}
+
+int cgf_graph_radius(int64_t n, const double* pos, double r_cut, int64_t* row_ptr, int32_t* nbr, int64_t cap,
+                     int64_t* out_edges, void* stream) {
+  return guarded([&] {
+    need(out_edges, "out_edges");
+    if (n > 0) need(pos, "pos");
+    cgf::ensure_context();
+    *out_edges = cgf::gops::radius_graph(n, pos, r_cut, row_ptr, nbr, cap, stream);
+  });
 }
 
 // ---- host-pointer conv (the C++ drop-in shim's path) ---------------------
@@ -907,6 +1167,12 @@ int cgf_conv_forward_host(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, 
     if (mode != CGF_CONV_DETERMINISTIC && mode != CGF_CONV_ATOMIC) throw std::invalid_argument("bad conv mode");
     if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
     if (nodes == 0) return;
+    if (mode == CGF_CONV_ATOMIC) {
+      const auto src = csr_sources(nodes, edges, row_ptr);
+      if (cgf_conv_forward_atomic_host(p, dtype, nodes, edges, src.data(), nbr, node_x, edge_y, edge_w, node_z) != CGF_OK)
+        throw std::runtime_error(g_err);
+      return;
+    }
     cgf::ensure_context();
     const auto& pr = p->problem;
     const std::size_t V = static_cast<std::size_t>(nodes), E = static_cast<std::size_t>(edges);
@@ -934,6 +1200,13 @@ int cgf_conv_backward_host(cgf_plan* p, int dtype, int64_t nodes, int64_t edges,
     if (mode != CGF_CONV_DETERMINISTIC && mode != CGF_CONV_ATOMIC) throw std::invalid_argument("bad conv mode");
     if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
     if (nodes == 0) return;
+    if (mode == CGF_CONV_ATOMIC) {
+      const auto src = csr_sources(nodes, edges, row_ptr);
+      if (cgf_conv_backward_atomic_host(p, dtype, nodes, edges, src.data(), nbr, node_x, edge_y, edge_w, g_node_z,
+                                        g_node_x, g_edge_y, g_edge_w) != CGF_OK)
+        throw std::runtime_error(g_err);
+      return;
+    }
     cgf::ensure_context();
     const auto& pr = p->problem;
     const std::size_t V = static_cast<std::size_t>(nodes), E = static_cast<std::size_t>(edges);
@@ -957,6 +1230,132 @@ int cgf_conv_backward_host(cgf_plan* p, int dtype, int64_t nodes, int64_t edges,
                            static_cast<const int32_t*>(dts), static_cast<const int32_t*>(dte), dx, dy, dw, dgz, ogx,
                            ogy, ogw, CGF_CONV_DETERMINISTIC, nullptr);
     if (rc != CGF_OK) throw std::runtime_error(g_err);
+    CU_CHECK(cgf::drv::cuCtxSynchronize());
+    h.back(g_node_x, ogx, V * pr.dim_x);
+    h.back(g_edge_y, ogy, E * pr.dim_y);
+    h.back(g_edge_w, ogw, E * pr.n_w);
+  });
+}
+
+int cgf_conv_forward_atomic_host(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                                 const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                                 void* node_z) {
+  return guarded([&] {
+    need(p, "plan");
+    if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (nodes == 0) return;
+    check_edge_list(nodes, edges, src, dst);
+    cgf::ensure_context();
+    const auto& pr = p->problem;
+    const std::size_t V = static_cast<std::size_t>(nodes), E = static_cast<std::size_t>(edges);
+    HostCall h{dtype == CGF_F64 ? 8u : 4u, {}};
+    HostCall hi{1, {}};
+    void* ds = hi.in(src, E * 4);
+    void* dd = hi.in(dst, E * 4);
+    void* dx = h.in(node_x, V * pr.dim_x);
+    void* dy = h.in(edge_y, E * pr.dim_y);
+    void* dw = h.in(edge_w, E * pr.n_w);
+    void* dz = h.out(V * pr.dim_z);
+    if (cgf_conv_forward_atomic(p, dtype, nodes, edges, static_cast<const int32_t*>(ds), static_cast<const int32_t*>(dd),
+                                dx, dy, dw, dz, nullptr) != CGF_OK)
+      throw std::runtime_error(g_err);
+    CU_CHECK(cgf::drv::cuCtxSynchronize());
+    h.back(node_z, dz, V * pr.dim_z);
+  });
+}
+
+int cgf_conv_backward_atomic_host(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                                  const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                                  const void* g_node_z, void* g_node_x, void* g_edge_y, void* g_edge_w) {
+  return guarded([&] {
+    need(p, "plan");
+    if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (nodes == 0) return;
+    check_edge_list(nodes, edges, src, dst);
+    cgf::ensure_context();
+    const auto& pr = p->problem;
+    const std::size_t V = static_cast<std::size_t>(nodes), E = static_cast<std::size_t>(edges);
+    HostCall h{dtype == CGF_F64 ? 8u : 4u, {}};
+    HostCall hi{1, {}};
+    void* ds = hi.in(src, E * 4);
+    void* dd = hi.in(dst, E * 4);
+    void* dx = h.in(node_x, V * pr.dim_x);
+    void* dy = h.in(edge_y, E * pr.dim_y);
+    void* dw = h.in(edge_w, E * pr.n_w);
+    void* dgz = h.in(g_node_z, V * pr.dim_z);
+    void* ogx = h.out(V * pr.dim_x);
+    void* ogy = h.out(E * pr.dim_y);
+    void* ogw = h.out(E * pr.n_w);
+    if (cgf_conv_backward_atomic(p, dtype, nodes, edges, static_cast<const int32_t*>(ds),
+                                 static_cast<const int32_t*>(dd), dx, dy, dw, dgz, ogx, ogy, ogw, nullptr) != CGF_OK)
+      throw std::runtime_error(g_err);
+    CU_CHECK(cgf::drv::cuCtxSynchronize());
+    h.back(g_node_x, ogx, V * pr.dim_x);
+    h.back(g_edge_y, ogy, E * pr.dim_y);
+    h.back(g_edge_w, ogw, E * pr.n_w);
+  });
+}
+
+int cgf_conv_unfused_forward_host(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                                  const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                                  void* node_z) {
+  return guarded([&] {
+    need(p, "plan");
+    if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (nodes == 0) return;
+    check_edge_list(nodes, edges, src, dst);
+    cgf::ensure_context();
+    const auto& pr = p->problem;
+    const std::size_t V = static_cast<std::size_t>(nodes), E = static_cast<std::size_t>(edges);
+    std::vector<std::int64_t> rp;
+    std::vector<std::int32_t> ridx;
+    host_bucket(nodes, edges, src, rp, ridx);
+    HostCall h{dtype == CGF_F64 ? 8u : 4u, {}};
+    HostCall hi{1, {}};
+    void* drp = hi.in(rp.data(), (V + 1) * 8);
+    void* dri = hi.in(ridx.data(), E * 4);
+    void* dd = hi.in(dst, E * 4);
+    void* dx = h.in(node_x, V * pr.dim_x);
+    void* dy = h.in(edge_y, E * pr.dim_y);
+    void* dw = h.in(edge_w, E * pr.n_w);
+    void* dz = h.out(V * pr.dim_z);
+    unfused_fwd(p, dtype, nodes, edges, static_cast<const std::int64_t*>(drp), static_cast<const std::int32_t*>(dri),
+                static_cast<const std::int32_t*>(dd), dx, dy, dw, dz, nullptr);
+    CU_CHECK(cgf::drv::cuCtxSynchronize());
+    h.back(node_z, dz, V * pr.dim_z);
+  });
+}
+
+int cgf_conv_unfused_backward_host(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int32_t* src,
+                                   const int32_t* dst, const void* node_x, const void* edge_y, const void* edge_w,
+                                   const void* g_node_z, void* g_node_x, void* g_edge_y, void* g_edge_w) {
+  return guarded([&] {
+    need(p, "plan");
+    if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (nodes == 0) return;
+    check_edge_list(nodes, edges, src, dst);
+    cgf::ensure_context();
+    const auto& pr = p->problem;
+    const std::size_t V = static_cast<std::size_t>(nodes), E = static_cast<std::size_t>(edges);
+    std::vector<std::int64_t> trp;
+    std::vector<std::int32_t> tidx;
+    host_bucket(nodes, edges, dst, trp, tidx);
+    HostCall h{dtype == CGF_F64 ? 8u : 4u, {}};
+    HostCall hi{1, {}};
+    void* ds = hi.in(src, E * 4);
+    void* dd = hi.in(dst, E * 4);
+    void* dtrp = hi.in(trp.data(), (V + 1) * 8);
+    void* dti = hi.in(tidx.data(), E * 4);
+    void* dx = h.in(node_x, V * pr.dim_x);
+    void* dy = h.in(edge_y, E * pr.dim_y);
+    void* dw = h.in(edge_w, E * pr.n_w);
+    void* dgz = h.in(g_node_z, V * pr.dim_z);
+    void* ogx = h.out(V * pr.dim_x);
+    void* ogy = h.out(E * pr.dim_y);
+    void* ogw = h.out(E * pr.n_w);
+    unfused_bwd(p, dtype, nodes, edges, static_cast<const std::int32_t*>(ds), static_cast<const std::int32_t*>(dd),
+                static_cast<const std::int64_t*>(dtrp), static_cast<const std::int32_t*>(dti), dx, dy, dw, dgz, ogx,
+                ogy, ogw, nullptr);
     CU_CHECK(cgf::drv::cuCtxSynchronize());
     h.back(g_node_x, ogx, V * pr.dim_x);
     h.back(g_edge_y, ogy, E * pr.dim_y);

@@ -59,6 +59,21 @@ DEVI void coop_store16(void* dst, const void* src, int n16, int lane) {
   float4* d = (float4*)dst;
   for (int i = lane; i < n16; i += 32) __stcs(d + i, s[i]);
 }
+// Atomic accumulation of a staged run into global memory (atomic-mode conv):
+// 16-byte vector reductions for FP32, scalar for FP64; results unused -> RED.
+DEVI void coop_red16(float* dst, const float* src, int n16, int lane) {
+  for (int i = lane; i < n16; i += 32) {
+    const float4 v = ((const float4*)src)[i];
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"((float4*)dst + i), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w) : "memory");
+  }
+}
+DEVI void coop_red16(double* dst, const double* src, int n16, int lane) {
+  for (int i = lane; i < 2 * n16; i += 32) atomicAdd(dst + i, src[i]);
+}
+template <class T> DEVI void coop_red(T* dst, const T* src, int n, int lane) {
+  for (int i = lane; i < n; i += 32) atomicAdd(dst + i, src[i]);
+}
 template <class T> DEVI T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -139,9 +154,10 @@ class Gen {
   bool out_w() const { return out_x(); }
   bool conv() const { return cfg_.loop != Loop::Rows; }
   bool by_input() const { return cfg_.loop == Loop::ConvByInput; }
-  bool yreg() const { return cfg_.y_regs && cfg_.loop == Loop::Rows; }
+  bool edges() const { return cfg_.loop == Loop::ConvEdges; }
+  bool yreg() const { return cfg_.y_regs && (cfg_.loop == Loop::Rows || edges()); }
   bool gy_flush() const { return out_y() && (dual() || cfg_.f64); }
-  Src x_src() const { return cfg_.loop == Loop::ConvByOutput ? Src::Nbr : Src::Row; }
+  Src x_src() const { return cfg_.loop == Loop::ConvByOutput || edges() ? Src::Nbr : Src::Row; }
   Src z_src() const { return cfg_.loop == Loop::ConvByInput ? Src::Nbr : Src::Row; }
   Src e_src() const { return conv() ? Src::Edge : Src::Row; }
   const char* idx(Src s) const { return s == Src::Row ? "row" : s == Src::Nbr ? "nbr" : "eid"; }
@@ -158,11 +174,10 @@ class Gen {
   void emit_wait_and_sync(int k);
   void emit_release();
   void emit_store(const std::string& dst, const std::string& rowexpr, std::uint32_t stride, long long off,
-                  long long step, std::uint32_t words, int guard_rows, int width, const std::string& reg);
+                  long long step, std::uint32_t words, int guard_rows, int width, const std::string& reg,
+                  bool atomic = false);
   void emit_unit_body(int k, const std::function<void(int)>& post_sub = {});
   std::string wsrc(const Sub& s, long long step, const std::string& arr) const;
-  std::string yv(int j) const { return yreg() ? "y[" + S(j) + "]" : "sl[ys + " + S(j) + "]"; }
-  std::string dbv(int j) const { return yreg() ? "db[" + S(j) + "]" : "sl[dbs + " + S(j) + "]"; }
   void emit_gy_reduce(const std::string& rowexpr);
   void emit_gy_flush_row(const std::string& rowexpr);
   void emit_class_loop_open(int k);
@@ -449,185 +464,223 @@ void Gen::emit_release() {
 }
 
 void Gen::emit_store(const std::string& dst, const std::string& rowexpr, std::uint32_t stride, long long off,
-                     long long step, std::uint32_t words, int guard_rows, int width, const std::string& reg) {
+                     long long step, std::uint32_t words, int guard_rows, int width, const std::string& reg,
+                     bool atomic) {
   o_ << "      if (lane < " << guard_rows << ") {";
   for (int k = 0; k < width; ++k) o_ << " scr[lane * " << width << " + " << k << "] = " << reg << "[" << k << "];";
   o_ << " }\n      __syncwarp();\n";
   const bool vec = cfg_.aligned && al16(stride) && al16(off) && al16(step) && al16(words);
   if (vec)
-    o_ << "      coop_store16(" << dst << " + " << rowexpr << " * (i64)" << stride << " + " << O(off, step)
-       << ", scr, " << words * sz_ / 16 << ", lane);\n";
+    o_ << "      " << (atomic ? "coop_red16(" : "coop_store16(") << dst << " + " << rowexpr << " * (i64)" << stride
+       << " + " << O(off, step) << ", scr, " << words * sz_ / 16 << ", lane);\n";
   else
-    o_ << "      coop_store(" << dst << " + " << rowexpr << " * (i64)" << stride << " + " << O(off, step) << ", scr, "
-       << words << ", lane);\n";
+    o_ << "      " << (atomic ? "coop_red(" : "coop_store(") << dst << " + " << rowexpr << " * (i64)" << stride << " + "
+       << O(off, step) << ", scr, " << words << ", lane);\n";
   o_ << "      __syncwarp();\n";
 }
 
 // Compute of one unit (class k, chunk kc) on its staged slot. The caller
 // declares x-chunk accumulators ax<c> (when the unit owns them) and z-piece
-// accumulators pz<c>.
+// accumulators pz<c>. A unit merged from m same-shape chunks (merge_units)
+// is emitted sub by sub with its m chunks side by side: the lane-uniform CG
+// products v*y[j] (and v*db[j]) are computed once and feed all m chunks.
 void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
   const UClass& Cl = cls_[k];
   const Unit& u = U0(k);
   const Layout& L = lay_[k];
   const std::string nw = S(p_.n_w);
   const std::string wrow = cfg_.w_shared ? "0" : idx(e_src());
-  for (size_t q = 0; q < u.subs.size(); ++q) {
-    const int qi = static_cast<int>(q);
-    const Sub& s = p_.subs[u.subs[q]];
-    const int dx = s.dx(), dz = s.dz();
-    const int xc = u.x_chunk_of(s), zc = u.z_piece_of(s);
-    const std::string AX = "ax" + S(xc), PZ = "pz" + S(zc);
-    const long long swq = Cl.sw[q];
-    if (q && cfg_.sub_barrier) o_ << "      asm volatile(\"\" ::: \"memory\");\n";
-    o_ << "      { // sub " << u.subs[q] << ": " << (s.kind == Kind::B ? "B" : "C") << " l=(" << s.l1 << "," << s.l2
-       << "," << s.l3 << ") b=" << s.b << " b'=" << s.bp << " nnz=" << s.cg->entries.size() << "\n";
-    const bool gfl = gy_flush();
-    if (gfl && out_y()) o_ << "        T gyl[" << s.dy() << "] = {};\n";
-    auto GY = [&](int j) { return gfl ? "gyl[" + S(j) + "]" : "gy[" + S(s.y_off + j) + "]"; };
-    const std::uint32_t xs = L.x_slot.at(s.x_off);
-    o_ << "        T xv[" << dx << "];" << (dual() ? " T av[" + S(dx) + "];" : "") << "\n        if (lane < " << s.bp
-       << ") {";
-    for (int i = 0; i < dx; ++i) o_ << " xv[" << i << "] = sl[" << xs << " + lane * " << dx << " + " << i << "];";
-    if (dual())
-      for (int i = 0; i < dx; ++i)
-        o_ << " av[" << i << "] = sl[" << L.a_slot.at(s.x_off) << " + lane * " << dx << " + " << i << "];";
-    o_ << " } else {";
-    for (int i = 0; i < dx; ++i) o_ << " xv[" << i << "] = 0;";
-    if (dual())
-      for (int i = 0; i < dx; ++i) o_ << " av[" << i << "] = 0;";
-    o_ << " }\n";
-    std::string gzs;
-    if (reads_gz()) {
-      gzs = S(L.gz_slot.at(s.z_off));
-      if (s.kind == Kind::B) {
-        o_ << "        T gz[" << dz << "];\n        if (lane < " << s.b << ") {";
-        for (int kk = 0; kk < dz; ++kk) o_ << " gz[" << kk << "] = sl[" << gzs << " + lane * " << dz << " + " << kk << "];";
-        o_ << " } else {";
-        for (int kk = 0; kk < dz; ++kk) o_ << " gz[" << kk << "] = 0;";
-        o_ << " }\n";
-      }
-    }
-    if (s.kind == Kind::B) {
-      auto wexpr = [&](const std::string& arr, const std::map<int, std::uint32_t>& slot) {
-        if (cfg_.w_shared) return "__ldg(" + wsrc(s, swq, arr) + " + lane)";
-        return "sl[" + S(slot.at(qi)) + " + lane]";
-      };
-      o_ << "        const T wt = (lane < " << s.b << ") ? " << wexpr("W", L.w_slot) << " : (T)0;\n";
-      if (dual()) o_ << "        const T ct = (lane < " << s.b << ") ? " << wexpr("DC", L.c_slot) << " : (T)0;\n";
-    }
-    const bool need_gzc = cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdX;
-    if (reads_gz()) {
-      o_ << "        T gzp[" << dz << "];" << (need_gzc ? " T gzc[" + S(dz) + "];" : "") << "\n";
-      if (s.kind == Kind::B) {
-        for (int kk = 0; kk < dz; ++kk)
-          o_ << "        gzp[" << kk << "] = wt * gz[" << kk << "];"
-             << (need_gzc ? " gzc[" + S(kk) + "] = ct * gz[" + S(kk) + "];" : "") << "\n";
-      } else {
-        o_ << "        {";
-        for (int kk = 0; kk < dz; ++kk) o_ << " gzp[" << kk << "] = 0;" << (need_gzc ? " gzc[" + S(kk) + "] = 0;" : "");
-        o_ << "\n          const T* wg = " << wsrc(s, swq, "W") << ";\n";
-        if (need_gzc) o_ << "          const T* cg = " << wsrc(s, swq, "DC") << ";\n";
-        o_ << "#pragma unroll 2\n          for (int r = 0; r < " << s.b << "; ++r) {\n"
-           << "            const T wv = (lane < " << s.bp << ") ? __ldg(wg + r * " << s.w_stride << " + lane) : (T)0;\n";
-        if (need_gzc)
-          o_ << "            const T cv = (lane < " << s.bp << ") ? __ldg(cg + r * " << s.w_stride << " + lane) : (T)0;\n";
-        for (int kk = 0; kk < dz; ++kk) {
-          o_ << "            { const T g = sl[" << gzs << " + r * " << dz << " + " << kk << "]; gzp[" << kk
-             << "] = fma(wv, g, gzp[" << kk << "]);";
-          if (need_gzc) o_ << " gzc[" << kk << "] = fma(cv, g, gzc[" << kk << "]);";
+  const int nsub = static_cast<int>(u.subs.size());
+  const int m = (cfg_.joint && u.merged > 1 && nsub % u.merged == 0) ? u.merged : 1;
+  const int n = nsub / m;
+  const bool need_gzc = cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdX;
+  const bool zx_on = cfg_.comp == Comp::Fwd || cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ;
+  const bool zab = cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX;
+  const bool gfl = gy_flush();
+  if (!yreg()) {
+    // the item's y (and db) into registers once: no per-entry shared-memory
+    // reads, and the products below can be shared across chunks
+    o_ << "      T yq[" << p_.dim_y << "];" << (dual() ? " T dbq[" + S(p_.dim_y) + "];" : "");
+    for (int j = 0; j < p_.dim_y; ++j)
+      o_ << " yq[" << j << "] = sl[ys + " << j << "];" << (dual() ? " dbq[" + S(j) + "] = sl[dbs + " + S(j) + "];" : "");
+    o_ << "\n";
+  }
+  auto Y = [&](int j) { return yreg() ? "y[" + S(j) + "]" : "yq[" + S(j) + "]"; };
+  auto DB = [&](int j) { return yreg() ? "db[" + S(j) + "]" : "dbq[" + S(j) + "]"; };
+  for (int g = 0; g < n; ++g) {
+    if (g && cfg_.sub_barrier) o_ << "      asm volatile(\"\" ::: \"memory\");\n";
+    const Sub& s0 = p_.subs[u.subs[g]];
+    const int dx = s0.dx(), dz = s0.dz();
+    o_ << "      { // sub";
+    for (int c = 0; c < m; ++c) o_ << " " << u.subs[g + c * n];
+    o_ << ": " << (s0.kind == Kind::B ? "B" : "C") << " l=(" << s0.l1 << "," << s0.l2 << "," << s0.l3 << ") b=" << s0.b
+       << " b'=" << s0.bp << " nnz=" << s0.cg->entries.size() << (m > 1 ? " x" + S(m) + " chunks" : "") << "\n";
+    // ---- per-chunk operands ----
+    for (int c = 0; c < m; ++c) {
+      const int qi = g + c * n;
+      const Sub& s = p_.subs[u.subs[qi]];
+      const std::string X = "_" + S(c);
+      const long long swq = Cl.sw[qi];
+      if (gfl && out_y()) o_ << "        T gyl" << X << "[" << s.dy() << "] = {};\n";
+      const std::uint32_t xs = L.x_slot.at(s.x_off);
+      o_ << "        T xv" << X << "[" << dx << "];" << (dual() ? " T av" + X + "[" + S(dx) + "];" : "")
+         << "\n        if (lane < " << s.bp << ") {";
+      for (int i = 0; i < dx; ++i) o_ << " xv" << X << "[" << i << "] = sl[" << xs << " + lane * " << dx << " + " << i << "];";
+      if (dual())
+        for (int i = 0; i < dx; ++i)
+          o_ << " av" << X << "[" << i << "] = sl[" << L.a_slot.at(s.x_off) << " + lane * " << dx << " + " << i << "];";
+      o_ << " } else {";
+      for (int i = 0; i < dx; ++i) o_ << " xv" << X << "[" << i << "] = 0;";
+      if (dual())
+        for (int i = 0; i < dx; ++i) o_ << " av" << X << "[" << i << "] = 0;";
+      o_ << " }\n";
+      std::string gzs;
+      if (reads_gz()) {
+        gzs = S(L.gz_slot.at(s.z_off));
+        if (s.kind == Kind::B) {
+          o_ << "        T gz" << X << "[" << dz << "];\n        if (lane < " << s.b << ") {";
+          for (int kk = 0; kk < dz; ++kk) o_ << " gz" << X << "[" << kk << "] = sl[" << gzs << " + lane * " << dz << " + " << kk << "];";
+          o_ << " } else {";
+          for (int kk = 0; kk < dz; ++kk) o_ << " gz" << X << "[" << kk << "] = 0;";
           o_ << " }\n";
         }
-        o_ << "          }\n        }\n";
       }
+      if (s.kind == Kind::B) {
+        auto wexpr = [&](const std::string& arr, const std::map<int, std::uint32_t>& slot) {
+          if (cfg_.w_shared) return "__ldg(" + wsrc(s, swq, arr) + " + lane)";
+          return "sl[" + S(slot.at(qi)) + " + lane]";
+        };
+        o_ << "        const T wt" << X << " = (lane < " << s.b << ") ? " << wexpr("W", L.w_slot) << " : (T)0;\n";
+        if (dual()) o_ << "        const T ct" << X << " = (lane < " << s.b << ") ? " << wexpr("DC", L.c_slot) << " : (T)0;\n";
+      }
+      if (reads_gz()) {
+        o_ << "        T gzp" << X << "[" << dz << "];" << (need_gzc ? " T gzc" + X + "[" + S(dz) + "];" : "") << "\n";
+        if (s.kind == Kind::B) {
+          for (int kk = 0; kk < dz; ++kk)
+            o_ << "        gzp" << X << "[" << kk << "] = wt" << X << " * gz" << X << "[" << kk << "];"
+               << (need_gzc ? " gzc" + X + "[" + S(kk) + "] = ct" + X + " * gz" + X + "[" + S(kk) + "];" : "") << "\n";
+        } else {
+          o_ << "        {";
+          for (int kk = 0; kk < dz; ++kk)
+            o_ << " gzp" << X << "[" << kk << "] = 0;" << (need_gzc ? " gzc" + X + "[" + S(kk) + "] = 0;" : "");
+          o_ << "\n          const T* wg = " << wsrc(s, swq, "W") << ";\n";
+          if (need_gzc) o_ << "          const T* cg = " << wsrc(s, swq, "DC") << ";\n";
+          o_ << "#pragma unroll 2\n          for (int r = 0; r < " << s.b << "; ++r) {\n"
+             << "            const T wv = (lane < " << s.bp << ") ? __ldg(wg + r * " << s.w_stride << " + lane) : (T)0;\n";
+          if (need_gzc)
+            o_ << "            const T cv = (lane < " << s.bp << ") ? __ldg(cg + r * " << s.w_stride << " + lane) : (T)0;\n";
+          for (int kk = 0; kk < dz; ++kk) {
+            o_ << "            { const T g = sl[" << gzs << " + r * " << dz << " + " << kk << "]; gzp" << X << "[" << kk
+               << "] = fma(wv, g, gzp" << X << "[" << kk << "]);";
+            if (need_gzc) o_ << " gzc" << X << "[" << kk << "] = fma(cv, g, gzc" << X << "[" << kk << "]);";
+            o_ << " }\n";
+          }
+          o_ << "          }\n        }\n";
+        }
+      }
+      if (zx_on) o_ << "        T zx" << X << "[" << dz << "] = {};\n";
+      if (zab) o_ << "        T za" << X << "[" << dz << "] = {}; T zb" << X << "[" << dz << "] = {};\n";
     }
-    // ---- the unrolled CG stream (one line per nonzero entry) ----
-    const bool zx = cfg_.comp == Comp::Fwd || cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ;
-    const bool zab = cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX;
-    if (zx) o_ << "        T zx[" << dz << "] = {};\n";
-    if (zab) o_ << "        T za[" << dz << "] = {}; T zb[" << dz << "] = {};\n";
-    for (const auto& e : s.cg->entries) {
+    // ---- the unrolled CG stream (one line per nonzero entry, all chunks) ----
+    for (const auto& e : s0.cg->entries) {
       const std::string v = "(T)" + hexd(e.v), I = S(e.i), K = S(e.k);
-      const int J = s.y_off + e.j;
+      const int J = s0.y_off + e.j;
       std::ostringstream l;
-      l << "        { const T cy = " << v << " * " << yv(J) << ";";
-      if (dual()) l << " const T cb = " << v << " * " << dbv(J) << ";";
-      if (zx) l << " zx[" << K << "] = fma(cy, xv[" << I << "], zx[" << K << "]);";
-      if (zab)
-        l << " za[" << K << "] = fma(cy, av[" << I << "], za[" << K << "]); zb[" << K << "] = fma(cb, xv[" << I
-          << "], zb[" << K << "]);";
-      if (cfg_.comp == Comp::Bwd)
-        l << " " << AX << "[" << I << "] = fma(cy, gzp[" << K << "], " << AX << "[" << I << "]);"
-          << " " << GY(e.j) << " = fma(" << v << " * xv[" << I << "], gzp[" << K << "], " << GY(e.j) << ");";
-      if (need_gzc)
-        l << " " << AX << "[" << I << "] = fma(cb, gzp[" << K << "], fma(cy, gzc[" << K << "], " << AX << "[" << I
-          << "]));"
-          << " " << GY(e.j) << " = fma(" << v << " * av[" << I << "], gzp[" << K << "], fma(" << v << " * xv[" << I
-          << "], gzc[" << K << "], " << GY(e.j) << "));";
+      l << "        { const T cy = " << v << " * " << Y(J) << ";";
+      if (dual()) l << " const T cb = " << v << " * " << DB(J) << ";";
+      for (int c = 0; c < m; ++c) {
+        const int qi = g + c * n;
+        const Sub& s = p_.subs[u.subs[qi]];
+        const std::string X = "_" + S(c);
+        const std::string AX = "ax" + S(u.x_chunk_of(s));
+        auto GY = [&](int j) { return gfl ? "gyl" + X + "[" + S(j) + "]" : "gy[" + S(s.y_off + j) + "]"; };
+        if (zx_on) l << " zx" << X << "[" << K << "] = fma(cy, xv" << X << "[" << I << "], zx" << X << "[" << K << "]);";
+        if (zab)
+          l << " za" << X << "[" << K << "] = fma(cy, av" << X << "[" << I << "], za" << X << "[" << K << "]); zb" << X << "[" << K
+            << "] = fma(cb, xv" << X << "[" << I << "], zb" << X << "[" << K << "]);";
+        if (cfg_.comp == Comp::Bwd)
+          l << " " << AX << "[" << I << "] = fma(cy, gzp" << X << "[" << K << "], " << AX << "[" << I << "]);"
+            << " " << GY(e.j) << " = fma(" << v << " * xv" << X << "[" << I << "], gzp" << X << "[" << K << "], " << GY(e.j) << ");";
+        if (need_gzc)
+          l << " " << AX << "[" << I << "] = fma(cb, gzp" << X << "[" << K << "], fma(cy, gzc" << X << "[" << K << "], " << AX
+            << "[" << I << "]));"
+            << " " << GY(e.j) << " = fma(" << v << " * av" << X << "[" << I << "], gzp" << X << "[" << K << "], fma(" << v
+            << " * xv" << X << "[" << I << "], gzc" << X << "[" << K << "], " << GY(e.j) << "));";
+      }
       l << " }\n";
       o_ << l.str();
     }
-    // ---- weight application (z-type outputs) ----
-    if (out_z()) {
-      const bool dzm = cfg_.comp != Comp::Fwd;  // dgz = W.(za+zb) + dC.zx
-      if (s.kind == Kind::B) {
-        for (int kk = 0; kk < dz; ++kk) {
-          if (dzm)
-            o_ << "        " << PZ << "[" << kk << "] = fma(ct, zx[" << kk << "], fma(wt, za[" << kk << "] + zb[" << kk
-               << "], " << PZ << "[" << kk << "]));\n";
-          else
-            o_ << "        " << PZ << "[" << kk << "] = fma(wt, zx[" << kk << "], " << PZ << "[" << kk << "]);\n";
+    // ---- per-chunk epilogues ----
+    for (int c = 0; c < m; ++c) {
+      const int qi = g + c * n;
+      const Sub& s = p_.subs[u.subs[qi]];
+      const std::string X = "_" + S(c);
+      const std::string PZ = "pz" + S(u.z_piece_of(s));
+      const long long swq = Cl.sw[qi];
+      const std::string gzs = reads_gz() ? S(L.gz_slot.at(s.z_off)) : "";
+      // weight application (z-type outputs)
+      if (out_z()) {
+        const bool dzm = cfg_.comp != Comp::Fwd;  // dgz = W.(za+zb) + dC.zx
+        if (s.kind == Kind::B) {
+          for (int kk = 0; kk < dz; ++kk) {
+            if (dzm)
+              o_ << "        " << PZ << "[" << kk << "] = fma(ct" << X << ", zx" << X << "[" << kk << "], fma(wt" << X << ", za" << X
+                 << "[" << kk << "] + zb" << X << "[" << kk << "], " << PZ << "[" << kk << "]));\n";
+            else
+              o_ << "        " << PZ << "[" << kk << "] = fma(wt" << X << ", zx" << X << "[" << kk << "], " << PZ << "[" << kk << "]);\n";
+          }
+        } else {
+          o_ << "        if (lane < " << s.bp << ") {";
+          for (int kk = 0; kk < dz; ++kk) {
+            if (dzm)
+              o_ << " zs[lane * " << dz << " + " << kk << "] = za" << X << "[" << kk << "] + zb" << X << "[" << kk << "]; zs["
+                 << 32 * dz << " + lane * " << dz << " + " << kk << "] = zx" << X << "[" << kk << "];";
+            else
+              o_ << " zs[lane * " << dz << " + " << kk << "] = zx" << X << "[" << kk << "];";
+          }
+          o_ << " }\n        { const T* wg = " << wsrc(s, swq, "W") << ";"
+             << (dzm ? " const T* cg = " + wsrc(s, swq, "DC") + ";" : "") << "\n"
+             << "#pragma unroll 4\n          for (int r = 0; r < " << s.b << "; ++r) if (lane < " << s.bp
+             << ") { wts[r * 33 + lane] = __ldg(wg + r * " << s.w_stride << " + lane);";
+          if (dzm) o_ << " cts[r * 33 + lane] = __ldg(cg + r * " << s.w_stride << " + lane);";
+          o_ << " } }\n        __syncwarp();\n        if (lane < " << s.b << ") {\n#pragma unroll 4\n"
+             << "          for (int c = 0; c < " << s.bp << "; ++c) { const T wv = wts[lane * 33 + c];"
+             << (dzm ? " const T cv = cts[lane * 33 + c];" : "");
+          for (int kk = 0; kk < dz; ++kk) {
+            if (dzm)
+              o_ << " " << PZ << "[" << kk << "] = fma(cv, zs[" << 32 * dz << " + c * " << dz << " + " << kk
+                 << "], fma(wv, zs[c * " << dz << " + " << kk << "], " << PZ << "[" << kk << "]));";
+            else
+              o_ << " " << PZ << "[" << kk << "] = fma(wv, zs[c * " << dz << " + " << kk << "], " << PZ << "[" << kk << "]);";
+          }
+          o_ << " }\n        }\n        __syncwarp();\n";
         }
-      } else {
-        o_ << "        if (lane < " << s.bp << ") {";
-        for (int kk = 0; kk < dz; ++kk) {
-          if (dzm)
-            o_ << " zs[lane * " << dz << " + " << kk << "] = za[" << kk << "] + zb[" << kk << "]; zs[" << 32 * dz
-               << " + lane * " << dz << " + " << kk << "] = zx[" << kk << "];";
-          else
-            o_ << " zs[lane * " << dz << " + " << kk << "] = zx[" << kk << "];";
-        }
-        o_ << " }\n        { const T* wg = " << wsrc(s, swq, "W") << ";"
-           << (dzm ? " const T* cg = " + wsrc(s, swq, "DC") + ";" : "") << "\n"
-           << "#pragma unroll 4\n          for (int r = 0; r < " << s.b << "; ++r) if (lane < " << s.bp
-           << ") { wts[r * 33 + lane] = __ldg(wg + r * " << s.w_stride << " + lane);";
-        if (dzm) o_ << " cts[r * 33 + lane] = __ldg(cg + r * " << s.w_stride << " + lane);";
-        o_ << " } }\n        __syncwarp();\n        if (lane < " << s.b << ") {\n#pragma unroll 4\n"
-           << "          for (int c = 0; c < " << s.bp << "; ++c) { const T wv = wts[lane * 33 + c];"
-           << (dzm ? " const T cv = cts[lane * 33 + c];" : "");
-        for (int kk = 0; kk < dz; ++kk) {
-          if (dzm)
-            o_ << " " << PZ << "[" << kk << "] = fma(cv, zs[" << 32 * dz << " + c * " << dz << " + " << kk
-               << "], fma(wv, zs[c * " << dz << " + " << kk << "], " << PZ << "[" << kk << "]));";
-          else
-            o_ << " " << PZ << "[" << kk << "] = fma(wv, zs[c * " << dz << " + " << kk << "], " << PZ << "[" << kk << "]);";
-        }
-        o_ << " }\n        }\n        __syncwarp();\n";
       }
-    }
-    // ---- weight gradients (per sub, written directly) ----
-    if (out_w()) {
-      auto zk = [&](int kk) {
-        return cfg_.comp == Comp::Bwd ? "zx[" + S(kk) + "]" : "(za[" + S(kk) + "] + zb[" + S(kk) + "])";
-      };
-      if (s.kind == Kind::B) {
-        o_ << "        { T g = 0;";
-        for (int kk = 0; kk < dz; ++kk) o_ << " g = fma(gz[" << kk << "], " << zk(kk) << ", g);";
-        o_ << " if (lane < " << s.b << ") O2[" << wrow << " * (i64)" << nw << " + " << O(s.w_off, swq) << " + lane] = g; }\n";
-      } else {
-        o_ << "#pragma unroll 2\n        for (int r = 0; r < " << s.b << "; ++r) { T g = 0;";
-        for (int kk = 0; kk < dz; ++kk)
-          o_ << " g = fma(sl[" << gzs << " + r * " << dz << " + " << kk << "], " << zk(kk) << ", g);";
-        o_ << " if (lane < " << s.bp << ") O2[" << wrow << " * (i64)" << nw << " + " << O(s.w_off, swq) << " + r * "
-           << s.w_stride << " + lane] = g; }\n";
+      // weight gradients (per sub, written directly)
+      if (out_w()) {
+        auto zk = [&](int kk) {
+          return cfg_.comp == Comp::Bwd ? "zx" + X + "[" + S(kk) + "]" : "(za" + X + "[" + S(kk) + "] + zb" + X + "[" + S(kk) + "])";
+        };
+        if (s.kind == Kind::B) {
+          o_ << "        { T g = 0;";
+          for (int kk = 0; kk < dz; ++kk) o_ << " g = fma(gz" << X << "[" << kk << "], " << zk(kk) << ", g);";
+          o_ << " if (lane < " << s.b << ") O2[" << wrow << " * (i64)" << nw << " + " << O(s.w_off, swq) << " + lane] = g; }\n";
+        } else {
+          o_ << "#pragma unroll 2\n        for (int r = 0; r < " << s.b << "; ++r) { T g = 0;";
+          for (int kk = 0; kk < dz; ++kk)
+            o_ << " g = fma(sl[" << gzs << " + r * " << dz << " + " << kk << "], " << zk(kk) << ", g);";
+          o_ << " if (lane < " << s.bp << ") O2[" << wrow << " * (i64)" << nw << " + " << O(s.w_off, swq) << " + r * "
+             << s.w_stride << " + lane] = g; }\n";
+        }
       }
+      if (gfl && out_y())
+        for (int j = 0; j < s.dy(); ++j)
+          o_ << "        { const T s_ = warp_sum(gyl" << X << "[" << j << "]); if (lane == " << j % 32 << ") gya["
+             << s.y_off + j << "] += s_; }\n";
     }
-    if (gfl && out_y())
-      for (int j = 0; j < s.dy(); ++j)
-        o_ << "        { const T s_ = warp_sum(gyl[" << j << "]); if (lane == " << j % 32 << ") gya[" << s.y_off + j
-           << "] += s_; }\n";
     o_ << "      }\n";
-    if (post_sub) post_sub(qi);
+    if (post_sub)
+      for (int c = 0; c < m; ++c) post_sub(g + c * n);
   }
 }
 
@@ -668,26 +721,34 @@ void Gen::emit_rows_loop() {
         "#define producer_next() do { if (pn < total) {\\\n"
         "    const i64 rr_ = pn / NU; const int u_ = (int)(pn - rr_ * NU); const i64 r_ = gwarp + rr_ * nwarp;\\\n"
         "    const int s_ = (int)(pn % D);\\\n"
-        "    issue_unit(u_, r_, r_, r_, rows, rows, wsm + s_ * SLOT_WORDS, &bars[s_], X, Y, W, GZ, DA, DB, DC" << (cfg_.lane_copy ? ", lane" : "") << ");\\\n"
+     << (edges() ? "    issue_unit(u_, (i64)EID[r_], (i64)NB[r_], r_, rows, edges_tot,"
+                 : "    issue_unit(u_, r_, r_, r_, rows, rows,")
+     << " wsm + s_ * SLOT_WORDS, &bars[s_], X, Y, W, GZ, DA, DB, DC" << (cfg_.lane_copy ? ", lane" : "") << ");\\\n"
         "    ++pn; } } while (0)\n"
         "  " << (cfg_.lane_copy ? "" : "if (lane == 0) ") << "for (int d = 0; d < D; ++d) producer_next();\n"
         "  int slot = 0; u32 phase = 0;\n"
-        "  for (i64 rr = 0; rr < my_rows; ++rr) {\n    const i64 row = gwarp + rr * nwarp;\n"
-        "    const i64 nbr = row, eid = row; (void)nbr; (void)eid;\n";
+        "  for (i64 rr = 0; rr < my_rows; ++rr) {\n";
+  // the item index: a batch row, or (atomic conv) an edge with its output node
+  // (row = src) and neighbour (nbr = dst)
+  const std::string it = edges() ? "eid" : "row";
+  if (edges())
+    o_ << "    const i64 eid = gwarp + rr * nwarp;\n    const i64 row = EID[eid], nbr = NB[eid];\n";
+  else
+    o_ << "    const i64 row = gwarp + rr * nwarp;\n    const i64 nbr = row, eid = row; (void)nbr; (void)eid;\n";
   if (yreg()) {
     const int dy = p_.dim_y;
     o_ << "    if (rr == 0) {";
     for (int j = 0; j < dy; ++j) {
-      o_ << " yn[" << j << "] = __ldg(Y + row * " << dy << " + " << j << ");";
-      if (dual()) o_ << " dbn[" << j << "] = __ldg(DB + row * " << dy << " + " << j << ");";
+      o_ << " yn[" << j << "] = __ldg(Y + " << it << " * " << dy << " + " << j << ");";
+      if (dual()) o_ << " dbn[" << j << "] = __ldg(DB + " << it << " * " << dy << " + " << j << ");";
     }
     o_ << " }\n   ";
     for (int j = 0; j < dy; ++j)
       o_ << " y[" << j << "] = yn[" << j << "];" << (dual() ? " db[" + S(j) + "] = dbn[" + S(j) + "];" : "");
     o_ << "\n    if (rr + 1 < my_rows) {";
     for (int j = 0; j < dy; ++j) {
-      o_ << " yn[" << j << "] = __ldg(Y + (row + nwarp) * " << dy << " + " << j << ");";
-      if (dual()) o_ << " dbn[" << j << "] = __ldg(DB + (row + nwarp) * " << dy << " + " << j << ");";
+      o_ << " yn[" << j << "] = __ldg(Y + (" << it << " + nwarp) * " << dy << " + " << j << ");";
+      if (dual()) o_ << " dbn[" << j << "] = __ldg(DB + (" << it << " + nwarp) * " << dy << " + " << j << ");";
     }
     o_ << " }\n";
   }
@@ -727,13 +788,14 @@ void Gen::emit_rows_loop() {
       if (out_x())
         for (int c : x_done[q]) {
           const auto& xc = u.x_chunks[c];
-          emit_store("O0", "row", p_.dim_x, xc.off, C.xstep[c], xc.words, xb[xc.off], xdx[xc.off], "ax" + S(c));
+          emit_store("O0", edges() ? "nbr" : "row", p_.dim_x, xc.off, C.xstep[c], xc.words, xb[xc.off],
+                     xdx[xc.off], "ax" + S(c), edges());
         }
       if (out_z())
         for (int z : z_done[q]) {
           const auto& zp = u.z_pieces[z];
           emit_store(cfg_.comp == Comp::Fwd ? "O0" : "O3", "row", p_.dim_z, zp.off, C.zstep[z], zp.words, zb[zp.off],
-                     zdz[zp.off], "pz" + S(z));
+                     zdz[zp.off], "pz" + S(z), edges());
         }
     });
     emit_release();
@@ -741,9 +803,9 @@ void Gen::emit_rows_loop() {
   }
   if (out_y()) {
     if (gy_flush())
-      emit_gy_flush_row("row");
+      emit_gy_flush_row(it);
     else
-      emit_gy_reduce("row");
+      emit_gy_reduce(it);
   }
   o_ << "  }\n";
 }
@@ -847,6 +909,8 @@ KernelSource Gen::run() {
     throw UnsupportedError("ConvByInput computes x-type outputs only");
   if (!conv() && (cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX))
     throw UnsupportedError("split double-backward passes are conv-only");
+  if (edges() && (cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX))
+    throw UnsupportedError("the atomic edge-list conv runs the double-backward in one pass");
   classify();
   layout();
   std::uint32_t slot_words = 0;
@@ -867,7 +931,7 @@ KernelSource Gen::run() {
     throw UnsupportedError("problem too large for one warp's shared-memory slot (" + S(warp_bytes(1)) + " bytes)");
   const std::uint64_t wb = (warp_bytes(depth) + 127) / 128 * 128;
   static const char* compn[] = {"fwd", "bwd", "dbwd", "dbwdz", "dbwdx"};
-  static const char* loopn[] = {"tp", "convo", "convi"};
+  static const char* loopn[] = {"tp", "convo", "convi", "conve"};
   KernelSource ks;
   ks.name = std::string("cgf_") + loopn[static_cast<int>(cfg_.loop)] + "_" + compn[static_cast<int>(cfg_.comp)] +
             (cfg_.f64 ? "_f64" : "_f32") + (cfg_.w_shared ? "_ws" : "") + (cfg_.aligned ? "" : "_u");
@@ -907,9 +971,10 @@ KernelSource Gen::run() {
         "  if (lane == 0) { for (int d = 0; d < D; ++d) mbar_init(&bars[d], " << (cfg_.lane_copy ? 32 : 1) << "); mbar_fence_init(); }\n"
         "  __syncwarp();\n"
         "  const i64 gwarp = (i64)blockIdx.x * NW + wid, nwarp = (i64)gridDim.x * NW;\n"
-        "  const i64 my_rows = gwarp < rows ? (rows - 1 - gwarp) / nwarp + 1 : 0;\n"
+        "  const i64 n_items = " << (edges() ? "edges_tot" : "rows") << ";\n"
+        "  const i64 my_rows = gwarp < n_items ? (n_items - 1 - gwarp) / nwarp + 1 : 0;\n"
         "  const i64 total = my_rows * NU; (void)total;\n";
-  if (conv())
+  if (conv() && !edges())
     emit_conv_loop();
   else
     emit_rows_loop();
@@ -939,6 +1004,8 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "bulk") cfg.lane_copy = false;
     else if (k == "merge") cfg.merge = std::max(1, v);
     else if (k == "lanecopy") cfg.lane_copy = true;
+    else if (k == "nojoint") cfg.joint = false;
+    else if (k == "joint") cfg.joint = true;
   }
 }
 
@@ -955,6 +1022,7 @@ std::vector<Unit> merge_units(const Problem& p, const std::vector<Unit>& units, 
     size_t j = i + 1;
     while (j < units.size() && static_cast<int>(j - i) < m && same_shape(p, units[i], units[j])) ++j;
     Unit u = units[i];
+    u.merged = static_cast<int>(j - i);
     for (size_t k = i + 1; k < j; ++k) {
       const Unit& v = units[k];
       u.subs.insert(u.subs.end(), v.subs.begin(), v.subs.end());

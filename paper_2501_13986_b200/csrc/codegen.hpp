@@ -16,6 +16,10 @@
 //   ConvByInput   fused conv, row = neighbour node d (transposed CSR):
 //                 for each edge, all units; gx_d accumulated in registers,
 //                 per-edge gy / gW written directly (conv.cpp:357-528).
+//   ConvEdges     atomic-mode conv over an edge list in any order (ConvPlan
+//                 Mode::atomic, conv.cpp:311-324): item = (edge, unit); node
+//                 outputs (z at src, gx at dst) accumulate with vector float
+//                 atomics, per-edge gy / gW written directly.
 #pragma once
 
 #include <string>
@@ -36,7 +40,7 @@ enum class Comp : int {
   DBwdX = 4,  // conv double-backward pass 2: dx, dy, dW
 };
 
-enum class Loop : int { Rows = 0, ConvByOutput = 1, ConvByInput = 2 };
+enum class Loop : int { Rows = 0, ConvByOutput = 1, ConvByInput = 2, ConvEdges = 3 };
 
 struct KernelConfig {
   Comp comp = Comp::Fwd;
@@ -51,13 +55,15 @@ struct KernelConfig {
   bool y_regs = false;    // Rows loop: y / db in registers (prefetched) instead of the slot
   int max_class = 1 << 20;  // max units folded into one code body (1 = fully unrolled units)
   int merge = 1;            // chunks (same-shape units) per staged item and code body
+  bool joint = false;       // emit a merged unit's chunks side by side (shared v*y[j] products); measured
+                            // neutral on the TP, +15 % on the C4 conv forward (profiles/r01_ab_joint.log)
   bool lane_copy = true;    // stage inputs with per-lane 16-byte cp.async (whole warp) instead of
                             // one lane's cp.async.bulk: no single-lane issue loop per range
 };
 
 // Applies "k=v,flag,..." overrides (env CGF_GEN) to a config: depth=N,
 // warps=N, minb=N, nobarrier, barrier, yreg, yslot, class=N, bulk (one-lane bulk copies), lanecopy,
-// merge=N.
+// merge=N, joint / nojoint.
 void apply_gen_flags(KernelConfig& cfg, const std::string& flags);
 
 struct KernelSource {
@@ -80,6 +86,8 @@ struct KernelSource {
 //   neighbour read by edge e (reference `dst`); edge id = CSR position.
 // ConvByInput: rows = nodes, RP = transposed row_ptr, NB[q] = output node of
 //   transposed position q, EID[q] = its edge id.
+// ConvEdges: rows = nodes, edges_tot = edges, EID[e] = output node (src) of
+//   edge e, NB[e] = its neighbour (dst); RP unused. Node outputs must be zeroed.
 // Outputs: Fwd O0=z; Bwd O0=gx O1=gy O2=gW; DBwd O0=dx O1=dy O2=dW O3=dgz;
 //   DBwdZ O3=dgz; DBwdX O0=dx O1=dy O2=dW.
 KernelSource generate_kernel(const Problem& p, const std::vector<Unit>& units,

@@ -125,6 +125,7 @@ struct Unit {
   std::vector<int> subs;        // indices into Problem::subs, schedule order
   std::vector<Piece> x_chunks;  // distinct x chunks read (and gx / dx written)
   std::vector<Piece> z_pieces;  // distinct z pieces written (gz / dgz read)
+  int merged = 1;               // same-shape chunks folded in (subs = merged groups of equal length)
   int x_chunk_of(const Sub& s) const;
   int z_piece_of(const Sub& s) const;
 };

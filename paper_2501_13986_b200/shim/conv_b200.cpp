@@ -1,14 +1,16 @@
 // Drop-in replacement for cgforge's src/conv.cpp (include/cgforge/conv.hpp,
 // unchanged): the fused convolution and the unfused gather -> TP -> scatter
-// comparator run on the B200 kernels through the C ABI; the graph utilities
+// comparator (gather, batched TP, per-node sums) run on the B200 kernels
+// through the C ABI; the graph utilities
 // (XYZ loading, CSR build, radius graph, transpose permutation, lattice) are
 // host code with the reference's contracts (conv.hpp:20-91).
 //
 // ConvStats follow a store/load model of the GPU kernels: the fused conv
 // writes each output row once (output_store_ops = |V|, stores |V| dim_z) and
 // streams y, W per edge plus x per edge from L2; the unfused path stores one
-// z row per edge and reads the gathered x twice (gather + TP). Mode::atomic is
-// served by the deterministic kernels (identical results).
+// z row per edge and reads the gathered x twice (gather + TP). Mode::atomic
+// runs the atomic edge-list kernels (no sortedness or permutation required,
+// as in conv.cpp:240 / 371-374).
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -195,7 +197,11 @@ std::vector<std::int32_t> neighbours(const GraphCSR& g) {
   return nb;
 }
 
-int gpu_mode(Mode m) { return m == Mode::atomic ? CGF_CONV_ATOMIC : CGF_CONV_DETERMINISTIC; }
+std::vector<std::int32_t> sources(const GraphCSR& g) {
+  std::vector<std::int32_t> s(g.edges.size());
+  for (std::size_t e = 0; e < g.edges.size(); ++e) s[e] = g.edges[e].src;
+  return s;
+}
 
 }  // namespace
 
@@ -205,18 +211,22 @@ ConvStats ConvPlan::forward(const GraphCSR& g, const std::vector<T>& node_x, con
                             const ConvOptions&) const {
   const auto& p = prob(*plan_);
   require_conv_shapes(p, g, node_x, edge_y, edge_w);
-  require_sorted(g);
+  if (mode == Mode::deterministic) require_sorted(g);
   node_z.assign(static_cast<std::size_t>(g.node_count) * p.dim_z, T(0));
   const auto nb = neighbours(g);
-  if (g.node_count > 0)
+  if (g.node_count > 0 && mode == Mode::atomic)
+    check(cgf_conv_forward_atomic_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(), sources(g).data(),
+                                       nb.data(), node_x.data(), edge_y.data(), edge_w.data(), node_z.data()));
+  else if (g.node_count > 0)
     check(cgf_conv_forward_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(), g.row_ptr.data(),
                                 nb.data(), node_x.data(), edge_y.data(), edge_w.data(), node_z.data(),
-                                gpu_mode(mode)));
+                                CGF_CONV_DETERMINISTIC));
   const auto E = static_cast<std::uint64_t>(g.edge_count()), V = static_cast<std::uint64_t>(g.node_count);
   ConvStats st;
   st.loads_words = E * (p.dim_x + p.dim_y + p.total_weights);
-  st.stores_words = V * p.dim_z;
-  st.output_store_ops = V;
+  // deterministic: each output row stored once; atomic: one reduction per edge
+  st.stores_words = mode == Mode::atomic ? E * p.dim_z : V * p.dim_z;
+  st.output_store_ops = mode == Mode::atomic ? E : V;
   st.flops = E * plan_->schedule().traffic.flops;
   return st;
 }
@@ -228,18 +238,24 @@ ConvStats ConvPlan::backward(const GraphCSR& g, const std::vector<std::int64_t>&
                              std::vector<T>& g_edge_w, Mode mode, const ConvOptions&) const {
   const auto& p = prob(*plan_);
   require_conv_shapes(p, g, node_x, edge_y, edge_w);
-  require_sorted(g);
   if (g_node_z.size() != static_cast<std::size_t>(g.node_count) * p.dim_z)
     throw engine::ShapeError("conv: g_node_z shape mismatch");
-  if (perm.size() != g.edges.size()) throw engine::ShapeError("conv: perm shape mismatch");
+  if (mode == Mode::deterministic) {
+    require_sorted(g);
+    if (perm.size() != g.edges.size()) throw engine::ShapeError("conv: transpose permutation size mismatch");
+  }
   g_node_x.assign(node_x.size(), T(0));
   g_edge_y.assign(edge_y.size(), T(0));
   g_edge_w.assign(edge_w.size(), T(0));
   const auto nb = neighbours(g);
-  if (g.node_count > 0)
+  if (g.node_count > 0 && mode == Mode::atomic)
+    check(cgf_conv_backward_atomic_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(),
+                                        sources(g).data(), nb.data(), node_x.data(), edge_y.data(), edge_w.data(),
+                                        g_node_z.data(), g_node_x.data(), g_edge_y.data(), g_edge_w.data()));
+  else if (g.node_count > 0)
     check(cgf_conv_backward_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(), g.row_ptr.data(),
                                  nb.data(), node_x.data(), edge_y.data(), edge_w.data(), g_node_z.data(),
-                                 g_node_x.data(), g_edge_y.data(), g_edge_w.data(), gpu_mode(mode)));
+                                 g_node_x.data(), g_edge_y.data(), g_edge_w.data(), CGF_CONV_DETERMINISTIC));
   const auto E = static_cast<std::uint64_t>(g.edge_count()), V = static_cast<std::uint64_t>(g.node_count);
   ConvStats st;
   st.loads_words = E * (p.dim_x + p.dim_y + p.total_weights + p.dim_z);
@@ -257,16 +273,12 @@ ConvStats unfused_forward(const engine::TpPlan& plan, const GraphCSR& g, const s
   const auto& p = prob(plan);
   require_conv_shapes(p, g, node_x, edge_y, edge_w);
   const std::size_t E = g.edges.size(), dx = p.dim_x, dz = p.dim_z;
-  std::vector<T> xg(E * dx), ze(E * dz);
-  for (std::size_t e = 0; e < E; ++e)
-    std::copy_n(node_x.begin() + static_cast<std::ptrdiff_t>(g.edges[e].dst * dx), dx, xg.begin() + e * dx);
-  if (E) check(cgf_tp_forward_host(plan.impl().gpu, dtype<T>(), xg.data(), edge_y.data(), edge_w.data(), ze.data(),
-                                   static_cast<std::int64_t>(E), 0));
   node_z.assign(static_cast<std::size_t>(g.node_count) * dz, T(0));
-  for (std::size_t e = 0; e < E; ++e) {
-    T* dst = node_z.data() + static_cast<std::size_t>(g.edges[e].src) * dz;
-    for (std::size_t k = 0; k < dz; ++k) dst[k] += ze[e * dz + k];
-  }
+  // gather, batched TP and per-node sums in edge order, all on the GPU
+  if (g.node_count > 0)
+    check(cgf_conv_unfused_forward_host(plan.impl().gpu, dtype<T>(), g.node_count, g.edge_count(), sources(g).data(),
+                                        neighbours(g).data(), node_x.data(), edge_y.data(), edge_w.data(),
+                                        node_z.data()));
   ConvStats st;
   st.loads_words = E * (2 * dx + p.dim_y + p.total_weights);
   st.stores_words = E * (dx + dz);
@@ -283,21 +295,14 @@ ConvStats unfused_backward(const engine::TpPlan& plan, const GraphCSR& g, const 
   const auto& p = prob(plan);
   require_conv_shapes(p, g, node_x, edge_y, edge_w);
   const std::size_t E = g.edges.size(), dx = p.dim_x, dz = p.dim_z;
-  std::vector<T> xg(E * dx), gzg(E * dz), gxe(E * dx);
-  for (std::size_t e = 0; e < E; ++e) {
-    std::copy_n(node_x.begin() + static_cast<std::ptrdiff_t>(g.edges[e].dst * dx), dx, xg.begin() + e * dx);
-    std::copy_n(g_node_z.begin() + static_cast<std::ptrdiff_t>(g.edges[e].src * dz), dz, gzg.begin() + e * dz);
-  }
+  g_node_x.assign(node_x.size(), T(0));
   g_edge_y.assign(edge_y.size(), T(0));
   g_edge_w.assign(edge_w.size(), T(0));
-  if (E)
-    check(cgf_tp_backward_host(plan.impl().gpu, dtype<T>(), xg.data(), edge_y.data(), edge_w.data(), gzg.data(),
-                               gxe.data(), g_edge_y.data(), g_edge_w.data(), static_cast<std::int64_t>(E), 0));
-  g_node_x.assign(node_x.size(), T(0));
-  for (std::size_t e = 0; e < E; ++e) {
-    T* dst = g_node_x.data() + static_cast<std::size_t>(g.edges[e].dst) * dx;
-    for (std::size_t i = 0; i < dx; ++i) dst[i] += gxe[e * dx + i];
-  }
+  if (g.node_count > 0)
+    check(cgf_conv_unfused_backward_host(plan.impl().gpu, dtype<T>(), g.node_count, g.edge_count(),
+                                         sources(g).data(), neighbours(g).data(), node_x.data(), edge_y.data(),
+                                         edge_w.data(), g_node_z.data(), g_node_x.data(), g_edge_y.data(),
+                                         g_edge_w.data()));
   ConvStats st;
   st.loads_words = E * (2 * dx + p.dim_y + p.total_weights + dz);
   st.stores_words = E * (2 * dx + p.dim_y + p.total_weights);

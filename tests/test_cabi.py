@@ -82,3 +82,34 @@ def test_compute_fails_loudly_without_cuda(monkeypatch):
     w = np.ones((2, plan.n_w), np.float64)
     with pytest.raises(cgf.CudaError):
         plan.forward(x, y, w)
+
+
+def test_device_entry_points_fail_loudly_without_cuda():
+    """Every device entry point returns CGF_E_CUDA without a driver (no crash:
+    the driver entry points are resolved before any use)."""
+    import paper_2501_13986_b200 as cgf
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    from oracle.oracle import config_json
+    plan = cgf.TpPlan(config_json("paper"))
+    L = cgf.lib()
+    f = C.c_void_p(0x10000)  # never dereferenced on the host
+    m = C.c_int64(0)
+    rp = np.array([0, 1, 2, 2], np.int64)
+    calls = {
+        "forward_atomic": lambda: L.cgf_conv_forward_atomic(plan._h, 1, 3, 2, *[f] * 6, None),
+        "backward_atomic": lambda: L.cgf_conv_backward_atomic(plan._h, 1, 3, 2, *[f] * 9, None),
+        "dbwd_atomic": lambda: L.cgf_conv_double_backward_atomic(plan._h, 1, 3, 2, *[f] * 13, None),
+        "unfused_fwd": lambda: L.cgf_conv_unfused_forward(plan._h, 1, 3, 2, *[f] * 6, None),
+        "unfused_bwd": lambda: L.cgf_conv_unfused_backward(plan._h, 1, 3, 2, *[f] * 11, None),
+        "graph_make": lambda: L.cgf_graph_make(3, 2, f, f, 0, f, f, None, C.byref(m), None),
+        "graph_transpose": lambda: L.cgf_graph_transpose(3, 3, 2, rp.ctypes.data, f, f, f, f, None),
+        "graph_radius": lambda: L.cgf_graph_radius(3, f, 1.0, f, None, 0, C.byref(m), None),
+        "conv_forward_csr_atomic": lambda: L.cgf_conv_forward(plan._h, 1, 3, 2, f, f, f, f, f, f, 1, None),
+    }
+    for name, call in calls.items():
+        assert call() == cgf.CudaError.code, name

@@ -134,10 +134,90 @@ def test_conv_deterministic_bitwise():
         assert torch.equal(u, v)
 
 
-def test_unsorted_edges_rejected():
+def test_unsorted_edges_rejected_by_deterministic_mode():
+    """conv.cpp:240 / 371-374: only the deterministic mode checks the order."""
     pkg = P()
+    js = config("paper")
+    cp = pkg.ConvPlan(pkg.TpPlan(js))
+    o = O.Oracle(js)
+    g = pkg.Graph(3, [1, 0], [0, 1])
+    nx = torch.zeros((3, o.dim_x), device="cuda", dtype=torch.float64)
+    ey = torch.zeros((2, o.dim_y), device="cuda", dtype=torch.float64)
+    ew = torch.zeros((2, o.n_w), device="cuda", dtype=torch.float64)
     with pytest.raises(pkg.InvalidArgument):
-        pkg.Graph(3, [1, 0], [0, 1])
+        cp.forward(g, nx, ey, ew)
+    cp.forward(g, nx, ey, ew, mode=pkg.ATOMIC)
+
+
+# ---- atomic mode (Mode::atomic, conv.cpp:311-324 / 470-486): edges in any
+# order, node outputs accumulated with float atomics.
+ATOMIC_CASES = [("paper", config("paper")), ("c1", config("c1")), ("c2", config("c2")), ("rand5", random_problem(5))]
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f32", "f64"])
+@pytest.mark.parametrize("gname", ["lat4", "ragged5"])
+@pytest.mark.parametrize("name,js", ATOMIC_CASES, ids=[c[0] for c in ATOMIC_CASES])
+def test_atomic_conv_shuffled_edges(name, js, gname, dt):
+    og = graphs()[gname]
+    o, pkg = O.Oracle(js), P()
+    cp = pkg.ConvPlan(pkg.TpPlan(js))
+    nx, ey, ew, gnz, dgx, dgy, dgw = conv_inputs(o, og, dt)
+    perm = np.random.default_rng(5).permutation(og.edges)  # edge list in random order
+    g = pkg.Graph(og.nodes, og.src[perm], og.nbr[perm])
+    assert og.edges < 2 or not g.sorted
+    A = pkg.ATOMIC
+    z = cp.forward(g, dev(nx), dev(ey[perm]), dev(ew[perm]), mode=A)
+    check(host(z), o.conv_forward(og, nx, ey, ew), dt, "atomic forward")
+    gx, gy, gw = cp.backward(g, dev(nx), dev(ey[perm]), dev(ew[perm]), dev(gnz), mode=A)
+    wx, wy, ww = o.conv_backward(og, nx, ey, ew, gnz)
+    check(host(gx), wx, dt, "atomic g_node_x")
+    check(host(gy), wy[perm], dt, "atomic g_edge_y")
+    check(host(gw), ww[perm], dt, "atomic g_edge_w")
+    outs = cp.double_backward(g, dev(nx), dev(ey[perm]), dev(ew[perm]), dev(gnz),
+                              (dev(dgx), dev(dgy[perm]), dev(dgw[perm])), mode=A)
+    want = o.conv_double_backward(og, nx, ey, ew, gnz, dgx, dgy, dgw)
+    for a, b, n in zip(outs, (want[0], want[1][perm], want[2][perm], want[3]),
+                       ("dnode_x", "dedge_y", "dedge_w", "dg_node_z")):
+        check(host(a), b, dt, "atomic " + n)
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f32", "f64"])
+def test_atomic_via_csr_entry_points(dt):
+    """The CSR C ABI entries with CGF_CONV_ATOMIC expand row_ptr on the device
+    and run the atomic kernels: within rounding of the deterministic mode
+    (test_conv.cpp:247-258)."""
+    import ctypes as C
+    js = config("c1")
+    o, pkg = O.Oracle(js), P()
+    plan = pkg.TpPlan(js)
+    og = graphs()["ragged5"]
+    g = pkg.Graph(og.nodes, og.src, og.nbr)
+    nx, ey, ew, gnz, *_ = conv_inputs(o, og, dt)
+    tx, ty, tw = dev(nx), dev(ey), dev(ew)
+    det = pkg.ConvPlan(plan).forward(g, tx, ty, tw)
+    z = torch.empty_like(det)
+    d = g.device(tx.device)
+    ptr = lambda t: C.c_void_p(t.data_ptr())
+    rc = pkg.lib().cgf_conv_forward(plan._h, pkg.F32 if dt == np.float32 else pkg.F64, g.nodes, g.edges,
+                                    ptr(d["row_ptr"]), ptr(d["nbr"]), ptr(tx), ptr(ty), ptr(tw), ptr(z), pkg.ATOMIC,
+                                    C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0, pkg.lib().cgf_last_error()
+    check(host(z), host(det), dt, "atomic (CSR entry) vs deterministic")
+
+
+def test_atomic_empty_graph_and_isolated_nodes():
+    js = config("paper")
+    o, pkg = O.Oracle(js), P()
+    cp = pkg.ConvPlan(pkg.TpPlan(js))
+    g = pkg.Graph(4, np.zeros(0, np.int64), np.zeros(0, np.int64))
+    nx = torch.randn((4, o.dim_x), device="cuda", dtype=torch.float64)
+    ey = torch.zeros((0, o.dim_y), device="cuda", dtype=torch.float64)
+    ew = torch.zeros((0, o.n_w), device="cuda", dtype=torch.float64)
+    z = cp.forward(g, nx, ey, ew, mode=pkg.ATOMIC)
+    assert z.shape == (4, o.dim_z) and not z.any()
+    gx, gy, gw = cp.backward(g, nx, ey, ew, torch.randn((4, o.dim_z), device="cuda", dtype=torch.float64),
+                             mode=pkg.ATOMIC)
+    assert not gx.any() and gy.shape == (0, o.dim_y) and gw.shape == (0, o.n_w)
 
 
 @pytest.mark.parametrize("dt", DTYPES, ids=["f32", "f64"])

@@ -2,7 +2,10 @@
 algorithmic byte counts: fwd |E|(dy+W) + |V|(dx+dz); bwd 2|E|(dy+W) +
 |V|(2dx+dz); dbwd 3|E|(dy+W) + |V|(3dx+2dz) words.
 
-    python tools/sweep_conv.py [--cases c4,c5] [--ops fwd,bwd,dbwd] [--dtypes f32,f64]
+    python tools/sweep_conv.py [--cases c4,c5] [--ops fwd,bwd,dbwd] [--dtypes f32,f64] [--modes det,atomic]
+
+The atomic mode's algorithmic bytes are counted with the same compulsory
+formula (its extra per-edge reductions are the price of non-determinism).
 """
 import argparse
 import json
@@ -35,6 +38,7 @@ def main():
     ap.add_argument("--ops", default="fwd,bwd,dbwd")
     ap.add_argument("--dtypes", default="f32,f64")
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--modes", default="det")
     a = ap.parse_args()
     pk = peak()
     for case in a.cases.split(","):
@@ -50,14 +54,15 @@ def main():
             t = lambda *s: torch.randn(s, device="cuda", dtype=tdt)
             nx, ey, ew = t(V, plan.dim_x), t(E, plan.dim_y), t(E, plan.n_w)
             gz = t(V, plan.dim_z)
-            for op in a.ops.split(","):
+            for mode_name, op in [(m, o) for m in a.modes.split(",") for o in a.ops.split(",")]:
+                mode = cgf.ATOMIC if mode_name == "atomic" else cgf.DETERMINISTIC
                 up = None
                 if op == "fwd":
-                    fn = lambda: cp.forward(g, nx, ey, ew)
+                    fn = lambda: cp.forward(g, nx, ey, ew, mode=mode)
                     words = E * (plan.dim_y + plan.n_w) + V * (plan.dim_x + plan.dim_z)
                     flops = plan.flops_fwd * E
                 elif op == "bwd":
-                    fn = lambda: cp.backward(g, nx, ey, ew, gz)
+                    fn = lambda: cp.backward(g, nx, ey, ew, gz, mode=mode)
                     words = 2 * E * (plan.dim_y + plan.n_w) + V * (2 * plan.dim_x + plan.dim_z)
                     flops = plan.flops_bwd * E
                 else:
@@ -66,7 +71,7 @@ def main():
                     except torch.OutOfMemoryError:
                         print(json.dumps({"case": case, "op": op, "dtype": dts, "error": "OOM"}))
                         continue
-                    fn = lambda: cp.double_backward(g, nx, ey, ew, gz, up)
+                    fn = lambda: cp.double_backward(g, nx, ey, ew, gz, up, mode=mode)
                     words = 3 * E * (plan.dim_y + plan.n_w) + V * (3 * plan.dim_x + 2 * plan.dim_z)
                     flops = plan.flops_dbwd * E
                 try:
@@ -84,7 +89,7 @@ def main():
                         del r
                     ms = statistics.median(ts)
                     gbs = words * es / (ms / 1e3) / 1e9
-                    rec = {"case": case, "tp": prob, "nodes": V, "edges": E, "op": op, "dtype": dts, "ms": ms,
+                    rec = {"case": case, "tp": prob, "mode": mode_name, "nodes": V, "edges": E, "op": op, "dtype": dts, "ms": ms,
                            "edges/s": E / (ms / 1e3), "GB/s": gbs, "frac_hbm": gbs / pk,
                            "GFLOP/s": flops / (ms / 1e3) / 1e9}
                 except Exception as exc:
