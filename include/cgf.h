@@ -27,6 +27,7 @@
 #ifndef CGF_H
 #define CGF_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -219,16 +220,20 @@ int cgf_conv_backward_atomic_host(cgf_plan* plan, int dtype, int64_t nodes, int6
  * Gathers node rows per edge (|E| x dim_x, and |E| x dim_z of g_node_z for the
  * backward), runs the batched TP kernels over |E| rows, and sums the per-edge
  * rows into the nodes in edge order (deterministic segmented sums over the
- * CSR / transposed CSR). Stream-ordered device scratch of |E| (dim_x + dim_z)
- * words (backward: |E| (2 dim_x + dim_z)); it exists to quantify what the
- * fused kernels save. */
+ * CSR / transposed CSR). Device workspace of |E| (dim_x + dim_z) words
+ * (backward: |E| (2 dim_x + dim_z) + |E| int32); it exists to quantify what
+ * the fused kernels save. */
 int cgf_conv_unfused_forward(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
                              const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
-                             void* node_z, void* stream);
+                             void* node_z, void* workspace, size_t workspace_bytes, void* stream);
 int cgf_conv_unfused_backward(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
                               const int32_t* nbr, const int64_t* t_row_ptr, const int32_t* t_eid, const void* node_x,
                               const void* edge_y, const void* edge_w, const void* g_node_z, void* g_node_x,
-                              void* g_edge_y, void* g_edge_w, void* stream);
+                              void* g_edge_y, void* g_edge_w, void* workspace, size_t workspace_bytes,
+                              void* stream);
+/* Device workspace the unfused calls need (op 0 forward, 1 backward). With
+ * workspace == NULL they allocate it stream-ordered per call instead. */
+size_t cgf_conv_unfused_workspace(const cgf_plan* plan, int dtype, int op, int64_t edges);
 /* Host-pointer variants over an edge list in any order (the reference's
  * unfused_forward / unfused_backward take any GraphCSR edge order). */
 int cgf_conv_unfused_forward_host(cgf_plan* plan, int dtype, int64_t nodes, int64_t edges, const int32_t* src,

@@ -127,8 +127,10 @@ def lib():
     L.cgf_conv_double_backward_atomic.argtypes = [P, I, I64, I64] + [P] * 13 + [P]
     L.cgf_conv_forward_atomic_host.argtypes = [P, I, I64, I64] + [P] * 6
     L.cgf_conv_backward_atomic_host.argtypes = [P, I, I64, I64] + [P] * 9
-    L.cgf_conv_unfused_forward.argtypes = [P, I, I64, I64] + [P] * 6 + [P]
-    L.cgf_conv_unfused_backward.argtypes = [P, I, I64, I64] + [P] * 11 + [P]
+    L.cgf_conv_unfused_forward.argtypes = [P, I, I64, I64] + [P] * 6 + [P, C.c_size_t, P]
+    L.cgf_conv_unfused_backward.argtypes = [P, I, I64, I64] + [P] * 11 + [P, C.c_size_t, P]
+    L.cgf_conv_unfused_workspace.argtypes = [P, I, I, I64]
+    L.cgf_conv_unfused_workspace.restype = C.c_size_t
     L.cgf_conv_unfused_forward_host.argtypes = [P, I, I64, I64] + [P] * 6
     L.cgf_conv_unfused_backward_host.argtypes = [P, I, I64, I64] + [P] * 9
     L.cgf_graph_make.argtypes = [I64, I64, P, P, I, P, P, P, P, P]
@@ -587,10 +589,17 @@ class ConvPlan:
         p = self.plan
         z = TpPlan._empty_like(node_x, (g.nodes, p.dim_z))
         d = self._ptrs(g, node_x)
+        ws = self._workspace(node_x, 0, g.edges)
         _check(lib().cgf_conv_unfused_forward(p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"],
                                               TpPlan._p(node_x), TpPlan._p(edge_y), TpPlan._p(edge_w), TpPlan._p(z),
-                                              TpPlan._stream(node_x)))
+                                              TpPlan._p(ws), ws.numel(), TpPlan._stream(node_x)))
         return z
+
+    def _workspace(self, ref, op, edges):
+        """Device workspace of the unfused path, from torch's caching allocator."""
+        import torch
+        n = lib().cgf_conv_unfused_workspace(self.plan._h, _dtype_code(ref), op, edges)
+        return torch.empty(max(n, 1), dtype=torch.uint8, device=ref.device)
 
     def unfused_backward(self, g, node_x, edge_y, edge_w, g_node_z):
         self._check_shapes(g, node_x, edge_y, edge_w)
@@ -600,9 +609,11 @@ class ConvPlan:
         gy = TpPlan._empty_like(node_x, (g.edges, p.dim_y))
         gw = TpPlan._empty_like(node_x, (g.edges, p.n_w))
         d = self._ptrs(g, node_x)
+        ws = self._workspace(node_x, 1, g.edges)
         _check(lib().cgf_conv_unfused_backward(
             p._h, _dtype_code(node_x), g.nodes, g.edges, d["row_ptr"], d["nbr"], d["t_row_ptr"], d["t_eid"],
-            *(TpPlan._p(a) for a in (node_x, edge_y, edge_w, g_node_z, gx, gy, gw)), TpPlan._stream(node_x)))
+            *(TpPlan._p(a) for a in (node_x, edge_y, edge_w, g_node_z, gx, gy, gw)), TpPlan._p(ws), ws.numel(),
+            TpPlan._stream(node_x)))
         return gx, gy, gw
 
     # -- sharded calls (one rank of a destination-partitioned graph) ---------

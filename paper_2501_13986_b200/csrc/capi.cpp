@@ -451,8 +451,12 @@ void conv_atomic(cgf_plan* p, int dtype, cgf::Comp comp, std::int64_t nodes, std
 struct Scratch {
   void* ptr = nullptr;
   void* st = nullptr;
+  bool owned = true;
   Scratch(std::size_t bytes, void* stream) : st(stream) { ptr = cgf::gops::scratch_alloc(bytes, stream); }
-  ~Scratch() { cgf::gops::scratch_free(ptr, st); }
+  Scratch(void* borrowed, void* stream) : ptr(borrowed), st(stream), owned(false) {}
+  ~Scratch() {
+    if (owned) cgf::gops::scratch_free(ptr, st);
+  }
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
   template <class T> T* as() const { return static_cast<T*>(ptr); }
@@ -474,9 +478,25 @@ struct CsrSrc : Scratch {
 // |E| rows, then per-node sums in edge order. The output node's edges are
 // positions [rp[v], rp[v+1]) of the edge list, through ridx when the list is
 // not in CSR order.
+// Workspace of the unfused path: 256-byte aligned pieces.
+std::size_t ws_round(std::size_t b) { return (b + 255) / 256 * 256; }
+std::size_t unfused_ws(const cgf::Problem& pr, int dtype, int op, std::int64_t edges) {
+  const std::size_t es = dtype == CGF_F64 ? 8 : 4, E = static_cast<std::size_t>(std::max<std::int64_t>(edges, 0));
+  if (op == 0) return ws_round(es * E * pr.dim_x) + ws_round(es * E * pr.dim_z);
+  return 2 * ws_round(es * E * pr.dim_x) + ws_round(es * E * pr.dim_z) + ws_round(4 * E);
+}
+struct Carver {
+  char* base;
+  void* carve(std::size_t b) {
+    void* r = base;
+    base += ws_round(b);
+    return r;
+  }
+};
+
 void unfused_fwd(cgf_plan* p, int dtype, std::int64_t nodes, std::int64_t edges, const std::int64_t* rp,
                  const std::int32_t* ridx, const std::int32_t* nbr, const void* node_x, const void* edge_y,
-                 const void* edge_w, void* node_z, void* stream) {
+                 const void* edge_w, void* node_z, void* ws, std::size_t ws_bytes, void* stream) {
   if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
   if (nodes == 0) return;
   need(node_z, "node_z");
@@ -488,7 +508,11 @@ void unfused_fwd(cgf_plan* p, int dtype, std::int64_t nodes, std::int64_t edges,
     return;
   }
   need(rp, "row_ptr"); need(nbr, "nbr"); need(node_x, "node_x"); need(edge_y, "edge_y"); need(edge_w, "edge_w");
-  Scratch xg(es * edges * pr.dim_x, stream), ze(es * edges * pr.dim_z, stream);
+  const std::size_t want = unfused_ws(pr, dtype, 0, edges);
+  if (ws && ws_bytes < want) throw std::invalid_argument("unfused conv: workspace too small");
+  Scratch all = ws ? Scratch(ws, stream) : Scratch(want, stream);
+  Carver cv{all.as<char>()};
+  Scratch xg(cv.carve(es * edges * pr.dim_x), stream), ze(cv.carve(es * edges * pr.dim_z), stream);
   cgf::gops::gather_rows(f64, node_x, nbr, xg.ptr, edges, pr.dim_x, stream);
   launch(p, CGF_OP_FORWARD, dtype, 0, edges, xg.ptr, edge_y, edge_w, nullptr, nullptr, nullptr, nullptr, ze.ptr,
          nullptr, nullptr, nullptr, stream);
@@ -500,7 +524,7 @@ void unfused_fwd(cgf_plan* p, int dtype, std::int64_t nodes, std::int64_t edges,
 void unfused_bwd(cgf_plan* p, int dtype, std::int64_t nodes, std::int64_t edges, const std::int32_t* src,
                  const std::int32_t* nbr, const std::int64_t* t_rp, const std::int32_t* t_idx, const void* node_x,
                  const void* edge_y, const void* edge_w, const void* g_node_z, void* g_node_x, void* g_edge_y,
-                 void* g_edge_w, void* stream) {
+                 void* g_edge_w, char* ws, void* stream) {
   if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
   if (nodes == 0) return;
   need(g_node_x, "g_node_x");
@@ -514,7 +538,9 @@ void unfused_bwd(cgf_plan* p, int dtype, std::int64_t nodes, std::int64_t edges,
   need(src, "src"); need(nbr, "nbr"); need(t_rp, "t_row_ptr"); need(t_idx, "t_eid");
   need(node_x, "node_x"); need(edge_y, "edge_y"); need(edge_w, "edge_w"); need(g_node_z, "g_node_z");
   need(g_edge_y, "g_edge_y"); need(g_edge_w, "g_edge_w");
-  Scratch xg(es * edges * pr.dim_x, stream), gzg(es * edges * pr.dim_z, stream), gxe(es * edges * pr.dim_x, stream);
+  Carver cv{ws};  // the caller sized it with unfused_ws(op 1); the last piece (src) is the caller's
+  Scratch xg(cv.carve(es * edges * pr.dim_x), stream), gzg(cv.carve(es * edges * pr.dim_z), stream),
+      gxe(cv.carve(es * edges * pr.dim_x), stream);
   cgf::gops::gather_rows(f64, node_x, nbr, xg.ptr, edges, pr.dim_x, stream);
   cgf::gops::gather_rows(f64, g_node_z, src, gzg.ptr, edges, pr.dim_z, stream);
   launch(p, CGF_OP_BACKWARD, dtype, 0, edges, xg.ptr, edge_y, edge_w, gzg.ptr, nullptr, nullptr, nullptr, gxe.ptr,
@@ -1101,24 +1127,42 @@ int cgf_conv_double_backward_atomic(cgf_plan* p, int dtype, int64_t nodes, int64
 
 int cgf_conv_unfused_forward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
                              const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
-                             void* node_z, void* stream) {
+                             void* node_z, void* workspace, size_t workspace_bytes, void* stream) {
   return guarded([&] {
     need(p, "plan");
-    unfused_fwd(p, dtype, nodes, edges, row_ptr, nullptr, nbr, node_x, edge_y, edge_w, node_z, stream);
+    unfused_fwd(p, dtype, nodes, edges, row_ptr, nullptr, nbr, node_x, edge_y, edge_w, node_z, workspace,
+                workspace_bytes, stream);
   });
 }
 
 int cgf_conv_unfused_backward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
                               const int32_t* nbr, const int64_t* t_row_ptr, const int32_t* t_eid, const void* node_x,
                               const void* edge_y, const void* edge_w, const void* g_node_z, void* g_node_x,
-                              void* g_edge_y, void* g_edge_w, void* stream) {
+                              void* g_edge_y, void* g_edge_w, void* workspace, size_t workspace_bytes,
+                              void* stream) {
   return guarded([&] {
     need(p, "plan");
     if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
-    const CsrSrc src(edges > 0 ? row_ptr : nullptr, nodes, nodes > 0 ? edges : 0, stream);
-    unfused_bwd(p, dtype, nodes, edges, src.get(), nbr, t_row_ptr, t_eid, node_x, edge_y, edge_w, g_node_z, g_node_x,
-                g_edge_y, g_edge_w, stream);
+    if (nodes == 0) return;
+    const std::size_t want = unfused_ws(p->problem, dtype, 1, edges);
+    if (workspace && workspace_bytes < want) throw std::invalid_argument("unfused conv: workspace too small");
+    Scratch all = workspace ? Scratch(workspace, stream) : Scratch(want, stream);
+    // per-edge output node in the workspace's tail
+    const std::size_t es = dtype == CGF_F64 ? 8 : 4;
+    const std::size_t E = static_cast<std::size_t>(edges);
+    std::int32_t* src = reinterpret_cast<std::int32_t*>(all.as<char>() + 2 * ws_round(es * E * p->problem.dim_x) +
+                                                        ws_round(es * E * p->problem.dim_z));
+    if (edges > 0) {
+      need(row_ptr, "row_ptr");
+      cgf::gops::rowptr_expand(row_ptr, nodes, src, stream);
+    }
+    unfused_bwd(p, dtype, nodes, edges, src, nbr, t_row_ptr, t_eid, node_x, edge_y, edge_w, g_node_z, g_node_x,
+                g_edge_y, g_edge_w, all.as<char>(), stream);
   });
+}
+
+size_t cgf_conv_unfused_workspace(const cgf_plan* p, int dtype, int op, int64_t edges) {
+  return p ? unfused_ws(p->problem, dtype, op, edges) : 0;
 }
 
 // ---- graph construction on the device (conv.cpp:64-151) -----------------
@@ -1320,7 +1364,7 @@ int cgf_conv_unfused_forward_host(cgf_plan* p, int dtype, int64_t nodes, int64_t
     void* dw = h.in(edge_w, E * pr.n_w);
     void* dz = h.out(V * pr.dim_z);
     unfused_fwd(p, dtype, nodes, edges, static_cast<const std::int64_t*>(drp), static_cast<const std::int32_t*>(dri),
-                static_cast<const std::int32_t*>(dd), dx, dy, dw, dz, nullptr);
+                static_cast<const std::int32_t*>(dd), dx, dy, dw, dz, nullptr, 0, nullptr);
     CU_CHECK(cgf::drv::cuCtxSynchronize());
     h.back(node_z, dz, V * pr.dim_z);
   });
@@ -1353,9 +1397,10 @@ int cgf_conv_unfused_backward_host(cgf_plan* p, int dtype, int64_t nodes, int64_
     void* ogx = h.out(V * pr.dim_x);
     void* ogy = h.out(E * pr.dim_y);
     void* ogw = h.out(E * pr.n_w);
+    Scratch ws(unfused_ws(pr, dtype, 1, edges), nullptr);
     unfused_bwd(p, dtype, nodes, edges, static_cast<const std::int32_t*>(ds), static_cast<const std::int32_t*>(dd),
                 static_cast<const std::int64_t*>(dtrp), static_cast<const std::int32_t*>(dti), dx, dy, dw, dgz, ogx,
-                ogy, ogw, nullptr);
+                ogy, ogw, ws.as<char>(), nullptr);
     CU_CHECK(cgf::drv::cuCtxSynchronize());
     h.back(g_node_x, ogx, V * pr.dim_x);
     h.back(g_edge_y, ogy, E * pr.dim_y);

@@ -497,16 +497,18 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
   const bool zx_on = cfg_.comp == Comp::Fwd || cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ;
   const bool zab = cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX;
   const bool gfl = gy_flush();
-  if (!yreg()) {
-    // the item's y (and db) into registers once: no per-entry shared-memory
-    // reads, and the products below can be shared across chunks
+  const bool yq = !yreg() && m > 1;
+  if (yq) {
+    // joint chunks: the item's y (and db) into registers once, so the products
+    // below are shared across chunks; otherwise y is read from the slot at each
+    // use (no registers held across the item)
     o_ << "      T yq[" << p_.dim_y << "];" << (dual() ? " T dbq[" + S(p_.dim_y) + "];" : "");
     for (int j = 0; j < p_.dim_y; ++j)
       o_ << " yq[" << j << "] = sl[ys + " << j << "];" << (dual() ? " dbq[" + S(j) + "] = sl[dbs + " + S(j) + "];" : "");
     o_ << "\n";
   }
-  auto Y = [&](int j) { return yreg() ? "y[" + S(j) + "]" : "yq[" + S(j) + "]"; };
-  auto DB = [&](int j) { return yreg() ? "db[" + S(j) + "]" : "dbq[" + S(j) + "]"; };
+  auto Y = [&](int j) { return yreg() ? "y[" + S(j) + "]" : yq ? "yq[" + S(j) + "]" : "sl[ys + " + S(j) + "]"; };
+  auto DB = [&](int j) { return yreg() ? "db[" + S(j) + "]" : yq ? "dbq[" + S(j) + "]" : "sl[dbs + " + S(j) + "]"; };
   for (int g = 0; g < n; ++g) {
     if (g && cfg_.sub_barrier) o_ << "      asm volatile(\"\" ::: \"memory\");\n";
     const Sub& s0 = p_.subs[u.subs[g]];
@@ -924,7 +926,7 @@ KernelSource Gen::run() {
                              : static_cast<int>(std::clamp<std::uint64_t>(12288 / std::max<std::uint64_t>(1, slot_words * sz_), 2, 4));
   int warps = cfg_.warps;
   auto warp_bytes = [&](int d) { return (static_cast<std::uint64_t>(d) * slot_words + scr_words_) * sz_; };
-  const std::uint64_t budget = 200 * 1024;
+  const std::uint64_t budget = 224 * 1024;  // of the 227 KB a CTA may use
   while (depth > 1 && warp_bytes(depth) * warps + 8ull * depth * warps > budget) --depth;
   while (warps > 1 && warp_bytes(depth) * warps + 8ull * depth * warps > budget) --warps;
   if (warp_bytes(depth) * warps + 8ull * depth * warps > 227 * 1024)

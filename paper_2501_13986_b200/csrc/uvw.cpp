@@ -12,7 +12,7 @@ namespace cgf {
 namespace {
 
 constexpr int kTileRows = 128;
-constexpr int kProdWarps = 16;    // producer warps (default); MMA warp, 4 epilogue warps, TMA warp follow
+constexpr int kProdWarps = 8;     // producer warps (default; 8 measured 3.28 ms vs 3.59 ms for 16 on C3); MMA warp, 4 epilogue warps, TMA warp follow
 
 
 
@@ -782,6 +782,9 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
   if (pw != 8 && pw != 16) throw UnsupportedError("CGF_UVW_PW must be 8 or 16");
   const int cpt = kCh * 4 / pw;  // channels per producer thread
   const int nwr = std::getenv("CGF_UVW_NW") ? std::atoi(std::getenv("CGF_UVW_NW")) : 6;  // W ring depth
+  // A blocks per TMEM-store round (<= NS / 2 so a batch is written while the other half is consumed);
+  // batches of 2 measured 3.45 ms vs 3.36 ms for 1 (profiles/r01_uvw_kb.log), so 1 is the default
+  const int kb = std::max(1, std::min(std::getenv("CGF_UVW_KB") ? std::atoi(std::getenv("CGF_UVW_KB")) : 1, na / 2));
   // warps: producers | MMA | 4 epilogue | W loader | x loader
   const int mma_warp = pw, wload_warp = pw + 5, xload_warp = pw + 6, nwarps = pw + 7;
   const int smem = 1024 /*align*/ + nx * xslot + nwr * wslot + 1024 /*barriers*/;
@@ -847,19 +850,31 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
         << "][" << e.i << "]);\n";
     // A block k -> TMEM columns [ACOL0 + 32 slot, +32): hi in the first 16, lo in
     // the next 16; this thread's row is its TMEM lane, its channels its columns.
-    o << "#pragma unroll\n  for (int k = 0; k < " << dz << "; ++k) {\n"
-      << "    mbar_wait_t(&aempty[slot], ph ^ 1u, 1);\n"
-      << "    tc_fence_after();\n"
-      << "    float h[" << cpt << "], l[" << cpt << "];\n"
-      << "#pragma unroll\n    for (int c = 0; c < " << cpt << "; ++c) {\n"
-      << "      float z = 0.f;\n#pragma unroll\n      for (int i = 0; i < " << dx
-      << "; ++i) z = fmaf(q[k][i], xv[c * " << dx << " + i], z);\n"
-      << "      h[c] = tf32_hi(z); l[c] = z - h[c];\n    }\n"
-      << "    const u32 ta = tq + ACOL0 + 32 * slot + " << cpt << " * sub;\n"
-      << "    if (!(UVW_EXP & 4)) { tc_st" << cpt << "(ta, h); tc_st" << cpt << "(ta + 16, l); }\n"
-      << "    tc_wait_st();\n    tc_fence_before();\n"
-      << "    __syncwarp();\n    if ((threadIdx.x & 31) == 0) mbar_arrive(&afull[slot]);\n"
-      << "    if (++slot == NS) { slot = 0; ph ^= 1u; }\n  }\n}\n\n";
+    // Blocks go out in batches of kb: all of a batch's values are computed
+    // before its slots are awaited, and one tcgen05.wait::st + fence + arrive
+    // round covers the batch (the per-block round trip dominated the loop).
+    for (int k0 = 0; k0 < dz; k0 += kb) {
+      const int nk = std::min(kb, dz - k0);
+      o << "  {\n    float h[" << nk << "][" << cpt << "], l[" << nk << "][" << cpt << "];\n";
+      for (int t = 0; t < nk; ++t)
+        o << "#pragma unroll\n    for (int c = 0; c < " << cpt << "; ++c) {\n"
+          << "      float z = 0.f;\n#pragma unroll\n      for (int i = 0; i < " << dx
+          << "; ++i) z = fmaf(q[" << k0 + t << "][i], xv[c * " << dx << " + i], z);\n"
+          << "      h[" << t << "][c] = tf32_hi(z); l[" << t << "][c] = z - h[" << t << "][c];\n    }\n";
+      o << "    u32 s_ = slot, p_ = ph;\n";
+      for (int t = 0; t < nk; ++t) {
+        o << "    mbar_wait_t(&aempty[s_], p_ ^ 1u, 1);\n";
+        if (t == 0) o << "    tc_fence_after();\n";
+        o << "    { const u32 ta = tq + ACOL0 + 32 * s_ + " << cpt << " * sub;\n"
+          << "      if (!(UVW_EXP & 4)) { tc_st" << cpt << "(ta, h[" << t << "]); tc_st" << cpt << "(ta + 16, l[" << t << "]); } }\n"
+          << "    if (++s_ == NS) { s_ = 0; p_ ^= 1u; }\n";
+      }
+      o << "    tc_wait_st();\n    tc_fence_before();\n    __syncwarp();\n"
+        << "    if ((threadIdx.x & 31) == 0) { u32 a_ = slot;";
+      for (int t = 0; t < nk; ++t) o << " mbar_arrive(&afull[a_]);" << (t + 1 < nk ? " if (++a_ == NS) a_ = 0;" : "");
+      o << " }\n    slot = s_; ph = p_;\n  }\n";
+    }
+    o << "}\n\n";
   }
 
   // ---- unit / segment tables

@@ -104,8 +104,8 @@ def test_device_entry_points_fail_loudly_without_cuda():
         "forward_atomic": lambda: L.cgf_conv_forward_atomic(plan._h, 1, 3, 2, *[f] * 6, None),
         "backward_atomic": lambda: L.cgf_conv_backward_atomic(plan._h, 1, 3, 2, *[f] * 9, None),
         "dbwd_atomic": lambda: L.cgf_conv_double_backward_atomic(plan._h, 1, 3, 2, *[f] * 13, None),
-        "unfused_fwd": lambda: L.cgf_conv_unfused_forward(plan._h, 1, 3, 2, *[f] * 6, None),
-        "unfused_bwd": lambda: L.cgf_conv_unfused_backward(plan._h, 1, 3, 2, *[f] * 11, None),
+        "unfused_fwd": lambda: L.cgf_conv_unfused_forward(plan._h, 1, 3, 2, *[f] * 6, None, 0, None),
+        "unfused_bwd": lambda: L.cgf_conv_unfused_backward(plan._h, 1, 3, 2, *[f] * 11, None, 0, None),
         "graph_make": lambda: L.cgf_graph_make(3, 2, f, f, 0, f, f, None, C.byref(m), None),
         "graph_transpose": lambda: L.cgf_graph_transpose(3, 3, 2, rp.ctypes.data, f, f, f, f, None),
         "graph_radius": lambda: L.cgf_graph_radius(3, f, 1.0, f, None, 0, C.byref(m), None),

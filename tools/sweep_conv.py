@@ -2,7 +2,7 @@
 algorithmic byte counts: fwd |E|(dy+W) + |V|(dx+dz); bwd 2|E|(dy+W) +
 |V|(2dx+dz); dbwd 3|E|(dy+W) + |V|(3dx+2dz) words.
 
-    python tools/sweep_conv.py [--cases c4,c5] [--ops fwd,bwd,dbwd] [--dtypes f32,f64] [--modes det,atomic]
+    python tools/sweep_conv.py [--cases c4,c5] [--ops fwd,bwd,dbwd] [--dtypes f32,f64] [--modes det,atomic,unfused]
 
 The atomic mode's algorithmic bytes are counted with the same compulsory
 formula (its extra per-edge reductions are the price of non-determinism).
@@ -56,13 +56,16 @@ def main():
             gz = t(V, plan.dim_z)
             for mode_name, op in [(m, o) for m in a.modes.split(",") for o in a.ops.split(",")]:
                 mode = cgf.ATOMIC if mode_name == "atomic" else cgf.DETERMINISTIC
+                unf = mode_name == "unfused"
+                if unf and op == "dbwd":
+                    continue
                 up = None
                 if op == "fwd":
-                    fn = lambda: cp.forward(g, nx, ey, ew, mode=mode)
+                    fn = (lambda: cp.unfused_forward(g, nx, ey, ew)) if unf else (lambda: cp.forward(g, nx, ey, ew, mode=mode))
                     words = E * (plan.dim_y + plan.n_w) + V * (plan.dim_x + plan.dim_z)
                     flops = plan.flops_fwd * E
                 elif op == "bwd":
-                    fn = lambda: cp.backward(g, nx, ey, ew, gz, mode=mode)
+                    fn = (lambda: cp.unfused_backward(g, nx, ey, ew, gz)) if unf else (lambda: cp.backward(g, nx, ey, ew, gz, mode=mode))
                     words = 2 * E * (plan.dim_y + plan.n_w) + V * (2 * plan.dim_x + plan.dim_z)
                     flops = plan.flops_bwd * E
                 else:
