@@ -131,8 +131,10 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   cfg.aligned = aligned != 0;
   // Batched fwd / bwd keep y in registers (prefetched a row ahead); the
   // double-backward needs those registers for its three z' accumulators.
+  // FP64 backward reads y from the slot instead: the 2 x dim_y doubles of
+  // registers pushed it to 255 registers + stack (measured 20.3 -> 17.4 ms).
   cfg.y_regs = (loop == cgf::Loop::Rows || loop == cgf::Loop::ConvEdges) &&
-               (comp == cgf::Comp::Fwd || comp == cgf::Comp::Bwd);
+               (comp == cgf::Comp::Fwd || (comp == cgf::Comp::Bwd && dtype == CGF_F32));
   // Two 32-lane chunks per staged item / code body: measured -4 % fwd, -11 %
   // bwd (TP) and -13 % (conv) in FP32; FP64 runs out of registers (keep 1).
   cfg.merge = (dtype == CGF_F32 && (comp == cgf::Comp::Fwd || comp == cgf::Comp::Bwd)) ? 2 : 1;

@@ -143,6 +143,17 @@ DEVI u64 sdesc64(u32 saddr) {
 // Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M = 128, N.
 DEVI constexpr u32 idesc_tf32(int n) { return (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(n >> 3) << 17) | ((u32)(128 >> 4) << 24); }
 // tf32 split: hi keeps the top 19 bits (exactly representable), lo the rest.
+// 16-byte shared-memory load through an explicit .shared address (a generic
+// pointer into the slot compiled to LD.E: generic-space loads, longer latency)
+DEVI float4 lds128(const unsigned char* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_addr(p)));
+  return v;
+}
+DEVI void sts128(unsigned char* p, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" :: "r"(smem_addr(p)), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+DEVI void sts32(unsigned char* p, float v) { asm volatile("st.shared.f32 [%0], %1;" :: "r"(smem_addr(p)), "f"(v) : "memory"); }
 DEVI float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 // Byte offset of 16-byte chunk `chunk` of row m in a K-major SW64 tile (64 B rows).
 DEVI u32 sw64(int m, int chunk) { return (u32)((m >> 3) * 512 + (m & 7) * 64 + ((chunk ^ ((m >> 1) & 3)) << 4)); }
@@ -263,7 +274,7 @@ DEVI u32 kmaj_rows(int r, int k) { return (u32)((k >> 4) * 4096 + sw64(r, (k & 1
 void emit_x_read(std::ostringstream& o, int dx) {
   o << "  float xv[" << 8 * dx << "];\n#pragma unroll\n  for (int t = 0; t < " << 2 * dx << "; ++t) {\n"
     << "    const int g = " << 2 * dx << " * sub + t, L = m * " << dx << " + (g >> 2), j = g & 3;\n"
-    << "    const float4 v = *(const float4*)(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4));\n"
+    << "    const float4 v = lds128(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4));\n"
     << "    xv[4 * t] = v.x; xv[4 * t + 1] = v.y; xv[4 * t + 2] = v.z; xv[4 * t + 3] = v.w;\n  }\n"
     << "  fence_proxy_async();\n  __syncwarp();\n  if ((threadIdx.x & 31) == 0) mbar_arrive(xempty);\n";
 }
@@ -379,8 +390,8 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "              h[a] = tf32_hi(v); l[a] = v - h[a];\n            }\n"
        "            const int c4 = 8 * sub + g;\n"
        "            const u32 off = (c4 >> 2) * 8192 + sw64(m, c4 & 3);\n"
-       "            *(float4*)(gzt + off) = make_float4(h[0], h[1], h[2], h[3]);\n"
-       "            *(float4*)(gzt + GZB / 2 + off) = make_float4(l[0], l[1], l[2], l[3]);\n          }\n"
+       "            sts128(gzt + off, make_float4(h[0], h[1], h[2], h[3]));\n"
+       "            sts128(gzt + GZB / 2 + off, make_float4(l[0], l[1], l[2], l[3]));\n          }\n"
        "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(gz_full);\n"
        "        }\n"
        "        mbar_wait_t(gzp_full, uq & 1u, 22);\n"
@@ -522,7 +533,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
     o << "  }\n"
       << "#pragma unroll\n  for (int c = 0; c < 8; ++c) {\n"
       << "    const float h = tf32_hi(zc[c]);\n    const u32 off = kmaj_rows(16 * cb + 8 * sub + c, m);\n"
-      << "    *(float*)(zt + off) = h; *(float*)(zt + TB / 2 + off) = zc[c] - h;\n  }\n}\n\n";
+      << "    sts32(zt + off, h); sts32(zt + TB / 2 + off, zc[c] - h);\n  }\n}\n\n";
   }
   o << "extern \"C\" __global__ void " << kname << "_reduce(const float* __restrict__ part, int nparts, "
        "float* __restrict__ gw, int w0, int w1) {\n"
@@ -567,7 +578,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "            const int r = 32 * sub + t;\n"
        "            const float v = valid ? __ldg(gzr + P_ZOFF[q] + r * dz + k) : 0.f;\n"
        "            const float h = tf32_hi(v);\n            const u32 off = kmaj_rows(r, m);\n"
-       "            *(float*)(gzt + off) = h; *(float*)(gzt + TB / 2 + off) = v - h;\n          }\n"
+       "            sts32(gzt + off, h); sts32(gzt + TB / 2 + off, v - h);\n          }\n"
        "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(gz_full);\n"
        "          mbar_wait_t(z_empty, (ug & 1u) ^ 1u, 21);\n"
        "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
@@ -836,7 +847,7 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
     const int nch = cpt * dx / 4;
     o << "  float xv[" << cpt * dx << "];\n#pragma unroll\n  for (int t = 0; t < " << nch
       << "; ++t) {\n    const int g = " << nch << " * sub + t, L = m * " << dx
-      << " + (g >> 2), j = g & 3;\n    const float4 v = *(const float4*)(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4));\n"
+      << " + (g >> 2), j = g & 3;\n    const float4 v = lds128(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4));\n"
          "    xv[4 * t] = v.x; xv[4 * t + 1] = v.y; xv[4 * t + 2] = v.z; xv[4 * t + 3] = v.w;\n  }\n"
          // generic-proxy reads of the slot must be ordered before the next
          // TMA (async proxy) write into it: without this fence the refill
