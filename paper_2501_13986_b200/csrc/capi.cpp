@@ -138,6 +138,11 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   // Two 32-lane chunks per staged item / code body: measured -4 % fwd, -11 %
   // bwd (TP) and -13 % (conv) in FP32; FP64 runs out of registers (keep 1).
   cfg.merge = (dtype == CGF_F32 && (comp == cgf::Comp::Fwd || comp == cgf::Comp::Bwd)) ? 2 : 1;
+  // Measured per kernel (profiles/r01_ab_issue.log): the forward keeps the
+  // per-range 64-bit source addresses in issue_unit (9.0 vs 9.15 ms); the FP64
+  // by-neighbour conv stages y as a window (145 vs 155 ms).
+  cfg.old_issue = comp == cgf::Comp::Fwd;
+  cfg.y_window = dtype == CGF_F64 && loop == cgf::Loop::ConvByInput;
   cgf::apply_gen_flags(cfg, flags);
   auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_kernel(p->problem, p->units, cfg));
   p->sources.emplace(key, ks);

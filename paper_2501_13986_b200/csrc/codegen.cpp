@@ -298,7 +298,7 @@ void Gen::layout() {
     if (!yreg()) {
       // y rows are copied as a 16-byte aligned window unless they are aligned
       // themselves (dim_y * sizeof(T) % 16 == 0): then a plain range
-      const bool win = !al16(p_.dim_y);
+      const bool win = cfg_.y_window || !al16(p_.dim_y);
       add(L, "Y", p_.dim_y, e_src(), 0, 0, p_.dim_y, so, win);
       if (dual()) add(L, "DB", p_.dim_y, e_src(), 0, 0, p_.dim_y, so, win);
     }
@@ -434,8 +434,12 @@ void Gen::emit_issue() {
           const auto& r = L.ranges[pieces[a].first];
           // lane l of this run copies piece (pieces[a].second + l - a + t0) of range r
           const long long p0 = pieces[a].second - static_cast<long long>(a - t0);
-          o_ << "      " << (first ? "" : "else ") << "if (lane < " << b - t0 << ") { s_ = B" << base_id(r) << " + "
-             << O(r.off * sz_ + 16 * p0, r.step * sz_) << "; d_ = " << r.slot_off * sz_ + 16 * p0 << "; }\n";
+          if (cfg_.old_issue)  // A/B: the 64-bit row address per range (pre-bases form)
+            o_ << "      " << (first ? "" : "else ") << "if (lane < " << b - t0 << ") { s_ = (const char*)(" << range_src(r)
+               << ") + " << 16 * p0 << "; d_ = " << r.slot_off * sz_ + 16 * p0 << "; }\n";
+          else
+            o_ << "      " << (first ? "" : "else ") << "if (lane < " << b - t0 << ") { s_ = B" << base_id(r) << " + "
+               << O(r.off * sz_ + 16 * p0, r.step * sz_) << "; d_ = " << r.slot_off * sz_ + 16 * p0 << "; }\n";
           first = false;
           a = b;
         }
@@ -1049,6 +1053,10 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "merge") cfg.merge = std::max(1, v);
     else if (k == "lanecopy") cfg.lane_copy = true;
     else if (k == "nojoint") cfg.joint = false;
+    else if (k == "ywin") cfg.y_window = true;
+    else if (k == "oldissue") cfg.old_issue = true;
+    else if (k == "newissue") cfg.old_issue = false;
+    else if (k == "noywin") cfg.y_window = false;
     else if (k == "joint") cfg.joint = true;
   }
 }

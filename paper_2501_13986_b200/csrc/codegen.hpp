@@ -57,13 +57,15 @@ struct KernelConfig {
   int merge = 1;            // chunks (same-shape units) per staged item and code body
   bool joint = false;       // emit a merged unit's chunks side by side (shared v*y[j] products); measured
                             // neutral on the TP, +15 % on the C4 conv forward (profiles/r01_ab_joint.log)
+  bool old_issue = false;   // A/B: per-range 64-bit source addresses in issue_unit
+  bool y_window = false;    // stage y as a 16-byte window even when its rows are aligned (A/B)
   bool lane_copy = true;    // stage inputs with per-lane 16-byte cp.async (whole warp) instead of
                             // one lane's cp.async.bulk: no single-lane issue loop per range
 };
 
 // Applies "k=v,flag,..." overrides (env CGF_GEN) to a config: depth=N,
 // warps=N, minb=N, nobarrier, barrier, yreg, yslot, class=N, bulk (one-lane bulk copies), lanecopy,
-// merge=N, joint / nojoint.
+// merge=N, joint / nojoint, ywin.
 void apply_gen_flags(KernelConfig& cfg, const std::string& flags);
 
 struct KernelSource {
