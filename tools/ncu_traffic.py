@@ -29,7 +29,9 @@ for rep in sorted(glob.glob(os.path.join(d, "full_*.ncu-rep"))):
     t, tu = get("gpu__time_duration.sum")
     t_ms = t * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(tu, 1)
     name = v[h.index("Kernel Name")]
-    op = {"fwd": "forward", "bwd": "backward"}[key.split("_")[-1]]
+    op = {"fwd": "forward", "bwd": "backward"}.get(key.split("_")[-1])
+    if op is None:  # not a bench kernel capture (e.g. an A/B variant)
+        continue
     out[key.rsplit("_", 1)[0] + "_" + op] = {"kernel": name, "dram_read_bytes": rd, "dram_write_bytes": wr,
                                               "traffic_bytes": rd + wr, "ncu_ms": t_ms, "report": os.path.basename(rep)}
 path = os.path.join(root, "profiles", "ncu_traffic.json")
