@@ -33,6 +33,7 @@ struct cgf_plan {
   // per-context device buffer of swizzled tf32 W images.
   std::map<std::string, std::shared_ptr<cgf::UvwSource>> uvw;  // by kernel tag
   std::map<std::pair<CUcontext, std::string>, CUdeviceptr> wimg;
+  std::map<std::pair<CUcontext, std::string>, std::size_t> scratch_cap;  // bytes of grown scratch buffers in wimg
   // host-pointer path: two streams + double-buffered device staging per context
   struct HostPipe {
     CUstream s[2] = {nullptr, nullptr};
@@ -138,10 +139,12 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   // Two 32-lane chunks per staged item / code body: measured -4 % fwd, -11 %
   // bwd (TP) and -13 % (conv) in FP32; FP64 runs out of registers (keep 1).
   cfg.merge = (dtype == CGF_F32 && (comp == cgf::Comp::Fwd || comp == cgf::Comp::Bwd)) ? 2 : 1;
-  // Measured per kernel (profiles/r01_ab_issue.log): the forward keeps the
-  // per-range 64-bit source addresses in issue_unit (9.0 vs 9.15 ms); the FP64
-  // by-neighbour conv stages y as a window (145 vs 155 ms).
-  cfg.old_issue = comp == cgf::Comp::Fwd;
+  // Measured per kernel (profiles/r01_ab_issue.log, r01_sweep_issue_bases.log):
+  // the batched forward keeps the per-range 64-bit source addresses in
+  // issue_unit (9.0 vs 9.15 ms; the conv forward is faster with row bases,
+  // 13.9 vs 14.6 ms); the FP64 by-neighbour conv stages y as a window (145 vs
+  // 155 ms).
+  cfg.old_issue = comp == cgf::Comp::Fwd && loop == cgf::Loop::Rows;
   cfg.y_window = dtype == CGF_F64 && loop == cgf::Loop::ConvByInput;
   cgf::apply_gen_flags(cfg, flags);
   auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_kernel(p->problem, p->units, cfg));
@@ -321,23 +324,73 @@ void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, c
   std::int64_t nrows = rows;
   const void* ya = y;
   const void* gza = gz;
+  // gz -> tf32 hi / lo planes in one pre-pass: [plane][row][64] for the gy
+  // kernel's A tiles and [plane][64][pitch] for the gW kernels' B tiles (plane =
+  // z segment component); both kernels then TMA-load gz tiles in MMA layout
+  const auto us_y = uvw_source(p, "bwdy");
+  const int nplanes = us_y->dims_x;
+  std::int64_t pitch = (rows + 127) / 128 * 128;
+  const std::size_t ybytes = static_cast<std::size_t>(nplanes) * static_cast<std::size_t>(rows) * 64 * 4;
+  const std::size_t wbytes = static_cast<std::size_t>(nplanes) * 64 * static_cast<std::size_t>(pitch) * 4;
+  CUdeviceptr pl;
+  {
+    std::lock_guard<std::mutex> g(p->mu);
+    auto& cap = p->scratch_cap[{ctx, "gzplanes"}];
+    auto it = p->wimg.find({ctx, "gzplanes"});
+    if (it == p->wimg.end() || cap < 2 * (ybytes + wbytes)) {
+      if (it != p->wimg.end()) CU_CHECK(cgf::drv::cuMemFree(it->second));
+      CU_CHECK(cgf::drv::cuMemAlloc(&pl, 2 * (ybytes + wbytes)));
+      p->wimg[{ctx, "gzplanes"}] = pl;
+      cap = 2 * (ybytes + wbytes);
+    } else {
+      pl = it->second;
+    }
+  }
+  void* yh = reinterpret_cast<void*>(pl);
+  void* yl = reinterpret_cast<void*>(pl + ybytes);
+  void* wh = reinterpret_cast<void*>(pl + 2 * ybytes);
+  void* wl = reinterpret_cast<void*>(pl + 2 * ybytes + wbytes);
+  {
+    const cgf::Kernel planes = cgf::load_kernel(us_y->prep);
+    void* pargs[] = {&gza, &yh, &yl, &wh, &wl, &nrows, &pitch};
+    const unsigned pgrid = static_cast<unsigned>(std::min<std::int64_t>((rows + 31) / 32, planes.max_grid));
+    CU_CHECK(cgf::drv::cuLaunchKernel(planes.fn, pgrid, 1, 1, 256, 1, 1, us_y->prep.smem_bytes, st, pargs, nullptr));
+  }
+  auto plane_map = [&](CUtensorMap* m, void* base, bool rows_inner) {
+    const cuuint64_t gdim_y[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(nplanes)};
+    const cuuint64_t gstr_y[2] = {256, static_cast<cuuint64_t>(rows) * 256};
+    const cuuint32_t box_y[3] = {16, 128, 1};
+    const cuuint64_t gdim_w[3] = {static_cast<cuuint64_t>(rows), 64, static_cast<cuuint64_t>(nplanes)};
+    const cuuint64_t gstr_w[2] = {static_cast<cuuint64_t>(pitch) * 4, static_cast<cuuint64_t>(pitch) * 256};
+    const cuuint32_t box_w[3] = {16, 64, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CU_CHECK(cgf::drv::cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, rows_inner ? gdim_w : gdim_y,
+                                              rows_inner ? gstr_w : gstr_y, rows_inner ? box_w : box_y, estr,
+                                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+  };
   // dL/dy
   {
-    const auto us = uvw_source(p, "bwdy");
-    const cgf::Kernel k = cgf::load_kernel(us->main);
+    const cgf::Kernel k = cgf::load_kernel(us_y->main);
     CUdeviceptr img;
     {
       std::lock_guard<std::mutex> g(p->mu);
       img = p->wimg.at({ctx, "bwdx"});
     }
+    CUtensorMap tg[2];
+    plane_map(&tg[0], yh, false);
+    plane_map(&tg[1], yl, false);
     const void* wi = reinterpret_cast<const void*>(img);
     void* gya = gy;
-    void* args[] = {&maps[0], &maps[1], &maps[2], &maps[3], &ya, &wi, &gza, &gya, &nrows};
+    void* args[] = {&maps[0], &maps[1], &maps[2], &maps[3], &tg[0], &tg[1], &ya, &wi, &gya, &nrows};
     const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(tiles, k.max_grid));
     CU_CHECK(cgf::drv::cuLaunchKernel(k.fn, grid, 1, 1, k.threads, 1, 1, k.smem_bytes, st, args, nullptr));
   }
   // shared dL/dW: <= 6 instructions per pass (TMEM), per-CTA partials, then a
   // fixed-order reduction of each pass's weight range
+  CUtensorMap tw[2];
+  plane_map(&tw[0], wh, true);
+  plane_map(&tw[1], wl, true);
   const int np = static_cast<int>(p->problem.resolved.size());
   for (int first = 0; first < np; first += 6) {
     const auto us = uvw_source(p, "bwdw" + std::to_string(first));
@@ -355,7 +408,7 @@ void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, c
       }
     }
     void* pa = reinterpret_cast<void*>(part);
-    void* args[] = {&maps[0], &maps[1], &maps[2], &maps[3], &ya, &gza, &pa, &nrows};
+    void* args[] = {&maps[0], &maps[1], &maps[2], &maps[3], &tw[0], &tw[1], &ya, &pa, &nrows};
     const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(tiles, k.max_grid));
     CU_CHECK(cgf::drv::cuLaunchKernel(k.fn, grid, 1, 1, k.threads, 1, 1, k.smem_bytes, st, args, nullptr));
     const int last = std::min(np, first + 6) - 1;

@@ -303,6 +303,18 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
   int max_dz = 1;
   for (const auto& sq : R) max_dz = std::max(max_dz, sq.dz());
   if (64 * max_dz > 512) throw UnsupportedError("uvw gy kernel: l3 too large");
+  // gz planes: for every z segment and component k, the 64 channels of gz
+  // contiguous per row ([plane][row][64], tf32 hi and lo arrays), written by
+  // the pre-pass so the gy kernel can TMA-load gz_k tiles in the MMA layout.
+  std::map<std::uint32_t, int> plane_of_seg;
+  int nplanes = 0;
+  std::vector<std::pair<std::uint32_t, int>> segs;  // (z_off, dz) in plane order
+  for (const auto& sq : R)
+    if (!plane_of_seg.count(sq.z_off)) {
+      plane_of_seg[sq.z_off] = nplanes;
+      nplanes += sq.dz();
+      segs.push_back({sq.z_off, sq.dz()});
+    }
   const int gz_bytes = 2 * kTileRows * 64 * 4;
   const int nx = 2;
   const int smem = 1024 + gz_bytes + nx * g.xslot + 4 * g.wslot + 1024 + 128 * p.dim_y * 4;
@@ -310,15 +322,51 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
   std::ostringstream o;
   if (std::getenv("CGF_UVW_DEBUG")) o << "#define CGF_UVW_DEBUG 1\n";
   o << device_runtime_source() << uvw_helpers() << grad_helpers();
-  o << "// uvw gy: " << np << " instructions\n#define DIMX " << p.dim_x << "\n#define DIMY " << p.dim_y
-    << "\n#define DIMZ " << p.dim_z << "\n#define NP " << np << "\n#define WSLOT " << g.wslot << "\n#define XSLOT "
-    << g.xslot << "\n#define GZB " << gz_bytes << "\n#define NX " << nx << "\n";
+  o << "// uvw gy: " << np << " instructions, " << nplanes << " gz planes\n#define DIMX " << p.dim_x << "\n#define DIMY "
+    << p.dim_y << "\n#define DIMZ " << p.dim_z << "\n#define NP " << np << "\n#define WSLOT " << g.wslot
+    << "\n#define XSLOT " << g.xslot << "\n#define GZB " << gz_bytes << "\n#define NX " << nx << "\n#define NPLANES "
+    << nplanes << "\n";
   emit_grad_tables(o, p);
   {
     o << "__constant__ int P_WIMG[" << np << "] = {";
     for (int q = 0; q < np; ++q) o << (q ? "," : "") << g.wimg_of[q];
+    o << "};\n__constant__ int P_PLANE[" << np << "] = {";
+    for (int q = 0; q < np; ++q) o << (q ? "," : "") << plane_of_seg.at(R[q].z_off);
     o << "};\n";
   }
+  // ---- pre-pass (one read of gz): tf32 hi / lo planes for both gradient
+  // kernels, one block per 32 rows staged in shared memory:
+  //   gy:  YH / YL [plane][row][64 r]      (the gy MMA's A tiles, K = r)
+  //   gW:  WH / WL [plane][64 r][pitch]    (the gW MMA's B tiles, K = rows)
+  o << "extern \"C\" __global__ void __launch_bounds__(256) cgf_uvw_bwd_planes_f32(const float* __restrict__ GZ,"
+       " float* __restrict__ YH, float* __restrict__ YL, float* __restrict__ WH, float* __restrict__ WL, i64 rows,"
+       " i64 pitch) {\n"
+       "  extern __shared__ float t[];  // [32][DIMZ + 1]\n"
+       "  const i64 chunks = (rows + 31) / 32;\n"
+       "  for (i64 cbk = blockIdx.x; cbk < chunks; cbk += gridDim.x) {\n"
+       "    const i64 r0 = cbk * 32;\n"
+       "    __syncthreads();\n"
+       "    for (int e = threadIdx.x; e < 32 * DIMZ; e += 256) {\n"
+       "      const int rr = e / DIMZ, c = e - rr * DIMZ;\n"
+       "      t[rr * (DIMZ + 1) + c] = r0 + rr < rows ? __ldg(GZ + (r0 + rr) * DIMZ + c) : 0.f;\n    }\n"
+       "    __syncthreads();\n";
+  for (size_t si = 0; si < segs.size(); ++si) {
+    const auto [zoff, dz] = segs[si];
+    const int pl0 = plane_of_seg.at(zoff);
+    o << "    // segment " << si << ": z offset " << zoff << ", " << dz << " components, planes " << pl0 << ".."
+      << pl0 + dz - 1 << "\n"
+      << "    for (int e = threadIdx.x; e < 32 * 64 * " << dz << "; e += 256) {\n"
+      << "      { const int r = e & 63, rr = (e >> 6) & 31, k = e >> 11;\n"
+      << "        if (r0 + rr < rows) { const float v = t[rr * (DIMZ + 1) + " << zoff << " + r * " << dz
+      << " + k], h = tf32_hi(v);\n"
+      << "          const i64 o = ((i64)(" << pl0 << " + k) * rows + r0 + rr) * 64 + r; __stcs(YH + o, h); __stcs(YL + o, v - h); } }\n"
+      << "      { const int rr = e & 31, r = (e >> 5) & 63, k = e >> 11;\n"
+      << "        if (r0 + rr < rows) { const float v = t[rr * (DIMZ + 1) + " << zoff << " + r * " << dz
+      << " + k], h = tf32_hi(v);\n"
+      << "          const i64 o = ((i64)(" << pl0 << " + k) * 64 + r) * pitch + r0 + rr; __stcs(WH + o, h); __stcs(WL + o, v - h); } }\n"
+      << "    }\n";
+  }
+  o << "  }\n}\n\n";
   // per instruction: x once per 16-channel block, then every component k
   // against gzp_k (TMEM columns 64 k of this thread's lane)
   for (int q = 0; q < np; ++q) {
@@ -345,12 +393,13 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
     }
     o << "}\n\n";
   }
-  o << "extern \"C\" __global__ void __launch_bounds__(352, 1) cgf_uvw_bwdy_f32("
+  // warps: 0-7 producers (gy), 8 MMA, 9 x TMA, 10 W images, 11 gz TMA
+  o << "extern \"C\" __global__ void __launch_bounds__(384, 1) cgf_uvw_bwdy_f32("
        "const __grid_constant__ TMap tx1, const __grid_constant__ TMap tx3, const __grid_constant__ TMap tx5, "
-       "const __grid_constant__ TMap tx7, const float* __restrict__ Y, const float* __restrict__ WIMG, "
-       "const float* __restrict__ GZ, float* __restrict__ GY, i64 rows) {\n"
+       "const __grid_constant__ TMap tx7, const __grid_constant__ TMap tgh, const __grid_constant__ TMap tgl, "
+       "const float* __restrict__ Y, const float* __restrict__ WIMG, float* __restrict__ GY, i64 rows) {\n"
     << grad_kernel_head()
-    << "  unsigned char* gzt = sm;                 // gz_k tile [rows][r]: hi [4][128][16], lo after GZB/2\n"
+    << "  unsigned char* gzt = sm;                 // gz_k tile [rows][r]: hi [4][128][16], lo after GZB/2 (TMA)\n"
        "  unsigned char* xs0 = gzt + GZB;          // x tile ring (TMA, SW64)\n"
        "  unsigned char* ws = xs0 + NX * XSLOT;    // W^T images of one instruction (4 r-blocks)\n"
        "  u64* bars = (u64*)(ws + 4 * WSLOT);\n"
@@ -359,7 +408,7 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "  u32* tmem_slot = (u32*)(bars + 6 + 2 * NX);\n"
        "  float* gys = (float*)(bars + 16);\n"
        "  if (threadIdx.x == 0) {\n"
-       "    mbar_init(gz_full, 8); mbar_init(gz_empty, 1); mbar_init(gzp_full, 1); mbar_init(gzp_empty, 8);\n"
+       "    mbar_init(gz_full, 1); mbar_init(gz_empty, 1); mbar_init(gzp_full, 1); mbar_init(gzp_empty, 8);\n"
        "    mbar_init(w_full, 1); mbar_init(w_empty, 1);\n"
        "    for (int i = 0; i < NX; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n"
        "    mbar_fence_init();\n  }\n"
@@ -372,28 +421,13 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "  if (warp < 8) {\n"
        "    const int m = 32 * (warp & 3) + lane, sub = warp >> 2;\n"
        "    const u32 tq = tmem + ((u32)(32 * (warp & 3)) << 16);\n"
-       "    u32 ug = 0, uq = 0, gx = 0;\n"
+       "    u32 uq = 0, gx = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
        "      const i64 row = tile * 128 + m;\n"
        "      const bool valid = row < rows;\n"
        "      float gy[DIMY];\n"
        "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) gy[j] = 0.f;\n"
-       "      const float* gzr = GZ + (valid ? row : 0) * DIMZ;\n"
        "#pragma unroll 1\n      for (int q = 0; q < NP; ++q, ++uq) {\n"
-       "        const int dz = P_DZ[q];\n"
-       "#pragma unroll 1\n        for (int k = 0; k < dz; ++k, ++ug) {\n"
-       "          mbar_wait_t(gz_empty, (ug & 1u) ^ 1u, 20);\n"
-       "#pragma unroll\n          for (int g = 0; g < 8; ++g) {\n"
-       "            float h[4], l[4];\n"
-       "#pragma unroll\n            for (int a = 0; a < 4; ++a) {\n"
-       "              const float v = valid ? __ldg(gzr + P_ZOFF[q] + (32 * sub + 4 * g + a) * dz + k) : 0.f;\n"
-       "              h[a] = tf32_hi(v); l[a] = v - h[a];\n            }\n"
-       "            const int c4 = 8 * sub + g;\n"
-       "            const u32 off = (c4 >> 2) * 8192 + sw64(m, c4 & 3);\n"
-       "            sts128(gzt + off, make_float4(h[0], h[1], h[2], h[3]));\n"
-       "            sts128(gzt + GZB / 2 + off, make_float4(l[0], l[1], l[2], l[3]));\n          }\n"
-       "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(gz_full);\n"
-       "        }\n"
        "        mbar_wait_t(gzp_full, uq & 1u, 22);\n"
        "        tc_fence_after();\n"
        "#pragma unroll 1\n        for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
@@ -473,16 +507,38 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "    }\n"
        "    __syncwarp();\n"
        "  }\n"
+       "  else if (warp == 11) {\n"
+       // gz_k tiles from the planes: 4 r-blocks of [128 rows][16] (SW64) for hi
+       // and for lo, the layout the MMA's K-major A descriptor reads
+       "    if (lane == 0) {\n"
+       "      u32 ug = 0;\n"
+       "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
+       "        for (int q = 0; q < NP; ++q)\n"
+       "          for (int k = 0; k < P_DZ[q]; ++k, ++ug) {\n"
+       "            mbar_wait_t(gz_empty, (ug & 1u) ^ 1u, 31);\n"
+       "            mbar_expect_tx(gz_full, GZB);\n"
+       "            for (int j = 0; j < 4; ++j) {\n"
+       "              tma_load3(gzt + j * 8192, &tgh, 16 * j, (int)(tile * 128), P_PLANE[q] + k, gz_full);\n"
+       "              tma_load3(gzt + GZB / 2 + j * 8192, &tgl, 16 * j, (int)(tile * 128), P_PLANE[q] + k, gz_full);\n"
+       "            }\n"
+       "          }\n"
+       "    }\n"
+       "    __syncwarp();\n"
+       "  }\n"
        "  tc_fence_before();\n  __syncthreads();\n"
        "  if (warp == 8) { tc_fence_after(); asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\" :: \"r\"(tmem)); }\n"
        "}\n";
   UvwSource out;
   out.main.name = out.main.module = "cgf_uvw_bwdy_f32";
   out.main.source = o.str();
-  out.main.threads = 352;
+  out.main.threads = 384;
   out.main.smem_bytes = smem;
   out.prep = out.main;
+  out.prep.name = "cgf_uvw_bwd_planes_f32";
+  out.prep.threads = 256;
+  out.prep.smem_bytes = 32 * (p.dim_z + 1) * 4;
   out.wimg_bytes = 0;
+  out.dims_x = nplanes;  // number of gz planes (the caller sizes the plane buffers)
   return out;
 }
 
@@ -503,6 +559,14 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   const int smem = 1024 + 2 * tb + 2 * g.xslot + 1024;
   if (smem > 227 * 1024) throw UnsupportedError("uvw gW kernel: shared memory too small");
   const std::string kname = "cgf_uvw_bwdw" + S(first) + "_f32";
+  // gz planes (same numbering as the gy pre-pass): segment component -> plane
+  std::map<std::uint32_t, int> plane_of_seg;
+  int nplanes = 0;
+  for (const auto& sq : R)
+    if (!plane_of_seg.count(sq.z_off)) {
+      plane_of_seg[sq.z_off] = nplanes;
+      nplanes += sq.dz();
+    }
   std::ostringstream o;
   if (std::getenv("CGF_UVW_DEBUG")) o << "#define CGF_UVW_DEBUG 1\n";
   o << device_runtime_source() << uvw_helpers() << grad_helpers();
@@ -510,6 +574,9 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
     << "\n#define DIMY " << p.dim_y << "\n#define DIMZ " << p.dim_z << "\n#define NW_ " << p.n_w << "\n#define Q0 "
     << first << "\n#define Q1 " << first + count << "\n#define XSLOT " << g.xslot << "\n#define TB " << tb << "\n";
   emit_grad_tables(o, p);
+  o << "__constant__ int P_PLANE[" << R.size() << "] = {";
+  for (size_t q = 0; q < R.size(); ++q) o << (q ? "," : "") << plane_of_seg.at(R[q].z_off);
+  o << "};\n";
   for (int q = first; q < first + count; ++q) {
     const auto& sq = R[q];
     const int dx = sq.dx(), dz = sq.dz();
@@ -539,10 +606,11 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "float* __restrict__ gw, int w0, int w1) {\n"
        "  const int e = w0 + blockIdx.x * blockDim.x + threadIdx.x;\n  if (e >= w1) return;\n"
        "  float s = 0.f;\n  for (int c = 0; c < nparts; ++c) s += part[(size_t)c * NW_ + e];\n  gw[e] = s;\n}\n\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(320, 1) " << kname << "("
+  // warps: 0-7 producers (z'), 8 MMA, 9 x TMA, 10 gz TMA (transposed planes)
+  o << "extern \"C\" __global__ void __launch_bounds__(352, 1) " << kname << "("
        "const __grid_constant__ TMap tx1, const __grid_constant__ TMap tx3, const __grid_constant__ TMap tx5, "
-       "const __grid_constant__ TMap tx7, const float* __restrict__ Y, const float* __restrict__ GZ, "
-       "float* __restrict__ PART, i64 rows) {\n"
+       "const __grid_constant__ TMap tx7, const __grid_constant__ TMap tgh, const __grid_constant__ TMap tgl, "
+       "const float* __restrict__ Y, float* __restrict__ PART, i64 rows) {\n"
     << grad_kernel_head()
     << "  unsigned char* gzt = sm;                 // gz_k tile [r][rows] K-major: hi, lo after TB/2\n"
        "  unsigned char* zt = sm + TB;             // z'_k tile [c][rows] K-major\n"
@@ -552,7 +620,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "  u64* x_full = bars + 8; u64* x_empty = bars + 10; u64* done = bars + 12;\n"
        "  u32* tmem_slot = (u32*)(bars + 13);\n"
        "  if (threadIdx.x == 0) {\n"
-       "    mbar_init(gz_full, 8); mbar_init(gz_empty, 1); mbar_init(z_full, 8); mbar_init(z_empty, 1);\n"
+       "    mbar_init(gz_full, 1); mbar_init(gz_empty, 1); mbar_init(z_full, 8); mbar_init(z_empty, 1);\n"
        "    for (int i = 0; i < 2; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n    mbar_init(done, 1);\n"
        "    mbar_fence_init();\n  }\n"
        "  if (warp == 8) {\n"
@@ -569,17 +637,9 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "      const bool valid = row < rows;\n"
        "      float yv[DIMY];\n"
        "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) yv[j] = valid ? __ldg(Y + row * DIMY + j) : 0.f;\n"
-       "      const float* gzr = GZ + (valid ? row : 0) * DIMZ;\n"
        "#pragma unroll 1\n      for (int q = Q0; q < Q1; ++q) {\n"
        "        const int dz = P_DZ[q];\n"
        "#pragma unroll 1\n        for (int k = 0; k < dz; ++k, ++ug) {\n"
-       "          mbar_wait_t(gz_empty, (ug & 1u) ^ 1u, 20);\n"
-       "#pragma unroll 4\n          for (int t = 0; t < 32; ++t) {\n"
-       "            const int r = 32 * sub + t;\n"
-       "            const float v = valid ? __ldg(gzr + P_ZOFF[q] + r * dz + k) : 0.f;\n"
-       "            const float h = tf32_hi(v);\n            const u32 off = kmaj_rows(r, m);\n"
-       "            sts32(gzt + off, h); sts32(gzt + TB / 2 + off, v - h);\n          }\n"
-       "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(gz_full);\n"
        "          mbar_wait_t(z_empty, (ug & 1u) ^ 1u, 21);\n"
        "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
        "            const u32 xsl = gx & 1u;\n"
@@ -658,13 +718,31 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "    }\n"
        "    __syncwarp();\n"
        "  }\n"
-    << "  tc_fence_before();\n  __syncthreads();\n"
+    << "  else if (warp == 10) {\n"
+       // gz_k^T tiles from the transposed planes: 8 K blocks of [64 r][16 rows]
+       // (SW64), hi and lo: the K-major B layout of the gW MMA
+       "    if (lane == 0) {\n"
+       "      u32 ug = 0;\n"
+       "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
+       "        for (int q = Q0; q < Q1; ++q)\n"
+       "          for (int k = 0; k < P_DZ[q]; ++k, ++ug) {\n"
+       "            mbar_wait_t(gz_empty, (ug & 1u) ^ 1u, 31);\n"
+       "            mbar_expect_tx(gz_full, TB);\n"
+       "            for (int b = 0; b < 8; ++b) {\n"
+       "              tma_load3(gzt + b * 4096, &tgh, (int)(tile * 128) + 16 * b, 0, P_PLANE[q] + k, gz_full);\n"
+       "              tma_load3(gzt + TB / 2 + b * 4096, &tgl, (int)(tile * 128) + 16 * b, 0, P_PLANE[q] + k, gz_full);\n"
+       "            }\n"
+       "          }\n"
+       "    }\n"
+       "    __syncwarp();\n"
+       "  }\n"
+       "  tc_fence_before();\n  __syncthreads();\n"
        "  if (warp == 8) { tc_fence_after(); asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\" :: \"r\"(tmem)); }\n"
        "}\n";
   UvwSource out;
   out.main.name = out.main.module = kname;
   out.main.source = o.str();
-  out.main.threads = 320;
+  out.main.threads = 352;
   out.main.smem_bytes = smem;
   out.prep = out.main;
   out.prep.name = kname + "_reduce";
