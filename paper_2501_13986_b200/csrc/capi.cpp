@@ -298,13 +298,13 @@ void memzero(void* ptr, std::size_t bytes, void* stream) {
 
 // Tensor maps over a [rows][dim] fp32 array viewed as [rows][dim / 16][16]:
 // boxes of 128 rows x dx lines (dx = 1, 3, 5, 7), 64-byte swizzle.
-void uvw_tmaps(CUtensorMap maps[4], const void* base, int dim, std::int64_t rows) {
+void uvw_tmaps(CUtensorMap maps[4], const void* base, int dim, std::int64_t rows, unsigned box_rows = 128) {
   if (reinterpret_cast<std::uintptr_t>(base) & 15u) throw cgf::ShapeError("uvw path: inputs must be 16-byte aligned");
   const int dxs[4] = {1, 3, 5, 7};
   for (int i = 0; i < 4; ++i) {
     const cuuint64_t gdim[3] = {16, static_cast<cuuint64_t>(dim / 16), static_cast<cuuint64_t>(rows)};
     const cuuint64_t gstride[2] = {64, static_cast<cuuint64_t>(dim) * 4};
-    const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(std::min(dxs[i], dim / 16)), 128};
+    const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(std::min(dxs[i], dim / 16)), box_rows};
     const cuuint32_t estr[3] = {1, 1, 1};
     CU_CHECK(cgf::drv::cuTensorMapEncodeTiled(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), gdim,
                                               gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -408,7 +408,9 @@ void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, c
       }
     }
     void* pa = reinterpret_cast<void*>(part);
-    void* args[] = {&maps[0], &maps[1], &maps[2], &maps[3], &tw[0], &tw[1], &ya, &pa, &nrows};
+    CUtensorMap xm[4];
+    uvw_tmaps(xm, x, p->problem.dim_x, rows, static_cast<unsigned>(us->tile_rows));
+    void* args[] = {&xm[0], &xm[1], &xm[2], &xm[3], &tw[0], &tw[1], &ya, &pa, &nrows};
     const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(tiles, k.max_grid));
     CU_CHECK(cgf::drv::cuLaunchKernel(k.fn, grid, 1, 1, k.threads, 1, 1, k.smem_bytes, st, args, nullptr));
     const int last = std::min(np, first + 6) - 1;

@@ -316,7 +316,7 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
       segs.push_back({sq.z_off, sq.dz()});
     }
   const int gz_bytes = 2 * kTileRows * 64 * 4;
-  const int nx = 2;
+  const int nx = std::getenv("CGF_UVW_GY_NX") ? std::atoi(std::getenv("CGF_UVW_GY_NX")) : 3;
   const int smem = 1024 + gz_bytes + nx * g.xslot + 4 * g.wslot + 1024 + 128 * p.dim_y * 4;
   if (smem > 227 * 1024) throw UnsupportedError("uvw gy kernel: shared memory too small");
   std::ostringstream o;
@@ -546,20 +546,28 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
 // for instructions [first, first + count) (count <= 6: one 64-column TMEM
 // accumulator each):
 //   gW_q[r][c] += sum_row sum_k gz[row][q.z][r][k] z'_k[row][c],  z'_k = CG(x, y)[.., k]
-// (kernelgen.cpp:639-650 summed over rows): tcgen05 M=64 (c), N=64 (r), K=128
-// rows per tile, both operands K-major over the batch rows (written by the
-// producers transposed), 3xTF32. Accumulators live in TMEM across all tiles of
-// the CTA and are written once as this CTA's partial; `prep` sums the
-// partials over CTAs in a fixed order (deterministic).
+// (kernelgen.cpp:639-650 summed over rows): tcgen05 M=64 (c), N=64 (r), K = 64
+// batch rows per stage, both operands K-major over the rows, 3xTF32. The z'
+// tiles are written transposed by the producers, the gz^T tiles come by TMA
+// from the transposed gz planes (cgf_uvw_bwd_planes_f32); both are double
+// buffered, so the producers write stage s+1 while the MMAs consume stage s.
+// Accumulators live in TMEM across all tiles of the CTA and are written once
+// as this CTA's partial; `prep` sums the partials over CTAs in a fixed order
+// (deterministic).
 UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   const GradInfo g = grad_info(p);
   const auto& R = p.resolved;
   if (count < 1 || count > 6 || first < 0 || first + count > g.np) throw std::logic_error("bad gW instruction range");
-  const int tb = 2 * 64 * kTileRows * 4;  // hi + lo of a [64][128 rows] K-major tile
-  const int smem = 1024 + 2 * tb + 2 * g.xslot + 1024;
+  constexpr int kRows = 64;                       // batch rows per stage (the MMA's K)
+  const int tb = 2 * 64 * kRows * 4;              // hi + lo of a [64][64 rows] K-major tile
+  const int xslot = (kRows * kCh * g.max_dx * 4 + 1023) / 1024 * 1024;
+  // x tiles: 4 per (instruction, component) stage, so the ring is deep
+  // enough to keep a stage's worth of TMA loads in flight (ring of 2: 4.4 ms)
+  const int nx = std::getenv("CGF_UVW_GW_NX") ? std::atoi(std::getenv("CGF_UVW_GW_NX")) : 4;
+  const int smem = 1024 + 4 * tb + nx * xslot + 1024;
   if (smem > 227 * 1024) throw UnsupportedError("uvw gW kernel: shared memory too small");
   const std::string kname = "cgf_uvw_bwdw" + S(first) + "_f32";
-  // gz planes (same numbering as the gy pre-pass): segment component -> plane
+  // gz planes (same numbering as the pre-pass): segment component -> plane
   std::map<std::uint32_t, int> plane_of_seg;
   int nplanes = 0;
   for (const auto& sq : R)
@@ -572,18 +580,25 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   o << device_runtime_source() << uvw_helpers() << grad_helpers();
   o << "// uvw gW: instructions [" << first << ", " << first + count << ")\n#define DIMX " << p.dim_x
     << "\n#define DIMY " << p.dim_y << "\n#define DIMZ " << p.dim_z << "\n#define NW_ " << p.n_w << "\n#define Q0 "
-    << first << "\n#define Q1 " << first + count << "\n#define XSLOT " << g.xslot << "\n#define TB " << tb << "\n";
+    << first << "\n#define Q1 " << first + count << "\n#define XSLOT " << xslot << "\n#define TB " << tb
+    << "\n#define KR " << kRows << "\n#define NX " << nx << "\n";
   emit_grad_tables(o, p);
   o << "__constant__ int P_PLANE[" << R.size() << "] = {";
   for (size_t q = 0; q < R.size(); ++q) o << (q ? "," : "") << plane_of_seg.at(R[q].z_off);
   o << "};\n";
+  // producer thread (row m < 64, sub < 4) owns channels [4 sub, 4 sub + 4) of
+  // the 16-channel block cb: x read (dx float4), z'_k for its 4 channels
   for (int q = first; q < first + count; ++q) {
     const auto& sq = R[q];
     const int dx = sq.dx(), dz = sq.dz();
     o << "DEVI void zw_" << q << "(int k, int cb, const unsigned char* xs, const float* yv, int m, int sub,"
-      << " unsigned char* zt, u64* xempty) {\n";
-    emit_x_read(o, dx);
-    o << "  float zc[8];\n#pragma unroll\n  for (int c = 0; c < 8; ++c) zc[c] = 0.f;\n  switch (k) {\n";
+      << " unsigned char* zt, u64* xempty) {\n"
+      << "  float xv[" << 4 * dx << "];\n#pragma unroll\n  for (int t = 0; t < " << dx << "; ++t) {\n"
+      << "    const int gq = " << dx << " * sub + t, L = m * " << dx << " + (gq >> 2), j = gq & 3;\n"
+      << "    const float4 v = lds128(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4));\n"
+      << "    xv[4 * t] = v.x; xv[4 * t + 1] = v.y; xv[4 * t + 2] = v.z; xv[4 * t + 3] = v.w;\n  }\n"
+      << "  fence_proxy_async();\n  __syncwarp();\n  if ((threadIdx.x & 31) == 0) mbar_arrive(xempty);\n";
+    o << "  float zc[4] = {0.f, 0.f, 0.f, 0.f};\n  switch (k) {\n";
     for (int k = 0; k < dz; ++k) {
       std::map<int, std::string> qk;
       for (const auto& e : sq.cg->entries) {
@@ -593,36 +608,40 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
       }
       o << "  case " << k << ": {\n";
       for (const auto& [i, ex] : qk) o << "    const float q" << i << " = " << ex << ";\n";
-      o << "#pragma unroll\n    for (int c = 0; c < 8; ++c) {\n";
+      o << "#pragma unroll\n    for (int c = 0; c < 4; ++c) {\n";
       for (const auto& kv : qk) o << "      zc[c] = fmaf(q" << kv.first << ", xv[c * " << dx << " + " << kv.first << "], zc[c]);\n";
       o << "    }\n    break; }\n";
     }
     o << "  }\n"
-      << "#pragma unroll\n  for (int c = 0; c < 8; ++c) {\n"
-      << "    const float h = tf32_hi(zc[c]);\n    const u32 off = kmaj_rows(16 * cb + 8 * sub + c, m);\n"
+      << "#pragma unroll\n  for (int c = 0; c < 4; ++c) {\n"
+      << "    const float h = tf32_hi(zc[c]);\n    const u32 off = kmaj_rows(16 * cb + 4 * sub + c, m);\n"
       << "    sts32(zt + off, h); sts32(zt + TB / 2 + off, zc[c] - h);\n  }\n}\n\n";
   }
   o << "extern \"C\" __global__ void " << kname << "_reduce(const float* __restrict__ part, int nparts, "
        "float* __restrict__ gw, int w0, int w1) {\n"
        "  const int e = w0 + blockIdx.x * blockDim.x + threadIdx.x;\n  if (e >= w1) return;\n"
        "  float s = 0.f;\n  for (int c = 0; c < nparts; ++c) s += part[(size_t)c * NW_ + e];\n  gw[e] = s;\n}\n\n";
-  // warps: 0-7 producers (z'), 8 MMA, 9 x TMA, 10 gz TMA (transposed planes)
+  // warps: 0-7 producers (z'), 8 MMA, 9 x TMA, 10 gz TMA
   o << "extern \"C\" __global__ void __launch_bounds__(352, 1) " << kname << "("
        "const __grid_constant__ TMap tx1, const __grid_constant__ TMap tx3, const __grid_constant__ TMap tx5, "
        "const __grid_constant__ TMap tx7, const __grid_constant__ TMap tgh, const __grid_constant__ TMap tgl, "
        "const float* __restrict__ Y, float* __restrict__ PART, i64 rows) {\n"
-    << grad_kernel_head()
-    << "  unsigned char* gzt = sm;                 // gz_k tile [r][rows] K-major: hi, lo after TB/2\n"
-       "  unsigned char* zt = sm + TB;             // z'_k tile [c][rows] K-major\n"
-       "  unsigned char* xs0 = zt + TB;            // x tile ring of 2 (TMA, SW64)\n"
-       "  u64* bars = (u64*)(xs0 + 2 * XSLOT);\n"
-       "  u64* gz_full = bars; u64* gz_empty = bars + 1; u64* z_full = bars + 2; u64* z_empty = bars + 3;\n"
-       "  u64* x_full = bars + 8; u64* x_empty = bars + 10; u64* done = bars + 12;\n"
-       "  u32* tmem_slot = (u32*)(bars + 13);\n"
+       "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n"
+       "  unsigned char* sm = (unsigned char*)(((unsigned long long)smem_raw + 1023) & ~1023ull);\n"
+       "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n"
+       "  const i64 ntiles = (rows + KR - 1) / KR;\n"
+       "  unsigned char* gzt = sm;                 // 2 x gz_k^T tile [r][KR rows] K-major: hi, lo after TB/2\n"
+       "  unsigned char* zt = sm + 2 * TB;         // 2 x z'_k^T tile [c][KR rows] K-major\n"
+       "  unsigned char* xs0 = zt + 2 * TB;        // x tile ring of NX (TMA, SW64)\n"
+       "  u64* bars = (u64*)(xs0 + NX * XSLOT);\n"
+       "  u64* gz_full = bars; u64* gz_empty = bars + 2; u64* z_full = bars + 4; u64* z_empty = bars + 6;\n"
+       "  u64* x_full = bars + 8; u64* x_empty = bars + 8 + NX; u64* done = bars + 8 + 2 * NX;\n"
+       "  u32* tmem_slot = (u32*)(done + 1);\n"
        "  if (threadIdx.x == 0) {\n"
-       "    mbar_init(gz_full, 1); mbar_init(gz_empty, 1); mbar_init(z_full, 8); mbar_init(z_empty, 1);\n"
-       "    for (int i = 0; i < 2; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n    mbar_init(done, 1);\n"
-       "    mbar_fence_init();\n  }\n"
+       "    for (int i = 0; i < 2; ++i) {\n"
+       "      mbar_init(&gz_full[i], 1); mbar_init(&gz_empty[i], 1); mbar_init(&z_full[i], 8); mbar_init(&z_empty[i], 1);\n    }\n"
+       "    for (int i = 0; i < NX; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n"
+       "    mbar_init(done, 1);\n    mbar_fence_init();\n  }\n"
        "  if (warp == 8) {\n"
        "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" :: \"r\"(smem_addr(tmem_slot)));\n"
        "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\");\n"
@@ -630,34 +649,36 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n"
        "  const u32 tmem = *tmem_slot;\n"
        "  if (warp < 8) {\n"
-       "    const int m = 32 * (warp & 3) + lane, sub = warp >> 2;\n"
+       "    const int m = 32 * (warp & 1) + lane, sub = warp >> 1;\n"
        "    u32 ug = 0, gx = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
-       "      const i64 row = tile * 128 + m;\n"
+       "      const i64 row = tile * KR + m;\n"
        "      const bool valid = row < rows;\n"
        "      float yv[DIMY];\n"
        "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) yv[j] = valid ? __ldg(Y + row * DIMY + j) : 0.f;\n"
        "#pragma unroll 1\n      for (int q = Q0; q < Q1; ++q) {\n"
        "        const int dz = P_DZ[q];\n"
        "#pragma unroll 1\n        for (int k = 0; k < dz; ++k, ++ug) {\n"
-       "          mbar_wait_t(z_empty, (ug & 1u) ^ 1u, 21);\n"
+       "          const u32 zs = ug & 1u;\n"
+       "          unsigned char* z = zt + zs * TB;\n"
+       "          mbar_wait_t(&z_empty[zs], ((ug >> 1) & 1u) ^ 1u, 21);\n"
        "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
-       "            const u32 xsl = gx & 1u;\n"
-       "            mbar_wait_t(&x_full[xsl], (gx >> 1) & 1u, 23);\n"
+       "            const u32 xsl = gx % NX;\n"
+       "            mbar_wait_t(&x_full[xsl], (gx / NX) & 1u, 23);\n"
        "            const unsigned char* xs = xs0 + xsl * XSLOT;\n"
        "            switch (q) {\n";
   for (int q = first; q < first + count; ++q)
-    o << "              case " << q << ": zw_" << q << "(k, cb, xs, yv, m, sub, zt, &x_empty[xsl]); break;\n";
+    o << "              case " << q << ": zw_" << q << "(k, cb, xs, yv, m, sub, z, &x_empty[xsl]); break;\n";
   o << "            }\n"
        "          }\n"
-       "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(z_full);\n"
+       "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(&z_full[zs]);\n"
        "        }\n"
        "      }\n"
        "    }\n"
        // this CTA's partial: M=64 accumulators use lanes 0-15 of each 32-lane
        // quadrant: quadrant w holds c in [16 w, 16 w + 16), all 64 r columns
        "    mbar_wait_t(done, 0, 24);\n    tc_fence_after();\n"
-       "    if (sub == 0) {\n"
+       "    if (warp < 4) {\n"
        "      const u32 tq = tmem + ((u32)(32 * warp) << 16);\n"
        "      const int c = 16 * warp + lane;\n"
        "      float* pr = PART + (size_t)blockIdx.x * NW_;\n"
@@ -673,27 +694,29 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "    }\n"
        "  }\n"
        "  else if (warp == 8) {\n"
-       "    const u64 gh = sdesc64(smem_addr(gzt)), gl = gh + (u64)((TB / 2) >> 4);\n"
-       "    const u64 zh = sdesc64(smem_addr(zt)), zl = zh + (u64)((TB / 2) >> 4);\n"
+       "    const u64 gh0 = sdesc64(smem_addr(gzt)), zh0 = sdesc64(smem_addr(zt));\n"
        "    const u32 id_w = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(64 >> 3) << 17) | ((u32)(64 >> 4) << 24);\n"
        "    u32 ug = 0; i64 lt = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {\n"
        "      for (int q = Q0; q < Q1; ++q) {\n"
        "        const int dz = P_DZ[q];\n"
        "        for (int k = 0; k < dz; ++k, ++ug) {\n"
-       "          mbar_wait_t(gz_full, ug & 1u, 26);\n"
-       "          mbar_wait_t(z_full, ug & 1u, 28);\n"
+       "          const u32 st = ug & 1u, ph = (ug >> 1) & 1u;\n"
+       "          mbar_wait_t(&gz_full[st], ph, 26);\n"
+       "          mbar_wait_t(&z_full[st], ph, 28);\n"
        "          tc_fence_after();\n"
        "          if (elect_one()) {\n"
+       "            const u64 gh = gh0 + (u64)((st * TB) >> 4), gl = gh + (u64)((TB / 2) >> 4);\n"
+       "            const u64 zh = zh0 + (u64)((st * TB) >> 4), zl = zh + (u64)((TB / 2) >> 4);\n"
        "            const u32 dw = tmem + 64 * (q - Q0);\n"
        "            const u32 first = (lt == 0 && k == 0) ? 1u : 0u;\n"
-       "#pragma unroll\n            for (int s = 0; s < 16; ++s) {\n"
+       "#pragma unroll\n            for (int s = 0; s < KR / 8; ++s) {\n"
        "              const u64 o = (u64)(((s >> 1) * 4096 + (s & 1) * 32) >> 4);\n"
        "              tc_mma(dw, zh + o, gh + o, id_w, (first && s == 0) ? 0u : 1u);\n"
        "              tc_mma(dw, zh + o, gl + o, id_w, 1u);\n"
        "              tc_mma(dw, zl + o, gh + o, id_w, 1u);\n"
        "            }\n"
-       "            tc_commit(gz_empty);\n            tc_commit(z_empty);\n"
+       "            tc_commit(&gz_empty[st]);\n            tc_commit(&z_empty[st]);\n"
        "          }\n"
        "          __syncwarp();\n"
        "        }\n"
@@ -701,36 +724,38 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "    }\n"
        "    if (elect_one()) tc_commit(done);\n    __syncwarp();\n"
        "  }\n"
-    << "  else if (warp == 9) {\n"
+       "  else if (warp == 9) {\n"
        "    if (lane == 0) {\n"
        "      u32 gx = 0;\n"
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
        "        for (int q = Q0; q < Q1; ++q)\n"
        "          for (int k = 0; k < P_DZ[q]; ++k)\n"
        "            for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
-       "              const u32 xsl = gx & 1u;\n"
-       "              mbar_wait_t(&x_empty[xsl], ((gx >> 1) & 1u) ^ 1u, 29);\n"
+       "              const u32 xsl = gx % NX;\n"
+       "              mbar_wait_t(&x_empty[xsl], ((gx / NX) & 1u) ^ 1u, 29);\n"
        "              const int dx = P_DX[q];\n"
-       "              mbar_expect_tx(&x_full[xsl], 128 * 64 * dx);\n"
+       "              mbar_expect_tx(&x_full[xsl], KR * 64 * dx);\n"
        "              const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
-       "              tma_load3(xs0 + xsl * XSLOT, mp, 0, P_XC[q] + cb * dx, (int)(tile * 128), &x_full[xsl]);\n"
+       "              tma_load3(xs0 + xsl * XSLOT, mp, 0, P_XC[q] + cb * dx, (int)(tile * KR), &x_full[xsl]);\n"
        "            }\n"
        "    }\n"
        "    __syncwarp();\n"
        "  }\n"
-    << "  else if (warp == 10) {\n"
-       // gz_k^T tiles from the transposed planes: 8 K blocks of [64 r][16 rows]
-       // (SW64), hi and lo: the K-major B layout of the gW MMA
+       "  else if (warp == 10) {\n"
+       // gz_k^T tiles from the transposed planes: KR / 16 K blocks of
+       // [64 r][16 rows] (SW64), hi and lo: the K-major B layout of the MMA
        "    if (lane == 0) {\n"
        "      u32 ug = 0;\n"
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
        "        for (int q = Q0; q < Q1; ++q)\n"
        "          for (int k = 0; k < P_DZ[q]; ++k, ++ug) {\n"
-       "            mbar_wait_t(gz_empty, (ug & 1u) ^ 1u, 31);\n"
-       "            mbar_expect_tx(gz_full, TB);\n"
-       "            for (int b = 0; b < 8; ++b) {\n"
-       "              tma_load3(gzt + b * 4096, &tgh, (int)(tile * 128) + 16 * b, 0, P_PLANE[q] + k, gz_full);\n"
-       "              tma_load3(gzt + TB / 2 + b * 4096, &tgl, (int)(tile * 128) + 16 * b, 0, P_PLANE[q] + k, gz_full);\n"
+       "            const u32 st = ug & 1u;\n"
+       "            mbar_wait_t(&gz_empty[st], ((ug >> 1) & 1u) ^ 1u, 31);\n"
+       "            mbar_expect_tx(&gz_full[st], TB);\n"
+       "            unsigned char* d = gzt + st * TB;\n"
+       "            for (int b = 0; b < KR / 16; ++b) {\n"
+       "              tma_load3(d + b * 4096, &tgh, (int)(tile * KR) + 16 * b, 0, P_PLANE[q] + k, &gz_full[st]);\n"
+       "              tma_load3(d + TB / 2 + b * 4096, &tgl, (int)(tile * KR) + 16 * b, 0, P_PLANE[q] + k, &gz_full[st]);\n"
        "            }\n"
        "          }\n"
        "    }\n"
@@ -748,6 +773,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   out.prep.name = kname + "_reduce";
   out.prep.threads = 256;
   out.prep.smem_bytes = 0;
+  out.tile_rows = kRows;
   return out;
 }
 
