@@ -312,16 +312,25 @@ void Gen::layout() {
       }
     }
     if (!cfg_.w_shared) {
-      for (size_t q = 0; q < u.subs.size(); ++q) {
-        const Sub& s = p_.subs[u.subs[q]];
+      // in source order, so slices adjacent in the W row are adjacent in the
+      // slot too (one contiguous copy for the parallel-bulk issue)
+      std::vector<int> order(u.subs.size());
+      for (size_t q = 0; q < order.size(); ++q) order[q] = static_cast<int>(q);
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int a, int b) { return p_.subs[u.subs[a]].w_off < p_.subs[u.subs[b]].w_off; });
+      for (int qi : order) {
+        const Sub& s = p_.subs[u.subs[qi]];
         if (s.kind != Kind::B) continue;
-        add(L, "W", nw, e_src(), s.w_off, C.sw[q], s.b, so);
-        L.w_slot[static_cast<int>(q)] = so;
-        if (dual()) {
-          add(L, "DC", nw, e_src(), s.w_off, C.sw[q], s.b, so);
-          L.c_slot[static_cast<int>(q)] = so;
-        }
+        add(L, "W", nw, e_src(), s.w_off, C.sw[qi], s.b, so);
+        L.w_slot[qi] = so;
       }
+      if (dual())
+        for (int qi : order) {
+          const Sub& s = p_.subs[u.subs[qi]];
+          if (s.kind != Kind::B) continue;
+          add(L, "DC", nw, e_src(), s.w_off, C.sw[qi], s.b, so);
+          L.c_slot[qi] = so;
+        }
     }
     if (reads_gz()) {
       for (size_t z = 0; z < u.z_pieces.size(); ++z) {
@@ -367,9 +376,13 @@ std::string Gen::range_src(const SlotRange& r) const {
 //     its lane range. Completion: one cp.async.mbarrier arrive per lane.
 //     (A table-driven variant -- one L1 table load per pass -- measured 1.8x
 //     slower on the TP backward: the load latency sat on the critical path.)
+//   parallel bulk (par_bulk, with lane copy): lane i issues one cp.async.bulk
+//     (TMA 1-D) for the class's i-th contiguous range, lane 0 arms the mbarrier
+//     with the item's byte count: one instruction per range, in parallel.
 //   bulk: lane 0 arms the mbarrier and issues one cp.async.bulk per range.
 void Gen::emit_issue() {
   const bool lc = cfg_.lane_copy;
+  const bool pb = lc && cfg_.par_bulk;
   // distinct (array, index) source bases of the fixed ranges
   std::vector<std::pair<std::string, Src>> bases;
   auto base_id = [&](const SlotRange& r) {
@@ -388,7 +401,8 @@ void Gen::emit_issue() {
         " const T* __restrict__ GZ, const T* __restrict__ DA, const T* __restrict__ DB, const T* __restrict__ DC"
      << (lc ? ", int lane" : "") << ") {\n"
         "  (void)nbr; (void)eid; (void)rows_tot; (void)edges_tot;\n"
-     << (lc ? "" : "  fence_proxy_async();\n");
+     << (lc && !pb ? "" : "  fence_proxy_async();\n");
+  int wlane = 31;  // parallel bulk: window ranges take lanes 31, 30, ...
   if (lc) {
     for (size_t i = 0; i < bases.size(); ++i) {
       const auto& [arr, src] = bases[i];
@@ -400,9 +414,21 @@ void Gen::emit_issue() {
       o_ << "  const char* B" << i << " = (const char*)(" << arr << " + " << I << " * (i64)" << stride << ");\n";
     }
     o_ << "  char* sb = (char*)sl;\n";
+    if (pb) o_ << "  u32 tx = 0; const char* s_ = nullptr; int d_ = 0; u32 b_ = 0;\n";
     // window ranges (y, db): same slot offsets in every class (laid out first)
     for (const auto& r : lay_[0].ranges) {
       if (!(r.bulk && r.window)) continue;
+      if (pb) {
+        // one lane per window range (from lane 31 down), bytes into the item's tx
+        const std::string I = r.src == Src::Edge ? "eid" : "row";
+        const std::string tot = r.src == Src::Edge && conv() ? "edges_tot" : "rows_tot";
+        o_ << "  { const i64 b0 = " << I << " * " << r.stride << ", a0 = b0 & ~(i64)" << A() - 1 << ", a1 = (b0 + "
+           << r.words << " + " << A() - 1 << ") & ~(i64)" << A() - 1 << ";\n    if (a1 <= " << tot << " * (i64)" << r.stride
+           << ") { const u32 n_ = (u32)((a1 - a0) * sizeof(T)); tx += n_; if (lane == " << wlane << ") { s_ = (const char*)("
+           << r.arr << " + a0); d_ = " << r.slot_off * sz_ << "; b_ = n_; } } }\n";
+        --wlane;
+        continue;
+      }
       const std::string I = r.src == Src::Edge ? "eid" : "row";
       const std::string tot = r.src == Src::Edge && conv() ? "edges_tot" : "rows_tot";
       o_ << "  { const i64 b0 = " << I << " * " << r.stride << ", a0 = b0 & ~(i64)" << A() - 1 << ", a1 = (b0 + " << r.words
@@ -416,7 +442,32 @@ void Gen::emit_issue() {
     const Layout& L = lay_[k];
     o_ << "  " << (k ? "else " : "") << "if (u < " << C.u0 + C.n << ") {\n    const int kc = u - " << C.u0
        << "; (void)kc;\n";
-    if (lc) {
+    if (pb) {
+      // contiguous runs of fixed ranges (same base, adjacent source and slot)
+      struct Run { int base; long long off, step; std::uint32_t dst, bytes; };
+      std::vector<Run> runs;
+      std::uint32_t fixed = 0;
+      for (const auto& r : L.ranges) {
+        if (!r.bulk || r.window) continue;
+        const Run x{base_id(r), r.off * sz_, r.step * sz_, r.slot_off * static_cast<std::uint32_t>(sz_),
+                    r.words * static_cast<std::uint32_t>(sz_)};
+        fixed += x.bytes;
+        if (!runs.empty()) {
+          Run& b = runs.back();
+          if (b.base == x.base && b.step == x.step && b.off + b.bytes == x.off && b.dst + b.bytes == x.dst) {
+            b.bytes += x.bytes;
+            continue;
+          }
+        }
+        runs.push_back(x);
+      }
+      if (runs.size() > static_cast<size_t>(wlane + 1))
+        throw UnsupportedError("parallel bulk issue: more ranges than lanes");
+      o_ << "    tx += " << fixed << "u;\n";
+      for (size_t i = 0; i < runs.size(); ++i)
+        o_ << "    " << (i ? "else " : "") << "if (lane == " << i << ") { s_ = B" << runs[i].base << " + "
+           << O(runs[i].off, runs[i].step) << "; d_ = " << runs[i].dst << "; b_ = " << runs[i].bytes << "u; }\n";
+    } else if (lc) {
       std::vector<std::pair<int, int>> pieces;  // (range, piece)
       for (size_t ri = 0; ri < L.ranges.size(); ++ri) {
         const auto& r = L.ranges[ri];
@@ -469,7 +520,10 @@ void Gen::emit_issue() {
     }
     o_ << "  }\n";
   }
-  if (lc) o_ << "  cp_async_arrive(bar);\n";
+  if (pb)
+    o_ << "  if (lane == 0) mbar_expect_tx(bar, tx);\n  __syncwarp();\n  if (b_) bulk_g2s(sb + d_, s_, b_, bar);\n";
+  else if (lc)
+    o_ << "  cp_async_arrive(bar);\n";
   o_ << "}\n\n";
 }
 
@@ -1016,7 +1070,7 @@ KernelSource Gen::run() {
   if (by_input())
     o_ << "  T* gxs = scr + " << off_gxs_ << ";\n  for (int j = lane; j < " << p_.dim_x << "; j += 32) gxs[j] = 0;\n";
   o_ << "  u64* bars = (u64*)(smem_raw + NW * WARP_BYTES) + wid * D;\n"
-        "  if (lane == 0) { for (int d = 0; d < D; ++d) mbar_init(&bars[d], " << (cfg_.lane_copy ? 32 : 1) << "); mbar_fence_init(); }\n"
+        "  if (lane == 0) { for (int d = 0; d < D; ++d) mbar_init(&bars[d], " << (cfg_.lane_copy && !cfg_.par_bulk ? 32 : 1) << "); mbar_fence_init(); }\n"
         "  __syncwarp();\n"
         "  const i64 gwarp = (i64)blockIdx.x * NW + wid, nwarp = (i64)gridDim.x * NW;\n"
         "  const i64 n_items = " << (edges() ? "edges_tot" : "rows") << ";\n"
@@ -1055,6 +1109,8 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "nojoint") cfg.joint = false;
     else if (k == "ywin") cfg.y_window = true;
     else if (k == "oldissue") cfg.old_issue = true;
+    else if (k == "pbulk") cfg.par_bulk = true;
+    else if (k == "nopbulk") cfg.par_bulk = false;
     else if (k == "newissue") cfg.old_issue = false;
     else if (k == "noywin") cfg.y_window = false;
     else if (k == "joint") cfg.joint = true;

@@ -1,5 +1,6 @@
 // tcgen05 kind::tf32 issue-rate microbenchmark: cycles per MMA for
-// M=128 x N x K=8 with A/B in shared memory (SS), K-major, SW128 or SW64.
+// M (128 or 64) x N x K=8 with A/B in shared memory (SS) or A in TMEM, K-major,
+// SW128 or SW64.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 tools/tc_bench.cu -o tools/tc_bench && ./tools/tc_bench
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -20,7 +21,7 @@ DEVI u64 sdesc(u32 saddr, int sw) {  // sw: 128 or 64
   return (u64)((saddr & 0x3FFFFu) >> 4) | ((u64)1 << 16) | ((sbo >> 4) << 32) | ((u64)1 << 46) | (lt << 61);
 }
 
-__global__ void bench(int n, int sw, int iters, long long* out, int a_tmem, int warp_issue, int fast) {
+__global__ void bench(int n, int sw, int iters, long long* out, int a_tmem, int warp_issue, int fast, int mdim) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = (unsigned char*)(((unsigned long long)smem_raw + 1023) & ~1023ull);
   u64* bar = (u64*)(sm + 65536 + 131072);
@@ -37,7 +38,7 @@ __global__ void bench(int n, int sw, int iters, long long* out, int a_tmem, int 
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const u32 tmem = *tslot;
   if (warp_issue ? threadIdx.x < 32 : threadIdx.x == 0) {
-    const u32 idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(n >> 3) << 17) | ((u32)(128 >> 4) << 24);
+    const u32 idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(n >> 3) << 17) | ((u32)(mdim >> 4) << 24);
     const u32 a = smem_addr(sm), b = smem_addr(sm + 65536);
     const int ksteps = sw == 128 ? 4 : 2;
     long long t0 = clock64();
@@ -91,18 +92,18 @@ int main() {
   cudaMallocManaged(&out, 148 * 8);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
   const int iters = 4096;
-  for (int wi = 0; wi < 1; ++wi)
+  for (int mdim : {128, 64})
   for (int at = 0; at < 2; ++at)
     for (int sw : {128})
-      for (int n : {64, 128, 256}) { if (at && n == 256) continue; {
-        bench<<<148, 128, 200000>>>(n, sw, iters, out, at, wi, 1);
-        printf("fast-unrolled "); fflush(stdout);
+      for (int n : {64, 128, 256}) { if (at && (n == 256 || mdim == 64)) continue; {
+        bench<<<148, 128, 200000>>>(n, sw, iters, out, at, 0, 1, mdim);
+        printf("fast-unrolled M=%d ", mdim); fflush(stdout);
         cudaError_t e = cudaDeviceSynchronize();
         long long mx = 0;
         for (int i = 0; i < 148; ++i) mx = out[i] > mx ? out[i] : mx;
         const double cyc = (double)mx / iters;
         printf("%s sw%-3d N=%-3d: %s  %.1f cycles/MMA  -> %.0f MAC/cycle/SM\n", at ? "A=TMEM" : "A=SMEM", sw, n,
-               cudaGetErrorString(e), cyc, 128.0 * n * 8 / cyc);
+               cudaGetErrorString(e), cyc, (double)mdim * n * 8 / cyc);
       } }
   return 0;
 }
