@@ -145,6 +145,10 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   // 13.9 vs 14.6 ms); the FP64 by-neighbour conv stages y as a window (145 vs
   // 155 ms).
   cfg.old_issue = comp == cgf::Comp::Fwd && loop == cgf::Loop::Rows;
+  // The FP32 batched forward issues one cp.async.bulk per contiguous range
+  // (8.65 vs 9.34 ms); every other kernel is faster with lane copies
+  // (profiles/r01_ab_pbulk.log).
+  cfg.par_bulk = comp == cgf::Comp::Fwd && loop == cgf::Loop::Rows && dtype == CGF_F32;
   cfg.y_window = dtype == CGF_F64 && loop == cgf::Loop::ConvByInput;
   cgf::apply_gen_flags(cfg, flags);
   auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_kernel(p->problem, p->units, cfg));
