@@ -341,30 +341,41 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
   o << "extern \"C\" __global__ void __launch_bounds__(256) cgf_uvw_bwd_planes_f32(const float* __restrict__ GZ,"
        " float* __restrict__ YH, float* __restrict__ YL, float* __restrict__ WH, float* __restrict__ WL, i64 rows,"
        " i64 pitch) {\n"
-       "  extern __shared__ float t[];  // [32][DIMZ + 1]\n"
+       "  extern __shared__ float t[];  // [32][DIMZ + 1] (odd pitch: conflict-free column reads)\n"
        "  const i64 chunks = (rows + 31) / 32;\n"
        "  for (i64 cbk = blockIdx.x; cbk < chunks; cbk += gridDim.x) {\n"
        "    const i64 r0 = cbk * 32;\n"
        "    __syncthreads();\n"
-       "    for (int e = threadIdx.x; e < 32 * DIMZ; e += 256) {\n"
-       "      const int rr = e / DIMZ, c = e - rr * DIMZ;\n"
-       "      t[rr * (DIMZ + 1) + c] = r0 + rr < rows ? __ldg(GZ + (r0 + rr) * DIMZ + c) : 0.f;\n    }\n"
+       "    for (int e = threadIdx.x; e < 8 * DIMZ; e += 256) {  // 16-byte loads\n"
+       "      const int rr = e / (DIMZ / 4), c = 4 * (e - rr * (DIMZ / 4));\n"
+       "      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);\n"
+       "      if (r0 + rr < rows) v = __ldg((const float4*)(GZ + (r0 + rr) * DIMZ + c));\n"
+       "      float* d = t + rr * (DIMZ + 1) + c; d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;\n    }\n"
        "    __syncthreads();\n";
   for (size_t si = 0; si < segs.size(); ++si) {
     const auto [zoff, dz] = segs[si];
     const int pl0 = plane_of_seg.at(zoff);
     o << "    // segment " << si << ": z offset " << zoff << ", " << dz << " components, planes " << pl0 << ".."
       << pl0 + dz - 1 << "\n"
-      << "    for (int e = threadIdx.x; e < 32 * 64 * " << dz << "; e += 256) {\n"
-      << "      { const int r = e & 63, rr = (e >> 6) & 31, k = e >> 11;\n"
-      << "        if (r0 + rr < rows) { const float v = t[rr * (DIMZ + 1) + " << zoff << " + r * " << dz
-      << " + k], h = tf32_hi(v);\n"
-      << "          const i64 o = ((i64)(" << pl0 << " + k) * rows + r0 + rr) * 64 + r; __stcs(YH + o, h); __stcs(YL + o, v - h); } }\n"
-      << "      { const int rr = e & 31, r = (e >> 5) & 63, k = e >> 11;\n"
-      << "        if (r0 + rr < rows) { const float v = t[rr * (DIMZ + 1) + " << zoff << " + r * " << dz
-      << " + k], h = tf32_hi(v);\n"
-      << "          const i64 o = ((i64)(" << pl0 << " + k) * 64 + r) * pitch + r0 + rr; __stcs(WH + o, h); __stcs(WL + o, v - h); } }\n"
-      << "    }\n";
+      // gy planes: 4 consecutive r per 16-byte store
+      << "    for (int e = threadIdx.x; e < 32 * 16 * " << dz << "; e += 256) {\n"
+      << "      const int j = e & 15, rr = (e >> 4) & 31, k = e >> 9;\n"
+      << "      if (r0 + rr < rows) {\n"
+      << "        const float* sr = t + rr * (DIMZ + 1) + " << zoff << " + k;\n"
+      << "        float v[4], h[4];\n#pragma unroll\n        for (int a = 0; a < 4; ++a) { v[a] = sr[(4 * j + a) * " << dz
+      << "]; h[a] = tf32_hi(v[a]); }\n"
+      << "        const i64 o = ((i64)(" << pl0 << " + k) * rows + r0 + rr) * 64 + 4 * j;\n"
+      << "        __stcs((float4*)(YH + o), make_float4(h[0], h[1], h[2], h[3]));\n"
+      << "        __stcs((float4*)(YL + o), make_float4(v[0] - h[0], v[1] - h[1], v[2] - h[2], v[3] - h[3]));\n      }\n    }\n"
+      // gW planes: 4 consecutive rows per 16-byte store
+      << "    for (int e = threadIdx.x; e < 8 * 64 * " << dz << "; e += 256) {\n"
+      << "      const int q4 = e & 7, r = (e >> 3) & 63, k = e >> 9;\n"
+      << "      float v[4], h[4];\n#pragma unroll\n      for (int a = 0; a < 4; ++a) { v[a] = t[(4 * q4 + a) * (DIMZ + 1) + "
+      << zoff << " + r * " << dz << " + k]; h[a] = tf32_hi(v[a]); }\n"
+      << "      const i64 o = ((i64)(" << pl0 << " + k) * 64 + r) * pitch + r0 + 4 * q4;\n"
+      << "      if (r0 + 4 * q4 < rows) {\n"
+      << "        __stcs((float4*)(WH + o), make_float4(h[0], h[1], h[2], h[3]));\n"
+      << "        __stcs((float4*)(WL + o), make_float4(v[0] - h[0], v[1] - h[1], v[2] - h[2], v[3] - h[3]));\n      }\n    }\n";
   }
   o << "  }\n}\n\n";
   // per instruction: x once per 16-channel block, then every component k
