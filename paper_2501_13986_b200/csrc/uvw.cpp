@@ -572,9 +572,10 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   constexpr int kRows = 64;                       // batch rows per stage (the MMA's K)
   const int tb = 2 * 64 * kRows * 4;              // hi + lo of a [64][64 rows] K-major tile
   const int xslot = (kRows * kCh * g.max_dx * 4 + 1023) / 1024 * 1024;
-  // x tiles: 4 per (instruction, component) stage, so the ring is deep
-  // enough to keep a stage's worth of TMA loads in flight (ring of 2: 4.4 ms)
-  const int nx = std::getenv("CGF_UVW_GW_NX") ? std::atoi(std::getenv("CGF_UVW_GW_NX")) : 4;
+  // x: the instruction's whole x segment (4 16-channel tiles) is loaded once
+  // per (tile, instruction) and reused by all its components k (loading
+  // per (k, block) moved dz x more x through L2: 4.4 ms per pass)
+  const int nx = 4;  // x tiles per instruction
   const int smem = 1024 + 4 * tb + nx * xslot + 1024;
   if (smem > 227 * 1024) throw UnsupportedError("uvw gW kernel: shared memory too small");
   const std::string kname = "cgf_uvw_bwdw" + S(first) + "_f32";
@@ -608,7 +609,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
       << "    const int gq = " << dx << " * sub + t, L = m * " << dx << " + (gq >> 2), j = gq & 3;\n"
       << "    const float4 v = lds128(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4));\n"
       << "    xv[4 * t] = v.x; xv[4 * t + 1] = v.y; xv[4 * t + 2] = v.z; xv[4 * t + 3] = v.w;\n  }\n"
-      << "  fence_proxy_async();\n  __syncwarp();\n  if ((threadIdx.x & 31) == 0) mbar_arrive(xempty);\n";
+      << "  (void)xempty;\n";
     o << "  float zc[4] = {0.f, 0.f, 0.f, 0.f};\n  switch (k) {\n";
     for (int k = 0; k < dz; ++k) {
       std::map<int, std::string> qk;
@@ -643,15 +644,15 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "  const i64 ntiles = (rows + KR - 1) / KR;\n"
        "  unsigned char* gzt = sm;                 // 2 x gz_k^T tile [r][KR rows] K-major: hi, lo after TB/2\n"
        "  unsigned char* zt = sm + 2 * TB;         // 2 x z'_k^T tile [c][KR rows] K-major\n"
-       "  unsigned char* xs0 = zt + 2 * TB;        // x tile ring of NX (TMA, SW64)\n"
+       "  unsigned char* xs0 = zt + 2 * TB;        // x segment of one instruction: NX tiles (TMA, SW64)\n"
        "  u64* bars = (u64*)(xs0 + NX * XSLOT);\n"
        "  u64* gz_full = bars; u64* gz_empty = bars + 2; u64* z_full = bars + 4; u64* z_empty = bars + 6;\n"
-       "  u64* x_full = bars + 8; u64* x_empty = bars + 8 + NX; u64* done = bars + 8 + 2 * NX;\n"
+       "  u64* x_full = bars + 8; u64* x_empty = bars + 9; u64* done = bars + 10;\n"
        "  u32* tmem_slot = (u32*)(done + 1);\n"
        "  if (threadIdx.x == 0) {\n"
        "    for (int i = 0; i < 2; ++i) {\n"
        "      mbar_init(&gz_full[i], 1); mbar_init(&gz_empty[i], 1); mbar_init(&z_full[i], 8); mbar_init(&z_empty[i], 1);\n    }\n"
-       "    for (int i = 0; i < NX; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n"
+       "    mbar_init(x_full, 1); mbar_init(x_empty, 8);\n"
        "    mbar_init(done, 1);\n    mbar_fence_init();\n  }\n"
        "  if (warp == 8) {\n"
        "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" :: \"r\"(smem_addr(tmem_slot)));\n"
@@ -661,29 +662,30 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "  const u32 tmem = *tmem_slot;\n"
        "  if (warp < 8) {\n"
        "    const int m = 32 * (warp & 1) + lane, sub = warp >> 1;\n"
-       "    u32 ug = 0, gx = 0;\n"
+       "    u32 ug = 0, uq = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
        "      const i64 row = tile * KR + m;\n"
        "      const bool valid = row < rows;\n"
        "      float yv[DIMY];\n"
        "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) yv[j] = valid ? __ldg(Y + row * DIMY + j) : 0.f;\n"
-       "#pragma unroll 1\n      for (int q = Q0; q < Q1; ++q) {\n"
+       "#pragma unroll 1\n      for (int q = Q0; q < Q1; ++q, ++uq) {\n"
        "        const int dz = P_DZ[q];\n"
+       "        mbar_wait_t(x_full, uq & 1u, 23);\n"
        "#pragma unroll 1\n        for (int k = 0; k < dz; ++k, ++ug) {\n"
        "          const u32 zs = ug & 1u;\n"
        "          unsigned char* z = zt + zs * TB;\n"
        "          mbar_wait_t(&z_empty[zs], ((ug >> 1) & 1u) ^ 1u, 21);\n"
-       "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
-       "            const u32 xsl = gx % NX;\n"
-       "            mbar_wait_t(&x_full[xsl], (gx / NX) & 1u, 23);\n"
-       "            const unsigned char* xs = xs0 + xsl * XSLOT;\n"
+       "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb) {\n"
+       "            const unsigned char* xs = xs0 + cb * XSLOT;\n"
        "            switch (q) {\n";
   for (int q = first; q < first + count; ++q)
-    o << "              case " << q << ": zw_" << q << "(k, cb, xs, yv, m, sub, z, &x_empty[xsl]); break;\n";
+    o << "              case " << q << ": zw_" << q << "(k, cb, xs, yv, m, sub, z, x_empty); break;\n";
   o << "            }\n"
        "          }\n"
        "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(&z_full[zs]);\n"
        "        }\n"
+       // the x segment's generic reads are done: release it to the next TMA
+       "        fence_proxy_async();\n        __syncwarp();\n        if (lane == 0) mbar_arrive(x_empty);\n"
        "      }\n"
        "    }\n"
        // this CTA's partial: M=64 accumulators use lanes 0-15 of each 32-lane
@@ -737,18 +739,16 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "  }\n"
        "  else if (warp == 9) {\n"
        "    if (lane == 0) {\n"
-       "      u32 gx = 0;\n"
+       "      u32 uq = 0;\n"
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
-       "        for (int q = Q0; q < Q1; ++q)\n"
-       "          for (int k = 0; k < P_DZ[q]; ++k)\n"
-       "            for (int cb = 0; cb < 4; ++cb, ++gx) {\n"
-       "              const u32 xsl = gx % NX;\n"
-       "              mbar_wait_t(&x_empty[xsl], ((gx / NX) & 1u) ^ 1u, 29);\n"
-       "              const int dx = P_DX[q];\n"
-       "              mbar_expect_tx(&x_full[xsl], KR * 64 * dx);\n"
-       "              const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
-       "              tma_load3(xs0 + xsl * XSLOT, mp, 0, P_XC[q] + cb * dx, (int)(tile * KR), &x_full[xsl]);\n"
-       "            }\n"
+       "        for (int q = Q0; q < Q1; ++q, ++uq) {\n"
+       "          mbar_wait_t(x_empty, (uq & 1u) ^ 1u, 29);\n"
+       "          const int dx = P_DX[q];\n"
+       "          mbar_expect_tx(x_full, 4 * KR * 64 * dx);\n"
+       "          const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
+       "          for (int cb = 0; cb < 4; ++cb)\n"
+       "            tma_load3(xs0 + cb * XSLOT, mp, 0, P_XC[q] + cb * dx, (int)(tile * KR), x_full);\n"
+       "        }\n"
        "    }\n"
        "    __syncwarp();\n"
        "  }\n"
