@@ -150,6 +150,11 @@ DEVI float4 lds128(const unsigned char* p) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_addr(p)));
   return v;
 }
+DEVI float2 lds64(const unsigned char* p) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(smem_addr(p)));
+  return v;
+}
 DEVI void sts128(unsigned char* p, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" :: "r"(smem_addr(p)), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
@@ -569,14 +574,15 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   const GradInfo g = grad_info(p);
   const auto& R = p.resolved;
   if (count < 1 || count > 6 || first < 0 || first + count > g.np) throw std::logic_error("bad gW instruction range");
-  constexpr int kRows = 64;                       // batch rows per stage (the MMA's K)
+  constexpr int kRows = 32;                       // batch rows per stage (the MMA's K)
   const int tb = 2 * 64 * kRows * 4;              // hi + lo of a [64][64 rows] K-major tile
   const int xslot = (kRows * kCh * g.max_dx * 4 + 1023) / 1024 * 1024;
   // x: the instruction's whole x segment (4 16-channel tiles) is loaded once
-  // per (tile, instruction) and reused by all its components k (loading
-  // per (k, block) moved dz x more x through L2: 4.4 ms per pass)
+  // per (tile, instruction) and reused by all its components k, double
+  // buffered so the next instruction's segment lands while this one is used
+  // (single-buffered, the producers spent a third of their time waiting on it)
   const int nx = 4;  // x tiles per instruction
-  const int smem = 1024 + 4 * tb + nx * xslot + 1024;
+  const int smem = 1024 + 4 * tb + 2 * nx * xslot + 1024;
   if (smem > 227 * 1024) throw UnsupportedError("uvw gW kernel: shared memory too small");
   const std::string kname = "cgf_uvw_bwdw" + S(first) + "_f32";
   // gz planes (same numbering as the pre-pass): segment component -> plane
@@ -598,19 +604,20 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   o << "__constant__ int P_PLANE[" << R.size() << "] = {";
   for (size_t q = 0; q < R.size(); ++q) o << (q ? "," : "") << plane_of_seg.at(R[q].z_off);
   o << "};\n";
-  // producer thread (row m < 64, sub < 4) owns channels [4 sub, 4 sub + 4) of
-  // the 16-channel block cb: x read (dx float4), z'_k for its 4 channels
+  // producer thread (row m < 32, sub < 8) owns channels [2 sub, 2 sub + 2) of
+  // the 16-channel block cb: x read (dx float2), z'_k for its 2 channels
   for (int q = first; q < first + count; ++q) {
     const auto& sq = R[q];
     const int dx = sq.dx(), dz = sq.dz();
     o << "DEVI void zw_" << q << "(int k, int cb, const unsigned char* xs, const float* yv, int m, int sub,"
       << " unsigned char* zt, u64* xempty) {\n"
-      << "  float xv[" << 4 * dx << "];\n#pragma unroll\n  for (int t = 0; t < " << dx << "; ++t) {\n"
-      << "    const int gq = " << dx << " * sub + t, L = m * " << dx << " + (gq >> 2), j = gq & 3;\n"
-      << "    const float4 v = lds128(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4));\n"
-      << "    xv[4 * t] = v.x; xv[4 * t + 1] = v.y; xv[4 * t + 2] = v.z; xv[4 * t + 3] = v.w;\n  }\n"
+      << "  float xv[" << 2 * dx << "];\n#pragma unroll\n  for (int t = 0; t < " << dx << "; ++t) {\n"
+      // float2 index f2 = dx * sub + t of the row's 16 dx floats: line f2 / 8, chunk (f2 / 2) & 3, half f2 & 1
+      << "    const int f2 = " << dx << " * sub + t, L = m * " << dx << " + (f2 >> 3), j = (f2 >> 1) & 3;\n"
+      << "    const float2 v = lds64(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4) + 8 * (f2 & 1));\n"
+      << "    xv[2 * t] = v.x; xv[2 * t + 1] = v.y;\n  }\n"
       << "  (void)xempty;\n";
-    o << "  float zc[4] = {0.f, 0.f, 0.f, 0.f};\n  switch (k) {\n";
+    o << "  float zc[2] = {0.f, 0.f};\n  switch (k) {\n";
     for (int k = 0; k < dz; ++k) {
       std::map<int, std::string> qk;
       for (const auto& e : sq.cg->entries) {
@@ -620,13 +627,13 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
       }
       o << "  case " << k << ": {\n";
       for (const auto& [i, ex] : qk) o << "    const float q" << i << " = " << ex << ";\n";
-      o << "#pragma unroll\n    for (int c = 0; c < 4; ++c) {\n";
+      o << "#pragma unroll\n    for (int c = 0; c < 2; ++c) {\n";
       for (const auto& kv : qk) o << "      zc[c] = fmaf(q" << kv.first << ", xv[c * " << dx << " + " << kv.first << "], zc[c]);\n";
       o << "    }\n    break; }\n";
     }
     o << "  }\n"
-      << "#pragma unroll\n  for (int c = 0; c < 4; ++c) {\n"
-      << "    const float h = tf32_hi(zc[c]);\n    const u32 off = kmaj_rows(16 * cb + 4 * sub + c, m);\n"
+      << "#pragma unroll\n  for (int c = 0; c < 2; ++c) {\n"
+      << "    const float h = tf32_hi(zc[c]);\n    const u32 off = kmaj_rows(16 * cb + 2 * sub + c, m);\n"
       << "    sts32(zt + off, h); sts32(zt + TB / 2 + off, zc[c] - h);\n  }\n}\n\n";
   }
   o << "extern \"C\" __global__ void " << kname << "_reduce(const float* __restrict__ part, int nparts, "
@@ -644,15 +651,15 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "  const i64 ntiles = (rows + KR - 1) / KR;\n"
        "  unsigned char* gzt = sm;                 // 2 x gz_k^T tile [r][KR rows] K-major: hi, lo after TB/2\n"
        "  unsigned char* zt = sm + 2 * TB;         // 2 x z'_k^T tile [c][KR rows] K-major\n"
-       "  unsigned char* xs0 = zt + 2 * TB;        // x segment of one instruction: NX tiles (TMA, SW64)\n"
-       "  u64* bars = (u64*)(xs0 + NX * XSLOT);\n"
+       "  unsigned char* xs0 = zt + 2 * TB;        // 2 x segments of one instruction: NX tiles each (TMA, SW64)\n"
+       "  u64* bars = (u64*)(xs0 + 2 * NX * XSLOT);\n"
        "  u64* gz_full = bars; u64* gz_empty = bars + 2; u64* z_full = bars + 4; u64* z_empty = bars + 6;\n"
-       "  u64* x_full = bars + 8; u64* x_empty = bars + 9; u64* done = bars + 10;\n"
+       "  u64* x_full = bars + 8; u64* x_empty = bars + 10; u64* done = bars + 12;\n"
        "  u32* tmem_slot = (u32*)(done + 1);\n"
        "  if (threadIdx.x == 0) {\n"
        "    for (int i = 0; i < 2; ++i) {\n"
        "      mbar_init(&gz_full[i], 1); mbar_init(&gz_empty[i], 1); mbar_init(&z_full[i], 8); mbar_init(&z_empty[i], 1);\n    }\n"
-       "    mbar_init(x_full, 1); mbar_init(x_empty, 8);\n"
+       "    for (int i = 0; i < 2; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n"
        "    mbar_init(done, 1);\n    mbar_fence_init();\n  }\n"
        "  if (warp == 8) {\n"
        "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" :: \"r\"(smem_addr(tmem_slot)));\n"
@@ -661,7 +668,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n"
        "  const u32 tmem = *tmem_slot;\n"
        "  if (warp < 8) {\n"
-       "    const int m = 32 * (warp & 1) + lane, sub = warp >> 1;\n"
+       "    const int m = lane, sub = warp;\n"
        "    u32 ug = 0, uq = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
        "      const i64 row = tile * KR + m;\n"
@@ -670,13 +677,14 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) yv[j] = valid ? __ldg(Y + row * DIMY + j) : 0.f;\n"
        "#pragma unroll 1\n      for (int q = Q0; q < Q1; ++q, ++uq) {\n"
        "        const int dz = P_DZ[q];\n"
-       "        mbar_wait_t(x_full, uq & 1u, 23);\n"
+       "        const u32 xb = uq & 1u;\n"
+       "        mbar_wait_t(&x_full[xb], (uq >> 1) & 1u, 23);\n"
        "#pragma unroll 1\n        for (int k = 0; k < dz; ++k, ++ug) {\n"
        "          const u32 zs = ug & 1u;\n"
        "          unsigned char* z = zt + zs * TB;\n"
        "          mbar_wait_t(&z_empty[zs], ((ug >> 1) & 1u) ^ 1u, 21);\n"
        "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb) {\n"
-       "            const unsigned char* xs = xs0 + cb * XSLOT;\n"
+       "            const unsigned char* xs = xs0 + (xb * NX + cb) * XSLOT;\n"
        "            switch (q) {\n";
   for (int q = first; q < first + count; ++q)
     o << "              case " << q << ": zw_" << q << "(k, cb, xs, yv, m, sub, z, x_empty); break;\n";
@@ -685,7 +693,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(&z_full[zs]);\n"
        "        }\n"
        // the x segment's generic reads are done: release it to the next TMA
-       "        fence_proxy_async();\n        __syncwarp();\n        if (lane == 0) mbar_arrive(x_empty);\n"
+       "        fence_proxy_async();\n        __syncwarp();\n        if (lane == 0) mbar_arrive(&x_empty[xb]);\n"
        "      }\n"
        "    }\n"
        // this CTA's partial: M=64 accumulators use lanes 0-15 of each 32-lane
@@ -742,12 +750,13 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "      u32 uq = 0;\n"
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
        "        for (int q = Q0; q < Q1; ++q, ++uq) {\n"
-       "          mbar_wait_t(x_empty, (uq & 1u) ^ 1u, 29);\n"
+       "          const u32 xb = uq & 1u;\n"
+       "          mbar_wait_t(&x_empty[xb], ((uq >> 1) & 1u) ^ 1u, 29);\n"
        "          const int dx = P_DX[q];\n"
-       "          mbar_expect_tx(x_full, 4 * KR * 64 * dx);\n"
+       "          mbar_expect_tx(&x_full[xb], 4 * KR * 64 * dx);\n"
        "          const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
        "          for (int cb = 0; cb < 4; ++cb)\n"
-       "            tma_load3(xs0 + cb * XSLOT, mp, 0, P_XC[q] + cb * dx, (int)(tile * KR), x_full);\n"
+       "            tma_load3(xs0 + (xb * NX + cb) * XSLOT, mp, 0, P_XC[q] + cb * dx, (int)(tile * KR), &x_full[xb]);\n"
        "        }\n"
        "    }\n"
        "    __syncwarp();\n"
