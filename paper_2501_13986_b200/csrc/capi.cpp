@@ -363,14 +363,15 @@ void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, c
   auto plane_map = [&](CUtensorMap* m, void* base, bool rows_inner) {
     const cuuint64_t gdim_y[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(nplanes)};
     const cuuint64_t gstr_y[2] = {256, static_cast<cuuint64_t>(rows) * 256};
-    const cuuint32_t box_y[3] = {16, 128, 1};
+    const cuuint32_t box_y[3] = {32, 128, 1};
     const cuuint64_t gdim_w[3] = {static_cast<cuuint64_t>(rows), 64, static_cast<cuuint64_t>(nplanes)};
     const cuuint64_t gstr_w[2] = {static_cast<cuuint64_t>(pitch) * 4, static_cast<cuuint64_t>(pitch) * 256};
-    const cuuint32_t box_w[3] = {16, 64, 1};
+    const cuuint32_t box_w[3] = {32, 64, 1};  // 128-byte lines: half the TMA requests of 64-byte ones
     const cuuint32_t estr[3] = {1, 1, 1};
     CU_CHECK(cgf::drv::cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, rows_inner ? gdim_w : gdim_y,
                                               rows_inner ? gstr_w : gstr_y, rows_inner ? box_w : box_y, estr,
-                                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                              CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_128B,
                                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
   };
   // dL/dy

@@ -140,6 +140,10 @@ DEVI void tma_load3(void* dst, const TMap* map, int c0, int c1, int c2, u64* bar
 DEVI u64 sdesc64(u32 saddr) {
   return (u64)((saddr & 0x3FFFFu) >> 4) | ((u64)1 << 16) | ((u64)(512 >> 4) << 32) | ((u64)1 << 46) | ((u64)4 << 61);
 }
+// K-major, 128-byte swizzle (rows of 32 fp32), 8-row groups 1024 B apart.
+DEVI u64 sdesc128(u32 saddr) {
+  return (u64)((saddr & 0x3FFFFu) >> 4) | ((u64)1 << 16) | ((u64)(1024 >> 4) << 32) | ((u64)1 << 46) | ((u64)2 << 61);
+}
 // Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M = 128, N.
 DEVI constexpr u32 idesc_tf32(int n) { return (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(n >> 3) << 17) | ((u32)(128 >> 4) << 24); }
 // tf32 split: hi keeps the top 19 bits (exactly representable), lo the rest.
@@ -465,7 +469,7 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "    }\n"
        "  }\n"
        "  else if (warp == 8) {\n"
-       "    const u64 gzh = sdesc64(smem_addr(gzt)), gzl = gzh + (u64)((GZB / 2) >> 4);\n"
+       "    const u64 gzh = sdesc128(smem_addr(gzt)), gzl = gzh + (u64)((GZB / 2) >> 4);\n"
        "    const u64 wd = sdesc64(smem_addr(ws));\n"
        "    const u32 id_gzp = idesc_tf32(64);\n"
        "    u32 ug = 0, uq = 0;\n"
@@ -481,7 +485,8 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "          const u32 dg = tmem + 64 * k;\n"
        "          if (elect_one()) {\n"
        "#pragma unroll\n            for (int s = 0; s < 8; ++s) {\n"
-       "              const u64 ao = (u64)(((s >> 1) * 8192 + (s & 1) * 32) >> 4);\n"
+       // gz (A): SW128 blocks of 32 r (16 KB: 128 rows x 128 B); W^T (B): SW64 blocks of 16
+       "              const u64 ao = (u64)(((s >> 2) * 16384 + (s & 3) * 32) >> 4);\n"
        "              const u64 bo = (u64)(((s >> 1) * WSLOT + (s & 1) * 32) >> 4);\n"
        "              tc_mma(dg, gzh + ao, wd + bo, id_gzp, s ? 1u : 0u);\n"
        "              tc_mma(dg, gzh + ao, wd + bo + (u64)((64 * 64) >> 4), id_gzp, 1u);\n"
@@ -524,8 +529,8 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "    __syncwarp();\n"
        "  }\n"
        "  else if (warp == 11) {\n"
-       // gz_k tiles from the planes: 4 r-blocks of [128 rows][16] (SW64) for hi
-       // and for lo, the layout the MMA's K-major A descriptor reads
+       // gz_k tiles from the planes: 2 r-blocks of [128 rows][32] (SW128,
+       // 128-byte box lines) for hi and for lo, the MMA's K-major A layout
        "    if (lane == 0) {\n"
        "      u32 ug = 0;\n"
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
@@ -533,9 +538,9 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "          for (int k = 0; k < P_DZ[q]; ++k, ++ug) {\n"
        "            mbar_wait_t(gz_empty, (ug & 1u) ^ 1u, 31);\n"
        "            mbar_expect_tx(gz_full, GZB);\n"
-       "            for (int j = 0; j < 4; ++j) {\n"
-       "              tma_load3(gzt + j * 8192, &tgh, 16 * j, (int)(tile * 128), P_PLANE[q] + k, gz_full);\n"
-       "              tma_load3(gzt + GZB / 2 + j * 8192, &tgl, 16 * j, (int)(tile * 128), P_PLANE[q] + k, gz_full);\n"
+       "            for (int j = 0; j < 2; ++j) {\n"
+       "              tma_load3(gzt + j * 16384, &tgh, 32 * j, (int)(tile * 128), P_PLANE[q] + k, gz_full);\n"
+       "              tma_load3(gzt + GZB / 2 + j * 16384, &tgl, 32 * j, (int)(tile * 128), P_PLANE[q] + k, gz_full);\n"
        "            }\n"
        "          }\n"
        "    }\n"
@@ -605,19 +610,14 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   for (size_t q = 0; q < R.size(); ++q) o << (q ? "," : "") << plane_of_seg.at(R[q].z_off);
   o << "};\n";
   // producer thread (row m < 32, sub < 8) owns channels [2 sub, 2 sub + 2) of
-  // the 16-channel block cb: x read (dx float2), z'_k for its 2 channels
+  // every 16-channel block: per (instruction, component) stage the CG·y
+  // coefficients are formed once, then the 4 blocks' x reads (float2) and
+  // z'_k values for its 2 channels
   for (int q = first; q < first + count; ++q) {
     const auto& sq = R[q];
     const int dx = sq.dx(), dz = sq.dz();
-    o << "DEVI void zw_" << q << "(int k, int cb, const unsigned char* xs, const float* yv, int m, int sub,"
-      << " unsigned char* zt, u64* xempty) {\n"
-      << "  float xv[" << 2 * dx << "];\n#pragma unroll\n  for (int t = 0; t < " << dx << "; ++t) {\n"
-      // float2 index f2 = dx * sub + t of the row's 16 dx floats: line f2 / 8, chunk (f2 / 2) & 3, half f2 & 1
-      << "    const int f2 = " << dx << " * sub + t, L = m * " << dx << " + (f2 >> 3), j = (f2 >> 1) & 3;\n"
-      << "    const float2 v = lds64(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4) + 8 * (f2 & 1));\n"
-      << "    xv[2 * t] = v.x; xv[2 * t + 1] = v.y;\n  }\n"
-      << "  (void)xempty;\n";
-    o << "  float zc[2] = {0.f, 0.f};\n  switch (k) {\n";
+    o << "DEVI void zw_" << q << "(int k, const unsigned char* xs0, const float* yv, int m, int sub, unsigned char* zt) {\n"
+      << "  switch (k) {\n";
     for (int k = 0; k < dz; ++k) {
       std::map<int, std::string> qk;
       for (const auto& e : sq.cg->entries) {
@@ -627,14 +627,19 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
       }
       o << "  case " << k << ": {\n";
       for (const auto& [i, ex] : qk) o << "    const float q" << i << " = " << ex << ";\n";
-      o << "#pragma unroll\n    for (int c = 0; c < 2; ++c) {\n";
-      for (const auto& kv : qk) o << "      zc[c] = fmaf(q" << kv.first << ", xv[c * " << dx << " + " << kv.first << "], zc[c]);\n";
-      o << "    }\n    break; }\n";
+      o << "#pragma unroll\n    for (int cb = 0; cb < 4; ++cb) {\n"
+        << "      const unsigned char* xs = xs0 + cb * XSLOT;\n"
+        << "      float xv[" << 2 * dx << "];\n#pragma unroll\n      for (int t = 0; t < " << dx << "; ++t) {\n"
+        // float2 index f2 = dx * sub + t of the row's 16 dx floats: line f2 / 8, chunk (f2 / 2) & 3, half f2 & 1
+        << "        const int f2 = " << dx << " * sub + t, L = m * " << dx << " + (f2 >> 3), j = (f2 >> 1) & 3;\n"
+        << "        const float2 v = lds64(xs + L * 64 + ((j ^ ((L >> 1) & 3)) << 4) + 8 * (f2 & 1));\n"
+        << "        xv[2 * t] = v.x; xv[2 * t + 1] = v.y;\n      }\n"
+        << "#pragma unroll\n      for (int c = 0; c < 2; ++c) {\n        float zc = 0.f;\n";
+      for (const auto& kv : qk) o << "        zc = fmaf(q" << kv.first << ", xv[c * " << dx << " + " << kv.first << "], zc);\n";
+      o << "        const float h = tf32_hi(zc);\n        const u32 off = kmaj_rows(16 * cb + 2 * sub + c, m);\n"
+        << "        sts32(zt + off, h); sts32(zt + TB / 2 + off, zc - h);\n      }\n    }\n    break; }\n";
     }
-    o << "  }\n"
-      << "#pragma unroll\n  for (int c = 0; c < 2; ++c) {\n"
-      << "    const float h = tf32_hi(zc[c]);\n    const u32 off = kmaj_rows(16 * cb + 2 * sub + c, m);\n"
-      << "    sts32(zt + off, h); sts32(zt + TB / 2 + off, zc[c] - h);\n  }\n}\n\n";
+    o << "  }\n}\n\n";
   }
   o << "extern \"C\" __global__ void " << kname << "_reduce(const float* __restrict__ part, int nparts, "
        "float* __restrict__ gw, int w0, int w1) {\n"
@@ -683,11 +688,11 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "          const u32 zs = ug & 1u;\n"
        "          unsigned char* z = zt + zs * TB;\n"
        "          mbar_wait_t(&z_empty[zs], ((ug >> 1) & 1u) ^ 1u, 21);\n"
-       "#pragma unroll 1\n          for (int cb = 0; cb < 4; ++cb) {\n"
-       "            const unsigned char* xs = xs0 + (xb * NX + cb) * XSLOT;\n"
+       "          {\n"
+       "            const unsigned char* xs = xs0 + (xb * NX) * XSLOT;\n"
        "            switch (q) {\n";
   for (int q = first; q < first + count; ++q)
-    o << "              case " << q << ": zw_" << q << "(k, cb, xs, yv, m, sub, z, x_empty); break;\n";
+    o << "              case " << q << ": zw_" << q << "(k, xs, yv, m, sub, z); break;\n";
   o << "            }\n"
        "          }\n"
        "          fence_proxy_async();\n          __syncwarp();\n          if (lane == 0) mbar_arrive(&z_full[zs]);\n"
@@ -715,7 +720,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "    }\n"
        "  }\n"
        "  else if (warp == 8) {\n"
-       "    const u64 gh0 = sdesc64(smem_addr(gzt)), zh0 = sdesc64(smem_addr(zt));\n"
+       "    const u64 gh0 = sdesc128(smem_addr(gzt)), zh0 = sdesc64(smem_addr(zt));\n"
        "    const u32 id_w = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(64 >> 3) << 17) | ((u32)(64 >> 4) << 24);\n"
        "    u32 ug = 0; i64 lt = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {\n"
@@ -732,10 +737,12 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "            const u32 dw = tmem + 64 * (q - Q0);\n"
        "            const u32 first = (lt == 0 && k == 0) ? 1u : 0u;\n"
        "#pragma unroll\n            for (int s = 0; s < KR / 8; ++s) {\n"
+       // z' (A): SW64 blocks of 16 rows (4 KB); gz (B): SW128 blocks of 32 rows (8 KB)
        "              const u64 o = (u64)(((s >> 1) * 4096 + (s & 1) * 32) >> 4);\n"
-       "              tc_mma(dw, zh + o, gh + o, id_w, (first && s == 0) ? 0u : 1u);\n"
-       "              tc_mma(dw, zh + o, gl + o, id_w, 1u);\n"
-       "              tc_mma(dw, zl + o, gh + o, id_w, 1u);\n"
+       "              const u64 ob = (u64)(((s >> 2) * 8192 + (s & 3) * 32) >> 4);\n"
+       "              tc_mma(dw, zh + o, gh + ob, id_w, (first && s == 0) ? 0u : 1u);\n"
+       "              tc_mma(dw, zh + o, gl + ob, id_w, 1u);\n"
+       "              tc_mma(dw, zl + o, gh + ob, id_w, 1u);\n"
        "            }\n"
        "            tc_commit(&gz_empty[st]);\n            tc_commit(&z_empty[st]);\n"
        "          }\n"
@@ -762,8 +769,9 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "    __syncwarp();\n"
        "  }\n"
        "  else if (warp == 10) {\n"
-       // gz_k^T tiles from the transposed planes: KR / 16 K blocks of
-       // [64 r][16 rows] (SW64), hi and lo: the K-major B layout of the MMA
+       // gz_k^T tiles from the transposed planes: KR / 32 K blocks of
+       // [64 r][32 rows] (SW128, 128-byte box lines), hi and lo: the K-major B
+       // layout of the MMA
        "    if (lane == 0) {\n"
        "      u32 ug = 0;\n"
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
@@ -773,9 +781,9 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "            mbar_wait_t(&gz_empty[st], ((ug >> 1) & 1u) ^ 1u, 31);\n"
        "            mbar_expect_tx(&gz_full[st], TB);\n"
        "            unsigned char* d = gzt + st * TB;\n"
-       "            for (int b = 0; b < KR / 16; ++b) {\n"
-       "              tma_load3(d + b * 4096, &tgh, (int)(tile * KR) + 16 * b, 0, P_PLANE[q] + k, &gz_full[st]);\n"
-       "              tma_load3(d + TB / 2 + b * 4096, &tgl, (int)(tile * KR) + 16 * b, 0, P_PLANE[q] + k, &gz_full[st]);\n"
+       "            for (int b = 0; b < KR / 32; ++b) {\n"
+       "              tma_load3(d + b * 8192, &tgh, (int)(tile * KR) + 32 * b, 0, P_PLANE[q] + k, &gz_full[st]);\n"
+       "              tma_load3(d + TB / 2 + b * 8192, &tgl, (int)(tile * KR) + 32 * b, 0, P_PLANE[q] + k, &gz_full[st]);\n"
        "            }\n"
        "          }\n"
        "    }\n"

@@ -48,7 +48,7 @@ __global__ void bench(int n, int sw, int iters, long long* out, int a_tmem, int 
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
           asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}"
-                       :: "r"(0u), "l"(ad0 + 2 * ks), "l"(bd0 + 2 * ks), "r"(idesc), "r"(1u) : "memory");
+                       :: "r"(0u), "l"(ad0 + (sw == 128 ? 2 * ks : 2 * (ks & 1) + 256 * (ks >> 1))), "l"(bd0 + (sw == 128 ? 2 * ks : 2 * (ks & 1) + 256 * (ks >> 1))), "r"(idesc), "r"(1u) : "memory");
       }
     }
     if (fast && a_tmem) {  // A from TMEM columns 384.., D rotating over 4 column blocks
@@ -94,7 +94,7 @@ int main() {
   const int iters = 4096;
   for (int mdim : {128, 64})
   for (int at = 0; at < 2; ++at)
-    for (int sw : {128})
+    for (int sw : {128, 64})
       for (int n : {64, 128, 256}) { if (at && (n == 256 || mdim == 64)) continue; {
         bench<<<148, 128, 200000>>>(n, sw, iters, out, at, 0, 1, mdim);
         printf("fast-unrolled M=%d ", mdim); fflush(stdout);
