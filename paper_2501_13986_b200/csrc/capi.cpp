@@ -429,6 +429,14 @@ void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, c
   }
 }
 
+// Batched double-backward as two kernels (CGF_DBWD_SPLIT=1 / 0 overrides).
+bool dbwd_split(int dtype) {
+  const char* env = std::getenv("CGF_DBWD_SPLIT");
+  if (env) return env[0] == '1';
+  (void)dtype;
+  return false;
+}
+
 void launch(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, const void* x,
             const void* y, const void* w, const void* gz, const void* da, const void* db,
             const void* dc, void* o0, void* o1, void* o2, void* o3, void* stream) {
@@ -452,6 +460,12 @@ void launch(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, con
       run_uvw(p, "bwdx", gz, pr.dim_z, y, w, o0, rows, stream);
       run_uvw_grad_yw(p, x, y, w, gz, o1, o2, rows, stream);
     }
+    return;
+  }
+  if (op == CGF_OP_DOUBLE_BACKWARD && dbwd_split(dtype)) {
+    // two passes over the rows: dL/dgz, then (dL/dx, dL/dy, dL/dW)
+    run_kernel(p, cgf::Comp::DBwdZ, cgf::Loop::Rows, dtype, w_shared, a, stream);
+    run_kernel(p, cgf::Comp::DBwdX, cgf::Loop::Rows, dtype, w_shared, a, stream);
     return;
   }
   run_kernel(p, static_cast<cgf::Comp>(op), cgf::Loop::Rows, dtype, w_shared, a, stream);

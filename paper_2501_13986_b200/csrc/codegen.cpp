@@ -1009,8 +1009,8 @@ KernelSource Gen::run() {
     throw UnsupportedError("ConvByOutput computes z-type outputs only");
   if (cfg_.loop == Loop::ConvByInput && !(cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwdX))
     throw UnsupportedError("ConvByInput computes x-type outputs only");
-  if (!conv() && (cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX))
-    throw UnsupportedError("split double-backward passes are conv-only");
+  // (the split double-backward passes also run on batched rows: two smaller
+  // kernels instead of one that overflows the instruction cache)
   if (edges() && (cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX))
     throw UnsupportedError("the atomic edge-list conv runs the double-backward in one pass");
   classify();
