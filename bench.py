@@ -283,9 +283,24 @@ def c3_leg(args, rank, world, dev):
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
+    # backward on the same rows: gx (transposed forward), gz planes, gy, shared gW (+ its reduction)
+    gz = torch.randn((R, plan.dim_z), device=dev, generator=g)
+    outs = plan.backward(x, y, w, gz, w_shared=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(steps):
+        outs = plan.backward(x, y, w, gz, w_shared=True, out=outs)
+    b.record(stream)
+    torch.cuda.synchronize()
+    bms = torch.tensor([a.elapsed_time(b) / steps], device=dev)
+    if world > 1:
+        dist.all_reduce(bms, op=dist.ReduceOp.MAX)
+    bms = float(bms.item())
+    del outs, gz
     byts = (plan.dim_x + plan.dim_y + plan.dim_z) * 4 * R + plan.n_w * 4
     peak, _ = measured_peak()
-    return {"workload": "c3: 64x0e+64x1o+64x2e x 0e+1o+2e -> 64x0e+64x1o+64x2e, 11 uvw paths, shared W, fwd",
+    return {"workload": "c3: 64x0e+64x1o+64x2e x 0e+1o+2e -> 64x0e+64x1o+64x2e, 11 uvw paths, shared W, fwd (+ bwd)",
+            "backward_ms": bms, "backward_GFLOP/s": plan.flops_bwd * R * world / (bms / 1e3) / 1e9,
             "kernel": "cgf_uvw_fwd_f32 (tcgen05 kind::tf32, 3xTF32, A in TMEM)", "rows_per_gpu": R,
             "ms": ms, "rows_per_s": R * world / (ms / 1e3), "GFLOP/s": plan.flops_fwd * R * world / (ms / 1e3) / 1e9,
             "GB/s": byts / (ms / 1e3) / 1e9, "hbm_frac": byts / (ms / 1e3) / 1e9 / peak, "dtype": "f32"}
