@@ -219,3 +219,22 @@ def test_c3_shared_w_tensor_core_backward(rows):
     check(host(gx), wx, np.float32, "c3 gx")
     check(host(gy), wy, np.float32, "c3 gy")
     check(host(gw).reshape(ww.shape), ww, np.float32, "c3 shared gW")
+
+
+# A wider sweep of the reference's random-problem generator (tests/helpers.hpp:29-109):
+# 20 more seeds, ragged batch sizes (1 row, a partial warp, several grid waves).
+WIDE = [(s, (1, 7, 131, 1000)[s % 4]) for s in range(11, 31)]
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f32", "f64"])
+@pytest.mark.parametrize("seed,rows", WIDE, ids=[f"rand{s}_r{r}" for s, r in WIDE])
+def test_random_problem_sweep(seed, rows, dt):
+    js = random_problem(seed)
+    o, plan = O.Oracle(js), P().TpPlan(js)
+    x, y, w, gz, da, db, dc = inputs(o, rows, dt, seed=seed)
+    check(host(plan.forward(dev(x), dev(y), dev(w))), o.forward(x, y, w), dt, f"{js} forward")
+    for g, r, n in zip(plan.backward(dev(x), dev(y), dev(w), dev(gz)), o.backward(x, y, w, gz), ("gx", "gy", "gw")):
+        check(host(g), r, dt, n)
+    outs = plan.double_backward(dev(x), dev(y), dev(w), dev(gz), (dev(da), dev(db), dev(dc)))
+    for g, r, n in zip(outs, o.double_backward(x, y, w, gz, da, db, dc), ("dx", "dy", "dw", "dgz")):
+        check(host(g), r, dt, n)
