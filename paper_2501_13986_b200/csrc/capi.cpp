@@ -150,6 +150,20 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   // (profiles/r01_ab_pbulk.log).
   cfg.par_bulk = comp == cgf::Comp::Fwd && loop == cgf::Loop::Rows && dtype == CGF_F32;
   cfg.y_window = dtype == CGF_F64 && loop == cgf::Loop::ConvByInput;
+  // Small problems (the whole output row fits a warp's registers: <= 64 words
+  // per lane) stage every unit as ONE item per row / edge. Measured
+  // (profiles/r01_ab_mergeall.log): C5 conv forward 25.2 -> 13.9 ms FP32,
+  // 32.1 -> 24.4 ms FP64; C1 forward / FP32 backward -4 / -6 %; the FP64
+  // backward is slower (register pressure), so it keeps per-unit items.
+  {
+    std::uint32_t zw = 0, xw = 0;
+    for (const auto& u : p->units) {
+      for (const auto& z : u.z_pieces) zw += (z.words + 31) / 32;
+      for (const auto& x : u.x_chunks) xw += (x.words + 31) / 32;
+    }
+    const bool small = zw <= 64 && xw <= 32;
+    cfg.merge_all = small && (comp == cgf::Comp::Fwd || (comp == cgf::Comp::Bwd && dtype == CGF_F32));
+  }
   cgf::apply_gen_flags(cfg, flags);
   auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_kernel(p->problem, p->units, cfg));
   p->sources.emplace(key, ks);

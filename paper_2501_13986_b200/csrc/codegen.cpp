@@ -1110,6 +1110,8 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "ywin") cfg.y_window = true;
     else if (k == "oldissue") cfg.old_issue = true;
     else if (k == "pbulk") cfg.par_bulk = true;
+    else if (k == "mergeall") cfg.merge_all = true;
+    else if (k == "nomergeall") cfg.merge_all = false;
     else if (k == "nopbulk") cfg.par_bulk = false;
     else if (k == "newissue") cfg.old_issue = false;
     else if (k == "noywin") cfg.y_window = false;
@@ -1152,8 +1154,20 @@ std::vector<Unit> merge_units(const Problem& p, const std::vector<Unit>& units, 
 }
 }  // namespace
 
+// All units as one (one staged item per row / edge): for problems whose whole
+// output row fits a warp's registers (merge_all).
+std::vector<Unit> fuse_units(const std::vector<Unit>& units) {
+  Unit u;
+  for (const auto& v : units) {
+    u.subs.insert(u.subs.end(), v.subs.begin(), v.subs.end());
+    u.x_chunks.insert(u.x_chunks.end(), v.x_chunks.begin(), v.x_chunks.end());
+    u.z_pieces.insert(u.z_pieces.end(), v.z_pieces.begin(), v.z_pieces.end());
+  }
+  return {u};
+}
+
 KernelSource generate_kernel(const Problem& p, const std::vector<Unit>& units, const KernelConfig& cfg) {
-  const std::vector<Unit> merged = merge_units(p, units, cfg.merge);
+  const std::vector<Unit> merged = cfg.merge_all ? fuse_units(units) : merge_units(p, units, cfg.merge);
   Gen g(p, merged, cfg);
   return g.run();
 }

@@ -57,6 +57,7 @@ struct KernelConfig {
   int merge = 1;            // chunks (same-shape units) per staged item and code body
   bool joint = false;       // emit a merged unit's chunks side by side (shared v*y[j] products); measured
                             // neutral on the TP, +15 % on the C4 conv forward (profiles/r01_ab_joint.log)
+  bool merge_all = false;   // every unit in one staged item (small problems: the whole row in registers)
   bool par_bulk = false;    // lane copy: one cp.async.bulk per contiguous range, one lane each
   bool old_issue = false;   // A/B: per-range 64-bit source addresses in issue_unit
   bool y_window = false;    // stage y as a 16-byte window even when its rows are aligned (A/B)
