@@ -162,7 +162,10 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
       for (const auto& x : u.x_chunks) xw += (x.words + 31) / 32;
     }
     const bool small = zw <= 64 && xw <= 32;
-    cfg.merge_all = small && (comp == cgf::Comp::Fwd || (comp == cgf::Comp::Bwd && dtype == CGF_F32));
+    // the FP32 conv double-backward passes too: 143.9 -> 133.6 ms on C5
+    // (profiles/r01_ab_mergeall2.log; the batched and atomic ones are not faster)
+    const bool conv_dbwd = (comp == cgf::Comp::DBwdZ || comp == cgf::Comp::DBwdX) && dtype == CGF_F32;
+    cfg.merge_all = small && (comp == cgf::Comp::Fwd || (comp == cgf::Comp::Bwd && dtype == CGF_F32) || conv_dbwd);
   }
   cgf::apply_gen_flags(cfg, flags);
   auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_kernel(p->problem, p->units, cfg));
