@@ -166,6 +166,10 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
     // (profiles/r01_ab_mergeall2.log; the batched and atomic ones are not faster)
     const bool conv_dbwd = (comp == cgf::Comp::DBwdZ || comp == cgf::Comp::DBwdX) && dtype == CGF_F32;
     cfg.merge_all = small && (comp == cgf::Comp::Fwd || (comp == cgf::Comp::Bwd && dtype == CGF_F32) || conv_dbwd);
+    // small problems' conv kernels also issue one cp.async.bulk per contiguous
+    // range (C5: FP32 bwd 44.8 -> 40.5 ms, FP64 fwd 24.7 -> 21.9, FP64 bwd 140.8 -> 130.3;
+    // profiles/r01_ab_pbulk_small.log); for the C2 TP's conv they are slower
+    if (small && (loop == cgf::Loop::ConvByOutput || loop == cgf::Loop::ConvByInput)) cfg.par_bulk = true;
   }
   cgf::apply_gen_flags(cfg, flags);
   auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_kernel(p->problem, p->units, cfg));
