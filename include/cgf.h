@@ -121,11 +121,37 @@ int cgf_tp_double_backward_host(cgf_plan* plan, int dtype, const void* x, const 
                                 const void* dc, void* ox, void* oy, void* ow, void* ogz,
                                 int64_t rows, int w_shared);
 
-/* Model-based traffic/flop counters of one call (engine::ExecStats,
- * engine.hpp:19-30): {loads_words, stores_words, flops} for `rows` rows of
- * `op` under the compulsory-traffic model (each input read once, each output
- * written once). */
+/* The counters the reference's TpPlan returns (engine::ExecStats,
+ * engine.hpp:19-30) for `rows` rows of `op`: {loads_words, stores_words,
+ * flops} of the reference's per-row schedule model (the plan's budget),
+ * computed here (scheduler.cpp:139-404, engine.cpp:115-168):
+ *   forward          = traffic_report x rows (test_engine.cpp:350-363);
+ *   backward         = phases' loaded x/y/w + staged g_z words, no stores,
+ *                      backward flops, x rows (engine_impl.hpp:143-181);
+ *   double_backward  = 3 forward + 4 backward rows (engine.cpp:350-391).
+ * w_shared is accepted for symmetry and does not change the model. */
 int cgf_tp_stats(const cgf_plan* plan, int op, int64_t rows, int w_shared, uint64_t stats[3]);
+/* The GPU kernels' compulsory traffic of one call in words: {loads, stores},
+ * each input read once and each output written once (the
+ * roofline's algorithmic bytes = words x sizeof(T)). */
+int cgf_tp_traffic(const cgf_plan* plan, int op, int64_t rows, int w_shared, uint64_t words[2]);
+/* scheduler::schedule_to_json (scheduler.cpp:406-445) of the plan's schedule
+ * model: same document, byte for byte. Returns the length (copies up to cap-1
+ * bytes + NUL). */
+int cgf_plan_schedule_json(const cgf_plan* plan, char* buf, int cap);
+/* kernelgen::emit_text(gen_forward / gen_backward) of split subkernel `pos`
+ * in schedule order (kernelgen.cpp:305-360): the op stream whose CG
+ * coefficients the generated kernels carry as immediates. Returns the length. */
+int cgf_plan_listing(const cgf_plan* plan, int pos, int backward, char* buf, int cap);
+
+/* ConvStats (conv.hpp:78-91) of one conv call under the GPU kernels' store /
+ * load model: op CGF_OP_FORWARD / CGF_OP_BACKWARD, mode CGF_CONV_* (fused),
+ * or unfused != 0 for the gather -> TP -> scatter comparator. stats =
+ * {loads_words, stores_words, output_store_ops, flops}. The fused
+ * deterministic conv writes each output row once (output_store_ops = nodes);
+ * atomic mode reduces once per edge; the unfused path stores one row per edge. */
+int cgf_conv_stats(const cgf_plan* plan, int op, int mode, int unfused, int64_t nodes, int64_t edges,
+                   uint64_t stats[4]);
 
 /* ---- kernel introspection ------------------------------------------------ */
 

@@ -497,6 +497,7 @@ def ref_lib():
         L.cgr_plan_info.argtypes = [P, P, P]
         L.cgr_plan_split.argtypes = [P, P, C.c_int]
         L.cgr_emit_text.argtypes = [P, C.c_int, C.c_int, C.c_char_p, C.c_int]
+        L.cgr_schedule_json.argtypes = [P, C.c_char_p, C.c_int]
         L.cgr_cg_block.argtypes = [C.c_int] * 4 + [P] * 4
         L.cgr_rng_new.restype = P
         L.cgr_rng_new.argtypes = [C.c_uint64]
@@ -554,6 +555,11 @@ class RefPlan:
         ref_lib().cgr_emit_text(self.h, pos, int(backward), buf, 1 << 20)
         return buf.value.decode()
 
+    def schedule_json(self) -> str:
+        buf = C.create_string_buffer(1 << 22)
+        ref_lib().cgr_schedule_json(self.h, buf, 1 << 22)
+        return buf.value.decode()
+
     def _chk(self, rc):
         if rc != 0:
             raise RuntimeError(ref_lib().cgr_last_error().decode())
@@ -589,6 +595,7 @@ class RefPlan:
         self._chk(getattr(ref_lib(), f"cgr_tp_double_backward_{self._suf(x)}")(
             self.h, rows, _ptr(x), _ptr(y), _ptr(w), _ptr(gz), _ptr(da), _ptr(db), _ptr(dc),
             _ptr(ox), _ptr(oy), _ptr(ow), _ptr(ogz), int(seven_call), workers, _ptr(st)))
+        self.last_stats = tuple(int(v) for v in st)
         return ox, oy, ow, ogz
 
     def conv_forward(self, g: Graph, node_x, edge_y, edge_w, atomic=False, workers=0, chunks=16,

@@ -411,6 +411,16 @@ int cgr_emit_text(void* h, int pos, int backward, char* buf, int cap) {
   return static_cast<int>(t.size());
 }
 
+// scheduler::schedule_to_json of the plan's schedule (scheduler.cpp:406-445).
+int cgr_schedule_json(void* h, char* buf, int cap) {
+  auto* rp = static_cast<RefPlan*>(h);
+  const std::string t = scheduler::schedule_to_json(rp->split, rp->sched);
+  const int n = std::min<int>(cap - 1, static_cast<int>(t.size()));
+  std::memcpy(buf, t.data(), n);
+  buf[n] = 0;
+  return static_cast<int>(t.size());
+}
+
 int cgr_cg_block(int l1, int l2, int l3, int cap, int* i, int* j, int* k, double* v) {
   try {
     const auto b = cg::cg_block(l1, l2, l3);

@@ -80,6 +80,8 @@ class InternalError(CgfError):
     code = 10
 
 
+from . import configs  # noqa: E402  (benchmark problem JSONs)
+
 _ERRORS = {c.code: c for c in (ParseError, ValidationError, ShapeError, BudgetError, TriangleError,
                                InvalidArgument, CudaError, JitError, UnsupportedError, InternalError)}
 
@@ -112,6 +114,10 @@ def lib():
     L.cgf_tp_backward_host.argtypes = [P, I] + [P] * 7 + [I64, I]
     L.cgf_tp_double_backward_host.argtypes = [P, I] + [P] * 11 + [I64, I]
     L.cgf_tp_stats.argtypes = [P, I, I64, I, P]
+    L.cgf_tp_traffic.argtypes = [P, I, I64, I, P]
+    L.cgf_plan_schedule_json.argtypes = [P, C.c_char_p, I]
+    L.cgf_plan_listing.argtypes = [P, I, I, C.c_char_p, I]
+    L.cgf_conv_stats.argtypes = [P, I, I, I, I64, I64, P]
     L.cgf_plan_kernel_source.argtypes = [P, I, I, I, I, I, C.c_char_p, I]
     L.cgf_plan_kernel_compile.argtypes = [P, I, I, I, I, I]
     L.cgf_conv_transpose_host.argtypes = [I64, I64, P, P, P, P, P]
@@ -214,9 +220,34 @@ class TpPlan:
         _check(lib().cgf_plan_compile(self._h, op, dtype, int(w_shared), int(aligned)))
 
     def stats(self, op, rows, w_shared=False):
+        """engine::ExecStats of a call: (loads_words, stores_words, flops) of
+        the reference's per-row schedule model x rows (engine.hpp:19-30)."""
         s = np.zeros(3, np.uint64)
         _check(lib().cgf_tp_stats(self._h, op, rows, int(w_shared), s.ctypes.data))
         return tuple(int(v) for v in s)
+
+    def traffic(self, op, rows, w_shared=False):
+        """Compulsory (loads, stores) words of the GPU kernels for one call."""
+        s = np.zeros(2, np.uint64)
+        _check(lib().cgf_tp_traffic(self._h, op, rows, int(w_shared), s.ctypes.data))
+        return tuple(int(v) for v in s)
+
+    @staticmethod
+    def _text(fn, *args) -> str:
+        n = fn(*args, None, 0)
+        if n < 0:
+            _check(-n)
+        buf = C.create_string_buffer(n + 1)
+        fn(*args, buf, n + 1)
+        return buf.value.decode()
+
+    def schedule_json(self) -> str:
+        """scheduler::schedule_to_json of this plan's schedule (scheduler.cpp:406-445)."""
+        return self._text(lib().cgf_plan_schedule_json, self._h)
+
+    def listing(self, pos: int, backward: bool = False) -> str:
+        """kernelgen::emit_text of split subkernel ``pos`` (schedule order)."""
+        return self._text(lib().cgf_plan_listing, self._h, pos, int(backward))
 
     # -- shape checks (engine.cpp:206-220) ----------------------------------
     def _rows(self, x, y, w, w_shared):
@@ -239,6 +270,14 @@ class TpPlan:
                 raise ShapeError("torch tensors must be CUDA tensors on one device")
             if _is_torch(a) and not a.is_contiguous():
                 raise ShapeError("tensors must be contiguous")
+
+    @staticmethod
+    def _out(name, a, shape):
+        """A caller-provided output: exact shape, dense (written as [rows, dim])."""
+        if tuple(a.shape) != tuple(shape):
+            raise ShapeError(f"shape mismatch for {name}: expected {tuple(shape)}, got {tuple(a.shape)}")
+        if not _is_torch(a) and not (a.flags.c_contiguous and a.flags.writeable):
+            raise ShapeError(f"{name} must be a writeable C-contiguous array")
 
     @staticmethod
     def _stream(ref):
@@ -269,6 +308,7 @@ class TpPlan:
         rows = self._rows(x, y, w, w_shared)
         if z is None:
             z = self._empty_like(x, (rows, self.dim_z))
+        self._out("z", z, (rows, self.dim_z))
         self._same(x, z)
         dt = _dtype_code(x)
         if _is_torch(x):
@@ -292,8 +332,7 @@ class TpPlan:
             gx, gy, gw = out
             for name, a, shp in (("gx", gx, (rows, self.dim_x)), ("gy", gy, (rows, self.dim_y)),
                                  ("gw", gw, (1 if w_shared else rows, self.n_w))):
-                if tuple(a.shape) != shp:
-                    raise ShapeError(f"shape mismatch for {name}: expected {shp}, got {tuple(a.shape)}")
+                self._out(name, a, shp)
             self._same(x, gx, gy, gw)
         else:
             gx = self._empty_like(x, (rows, self.dim_x))
@@ -511,6 +550,13 @@ class ConvPlan:
         if not _is_torch(node_x):
             raise ShapeError("conv: pass torch CUDA tensors")
 
+    def stats(self, op, g, mode=DETERMINISTIC, unfused=False):
+        """ConvStats (conv.hpp:78-91) of one call: (loads_words, stores_words,
+        output_store_ops, flops) under the GPU kernels' store / load model."""
+        s = np.zeros(4, np.uint64)
+        _check(lib().cgf_conv_stats(self.plan._h, op, mode, int(unfused), g.nodes, g.edges, s.ctypes.data))
+        return tuple(int(v) for v in s)
+
     def forward(self, g: Graph, node_x, edge_y, edge_w, mode=DETERMINISTIC):
         """node_z[s] = sum over edges (s, d) of TP(node_x[d], edge_y[e], edge_w[e])."""
         self._check_shapes(g, node_x, edge_y, edge_w)
@@ -623,10 +669,26 @@ class ConvPlan:
         d = sh.device(ref.device)
         return {k: C.c_void_p(v.data_ptr()) for k, v in d.items()}
 
+    def _check_shard(self, sh, **arrays):
+        """Shapes of a shard call's arrays (the checks ConvPlan._check_shapes
+        makes for a whole graph, over the shard's row counts)."""
+        p = self.plan
+        rows = {"node_x_all": (sh.in_nodes, p.dim_x), "d_gx_all": (sh.in_nodes, p.dim_x),
+                "edge_y": (sh.edges, p.dim_y), "d_gy": (sh.edges, p.dim_y),
+                "edge_w": (sh.edges, p.n_w), "d_gw": (sh.edges, p.n_w),
+                "g_node_z": (sh.out_nodes, p.dim_z)}
+        for name, a in arrays.items():
+            if tuple(a.shape) != rows[name]:
+                raise ShapeError(f"conv shard: {name} shape mismatch: expected {rows[name]}, got {tuple(a.shape)}")
+        ref = next(iter(arrays.values()))
+        TpPlan._same(ref, *arrays.values())
+        if not _is_torch(ref):
+            raise ShapeError("conv: pass torch CUDA tensors")
+
     def forward_shard(self, sh, node_x_all, edge_y, edge_w, mode=DETERMINISTIC):
         """Local output rows of the conv; node_x_all spans sh.in_nodes rows."""
         p = self.plan
-        TpPlan._same(node_x_all, edge_y, edge_w)
+        self._check_shard(sh, node_x_all=node_x_all, edge_y=edge_y, edge_w=edge_w)
         z = TpPlan._empty_like(node_x_all, (sh.out_nodes, p.dim_z))
         d = self._shard_ptrs(sh, node_x_all)
         _check(lib().cgf_conv_forward_shard(p._h, _dtype_code(node_x_all), sh.out_nodes, sh.in_nodes, sh.edges,
@@ -637,7 +699,7 @@ class ConvPlan:
     def backward_shard(self, sh, node_x_all, edge_y, edge_w, g_node_z, mode=DETERMINISTIC):
         """(partial g_node_x over sh.in_nodes rows, g_edge_y, g_edge_w)."""
         p = self.plan
-        TpPlan._same(node_x_all, edge_y, edge_w, g_node_z)
+        self._check_shard(sh, node_x_all=node_x_all, edge_y=edge_y, edge_w=edge_w, g_node_z=g_node_z)
         gx = TpPlan._empty_like(node_x_all, (sh.in_nodes, p.dim_x))
         gy = TpPlan._empty_like(node_x_all, (sh.edges, p.dim_y))
         gw = TpPlan._empty_like(node_x_all, (sh.edges, p.n_w))
@@ -653,7 +715,8 @@ class ConvPlan:
                               mode=DETERMINISTIC):
         """(partial dL/dnode_x over sh.in_nodes rows, dL/dedge_y, dL/dedge_w, dL/dg_node_z local)."""
         p = self.plan
-        TpPlan._same(node_x_all, edge_y, edge_w, g_node_z, d_gx_all, d_gy, d_gw)
+        self._check_shard(sh, node_x_all=node_x_all, edge_y=edge_y, edge_w=edge_w, g_node_z=g_node_z,
+                          d_gx_all=d_gx_all, d_gy=d_gy, d_gw=d_gw)
         ox = TpPlan._empty_like(node_x_all, (sh.in_nodes, p.dim_x))
         oy = TpPlan._empty_like(node_x_all, (sh.edges, p.dim_y))
         ow = TpPlan._empty_like(node_x_all, (sh.edges, p.n_w))

@@ -21,19 +21,25 @@
 #include "problem.hpp"
 #include "graph_ops.hpp"
 #include "uvw.hpp"
+#include "schedule.hpp"
 
 struct cgf_plan {
   cgf::Problem problem;
   std::vector<cgf::Unit> units;
   std::uint32_t budget = 4096;
+  cgf::ScheduleModel sched;  // the reference's per-row schedule model (counters, dumps)
   bool z_covered = true, x_covered = true;
   std::mutex mu;
   std::map<std::tuple<int, int, int, int, int, std::string>, std::shared_ptr<cgf::KernelSource>> sources;
   // uvw tensor-core path (all-C problems, shared W): generated source and the
-  // per-context device buffer of swizzled tf32 W images.
+  // device scratch (swizzled tf32 W images, gz planes, gW partials) keyed by
+  // (context, stream, buffer): each call re-images W into its stream's own
+  // buffers, so calls on different streams never share scratch, and calls on
+  // one stream are ordered by the stream.
   std::map<std::string, std::shared_ptr<cgf::UvwSource>> uvw;  // by kernel tag
-  std::map<std::pair<CUcontext, std::string>, CUdeviceptr> wimg;
-  std::map<std::pair<CUcontext, std::string>, std::size_t> scratch_cap;  // bytes of grown scratch buffers in wimg
+  using ScratchKey = std::tuple<CUcontext, CUstream, std::string>;
+  std::map<ScratchKey, CUdeviceptr> wimg;
+  std::map<ScratchKey, std::size_t> scratch_cap;  // bytes of each buffer in wimg
   // host-pointer path: two streams + double-buffered device staging per context
   struct HostPipe {
     CUstream s[2] = {nullptr, nullptr};
@@ -42,11 +48,12 @@ struct cgf_plan {
   };
   std::map<CUcontext, HostPipe> pipes;
   std::mutex host_mu;
+  int uvw_bwd_ok = -1;  // uvw backward kernels generate for this problem (-1: not yet known)
   ~cgf_plan() {
     CUcontext cur = nullptr;
     if (cgf::drv::cuCtxGetCurrent) cgf::drv::cuCtxGetCurrent(&cur);
     for (auto& [key, ptr] : wimg)
-      if (cur == key.first) cgf::drv::cuMemFree(ptr);
+      if (cur == std::get<0>(key)) cgf::drv::cuMemFree(ptr);
     for (auto& [ctx, pp] : pipes)
       if (cur == ctx) {
         for (int k = 0; k < 2; ++k) {
@@ -61,9 +68,7 @@ namespace {
 
 thread_local std::string g_err;
 
-struct BudgetError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
+using cgf::BudgetError;
 
 template <typename F>
 int guarded(F&& f) {
@@ -177,11 +182,34 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   return ks;
 }
 
+std::shared_ptr<cgf::UvwSource> uvw_source(cgf_plan* p, const std::string& tag);
+
+// The backward's gy / gW kernels need more than the forward (multiplicities
+// 64, l3 <= 3, their shared-memory plans): eligible when they generate.
+bool uvw_backward_ok(cgf_plan* p) {
+  {
+    std::lock_guard<std::mutex> g(p->mu);
+    if (p->uvw_bwd_ok >= 0) return p->uvw_bwd_ok == 1;
+  }
+  bool ok = true;
+  try {
+    uvw_source(p, "bwdx");
+    uvw_source(p, "bwdy");
+    for (std::size_t f = 0; f < p->problem.resolved.size(); f += 6) uvw_source(p, "bwdw" + std::to_string(f));
+  } catch (const cgf::UnsupportedError&) {
+    ok = false;
+  }
+  std::lock_guard<std::mutex> g(p->mu);
+  p->uvw_bwd_ok = ok ? 1 : 0;
+  return ok;
+}
+
 bool use_uvw(cgf_plan* p, int op, int dtype, int w_shared) {
   if ((op != CGF_OP_FORWARD && op != CGF_OP_BACKWARD) || dtype != CGF_F32 || !w_shared) return false;
   const char* env = std::getenv("CGF_UVW");
   if (env && env[0] == '0') return false;
-  return cgf::uvw_eligible(p->problem);
+  if (!cgf::uvw_eligible(p->problem)) return false;
+  return op == CGF_OP_FORWARD || uvw_backward_ok(p);
 }
 
 std::shared_ptr<cgf::UvwSource> uvw_source(cgf_plan* p, const std::string& tag) {
@@ -238,6 +266,28 @@ void run_kernel(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype, int w_sh
                                     reinterpret_cast<CUstream>(stream), args, nullptr));
 }
 
+// The plan's uvw scratch buffer `name` for (current context, stream), at
+// least `bytes` long. Grown buffers are freed only after the stream drained
+// (its earlier kernels may still read the old one).
+CUdeviceptr uvw_scratch(cgf_plan* p, CUstream st, const std::string& name, std::size_t bytes) {
+  CUcontext ctx = cgf::ensure_context();
+  std::lock_guard<std::mutex> g(p->mu);
+  const cgf_plan::ScratchKey key{ctx, st, name};
+  auto it = p->wimg.find(key);
+  std::size_t& cap = p->scratch_cap[key];
+  if (it != p->wimg.end() && cap >= bytes) return it->second;
+  if (it != p->wimg.end()) {
+    CU_CHECK(cgf::drv::cuStreamSynchronize(st));
+    CU_CHECK(cgf::drv::cuMemFree(it->second));
+    p->wimg.erase(it);
+  }
+  CUdeviceptr d = 0;
+  CU_CHECK(cgf::drv::cuMemAlloc(&d, std::max<std::size_t>(bytes, 256)));
+  p->wimg[key] = d;
+  cap = bytes;
+  return d;
+}
+
 // uvw forward on the tensor cores: W -> swizzled tf32 hi / lo images (one
 // small kernel), then the warp-specialised tcgen05 kernel over 128-row tiles.
 // One tcgen05 uvw kernel: `in` ([rows x in_dim], TMA-staged A source: x for
@@ -248,21 +298,10 @@ void run_uvw(cgf_plan* p, const std::string& tag, const void* in, int in_dim, co
   const auto us = uvw_source(p, tag);
   const cgf::Kernel prep = cgf::load_kernel(us->prep);
   const cgf::Kernel main = cgf::load_kernel(us->main);
-  CUcontext ctx = cgf::ensure_context();
-  CUdeviceptr img = 0;
-  {
-    std::lock_guard<std::mutex> g(p->mu);
-    auto it = p->wimg.find({ctx, tag});
-    if (it == p->wimg.end()) {
-      CU_CHECK(cgf::drv::cuMemAlloc(&img, us->wimg_bytes));
-      p->wimg.emplace(std::make_pair(ctx, tag), img);
-    } else {
-      img = it->second;
-    }
-  }
+  CUstream st = reinterpret_cast<CUstream>(stream);
+  CUdeviceptr img = uvw_scratch(p, st, tag, us->wimg_bytes);
   Args a;
   a.x = in; a.y = y; a.w = w; a.o0 = out; a.rows = rows;
-  CUstream st = reinterpret_cast<CUstream>(stream);
   const void* wsrc = a.w;
   void* pargs[] = {&wsrc, &img};
   const unsigned pgrid = static_cast<unsigned>((p->problem.n_w + 255) / 256);
@@ -341,7 +380,6 @@ void uvw_tmaps(CUtensorMap maps[4], const void* base, int dim, std::int64_t rows
 void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, const void* gz, void* gy, void* gw,
                      std::int64_t rows, void* stream) {
   (void)w;  // the W^T images were just written by the gx kernel's prep (same call, same stream)
-  CUcontext ctx = cgf::ensure_context();
   CUstream st = reinterpret_cast<CUstream>(stream);
   CUtensorMap maps[4];
   uvw_tmaps(maps, x, p->problem.dim_x, rows);
@@ -357,20 +395,7 @@ void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, c
   std::int64_t pitch = (rows + 127) / 128 * 128;
   const std::size_t ybytes = static_cast<std::size_t>(nplanes) * static_cast<std::size_t>(rows) * 64 * 4;
   const std::size_t wbytes = static_cast<std::size_t>(nplanes) * 64 * static_cast<std::size_t>(pitch) * 4;
-  CUdeviceptr pl;
-  {
-    std::lock_guard<std::mutex> g(p->mu);
-    auto& cap = p->scratch_cap[{ctx, "gzplanes"}];
-    auto it = p->wimg.find({ctx, "gzplanes"});
-    if (it == p->wimg.end() || cap < 2 * (ybytes + wbytes)) {
-      if (it != p->wimg.end()) CU_CHECK(cgf::drv::cuMemFree(it->second));
-      CU_CHECK(cgf::drv::cuMemAlloc(&pl, 2 * (ybytes + wbytes)));
-      p->wimg[{ctx, "gzplanes"}] = pl;
-      cap = 2 * (ybytes + wbytes);
-    } else {
-      pl = it->second;
-    }
-  }
+  const CUdeviceptr pl = uvw_scratch(p, st, "gzplanes", 2 * (ybytes + wbytes));
   void* yh = reinterpret_cast<void*>(pl);
   void* yl = reinterpret_cast<void*>(pl + ybytes);
   void* wh = reinterpret_cast<void*>(pl + 2 * ybytes);
@@ -398,11 +423,7 @@ void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, c
   // dL/dy
   {
     const cgf::Kernel k = cgf::load_kernel(us_y->main);
-    CUdeviceptr img;
-    {
-      std::lock_guard<std::mutex> g(p->mu);
-      img = p->wimg.at({ctx, "bwdx"});
-    }
+    const CUdeviceptr img = uvw_scratch(p, st, "bwdx", uvw_source(p, "bwdx")->wimg_bytes);
     CUtensorMap tg[2];
     plane_map(&tg[0], yh, false);
     plane_map(&tg[1], yl, false);
@@ -422,17 +443,7 @@ void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, c
     const auto us = uvw_source(p, "bwdw" + std::to_string(first));
     const cgf::Kernel k = cgf::load_kernel(us->main);
     const cgf::Kernel red = cgf::load_kernel(us->prep);
-    CUdeviceptr part;
-    {
-      std::lock_guard<std::mutex> g(p->mu);
-      auto it = p->wimg.find({ctx, "gw_part"});
-      if (it == p->wimg.end()) {
-        CU_CHECK(cgf::drv::cuMemAlloc(&part, 4ull * k.max_grid * p->problem.n_w));
-        p->wimg.emplace(std::make_pair(ctx, std::string("gw_part")), part);
-      } else {
-        part = it->second;
-      }
-    }
+    const CUdeviceptr part = uvw_scratch(p, st, "gw_part", 4ull * k.max_grid * p->problem.n_w);
     void* pa = reinterpret_cast<void*>(part);
     CUtensorMap xm[4];
     uvw_tmaps(xm, x, p->problem.dim_x, rows, static_cast<unsigned>(us->tile_rows));
@@ -700,15 +711,10 @@ int cgf_plan_create(const char* problem_json, int lane_width, uint32_t budget_wo
     auto p = std::make_unique<cgf_plan>();
     p->problem = cgf::parse_problem_json(problem_json, lane_width > 0 ? lane_width : 32);
     p->budget = budget_words ? budget_words : 4096;
-    // The reference's admission check: every subkernel's working set
-    // (x + y + w + z words) must fit the per-worker budget (scheduler.cpp:161-170).
-    for (const auto& s : p->problem.subs) {
-      const std::uint32_t ws = s.bp * s.dx() + s.dy() + (s.kind == cgf::Kind::B ? s.b : s.b * s.bp) + s.b * s.dz();
-      if (ws > p->budget)
-        throw BudgetError("budget " + std::to_string(p->budget) + " words below working set " + std::to_string(ws) +
-                          " of subkernel (l=(" + std::to_string(s.l1) + "," + std::to_string(s.l2) + "," +
-                          std::to_string(s.l3) + "), b=" + std::to_string(s.b) + ", b'=" + std::to_string(s.bp) + ")");
-    }
+    // The reference's schedule under the budget: its admission check (every
+    // subkernel's x + y + w + z words fit, scheduler.cpp:161-170) raises
+    // BudgetError here, and its phases drive the ExecStats counters.
+    p->sched = cgf::build_schedule_model(p->problem, p->budget);
     p->units = cgf::plan_units(p->problem);
     std::vector<std::pair<std::uint32_t, std::uint32_t>> zs, xs;
     for (const auto& s : p->problem.subs) {
@@ -762,12 +768,17 @@ int cgf_plan_source(cgf_plan* p, int op, int dtype, int w_shared, int aligned, c
 int cgf_plan_compile(cgf_plan* p, int op, int dtype, int w_shared, int aligned) {
   return guarded([&] {
     need(p, "plan");
-    if (use_uvw(p, op, dtype, w_shared) && op == CGF_OP_BACKWARD) {
-      std::vector<std::string> tags = {"bwdx", "bwdy"};
-      for (std::size_t f = 0; f < p->problem.resolved.size(); f += 6) tags.push_back("bwdw" + std::to_string(f));
+    if (use_uvw(p, op, dtype, w_shared)) {
+      // every tcgen05 kernel of the op and its prep / reduction kernel
+      std::vector<std::string> tags = {op == CGF_OP_FORWARD ? "fwd" : "bwdx"};
+      if (op == CGF_OP_BACKWARD) {
+        tags.push_back("bwdy");
+        for (std::size_t f = 0; f < p->problem.resolved.size(); f += 6) tags.push_back("bwdw" + std::to_string(f));
+      }
       for (const auto& tag : tags) {
         const auto us = uvw_source(p, tag);
-        cgf::compile_cubin(us->main.source, us->main.module.empty() ? us->main.name : us->main.module);
+        for (const auto* k : {&us->main, &us->prep})
+          if (!k->source.empty()) cgf::compile_cubin(k->source, k->module.empty() ? k->name : k->module);
       }
       return;
     }
@@ -970,22 +981,99 @@ int cgf_tp_double_backward_host(cgf_plan* p, int dtype, const void* x, const voi
 }
 
 int cgf_tp_stats(const cgf_plan* p, int op, int64_t rows, int w_shared, uint64_t stats[3]) {
+  (void)w_shared;
   return guarded([&] {
     need(p, "plan");
+    need(stats, "stats");
+    if (rows < 0) throw cgf::ShapeError("rows must be non-negative");
+    const auto& m = p->sched;
+    const std::uint64_t R = static_cast<std::uint64_t>(rows);
+    const std::uint64_t f[3] = {m.fwd_loads, m.fwd_stores, m.fwd_flops}, b[3] = {m.bwd_loads, 0, m.bwd_flops};
+    for (int k = 0; k < 3; ++k) {
+      switch (op) {
+        case CGF_OP_FORWARD: stats[k] = R * f[k]; break;
+        case CGF_OP_BACKWARD: stats[k] = R * b[k]; break;
+        case CGF_OP_DOUBLE_BACKWARD: stats[k] = R * (3 * f[k] + 4 * b[k]); break;
+        default: throw std::invalid_argument("bad op");
+      }
+    }
+  });
+}
+
+int cgf_tp_traffic(const cgf_plan* p, int op, int64_t rows, int w_shared, uint64_t words[2]) {
+  return guarded([&] {
+    need(p, "plan");
+    need(words, "words");
     const auto& pr = p->problem;
     const std::uint64_t R = static_cast<std::uint64_t>(rows);
     const std::uint64_t W = w_shared ? pr.n_w : R * pr.n_w;
     const std::uint64_t X = R * pr.dim_x, Y = R * pr.dim_y, Z = R * pr.dim_z;
-    const std::uint64_t f = pr.fwd_flops_per_row(), b = pr.bwd_flops_per_row();
     switch (op) {
-      case CGF_OP_FORWARD: stats[0] = X + Y + W; stats[1] = Z; stats[2] = R * f; break;
-      case CGF_OP_BACKWARD: stats[0] = X + Y + W + Z; stats[1] = X + Y + W; stats[2] = R * b; break;
-      case CGF_OP_DOUBLE_BACKWARD:
-        stats[0] = 2 * (X + Y + W) + Z + X + Y + W;
-        stats[1] = X + Y + W + Z;
-        stats[2] = R * (3 * f + 4 * b);
-        break;
+      case CGF_OP_FORWARD: words[0] = X + Y + W; words[1] = Z; break;
+      case CGF_OP_BACKWARD: words[0] = X + Y + W + Z; words[1] = X + Y + W; break;
+      case CGF_OP_DOUBLE_BACKWARD: words[0] = 3 * (X + Y + W) + Z; words[1] = X + Y + W + Z; break;
       default: throw std::invalid_argument("bad op");
+    }
+  });
+}
+
+namespace {
+int copy_out(const std::string& t, char* buf, int cap) {
+  if (buf && cap > 0) {
+    const int m = std::min<int>(cap - 1, static_cast<int>(t.size()));
+    std::memcpy(buf, t.data(), m);
+    buf[m] = 0;
+  }
+  return static_cast<int>(t.size());
+}
+}  // namespace
+
+int cgf_plan_schedule_json(const cgf_plan* p, char* buf, int cap) {
+  int n = 0;
+  const int rc = guarded([&] {
+    need(p, "plan");
+    n = copy_out(cgf::schedule_json(p->problem, p->sched), buf, cap);
+  });
+  return rc == CGF_OK ? n : -rc;
+}
+
+int cgf_plan_listing(const cgf_plan* p, int pos, int backward, char* buf, int cap) {
+  int n = 0;
+  const int rc = guarded([&] {
+    need(p, "plan");
+    if (pos < 0 || pos >= static_cast<int>(p->problem.subs.size())) throw std::invalid_argument("subkernel position out of range");
+    n = copy_out(cgf::listing_text(p->problem.subs[pos], backward != 0), buf, cap);
+  });
+  return rc == CGF_OK ? n : -rc;
+}
+
+int cgf_conv_stats(const cgf_plan* p, int op, int mode, int unfused, int64_t nodes, int64_t edges,
+                   uint64_t st[4]) {
+  return guarded([&] {
+    need(p, "plan");
+    need(st, "stats");
+    if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (mode != CGF_CONV_DETERMINISTIC && mode != CGF_CONV_ATOMIC) throw std::invalid_argument("bad conv mode");
+    const auto& pr = p->problem;
+    const std::uint64_t E = static_cast<std::uint64_t>(edges), V = static_cast<std::uint64_t>(nodes);
+    const std::uint64_t dx = pr.dim_x, dy = pr.dim_y, dz = pr.dim_z, nw = pr.n_w;
+    const bool atomic = mode == CGF_CONV_ATOMIC;
+    if (op == CGF_OP_FORWARD) {
+      if (unfused) {  // gather x per edge, TP over |E| rows, per-node sums of |E| z rows
+        st[0] = E * (2 * dx + dy + nw); st[1] = E * (dx + dz); st[2] = E;
+      } else {  // per edge: x[nbr] (L2), y_e, W_e; z once per row, or one reduction per edge
+        st[0] = E * (dx + dy + nw); st[1] = atomic ? E * dz : V * dz; st[2] = atomic ? E : V;
+      }
+      st[3] = E * p->sched.fwd_flops;
+    } else if (op == CGF_OP_BACKWARD) {
+      if (unfused) {
+        st[0] = E * (2 * dx + dy + nw + dz); st[1] = E * (2 * dx + dy + nw); st[2] = E;
+      } else {
+        st[0] = E * (dx + dy + nw + dz); st[1] = (atomic ? E : V) * dx + E * (dy + nw); st[2] = (atomic ? E : V) + E;
+      }
+      st[3] = E * p->sched.bwd_flops;
+    } else {
+      throw std::invalid_argument("bad op");
     }
   });
 }
@@ -1302,9 +1390,8 @@ int cgf_graph_radius(int64_t n, const double* pos, double r_cut, int64_t* row_pt
 
 // ---- host-pointer conv (the C++ drop-in shim's path) ---------------------
 // Copies the graph and arrays in, runs the device entry points on the
-// default stream, copies results back. Mode::atomic is served by the
-// deterministic kernels: they satisfy its contract (results within rounding
-// of the deterministic mode) and are bitwise reproducible on top.
+// default stream, copies results back. Mode::atomic runs the atomic
+// edge-list kernels (cgf_conv_*_atomic_host) over the CSR's expanded sources.
 int cgf_conv_forward_host(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, const int64_t* row_ptr,
                           const int32_t* nbr, const void* node_x, const void* edge_y, const void* edge_w,
                           void* node_z, int mode) {

@@ -288,6 +288,7 @@ Problem make_problem(const Irreps& x, const Irreps& y, const Irreps& z,
         }
     }
   }
+  for (size_t i = 0; i < split.size(); ++i) split[i].split_index = static_cast<int>(i);
   std::stable_sort(split.begin(), split.end(),
                    [](const Sub& a, const Sub& b) { return a.z_off < b.z_off; });
   p.subs = std::move(split);

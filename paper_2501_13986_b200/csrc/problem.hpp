@@ -82,7 +82,8 @@ struct Sub {
   int l1 = 0, l2 = 0, l3 = 0;
   int b = 0, bp = 0;  // z-side rows, x-side lanes
   std::uint32_t x_off = 0, y_off = 0, z_off = 0, w_off = 0, w_stride = 1;
-  int origin = 0;
+  int origin = 0;       // user instruction index
+  int split_index = 0;  // position in the split (pre-schedule) order
   std::shared_ptr<const CGBlock> cg;
   int dx() const { return 2 * l1 + 1; }
   int dy() const { return 2 * l2 + 1; }

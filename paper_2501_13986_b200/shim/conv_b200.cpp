@@ -197,6 +197,19 @@ std::vector<std::int32_t> neighbours(const GraphCSR& g) {
   return nb;
 }
 
+// ConvStats from libcgf's store / load model of the GPU kernels (cgf_conv_stats).
+ConvStats conv_stats(const engine::TpPlan& plan, int op, Mode mode, bool unfused, const GraphCSR& g) {
+  std::uint64_t s[4] = {0, 0, 0, 0};
+  check(cgf_conv_stats(plan.impl().gpu, op, mode == Mode::atomic ? CGF_CONV_ATOMIC : CGF_CONV_DETERMINISTIC,
+                       unfused ? 1 : 0, g.node_count, g.edge_count(), s));
+  ConvStats st;
+  st.loads_words = s[0];
+  st.stores_words = s[1];
+  st.output_store_ops = s[2];
+  st.flops = s[3];
+  return st;
+}
+
 std::vector<std::int32_t> sources(const GraphCSR& g) {
   std::vector<std::int32_t> s(g.edges.size());
   for (std::size_t e = 0; e < g.edges.size(); ++e) s[e] = g.edges[e].src;
@@ -221,14 +234,7 @@ ConvStats ConvPlan::forward(const GraphCSR& g, const std::vector<T>& node_x, con
     check(cgf_conv_forward_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(), g.row_ptr.data(),
                                 nb.data(), node_x.data(), edge_y.data(), edge_w.data(), node_z.data(),
                                 CGF_CONV_DETERMINISTIC));
-  const auto E = static_cast<std::uint64_t>(g.edge_count()), V = static_cast<std::uint64_t>(g.node_count);
-  ConvStats st;
-  st.loads_words = E * (p.dim_x + p.dim_y + p.total_weights);
-  // deterministic: each output row stored once; atomic: one reduction per edge
-  st.stores_words = mode == Mode::atomic ? E * p.dim_z : V * p.dim_z;
-  st.output_store_ops = mode == Mode::atomic ? E : V;
-  st.flops = E * plan_->schedule().traffic.flops;
-  return st;
+  return conv_stats(*plan_, CGF_OP_FORWARD, mode, false, g);
 }
 
 template <typename T>
@@ -256,12 +262,7 @@ ConvStats ConvPlan::backward(const GraphCSR& g, const std::vector<std::int64_t>&
     check(cgf_conv_backward_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(), g.row_ptr.data(),
                                  nb.data(), node_x.data(), edge_y.data(), edge_w.data(), g_node_z.data(),
                                  g_node_x.data(), g_edge_y.data(), g_edge_w.data(), CGF_CONV_DETERMINISTIC));
-  const auto E = static_cast<std::uint64_t>(g.edge_count()), V = static_cast<std::uint64_t>(g.node_count);
-  ConvStats st;
-  st.loads_words = E * (p.dim_x + p.dim_y + p.total_weights + p.dim_z);
-  st.stores_words = V * p.dim_x + E * (p.dim_y + p.total_weights);
-  st.output_store_ops = V + E;
-  return st;
+  return conv_stats(*plan_, CGF_OP_BACKWARD, mode, false, g);
 }
 
 // ---- unfused gather -> batched TP -> scatter (the GPU TP on gathered rows) --
@@ -272,19 +273,13 @@ ConvStats unfused_forward(const engine::TpPlan& plan, const GraphCSR& g, const s
                           const engine::Options&) {
   const auto& p = prob(plan);
   require_conv_shapes(p, g, node_x, edge_y, edge_w);
-  const std::size_t E = g.edges.size(), dx = p.dim_x, dz = p.dim_z;
-  node_z.assign(static_cast<std::size_t>(g.node_count) * dz, T(0));
+  node_z.assign(static_cast<std::size_t>(g.node_count) * p.dim_z, T(0));
   // gather, batched TP and per-node sums in edge order, all on the GPU
   if (g.node_count > 0)
     check(cgf_conv_unfused_forward_host(plan.impl().gpu, dtype<T>(), g.node_count, g.edge_count(), sources(g).data(),
                                         neighbours(g).data(), node_x.data(), edge_y.data(), edge_w.data(),
                                         node_z.data()));
-  ConvStats st;
-  st.loads_words = E * (2 * dx + p.dim_y + p.total_weights);
-  st.stores_words = E * (dx + dz);
-  st.output_store_ops = E;
-  st.flops = E * plan.schedule().traffic.flops;
-  return st;
+  return conv_stats(plan, CGF_OP_FORWARD, Mode::deterministic, true, g);
 }
 
 template <typename T>
@@ -294,7 +289,6 @@ ConvStats unfused_backward(const engine::TpPlan& plan, const GraphCSR& g, const 
                            const engine::Options&) {
   const auto& p = prob(plan);
   require_conv_shapes(p, g, node_x, edge_y, edge_w);
-  const std::size_t E = g.edges.size(), dx = p.dim_x, dz = p.dim_z;
   g_node_x.assign(node_x.size(), T(0));
   g_edge_y.assign(edge_y.size(), T(0));
   g_edge_w.assign(edge_w.size(), T(0));
@@ -303,11 +297,7 @@ ConvStats unfused_backward(const engine::TpPlan& plan, const GraphCSR& g, const 
                                          sources(g).data(), neighbours(g).data(), node_x.data(), edge_y.data(),
                                          edge_w.data(), g_node_z.data(), g_node_x.data(), g_edge_y.data(),
                                          g_edge_w.data()));
-  ConvStats st;
-  st.loads_words = E * (2 * dx + p.dim_y + p.total_weights + dz);
-  st.stores_words = E * (2 * dx + p.dim_y + p.total_weights);
-  st.output_store_ops = E;
-  return st;
+  return conv_stats(plan, CGF_OP_BACKWARD, Mode::deterministic, true, g);
 }
 
 #define CGF_CONV_INST(T)                                                                                            \

@@ -9,12 +9,15 @@
 //  * shape checks before any compute, same ShapeError messages (engine.cpp:206-220);
 //  * outputs resized only when the size differs and fully overwritten
 //    (ensure_zeroed, engine.cpp:270-274);
-//  * forward ExecStats = the schedule's traffic model x rows (the counters the
-//    reference's own test asserts, test_engine.cpp:350-363); backward /
-//    double-backward report the compulsory-traffic model of cgf_tp_stats;
+//  * ExecStats come from libcgf's own restatement of the reference's per-row
+//    schedule model (cgf_tp_stats: forward = traffic_report x rows, the
+//    counters test_engine.cpp:350-363 asserts; backward / double-backward the
+//    reference's phase counters) -- nothing is read from the reference's
+//    scheduler objects;
 //  * results are bitwise independent of Options::workers and ExecMode (the GPU
 //    kernels ignore both) and of DispatchStyle (one fused pass);
 //  * C ABI codes are rethrown as the reference's exception types.
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -84,10 +87,13 @@ TpPlan::TpPlan(const tpspec::ValidatedProblem& p, const scheduler::Schedule& s)
   impl_->problem = p;
   impl_->schedule = s;
   // The GPU planner re-splits the ORIGINAL instructions (problem_to_json
-  // writes those) at 32 lanes; the schedule's budget keeps the reference's
-  // admission check (scheduler.cpp:161-170).
+  // writes those) at the lane width the caller split with: the largest chunk
+  // of `p` (split_multiplicities(p, L) leaves chunks of min(L, mult)), so the
+  // split -- and the schedule model under the same budget -- is the caller's.
+  int lanes = 1;
+  for (const auto& r : p.resolved) lanes = std::max({lanes, r.b, r.b_prime});
   const std::string js = tpspec::problem_to_json(p);
-  b200::check(cgf_plan_create(js.c_str(), 32, s.budget_words, &impl_->gpu));
+  b200::check(cgf_plan_create(js.c_str(), std::min(lanes, 32), s.budget_words, &impl_->gpu));
 }
 
 TpPlan::~TpPlan() = default;
@@ -105,12 +111,7 @@ ExecStats TpPlan::forward(const Batch<T>& in, std::vector<T>& z, const Options&)
   if (in.rows > 0)
     b200::check(cgf_tp_forward_host(impl_->gpu, b200::dtype<T>(), in.x.data(), in.y.data(), in.w.data(), z.data(),
                                     in.rows, 0));
-  const auto& tr = impl_->schedule.traffic;
-  ExecStats st;
-  st.loads_words = tr.loads_words * static_cast<std::uint64_t>(in.rows);
-  st.stores_words = tr.stores_words * static_cast<std::uint64_t>(in.rows);
-  st.flops = tr.flops * static_cast<std::uint64_t>(in.rows);
-  return st;
+  return model_stats(impl_->gpu, CGF_OP_FORWARD, in.rows);
 }
 
 template <typename T>
