@@ -7,23 +7,38 @@ forward + backward, FP32, batch 1M rows per GPU, on the generated sm_100a kernel
 One step = TP forward (z = TP(x, y, W)) + TP backward ((gx, gy, gW) from gz)
 over the whole batch, inputs resident in HBM. Metric = GFLOP/s under the
 reference's flop rule (kernelgen::flop_count, kernelgen.cpp:253-276):
-(100,736 + 292,836) flop per row. N > 1: one process per GPU, each with its own
-1M-row batch (rows are independent — "replicas / batch split"),
-no data-path collective; time = max over ranks.
+(100,736 + 292,836) flop per row. N > 1: one process per GPU (the script
+re-launches itself under torch.distributed.run when started without
+RANK/WORLD_SIZE), each with its own 1M-row batch (rows are independent —
+"replicas / batch split"), no data-path collective; time = max
+over ranks.
 
-The line also carries "conv": the fused graph convolution of config C5 (C1 TP
-on radius_graph(cubic_lattice(58^3), 3.0), 22.4M edges) as forward + backward
-per step, destination-partitioned over the N ranks with NCCL all-gather of
-node_x and reduce-scatter of g_node_x (paper_2501_13986_b200/dist.py);
-edges/s over the whole graph, max over ranks ("scaling": "strong").
+Sub-objects of the line (each its own CUDA-event timing, max over ranks):
+  conv    C5: the fused graph convolution (C1 TP on radius_graph(cubic_lattice
+          (58^3), 3.0), 22.4M edges), forward + backward, destination-
+          partitioned over the N ranks (NCCL all-gather of node_x, all-to-all
+          + rank-ordered sum of g_node_x); edges/s over the whole graph
+          ("scaling": "strong"), per-rank kernel and collective ms.
+  legs    C1 (50K rows FP32 forward, BASELINE configs[0]), C2 FP64 forward /
+          backward at 1M rows, C3 (uvw, shared W, tcgen05) forward / backward,
+          C4 (C2 TP on the 29^3 lattice, 2.63M edges) conv forward / backward /
+          double-backward in FP32 and forward / backward in FP64: ms, GB/s and
+          the fraction of measured HBM per kernel.
+  e2e     the same fwd+bwd step through the public API with pinned HOST
+          buffers (TpPlan.forward_backward -> cgf_tp_forward_backward_host, one
+          pipelined pass) with the measured PCIe roofline beside it; also the
+          two separate calls (TpPlan.forward + TpPlan.backward).
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
 unmodified cgforge built from /root/reference) on this box's host cores, same
-metric, a bounded row sample per step.
+metric, a bounded row sample per step. The in-line cpu_baseline runs the same
+code in a separate process before this process touches the GPU.
 """
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,6 +50,7 @@ sys.path.insert(0, ROOT)
 
 CONFIG = "c2"
 HBM_FALLBACK_GBS = 6650.0
+METRIC = "CG TP fwd+bwd GFLOP/s (C2 MACE-large uvu)"
 
 
 def parse():
@@ -48,10 +64,15 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-rows", type=int, default=50_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-baseline-only", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--conv-n", type=int, default=58, help="lattice side of the conv leg (58 = C5); 0 = skip")
     ap.add_argument("--conv-config", default="c1", help="TP of the conv leg (C5 uses the C1 TP)")
     ap.add_argument("--conv-steps", type=int, default=5)
-    ap.add_argument("--c3-rows", type=int, default=1_000_000, help="rows of the C3 (uvw, shared W) leg; 0 = skip")
+    ap.add_argument("--legs", default="c1,c2f64,c3,c4", help="comma list of sub-legs; '' = none")
+    ap.add_argument("--leg-steps", type=int, default=3)
+    ap.add_argument("--harness-check", action="store_true",
+                    help="CPU/gloo plumbing check of the multi-rank conv leg with a torch stand-in for the "
+                         "kernels (numbers meaningless; never a bench value)")
     return ap.parse_args()
 
 
@@ -85,7 +106,7 @@ class ClockSampler:
                     self.samples.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -107,25 +128,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+# ------------------------------------------------------------ CPU baseline --
+
 def cpu_baseline(dtype, rows):
     """The unmodified reference (oracle/_ref) timed on this host: TpPlan
     forward + backward, all hardware threads, median of 3 after 1 warm-up
     (the CLI's methodology, tools/cgforge.cpp:336-348)."""
     from oracle import oracle as O
-    if not O.ref_available():
-        ref = None
-    else:
-        ref = O.RefPlan(O.config_json(CONFIG), budget=4096)
+    from paper_2501_13986_b200.configs import config_json
     import numpy as np
     dt = np.float32 if dtype == "f32" else np.float64
     cores = os.cpu_count()
     flops = (100_736 + 292_836) * rows
-    if ref is not None:
+    if O.ref_available():
+        ref = O.RefPlan(config_json(CONFIG), budget=4096)
         secs = ref.bench_tp(dt, rows, ops=3, warmup=1, iters=3, workers=cores)
         t = float(secs[0] + secs[1])
         kind = "reference"
     else:  # oracle port, single thread
-        o = O.Oracle(O.config_json(CONFIG))
+        o = O.Oracle(config_json(CONFIG))
         x, y, w = O.random_batch(o, rows, 1234, dt)
         gz = O.NormalGen(1235).normal_vec(rows * o.dim_z, dt).reshape(rows, -1)
         t0 = time.perf_counter()
@@ -139,11 +160,23 @@ def cpu_baseline(dtype, rows):
             "rows_per_s": rows / t}
 
 
+def cpu_baseline_subprocess(args):
+    """cpu_baseline in a fresh process, before this one initialises CUDA (no
+    GPU-side threads or pinned-memory traffic competing for the host cores)."""
+    p = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-baseline-only", "--dtype", args.dtype,
+                        "--cpu-rows", str(args.cpu_rows)], capture_output=True, text=True, timeout=900)
+    if p.returncode != 0:
+        return {"error": (p.stderr or p.stdout)[-400:]}
+    rec = json.loads(p.stdout.strip().splitlines()[-1])
+    rec["process"] = "separate, before CUDA init"
+    return rec
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     cb = cpu_baseline(args.dtype, args.cpu_rows)
-    line = {"impl": "reference", "metric": "CG TP fwd+bwd GFLOP/s (C2 MACE-large uvu)", "value": cb["value"],
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"],
             "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * (100_736 + 292_836) * args.cpu_rows / (cb["value"] * 1e9),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
@@ -155,17 +188,212 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def conv_leg(args, rank, world, dev, clk_index):
+# -------------------------------------------------------------- helpers ----
+
+def event_ms(fn, steps, stream):
+    """Average device ms of fn() over `steps` back-to-back calls (CUDA events
+    on the launching stream, synchronised on both sides)."""
+    import torch
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def max_over_ranks(vals, dev, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
+def kernel_source_sha(plan, op, dtype_code):
+    import paper_2501_13986_b200 as cgf
+    return hashlib.sha256(plan.source(op, dtype_code).encode()).hexdigest()[:16]
+
+
+def ncu_traffic(key, src_sha, R):
+    """Per-launch DRAM bytes of this kernel from the committed `ncu --set full`
+    capture (profiles/ncu_traffic.json, tools/ncu_traffic.py), scaled to R rows;
+    None unless the capture was taken of the same generated kernel source."""
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        rec = json.load(open(tfile)).get(key)
+    except Exception:
+        return None, "no capture"
+    if rec is None:
+        return None, "no capture"
+    if rec.get("source_sha16") != src_sha:
+        return None, f"stale capture (kernel source {rec.get('source_sha16')} != {src_sha})"
+    return rec["traffic_bytes"] * R / rec.get("rows", 1_000_000), rec.get("report")
+
+
+def measure_pcie(dev, gib=1.0):
+    """Pinned host <-> device copy bandwidth (GB/s): H2D alone, D2H alone and
+    both directions at once (two streams) — the ceiling of the e2e path."""
+    import torch
+    n = int(gib * (1 << 30)) // 4
+    h1 = torch.empty(n, dtype=torch.float32).pin_memory()
+    h2 = torch.empty(n, dtype=torch.float32).pin_memory()
+    d1 = torch.empty(n, dtype=torch.float32, device=dev)
+    d2 = torch.empty(n, dtype=torch.float32, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    nbytes = 4 * n
+
+    def timed(do_h2d, do_d2h, reps=3):
+        best = float("inf")
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if do_h2d:
+                with torch.cuda.stream(s1):
+                    d1.copy_(h1, non_blocking=True)
+            if do_d2h:
+                with torch.cuda.stream(s2):
+                    h2.copy_(d2, non_blocking=True)
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    timed(True, True, 1)
+    h2d = nbytes / timed(True, False) / 1e9
+    d2h = nbytes / timed(False, True) / 1e9
+    both = 2 * nbytes / timed(True, True) / 1e9
+    del h1, h2, d1, d2
+    return {"h2d_GBps": h2d, "d2h_GBps": d2h, "bidirectional_GBps": both,
+            "how": f"pinned torch copies of {gib:g} GiB, best of 3, host wall clock"}
+
+
+# ------------------------------------------------------------ legs ---------
+
+def tp_leg(cgf, plan, name, R, dtype, ops, steps, dev, world, w_shared=False, peak=None):
+    """Device-resident TP ops on R rows (torch.randn inputs), CUDA events per
+    op; algorithmic bytes from cgf_tp_traffic (each input read once, each
+    output written once)."""
+    import torch
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    es = 4 if dtype == "f32" else 8
+    g = torch.Generator(device=dev).manual_seed(7)
+    x = torch.randn((R, plan.dim_x), device=dev, dtype=tdt, generator=g)
+    y = torch.randn((R, plan.dim_y), device=dev, dtype=tdt, generator=g)
+    w = torch.randn((1 if w_shared else R, plan.n_w), device=dev, dtype=tdt, generator=g)
+    zbuf = torch.randn((R, plan.dim_z), device=dev, dtype=tdt, generator=g)  # z of the forward, gz of the backward
+    stream = torch.cuda.current_stream(dev)
+    out = {"workload": name, "rows": R, "dtype": dtype}
+    bwd_out = None
+    for op in ops:
+        if op == "forward":
+            fn = lambda: plan.forward(x, y, w, z=zbuf, w_shared=w_shared)
+            code = 0
+        else:
+            if bwd_out is None:
+                bwd_out = plan.backward(x, y, w, zbuf, w_shared=w_shared)
+            fn = lambda: plan.backward(x, y, w, zbuf, w_shared=w_shared, out=bwd_out)
+            code = 1
+        fn()
+        ms = max_over_ranks([event_ms(fn, steps, stream)], dev, world)[0]
+        words = sum(plan.traffic(code, R, w_shared))
+        gbs = words * es / (ms / 1e3) / 1e9
+        flops = (plan.flops_fwd if code == 0 else plan.flops_bwd) * R
+        out[op] = {"ms": ms, "GB/s": gbs, "hbm_frac": gbs / peak, "GFLOP/s": flops / (ms / 1e3) / 1e9,
+                   "algorithmic_bytes": words * es}
+    del x, y, w, zbuf, bwd_out
+    torch.cuda.empty_cache()
+    return out
+
+
+def conv_single_leg(cgf, cdist, name, tp_name, n, dtypes_ops, steps, dev, peak):
+    """Fused conv on one GPU (C4: C2 TP on radius_graph(cubic_lattice(n^3), 3.0))."""
+    import torch
+    from paper_2501_13986_b200.configs import config_json
+    plan = cgf.TpPlan(config_json(tp_name))
+    cp = cgf.ConvPlan(plan)
+    nodes, src, nbr = cdist.lattice_radius_graph(n, 1.0, 3.0)
+    g = cgf.Graph(nodes, src, nbr)
+    del src, nbr
+    E, V = g.edges, g.nodes
+    stream = torch.cuda.current_stream(dev)
+    out = {"workload": f"{name}: {tp_name} TP on radius_graph(cubic_lattice({n}^3), 3.0), {V} nodes / {E} edges",
+           "nodes": V, "edges": E}
+    dyw = plan.dim_y + plan.n_w
+    words = {"forward": E * dyw + V * (plan.dim_x + plan.dim_z),
+             "backward": 2 * E * dyw + V * (2 * plan.dim_x + plan.dim_z),
+             "double_backward": 3 * E * dyw + V * (3 * plan.dim_x + 2 * plan.dim_z)}
+    flops = {"forward": plan.flops_fwd, "backward": plan.flops_bwd, "double_backward": plan.flops_dbwd}
+    for dtype, ops in dtypes_ops:
+        tdt = torch.float32 if dtype == "f32" else torch.float64
+        es = 4 if dtype == "f32" else 8
+        gen = torch.Generator(device=dev).manual_seed(11)
+        rnd = lambda *s: torch.randn(s, device=dev, dtype=tdt, generator=gen)
+        nx, ey, ew, gnz = rnd(V, plan.dim_x), rnd(E, plan.dim_y), rnd(E, plan.n_w), rnd(V, plan.dim_z)
+        res = {}
+        for op in ops:
+            if op == "forward":
+                fn = lambda: cp.forward(g, nx, ey, ew)
+            elif op == "backward":
+                fn = lambda: cp.backward(g, nx, ey, ew, gnz)
+            else:
+                up = (rnd(V, plan.dim_x), rnd(E, plan.dim_y), rnd(E, plan.n_w))
+                fn = lambda: cp.double_backward(g, nx, ey, ew, gnz, up)
+            r = fn()
+            del r
+            ms = event_ms(fn, steps, stream)
+            gbs = words[op] * es / (ms / 1e3) / 1e9
+            res[op] = {"ms": ms, "GB/s": gbs, "hbm_frac": gbs / peak, "edges_per_s": E / (ms / 1e3),
+                       "GFLOP/s": flops[op] * E / (ms / 1e3) / 1e9}
+            if op == "double_backward":
+                del up
+            torch.cuda.empty_cache()
+        out[dtype] = res
+        del nx, ey, ew, gnz
+        torch.cuda.empty_cache()
+    return out
+
+
+class _TorchShardStandIn:
+    """--harness-check only: stands in for the CUDA shard kernels on CPU ranks
+    (a linear map of the gathered neighbour rows), so the multi-rank plumbing
+    — partition, all-gather, all-to-all reduction, timing, max over ranks,
+    the JSON line — runs under gloo. Its numbers are not a measurement."""
+
+    def __init__(self, plan):
+        self.plan = plan
+
+    def forward_shard(self, sh, x_all, ey, ew):
+        import torch
+        d = sh.device(x_all.device)
+        src = torch.repeat_interleave(torch.arange(sh.out_nodes), d["row_ptr"].diff())
+        z = x_all.new_zeros((sh.out_nodes, self.plan.dim_z))
+        z[:, :self.plan.dim_x].index_add_(0, src, x_all[d["nbr"].long()])
+        return z
+
+    def backward_shard(self, sh, x_all, ey, ew, gz):
+        import torch
+        d = sh.device(x_all.device)
+        src = torch.repeat_interleave(torch.arange(sh.out_nodes), d["row_ptr"].diff())
+        gx = x_all.new_zeros((sh.in_nodes, self.plan.dim_x))
+        gx.index_add_(0, d["nbr"].long(), gz[src, :self.plan.dim_x])
+        return gx, torch.zeros_like(ey), torch.zeros_like(ew)
+
+
+def conv_leg(args, rank, world, dev, harness=False):
     """C5: fused conv (C1 TP) on radius_graph(cubic_lattice(n^3), 3.0),
     destination-partitioned over the ranks (dist.DistConvPlan: NCCL all-gather
-    of node_x, local fused conv, reduce-scatter of g_node_x). One step =
-    forward + backward, collectives included; strong scaling (|E| fixed)."""
+    of node_x, local fused conv, all-to-all + rank-ordered sum of g_node_x).
+    One step = forward + backward, collectives included; strong scaling (|E|
+    fixed)."""
     import torch
     import torch.distributed as dist
 
     import paper_2501_13986_b200 as cgf
     from paper_2501_13986_b200 import dist as cdist
-    from oracle.oracle import config_json
+    from paper_2501_13986_b200.configs import config_json
 
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     es = 4 if args.dtype == "f32" else 8
@@ -174,74 +402,75 @@ def conv_leg(args, rank, world, dev, clk_index):
     g = cgf.Graph(nodes, src, nbr)
     del src, nbr
     sh = cdist.GraphShard(g, world, rank)
-    dc = cdist.DistConvPlan(plan, sh, group=None)
+    dc = cdist.DistConvPlan(plan, sh, group=None, local=_TorchShardStandIn(plan) if harness else None)
     gen = torch.Generator(device=dev).manual_seed(4321 + rank)
     rnd = lambda *s: torch.randn(s, device=dev, dtype=tdt, generator=gen)
     nx, ey, ew, gnz = rnd(sh.out_nodes, plan.dim_x), rnd(sh.edges, plan.dim_y), rnd(sh.edges, plan.n_w), \
         rnd(sh.out_nodes, plan.dim_z)
-    stream = torch.cuda.current_stream(dev)
-    fwd_ms, bwd_ms, coll_ms = [], [], []
+    cuda = dev.type == "cuda"
+    stream = torch.cuda.current_stream(dev) if cuda else None
+    laps = []
+
+    def mark():
+        if cuda:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            return e
+        return time.perf_counter()
+
+    def lap(a, b):
+        return a.elapsed_time(b) if cuda else (b - a) * 1e3
 
     def step(record=False):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if record else None
-        if record:
-            evs[0].record(stream)
+        t0 = mark()
         x_all = dc.gather_x(nx)
-        if record:
-            evs[1].record(stream)
+        t1 = mark()
         z = dc.local.forward_shard(sh, x_all, ey, ew)
-        if record:
-            evs[2].record(stream)
+        t2 = mark()
         gx_part, gy, gw = dc.local.backward_shard(sh, x_all, ey, ew, gnz)
-        if record:
-            evs[3].record(stream)
+        t3 = mark()
         gx = dc._reduce_scatter(gx_part)
+        t4 = mark()
         if record:
-            evs[4].record(stream)
-            fwd_ms.append((evs[1], evs[2]))
-            bwd_ms.append((evs[2], evs[3]))
-            coll_ms.append(((evs[0], evs[1]), (evs[3], evs[4])))
+            laps.append((t0, t1, t2, t3, t4))
         return z, gx, gy, gw
 
     for _ in range(max(3, args.warmup)):
         step()
-    torch.cuda.synchronize()
+    if cuda:
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
+    if cuda:
+        torch.cuda.synchronize()
+    a = mark()
     for _ in range(args.conv_steps):
         step(record=True)
-    b.record(stream)
-    torch.cuda.synchronize()
+    b = mark()
+    if cuda:
+        torch.cuda.synchronize()
+    ms = lap(a, b) / args.conv_steps
+    f_ms = sum(lap(t[1], t[2]) for t in laps) / len(laps)
+    b_ms = sum(lap(t[2], t[3]) for t in laps) / len(laps)
+    ag_ms = sum(lap(t[0], t[1]) for t in laps) / len(laps)
+    rs_ms = sum(lap(t[3], t[4]) for t in laps) / len(laps)
+    t = torch.tensor([ms, f_ms, b_ms, ag_ms, rs_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.barrier()
-    ms = torch.tensor([a.elapsed_time(b)], device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item()) / args.conv_steps
-    avg = lambda L: sum(x.elapsed_time(y) for x, y in L) / len(L)
-    f_ms, b_ms = avg(fwd_ms), avg(bwd_ms)
-    c_ms = sum(p.elapsed_time(q) + r.elapsed_time(t) for (p, q), (r, t) in coll_ms) / len(coll_ms)
-    # algorithmic bytes of this rank's kernels (SURVEY.md §8d conv rules; node
-    # terms over the rows each kernel owns)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, f_mx, b_mx, ag_mx, rs_mx = (float(v) for v in t.tolist())
     E, Vo, Vi = sh.edges, sh.out_nodes, sh.in_nodes
     fb = (E * (plan.dim_y + plan.n_w) + Vi * plan.dim_x + Vo * plan.dim_z) * es
     bb = (2 * E * (plan.dim_y + plan.n_w) + Vi * 2 * plan.dim_x + Vo * plan.dim_z) * es
     peak, _ = measured_peak()
-    per_rank = torch.tensor([f_ms, b_ms, c_ms], device=dev)
-    if world > 1:
-        dist.all_reduce(per_rank, op=dist.ReduceOp.MAX)
     return {
         "workload": f"c5: {args.conv_config} TP on radius_graph(cubic_lattice({args.conv_n}^3), 3.0), "
                     f"{nodes} nodes / {g.edges} edges, fwd+bwd, destination-partitioned",
         "edges_per_s": g.edges / (ms / 1e3), "ms_per_step": ms, "steps": args.conv_steps, "n_gpus": world,
         "scaling": "strong", "dtype": args.dtype,
-        "collectives": "NCCL all_gather_into_tensor(node_x) + reduce_scatter_tensor(g_node_x)" if world > 1
-        else "none (1 rank)",
-        "max_over_ranks_ms": {"forward_kernel": float(per_rank[0]), "backward_kernel": float(per_rank[1]),
-                              "collectives": float(per_rank[2])},
+        "collectives": "all_gather_into_tensor(node_x) + all_to_all_single(g_node_x partials) + rank-ordered sum"
+        if world > 1 else "none (1 rank)",
+        "max_over_ranks_ms": {"step": ms, "forward_kernel": f_mx, "backward_kernel": b_mx,
+                              "all_gather": ag_mx, "reduce": rs_mx},
         "rank0_roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
                            "forward": {"GB/s": fb / (f_ms / 1e3) / 1e9, "frac": fb / (f_ms / 1e3) / 1e9 / peak},
                            "backward": {"GB/s": bb / (b_ms / 1e3) / 1e9, "frac": bb / (b_ms / 1e3) / 1e9 / peak}},
@@ -249,77 +478,63 @@ def conv_leg(args, rank, world, dev, clk_index):
     }
 
 
-def c3_leg(args, rank, world, dev):
-    """C3: e3nn FullyConnectedTP-style uvw TP with one shared W (64x0e+64x1o+64x2e
-    x 0e+1o+2e, 11 kind-C paths), FP32 forward on the tcgen05 kernel
-    (3xTF32, A operand in TMEM). Per rank its own batch (replicas)."""
+def harness_check(args):
+    """CPU / gloo run of the multi-rank conv leg with the torch stand-in."""
     import torch
     import torch.distributed as dist
-
-    import paper_2501_13986_b200 as cgf
-    from oracle.oracle import config_json
-
-    plan = cgf.TpPlan(config_json("c3"))
-    R = args.c3_rows
-    g = torch.Generator(device=dev).manual_seed(99 + rank)
-    x = torch.randn((R, plan.dim_x), device=dev, generator=g)
-    y = torch.randn((R, plan.dim_y), device=dev, generator=g)
-    w = torch.randn((1, plan.n_w), device=dev, generator=g)
-    z = torch.empty((R, plan.dim_z), device=dev)
-    stream = torch.cuda.current_stream(dev)
-    for _ in range(max(3, args.warmup)):
-        plan.forward(x, y, w, z=z, w_shared=True)
-    torch.cuda.synchronize()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
-        dist.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(3, args.steps)
-    a.record(stream)
-    for _ in range(steps):
-        plan.forward(x, y, w, z=z, w_shared=True)
-    b.record(stream)
-    torch.cuda.synchronize()
-    ms = torch.tensor([a.elapsed_time(b) / steps], device=dev)
+        dist.init_process_group("gloo")
+    conv = conv_leg(args, rank, world, torch.device("cpu"), harness=True)
+    if rank == 0:
+        print(json.dumps({"harness": True, "n_gpus": world, "conv": conv}), flush=True)
     if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-    # backward on the same rows: gx (transposed forward), gz planes, gy, shared gW (+ its reduction)
-    gz = torch.randn((R, plan.dim_z), device=dev, generator=g)
-    outs = plan.backward(x, y, w, gz, w_shared=True)
-    torch.cuda.synchronize()
-    a.record(stream)
-    for _ in range(steps):
-        outs = plan.backward(x, y, w, gz, w_shared=True, out=outs)
-    b.record(stream)
-    torch.cuda.synchronize()
-    bms = torch.tensor([a.elapsed_time(b) / steps], device=dev)
-    if world > 1:
-        dist.all_reduce(bms, op=dist.ReduceOp.MAX)
-    bms = float(bms.item())
-    del outs, gz
-    byts = (plan.dim_x + plan.dim_y + plan.dim_z) * 4 * R + plan.n_w * 4
-    peak, _ = measured_peak()
-    return {"workload": "c3: 64x0e+64x1o+64x2e x 0e+1o+2e -> 64x0e+64x1o+64x2e, 11 uvw paths, shared W, fwd (+ bwd)",
-            "backward_ms": bms, "backward_GFLOP/s": plan.flops_bwd * R * world / (bms / 1e3) / 1e9,
-            "kernel": "cgf_uvw_fwd_f32 (tcgen05 kind::tf32, 3xTF32, A in TMEM)", "rows_per_gpu": R,
-            "ms": ms, "rows_per_s": R * world / (ms / 1e3), "GFLOP/s": plan.flops_fwd * R * world / (ms / 1e3) / 1e9,
-            "GB/s": byts / (ms / 1e3) / 1e9, "hbm_frac": byts / (ms / 1e3) / 1e9 / peak, "dtype": "f32"}
+        dist.destroy_process_group()
 
+
+def respawn(args):
+    """`--gpus N` without a torch.distributed environment: re-launch this
+    script as N ranks (one per GPU) under torch.distributed.run."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+# ---------------------------------------------------------------- main -----
 
 def main():
     args = parse()
+    if args.cpu_baseline_only:
+        print(json.dumps(cpu_baseline(args.dtype, args.cpu_rows)), flush=True)
+        return 0
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return respawn(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.harness_check:
+        return harness_check(args)
 
-    import numpy as np
+    # the CPU baseline first, in its own process, before CUDA is initialised here
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline_subprocess(args)
+        except Exception as exc:  # the baseline must never sink the GPU line
+            cb = {"error": repr(exc)}
+
     import torch
     import torch.distributed as dist
 
     import paper_2501_13986_b200 as cgf
-    from oracle.oracle import config_json
+    from paper_2501_13986_b200 import dist as cdist
+    from paper_2501_13986_b200.configs import config_json
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -327,6 +542,8 @@ def main():
     dev = torch.device("cuda", local)
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     es = 4 if args.dtype == "f32" else 8
+    dcode = cgf.F32 if args.dtype == "f32" else cgf.F64
+    peak, peak_kind = measured_peak()
     plan = cgf.TpPlan(config_json(CONFIG))
     R = args.rows
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -335,6 +552,7 @@ def main():
     w = torch.randn((R, plan.n_w), device=dev, dtype=tdt, generator=g)
     gz = torch.randn((R, plan.dim_z), device=dev, dtype=tdt, generator=g)
     z = torch.empty((R, plan.dim_z), device=dev, dtype=tdt)
+    grads = plan.backward(x, y, w, gz)
     stream = torch.cuda.current_stream(dev)
 
     fwd_ev, bwd_ev = [], []
@@ -346,12 +564,11 @@ def main():
         plan.forward(x, y, w, z=z)
         if record:
             e1.record(stream)
-        out = plan.backward(x, y, w, gz)
+        plan.backward(x, y, w, gz, out=grads)
         if record:
             e2.record(stream)
             fwd_ev.append((e0, e1))
             bwd_ev.append((e1, e2))
-        return out
 
     for _ in range(args.warmup):
         step()
@@ -369,101 +586,117 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ms = start.elapsed_time(stop)
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
     fwd_ms = sum(a.elapsed_time(b) for a, b in fwd_ev) / len(fwd_ev)
     bwd_ms = sum(a.elapsed_time(b) for a, b in bwd_ev) / len(bwd_ev)
+    ms, fwd_ms, bwd_ms = max_over_ranks([start.elapsed_time(stop), fwd_ms, bwd_ms], dev, world)
 
     flops_row = plan.flops_fwd + plan.flops_bwd
     value = flops_row * R * world * args.steps / (ms / 1e3) / 1e9
     # Algorithmic (compulsory) bytes per launch: every input read once, every
     # output written once: fwd (x+y+W+z), bwd (2x+2y+2W+z) words/row.
-    fwd_bytes = (plan.dim_x + plan.dim_y + plan.n_w + plan.dim_z) * es * R
-    bwd_bytes = (2 * plan.dim_x + 2 * plan.dim_y + 2 * plan.n_w + plan.dim_z) * es * R
-    peak, peak_kind = measured_peak()
-    kern = {"forward": {"ms": fwd_ms, "gbs": fwd_bytes / (fwd_ms / 1e3) / 1e9, "bytes": fwd_bytes},
-            "backward": {"ms": bwd_ms, "gbs": bwd_bytes / (bwd_ms / 1e3) / 1e9, "bytes": bwd_bytes}}
+    fwd_bytes = sum(plan.traffic(cgf.OP_FORWARD, R)) * es
+    bwd_bytes = sum(plan.traffic(cgf.OP_BACKWARD, R)) * es
+    kern = {"forward": {"ms": fwd_ms, "gbs": fwd_bytes / (fwd_ms / 1e3) / 1e9, "bytes": fwd_bytes, "op": 0},
+            "backward": {"ms": bwd_ms, "gbs": bwd_bytes / (bwd_ms / 1e3) / 1e9, "bytes": bwd_bytes, "op": 1}}
     dom = max(kern, key=lambda k: kern[k]["ms"])
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tfile):
-        try:  # per-launch DRAM bytes of this kernel from one ncu --set full capture (tools/ncu_traffic.py)
-            rec = json.load(open(tfile)).get(f"{CONFIG}_{args.dtype}_{dom}")
-            traffic = None if rec is None else rec["traffic_bytes"] * R / 1_000_000
-        except Exception:
-            traffic = None
-    roof = {"bound": "hbm", "kernel": f"cgf_tp_{'fwd' if dom == 'forward' else 'bwd'}_{args.dtype}",
-            "achieved": kern[dom]["gbs"], "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-            "frac": kern[dom]["gbs"] / peak, "traffic": traffic,
-            "algorithmic_bytes_per_launch": kern[dom]["bytes"],
+    kname = f"cgf_tp_{'fwd' if dom == 'forward' else 'bwd'}_{args.dtype}"
+    src_sha = kernel_source_sha(plan, kern[dom]["op"], dcode)
+    traffic, traffic_src = ncu_traffic(f"{CONFIG}_{args.dtype}_{dom}", src_sha, R)
+    roof = {"bound": "hbm", "kernel": kname, "achieved": kern[dom]["gbs"], "peak": peak, "peak_kind": peak_kind,
+            "unit": "GB/s", "frac": kern[dom]["gbs"] / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "kernel_source_sha16": src_sha, "algorithmic_bytes_per_launch": kern[dom]["bytes"],
             "per_kernel": {k: {"ms": v["ms"], "GB/s": v["gbs"], "frac": v["gbs"] / peak} for k, v in kern.items()}}
-
-    # End to end through the public API with HOST buffers: the C ABI host
-    # entry points (cgf_tp_forward_host / cgf_tp_backward_host via TpPlan on
-    # numpy arrays) copy each call's inputs in and outputs back, pipelined in
-    # row chunks on two streams; host wall clock around the synchronous calls.
-    Re = min(args.e2e_rows, R)
-    hx = x[:Re].cpu().pin_memory()
-    hy = y[:Re].cpu().pin_memory()
-    hw = w[:Re].cpu().pin_memory()
-    hg = gz[:Re].cpu().pin_memory()
-    oz = torch.empty((Re, plan.dim_z), dtype=tdt).pin_memory()
-    ogx = torch.empty((Re, plan.dim_x), dtype=tdt).pin_memory()
-    ogy = torch.empty((Re, plan.dim_y), dtype=tdt).pin_memory()
-    ogw = torch.empty((Re, plan.n_w), dtype=tdt).pin_memory()
-    nx_, ny_, nw_, ng_ = hx.numpy(), hy.numpy(), hw.numpy(), hg.numpy()
-    noz, ngx, ngy, ngw = oz.numpy(), ogx.numpy(), ogy.numpy(), ogw.numpy()
-
-    def e2e_step():
-        plan.forward(nx_, ny_, nw_, z=noz)
-        plan.backward(nx_, ny_, nw_, ng_, out=(ngx, ngy, ngw))
-
-    for _ in range(2):
-        e2e_step()
-    if world > 1:
-        dist.barrier()
-    ke = max(3, args.steps // 2)
-    t0 = time.perf_counter()
-    for _ in range(ke):
-        e2e_step()
-    ems = torch.tensor([(time.perf_counter() - t0) * 1e3 / ke], device=dev)
-    if world > 1:
-        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-    e2e_val = flops_row * Re * world / (float(ems.item()) / 1e3) / 1e9
-    # bytes actually copied: forward (x, y, W in; z out) + backward (x, y, W, gz in; gx, gy, gW out)
-    h2d = (2 * (hx.numel() + hy.numel() + hw.numel()) + hg.numel()) * es
-    d2h = (oz.numel() + ogx.numel() + ogy.numel() + ogw.numel()) * es
-
-    del x, y, w, gz, z, hx, hy, hw, hg, oz, ogx, ogy, ogw
+    del x, y, w, gz, z, grads
     torch.cuda.empty_cache()
-    c3 = None
-    if args.c3_rows > 0:
+
+    # ---- end to end through the public API with HOST buffers --------------
+    pcie = measure_pcie(dev)
+    Re = args.e2e_rows
+    gh = torch.Generator().manual_seed(99 + rank)
+    pin = lambda *s: torch.randn(s, dtype=tdt, generator=gh).pin_memory()
+    hx, hy, hw, hg = pin(Re, plan.dim_x), pin(Re, plan.dim_y), pin(Re, plan.n_w), pin(Re, plan.dim_z)
+    outs = [torch.empty(s, dtype=tdt).pin_memory() for s in
+            ((Re, plan.dim_z), (Re, plan.dim_x), (Re, plan.dim_y), (Re, plan.n_w))]
+    nin = [a.numpy() for a in (hx, hy, hw, hg)]
+    nout = tuple(a.numpy() for a in outs)
+
+    def e2e_fused():
+        plan.forward_backward(*nin, out=nout)
+
+    def e2e_separate():
+        plan.forward(nin[0], nin[1], nin[2], z=nout[0])
+        plan.backward(*nin, out=nout[1:])
+
+    e2e = {}
+    ke = max(3, args.steps // 2)
+    for name, fn in (("fused", e2e_fused), ("separate", e2e_separate)):
+        for _ in range(2):
+            fn()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            fn()
+        e2e[name] = max_over_ranks([(time.perf_counter() - t0) * 1e3 / ke], dev, world)[0]
+    in_b = sum(a.numel() for a in (hx, hy, hw, hg)) * es
+    out_b = sum(a.numel() for a in outs) * es
+    sep_h2d = in_b + (hx.numel() + hy.numel() + hw.numel()) * es  # the backward re-uploads x, y, W
+    e2e_val = flops_row * Re * world / (e2e["fused"] / 1e3) / 1e9
+    pcie_bound_ms = max(in_b / pcie["h2d_GBps"], out_b / pcie["d2h_GBps"],
+                        (in_b + out_b) / pcie["bidirectional_GBps"]) / 1e6
+    e2e_line = {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": in_b, "d2h_bytes_per_step": out_b,
+                "rows_per_step": Re, "ms_per_step": e2e["fused"],
+                "path": "pinned host arrays -> TpPlan.forward_backward -> cgf_tp_forward_backward_host (C ABI; "
+                        "row chunks pipelined on 3 streams: H2D | fwd+bwd kernels | D2H) -> pinned host",
+                "timer": "host wall clock, max over ranks",
+                "pcie": pcie, "pcie_bound_ms": pcie_bound_ms, "pcie_frac": pcie_bound_ms / e2e["fused"],
+                "separate_calls": {"value": flops_row * Re * world / (e2e["separate"] / 1e3) / 1e9,
+                                   "ms_per_step": e2e["separate"], "h2d_bytes_per_step": sep_h2d,
+                                   "d2h_bytes_per_step": out_b,
+                                   "path": "TpPlan.forward then TpPlan.backward (cgf_tp_forward_host, "
+                                           "cgf_tp_backward_host)"}}
+    del hx, hy, hw, hg, outs, nin, nout
+    torch.cuda.empty_cache()
+
+    # ---- sub-legs ------------------------------------------------------------
+    legs = {}
+    want = [s for s in args.legs.split(",") if s]
+    ls = args.leg_steps
+
+    def run_leg(name, fn):
         try:
-            c3 = c3_leg(args, rank, world, dev)
-        except Exception as exc:
-            c3 = {"error": repr(exc)}
+            legs[name] = fn()
+        except Exception as exc:  # report, never sink the headline line
+            legs[name] = {"error": repr(exc)[:400]}
         torch.cuda.empty_cache()
+
+    if "c1" in want:
+        c1 = cgf.TpPlan(config_json("c1"))
+        run_leg("c1", lambda: tp_leg(cgf, c1, "c1: 32x0e+32x1o+32x2e x 0e+1o+2e, 15 uvu paths (BASELINE configs[0])",
+                                     50_000, "f32", ("forward", "backward"), max(20, ls), dev, world, peak=peak))
+    if "c2f64" in want:
+        run_leg("c2_f64", lambda: tp_leg(cgf, plan, "c2 FP64", 1_000_000, "f64", ("forward", "backward"), ls, dev,
+                                         world, peak=peak))
+    if "c3" in want:
+        c3 = cgf.TpPlan(config_json("c3"))
+        run_leg("c3", lambda: tp_leg(cgf, c3, "c3: 64x0e+64x1o+64x2e x 0e+1o+2e, 11 uvw paths, shared W "
+                                              "(tcgen05 kind::tf32, 3xTF32)", 1_000_000, "f32",
+                                     ("forward", "backward"), ls, dev, world, w_shared=True, peak=peak))
+    if "c4" in want and world == 1:
+        run_leg("c4", lambda: conv_single_leg(cgf, cdist, "c4", "c2", 29,
+                                              (("f32", ("forward", "backward", "double_backward")),
+                                               ("f64", ("forward", "backward"))), ls, dev, peak))
     conv = None
     if args.conv_n > 0:
         try:
-            conv = conv_leg(args, rank, world, dev, local)
+            conv = conv_leg(args, rank, world, dev)
         except Exception as exc:  # report, never sink the headline line
-            conv = {"error": repr(exc)}
+            conv = {"error": repr(exc)[:400]}
         torch.cuda.empty_cache()
-
-    cb = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cb = cpu_baseline(args.dtype, args.cpu_rows)
-        except Exception as exc:  # the baseline must never sink the GPU line
-            cb = {"error": repr(exc)}
 
     if rank == 0:
         line = {
-            "metric": "CG TP fwd+bwd GFLOP/s (C2 MACE-large uvu)", "value": value, "unit": "GFLOP/s",
+            "metric": METRIC, "value": value, "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (torch.randn inputs of the C2 shapes)",
@@ -473,17 +706,17 @@ def main():
                        "rows_per_s": R * world * args.steps / (ms / 1e3)},
             "roofline": roof,
             "cpu_baseline": cb,
-            "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "rows_per_step": Re, "path": "pinned host arrays -> TpPlan.forward/backward -> cgf_tp_*_host (C ABI; chunked, 2 streams) -> pinned host", "timer": "host wall clock"},
+            "e2e": e2e_line,
             "gpu_launches": 2 * args.steps,  # TP leg: one forward + one backward kernel per step
             "conv": conv,
-            "c3": c3,
+            "legs": legs,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

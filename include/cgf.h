@@ -116,6 +116,14 @@ int cgf_tp_forward_host(cgf_plan* plan, int dtype, const void* x, const void* y,
                         void* z, int64_t rows, int w_shared);
 int cgf_tp_backward_host(cgf_plan* plan, int dtype, const void* x, const void* y, const void* w,
                          const void* gz, void* gx, void* gy, void* gw, int64_t rows, int w_shared);
+/* Forward and backward of the same rows in ONE pipelined host pass (a
+ * training step's TP: z = TP(x, y, W) and (gx, gy, gw) from a given gz, as
+ * TpPlan::forward followed by TpPlan::backward, engine.hpp:82-88): x, y and W
+ * cross PCIe once, and host->device / device->host copies of different row
+ * chunks overlap. Same results as the two calls. */
+int cgf_tp_forward_backward_host(cgf_plan* plan, int dtype, const void* x, const void* y, const void* w,
+                                 const void* gz, void* z, void* gx, void* gy, void* gw, int64_t rows,
+                                 int w_shared);
 int cgf_tp_double_backward_host(cgf_plan* plan, int dtype, const void* x, const void* y,
                                 const void* w, const void* gz, const void* da, const void* db,
                                 const void* dc, void* ox, void* oy, void* ow, void* ogz,

@@ -113,6 +113,7 @@ def lib():
     L.cgf_tp_forward_host.argtypes = [P, I, P, P, P, P, I64, I]
     L.cgf_tp_backward_host.argtypes = [P, I] + [P] * 7 + [I64, I]
     L.cgf_tp_double_backward_host.argtypes = [P, I] + [P] * 11 + [I64, I]
+    L.cgf_tp_forward_backward_host.argtypes = [P, I] + [P] * 8 + [I64, I]
     L.cgf_tp_stats.argtypes = [P, I, I64, I, P]
     L.cgf_tp_traffic.argtypes = [P, I, I64, I, P]
     L.cgf_plan_schedule_json.argtypes = [P, C.c_char_p, I]
@@ -345,6 +346,31 @@ class TpPlan:
         else:
             _check(lib().cgf_tp_backward_host(self._h, dt, *args, rows, int(w_shared)))
         return gx, gy, gw
+
+    def forward_backward(self, x, y, w, gz, w_shared=False, out=None):
+        """z = forward(x, y, w) and (gx, gy, gw) = backward(x, y, w, gz) in one
+        call: on the device the two kernels run back to back on the current
+        stream; with host (numpy) arrays one pipelined pass through
+        cgf_tp_forward_backward_host moves x, y and W over PCIe once.
+        ``out``: optional preallocated (z, gx, gy, gw). Returns (z, gx, gy, gw)."""
+        if _is_torch(x):
+            z, gxyw = (None, None) if out is None else (out[0], out[1:])
+            z = self.forward(x, y, w, z=z, w_shared=w_shared)
+            return (z,) + tuple(self.backward(x, y, w, gz, w_shared=w_shared, out=gxyw))
+        x, y, w, gz = (self._host(a) for a in (x, y, w, gz))
+        self._same(x, y, w, gz)
+        rows = self._rows(x, y, w, w_shared)
+        if tuple(gz.shape) != (rows, self.dim_z):
+            raise ShapeError(f"shape mismatch for g_z: expected ({rows}, {self.dim_z}), got {tuple(gz.shape)}")
+        shapes = ((rows, self.dim_z), (rows, self.dim_x), (rows, self.dim_y), (1 if w_shared else rows, self.n_w))
+        if out is None:
+            out = tuple(self._empty_like(x, s) for s in shapes)
+        for name, a, shp in zip(("z", "gx", "gy", "gw"), out, shapes):
+            self._out(name, a, shp)
+        self._same(x, *out)
+        _check(lib().cgf_tp_forward_backward_host(self._h, _dtype_code(x), *(self._p(a) for a in (x, y, w, gz)),
+                                                  *(self._p(a) for a in out), rows, int(w_shared)))
+        return tuple(out)
 
     def double_backward(self, x, y, w, gz, upstream, w_shared=False):
         """Given upstream = (dL/da, dL/db, dL/dC) of backward's outputs, returns

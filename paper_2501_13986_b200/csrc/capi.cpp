@@ -41,9 +41,10 @@ struct cgf_plan {
   std::map<ScratchKey, CUdeviceptr> wimg;
   std::map<ScratchKey, std::size_t> scratch_cap;  // bytes of each buffer in wimg
   // host-pointer path: two streams + double-buffered device staging per context
+  static constexpr int kPipe = 3;  // chunks in flight: H2D(c+1) | kernels(c) | D2H(c-1)
   struct HostPipe {
-    CUstream s[2] = {nullptr, nullptr};
-    CUdeviceptr buf[2] = {0, 0};
+    CUstream s[kPipe] = {};
+    CUdeviceptr buf[kPipe] = {};
     std::size_t cap = 0;
   };
   std::map<CUcontext, HostPipe> pipes;
@@ -56,7 +57,7 @@ struct cgf_plan {
       if (cur == std::get<0>(key)) cgf::drv::cuMemFree(ptr);
     for (auto& [ctx, pp] : pipes)
       if (cur == ctx) {
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kPipe; ++k) {
           if (pp.buf[k]) cgf::drv::cuMemFree(pp.buf[k]);
           if (pp.s[k]) cgf::drv::cuStreamDestroy(pp.s[k]);
         }
@@ -851,11 +852,18 @@ struct HostCall {
 
 namespace {
 
-// Host-pointer path: rows stream through the GPU in chunks on two streams, so
-// one chunk's host->device copy, the previous chunk's kernel and the one
-// before's device->host copy overlap (PCIe is full duplex). Device staging is
+// Host-pointer path: rows stream through the GPU in chunks, each chunk on one
+// of kPipe streams with its own device staging, so one chunk's host->device
+// copy, another's kernels and a third's device->host copy overlap (PCIe is
+// full duplex: the two directions run on separate copy engines). Staging is
 // cached per plan and context. A shared-W backward reduces over all rows, so
 // it runs as one chunk.
+//
+// op CGF_OP_FORWARD / BACKWARD / DOUBLE_BACKWARD, or kFwdBwd: forward and
+// backward of the same rows in one pass (inputs x, y, w, gz; outputs z, gx,
+// gy, gw), so x, y and W cross PCIe once for both.
+constexpr int kFwdBwd = 3;
+
 void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, const void* const in[7],
               void* const out[4]) {
   const auto& pr = p->problem;
@@ -869,6 +877,8 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
   bool orow[4] = {true, true, true, true};
   if (op == CGF_OP_FORWARD) {
     ow[0] = pr.dim_z;
+  } else if (op == kFwdBwd) {  // z, gx, gy, gw
+    ow[0] = pr.dim_z; ow[1] = pr.dim_x; ow[2] = pr.dim_y; ow[3] = pr.n_w; orow[3] = !ws;
   } else {
     ow[0] = pr.dim_x; ow[1] = pr.dim_y; ow[2] = pr.n_w; orow[2] = !ws;
     if (op == CGF_OP_DOUBLE_BACKWARD) ow[3] = pr.dim_z;
@@ -881,8 +891,10 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
   const bool one_chunk = ws && op != CGF_OP_FORWARD;
   std::int64_t chunk = rows;
   if (!one_chunk) {
-    const std::int64_t target = static_cast<std::int64_t>((256ull << 20) / std::max<std::size_t>(1, row_words * es));
-    chunk = std::min<std::int64_t>(rows, std::max<std::int64_t>(4096, target / 128 * 128));
+    // ~128 MB of staging per chunk: large enough that each copy runs at PCIe
+    // speed, small enough that the pipeline fills quickly
+    const std::int64_t target = static_cast<std::int64_t>((128ull << 20) / std::max<std::size_t>(1, row_words * es));
+    chunk = std::min<std::int64_t>(rows, std::max<std::int64_t>(1024, target / 128 * 128));
   }
   const std::size_t need = (fixed_words + static_cast<std::size_t>(chunk) * row_words) * es + 11 * 256;
   CUcontext ctx = cgf::ensure_context();
@@ -892,13 +904,15 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
     std::lock_guard<std::mutex> g(p->mu);
     pipe = &p->pipes[ctx];
   }
-  if (!pipe->s[0]) {
-    CU_CHECK(cgf::drv::cuStreamCreate(&pipe->s[0], CU_STREAM_NON_BLOCKING));
-    CU_CHECK(cgf::drv::cuStreamCreate(&pipe->s[1], CU_STREAM_NON_BLOCKING));
-  }
+  constexpr int K = cgf_plan::kPipe;
+  if (!pipe->s[0])
+    for (int k = 0; k < K; ++k) CU_CHECK(cgf::drv::cuStreamCreate(&pipe->s[k], CU_STREAM_NON_BLOCKING));
   if (pipe->cap < need) {
-    for (int k = 0; k < 2; ++k) {
-      if (pipe->buf[k]) cgf::drv::cuMemFree(pipe->buf[k]);
+    for (int k = 0; k < K; ++k) {
+      if (pipe->buf[k]) {
+        CU_CHECK(cgf::drv::cuStreamSynchronize(pipe->s[k]));
+        cgf::drv::cuMemFree(pipe->buf[k]);
+      }
       pipe->buf[k] = 0;
       CU_CHECK(cgf::drv::cuMemAlloc(&pipe->buf[k], need));
     }
@@ -906,7 +920,7 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
   }
   const std::int64_t nchunks = (rows + chunk - 1) / chunk;
   for (std::int64_t c = 0; c < nchunks; ++c) {
-    const int k = static_cast<int>(c & 1);
+    const int k = static_cast<int>(c % K);
     CUstream st = pipe->s[k];
     const std::int64_t r0 = c * chunk, n = std::min(chunk, rows - r0);
     std::size_t off = 0;
@@ -921,7 +935,7 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
       const std::size_t words = irow[i] ? iw[i] * static_cast<std::size_t>(n) : iw[i];
       const CUdeviceptr d = carve(irow[i] ? iw[i] * static_cast<std::size_t>(chunk) : iw[i]);
       din[i] = reinterpret_cast<void*>(d);
-      if (irow[i] || c < 2) {
+      if (irow[i] || c < K) {  // a shared W is uploaded once per staging buffer
         const char* h = static_cast<const char*>(in[i]) + (irow[i] ? es * iw[i] * static_cast<std::size_t>(r0) : 0);
         CU_CHECK(cgf::drv::cuMemcpyHtoDAsync(d, h, words * es, st));
       }
@@ -929,8 +943,15 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
     void* dout[4] = {};
     for (int i = 0; i < 4; ++i)
       if (out[i]) dout[i] = reinterpret_cast<void*>(carve(orow[i] ? ow[i] * static_cast<std::size_t>(chunk) : ow[i]));
-    launch(p, op, dtype, w_shared, n, din[0], din[1], din[2], din[3], din[4], din[5], din[6], dout[0], dout[1], dout[2],
-           dout[3], st);
+    if (op == kFwdBwd) {
+      launch(p, CGF_OP_FORWARD, dtype, w_shared, n, din[0], din[1], din[2], nullptr, nullptr, nullptr, nullptr, dout[0],
+             nullptr, nullptr, nullptr, st);
+      launch(p, CGF_OP_BACKWARD, dtype, w_shared, n, din[0], din[1], din[2], din[3], nullptr, nullptr, nullptr, dout[1],
+             dout[2], dout[3], nullptr, st);
+    } else {
+      launch(p, op, dtype, w_shared, n, din[0], din[1], din[2], din[3], din[4], din[5], din[6], dout[0], dout[1],
+             dout[2], dout[3], st);
+    }
     for (int i = 0; i < 4; ++i) {
       if (!out[i]) continue;
       const std::size_t words = orow[i] ? ow[i] * static_cast<std::size_t>(n) : ow[i];
@@ -938,8 +959,7 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
       CU_CHECK(cgf::drv::cuMemcpyDtoHAsync(h, reinterpret_cast<CUdeviceptr>(dout[i]), words * es, st));
     }
   }
-  CU_CHECK(cgf::drv::cuStreamSynchronize(pipe->s[0]));
-  CU_CHECK(cgf::drv::cuStreamSynchronize(pipe->s[1]));
+  for (int k = 0; k < K; ++k) CU_CHECK(cgf::drv::cuStreamSynchronize(pipe->s[k]));
 }
 
 }  // namespace
@@ -965,6 +985,28 @@ int cgf_tp_backward_host(cgf_plan* p, int dtype, const void* x, const void* y, c
     const void* in[7] = {x, y, w, gz, nullptr, nullptr, nullptr};
     void* out[4] = {gx, gy, gw, nullptr};
     run_host(p, CGF_OP_BACKWARD, dtype, w_shared, rows, in, out);
+  });
+}
+
+int cgf_tp_forward_backward_host(cgf_plan* p, int dtype, const void* x, const void* y, const void* w,
+                                 const void* gz, void* z, void* gx, void* gy, void* gw, int64_t rows, int w_shared) {
+  return guarded([&] {
+    need(p, "plan");
+    if (rows <= 0) return;
+    need(x, "x"); need(y, "y"); need(w, "w"); need(gz, "gz");
+    need(z, "z"); need(gx, "gx"); need(gy, "gy"); need(gw, "gw");
+    if (w_shared) {  // the shared gW reduces over every row: two passes
+      const void* fin[7] = {x, y, w, nullptr, nullptr, nullptr, nullptr};
+      void* fout[4] = {z, nullptr, nullptr, nullptr};
+      run_host(p, CGF_OP_FORWARD, dtype, w_shared, rows, fin, fout);
+      const void* bin[7] = {x, y, w, gz, nullptr, nullptr, nullptr};
+      void* bout[4] = {gx, gy, gw, nullptr};
+      run_host(p, CGF_OP_BACKWARD, dtype, w_shared, rows, bin, bout);
+      return;
+    }
+    const void* in[7] = {x, y, w, gz, nullptr, nullptr, nullptr};
+    void* out[4] = {z, gx, gy, gw};
+    run_host(p, kFwdBwd, dtype, w_shared, rows, in, out);
   });
 }
 

@@ -10,7 +10,9 @@ their gradients). Per direction there is exactly one exchange step:
                     then the local fused conv writes its own node_z rows;
 * backward:         local conv backward over the shard's transposed CSR gives
                     PARTIAL g_node_x for every neighbour row, reduce-scattered
-                    back to the owners (the adjoint of the all-gather);
+                    back to the owners (the adjoint of the all-gather) as an
+                    all-to-all + a rank-ordered sum, so FP64 results are
+                    bitwise reproducible on any rank count's NCCL setup;
                     g_edge_y / g_edge_w are local;
 * double-backward:  all-gather node_x and dL/dg_node_x, reduce-scatter
                     dL/dnode_x; dL/dg_node_z and per-edge terms are local.
@@ -18,7 +20,7 @@ their gradients). Per direction there is exactly one exchange step:
 There is no weight all-reduce: the reference's conv weights are per edge. The
 all-gathered layout is padded: rank r's rows sit at [r*chunk, r*chunk + n_r)
 of a P*chunk buffer (``chunk`` = the largest range), so every collective is a
-plain equal-split NCCL all_gather_into_tensor / reduce_scatter_tensor, and
+plain equal-split NCCL all_gather_into_tensor / all_to_all_single, and
 ``GraphShard.nbr`` is pre-remapped into that padded index space on the host.
 
 The local compute is ``ConvPlan.*_shard`` (the generated sm_100a kernels via
@@ -126,14 +128,24 @@ class DistConvPlan:
         return out
 
     def _reduce_scatter(self, partial):
-        """[world * chunk, d] partial sums -> this rank's [out_nodes, d] totals."""
+        """[world * chunk, d] partial sums -> this rank's [out_nodes, d] totals.
+
+        Deterministic: an all-to-all delivers every rank's partial rows of this
+        rank's range (the same bytes a reduce-scatter moves), then they are
+        summed here in rank order, so the result does not depend on the NCCL
+        algorithm / protocol or on the number of channels (a plain
+        reduce_scatter_tensor may reduce in any order)."""
         import torch.distributed as dist
         sh = self.shard
         if sh.world == 1:
             return partial[:sh.out_nodes]
-        out = partial.new_empty((sh.chunk, partial.shape[1]))
-        dist.reduce_scatter_tensor(out, partial, group=self.group)
-        return out[:sh.out_nodes]
+        parts = partial.new_empty(partial.shape)
+        dist.all_to_all_single(parts, partial.contiguous(), group=self.group)
+        parts = parts.view(sh.world, sh.chunk, partial.shape[1])
+        out = parts[0, :sh.out_nodes].clone()
+        for r in range(1, sh.world):
+            out += parts[r, :sh.out_nodes]
+        return out
 
     # -- the three entry points -------------------------------------------------
     def forward(self, node_x, edge_y, edge_w):

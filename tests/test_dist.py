@@ -194,3 +194,23 @@ def test_gloo_distributed_conv_matches_whole_graph(world, tmp_path):
                     ("oy", want_d[1]), ("ow", want_d[2]), ("ogz", want_d[3])):
         assert cat[k].shape == want.shape, k
         assert O.rel_error(cat[k], want) <= 1e-12, k
+
+
+def test_bench_gpus_2_launches_two_ranks_cpu_harness():
+    """`bench.py --gpus 2` re-launches itself as 2 torch.distributed ranks; the
+    CPU harness mode (gloo, a torch stand-in for the shard kernels) runs the
+    multi-rank conv leg's partition / collectives / max-over-ranks plumbing
+    and rank 0 prints one line with n_gpus 2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--harness-check",
+                        "--conv-n", "6", "--conv-steps", "1", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    rec = json.loads(lines[0])
+    assert rec["harness"] and rec["n_gpus"] == 2 and rec["conv"]["n_gpus"] == 2
+    assert "all_to_all_single" in rec["conv"]["collectives"]

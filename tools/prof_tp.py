@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_2501_13986_b200 as cgf  # noqa: E402
-from oracle.oracle import config_json  # noqa: E402
+from paper_2501_13986_b200.configs import config_json  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
