@@ -169,6 +169,12 @@ int cgf_conv_stats(const cgf_plan* plan, int op, int mode, int unfused, int64_t 
 int cgf_plan_kernel_source(cgf_plan* plan, int comp, int loop, int dtype, int w_shared, int aligned, char* buf,
                            int cap);
 int cgf_plan_kernel_compile(cgf_plan* plan, int comp, int loop, int dtype, int w_shared, int aligned);
+/* Kernels per call of (comp, loop): the by-neighbour conv and the batched
+ * double-backward run their units in groups, one kernel each,
+ * and one group's source. */
+int cgf_plan_kernel_groups(const cgf_plan* plan, int comp, int loop, int dtype);
+int cgf_plan_kernel_source_group(cgf_plan* plan, int comp, int loop, int dtype, int w_shared, int aligned,
+                                 int group, char* buf, int cap);
 
 /* ---- fused tensor product + graph convolution (device pointers) ---------- */
 

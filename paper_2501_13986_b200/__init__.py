@@ -121,6 +121,8 @@ def lib():
     L.cgf_conv_stats.argtypes = [P, I, I, I, I64, I64, P]
     L.cgf_plan_kernel_source.argtypes = [P, I, I, I, I, I, C.c_char_p, I]
     L.cgf_plan_kernel_compile.argtypes = [P, I, I, I, I, I]
+    L.cgf_plan_kernel_groups.argtypes = [P, I, I, I]
+    L.cgf_plan_kernel_source_group.argtypes = [P, I, I, I, I, I, I, C.c_char_p, I]
     L.cgf_conv_transpose_host.argtypes = [I64, I64, P, P, P, P, P]
     L.cgf_conv_forward.argtypes = [P, I, I64, I64, P, P, P, P, P, P, I, P]
     L.cgf_conv_backward.argtypes = [P, I, I64, I64] + [P] * 12 + [I, P]
@@ -763,6 +765,15 @@ def _kernel_source(plan: TpPlan, comp, loop, dtype=F32, w_shared=False, aligned=
     buf = C.create_string_buffer(n + 1)
     lib().cgf_plan_kernel_source(plan._h, comp, loop, dtype, int(w_shared), int(aligned), buf, n + 1)
     return buf.value.decode()
+
+
+def _kernel_groups(plan: TpPlan, comp, loop, dtype=F32) -> int:
+    return lib().cgf_plan_kernel_groups(plan._h, comp, loop, dtype)
+
+
+def _kernel_source_group(plan: TpPlan, comp, loop, dtype, group, w_shared=False, aligned=True) -> str:
+    return TpPlan._text(lib().cgf_plan_kernel_source_group, plan._h, comp, loop, dtype, int(w_shared), int(aligned),
+                        group)
 
 
 def _kernel_compile(plan: TpPlan, comp, loop, dtype=F32, w_shared=False, aligned=True):

@@ -8,6 +8,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -118,14 +119,69 @@ bool covers(const std::vector<std::pair<std::uint32_t, std::uint32_t>>& pieces, 
   return true;
 }
 
+// The by-neighbour conv kernels (backward, double-backward pass 2) gather
+// g_node_z[s] (dim_z words) for every edge; the rows of the sources a grid
+// works on at one time exceed L2 when dim_z is large (C4: ~6K rows x 36 KB).
+// Running the units in G groups, one kernel launch each, shrinks each pass's
+// gz working set (and the per-warp gx accumulator) G-fold; per-edge gy is
+// summed across the groups in group order. G from the row size; CGF_CONVI_GROUPS
+// overrides.
+int convi_groups(const cgf_plan* p, int dtype) {
+  if (const char* env = std::getenv("CGF_CONVI_GROUPS")) return std::clamp(std::atoi(env), 1, static_cast<int>(p->units.size()));
+  const std::size_t zbytes = static_cast<std::size_t>(p->problem.dim_z) * (dtype == CGF_F64 ? 8 : 4);
+  return std::clamp(static_cast<int>((zbytes + 16383) / 16384), 1, static_cast<int>(p->units.size()));
+}
+
+// The batched double-backward computes seven ops per CG entry: with every unit
+// in one kernel its code overflows the instruction cache (no_instruction was
+// its top stall, profiles/r01_ncu_v8_dbwd.txt). Units split into groups, one
+// kernel each, keep each kernel's code small; the only shared outputs are the
+// per-row dy (dim_y words, summed in group order). CGF_ROW_GROUPS overrides.
+int row_groups(const cgf_plan* p, cgf::Comp comp, int dtype) {
+  const int nu = static_cast<int>(p->units.size());
+  if (comp != cgf::Comp::DBwd) return 1;
+  if (const char* env = std::getenv("CGF_ROW_GROUPS")) return std::clamp(std::atoi(env), 1, nu);
+  (void)dtype;
+  return 1;
+}
+
+int kernel_groups(const cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype) {
+  if (loop == cgf::Loop::ConvByInput) return convi_groups(p, dtype);
+  if (loop == cgf::Loop::Rows) return row_groups(p, comp, dtype);
+  return 1;
+}
+
+// n contiguous, non-empty runs of units with about equal z words each.
+std::vector<std::pair<int, int>> unit_groups(const cgf_plan* p, int n) {
+  const int m = static_cast<int>(p->units.size());
+  n = std::clamp(n, 1, std::max(m, 1));
+  std::vector<std::uint64_t> pre(m + 1, 0);  // z words of units [0, u)
+  for (int u = 0; u < m; ++u) {
+    pre[u + 1] = pre[u];
+    for (const auto& z : p->units[u].z_pieces) pre[u + 1] += z.words;
+  }
+  std::vector<std::pair<int, int>> out;
+  int b = 0;
+  for (int g = 0; g < n; ++g) {
+    int e = m;
+    if (g + 1 < n) {
+      e = b + 1;
+      while (e < m - (n - 1 - g) && pre[e] * n < pre[m] * (g + 1)) ++e;
+    }
+    out.emplace_back(b, e);
+    b = e;
+  }
+  return out;
+}
+
 std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype,
-                                              int w_shared, int aligned) {
+                                              int w_shared, int aligned, int group = 0, int ngroups = 1) {
   if (dtype != CGF_F32 && dtype != CGF_F64) throw std::invalid_argument("bad dtype");
   std::lock_guard<std::mutex> g(p->mu);
   const char* env = std::getenv("CGF_GEN");
   const std::string flags = env ? env : "";
   const auto key = std::make_tuple(static_cast<int>(comp), static_cast<int>(loop), dtype, w_shared ? 1 : 0,
-                                   aligned ? 1 : 0, flags);
+                                   aligned ? 1 : 0, flags + "|" + std::to_string(group) + "/" + std::to_string(ngroups));
   auto it = p->sources.find(key);
   if (it != p->sources.end()) return it->second;
   if (w_shared && comp != cgf::Comp::Fwd && !(comp == cgf::Comp::Bwd && cgf::uvw_eligible(p->problem) && dtype == CGF_F32))
@@ -178,7 +234,15 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
     if (small && (loop == cgf::Loop::ConvByOutput || loop == cgf::Loop::ConvByInput)) cfg.par_bulk = true;
   }
   cgf::apply_gen_flags(cfg, flags);
-  auto ks = std::make_shared<cgf::KernelSource>(cgf::generate_kernel(p->problem, p->units, cfg));
+  std::vector<cgf::Unit> subset;
+  if (ngroups > 1) {
+    const auto grp = unit_groups(p, ngroups).at(group);
+    subset.assign(p->units.begin() + grp.first, p->units.begin() + grp.second);
+    cfg.gy_accum = group > 0;
+    cfg.tag = "g" + std::to_string(group) + "of" + std::to_string(ngroups);
+  }
+  auto ks = std::make_shared<cgf::KernelSource>(
+      cgf::generate_kernel(p->problem, ngroups > 1 ? subset : p->units, cfg));
   p->sources.emplace(key, ks);
   return ks;
 }
@@ -255,16 +319,19 @@ void run_kernel(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype, int w_sh
   const std::int64_t items = loop == cgf::Loop::ConvEdges ? a.edges : a.rows;
   if (items <= 0) return;
   const bool al = aligned16({a.x, a.y, a.w, a.gz, a.da, a.db, a.dc, a.o0, a.o1, a.o2, a.o3});
-  const auto ks = source_for(p, comp, loop, dtype, w_shared, al);
-  const cgf::Kernel k = cgf::load_kernel(*ks);
-  const int warps = k.threads / 32;
-  const std::int64_t need = (items + warps - 1) / warps;
-  const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(need, k.max_grid));
-  Args c = a;
-  void* args[] = {&c.x, &c.y, &c.w, &c.gz, &c.da, &c.db, &c.dc, &c.o0, &c.o1, &c.o2, &c.o3, &c.rows,
-                  &c.rp, &c.nb, &c.eid, &c.edges};
-  CU_CHECK(cgf::drv::cuLaunchKernel(k.fn, grid, 1, 1, k.threads, 1, 1, k.smem_bytes,
-                                    reinterpret_cast<CUstream>(stream), args, nullptr));
+  const int ng = kernel_groups(p, comp, loop, dtype);
+  for (int grp = 0; grp < ng; ++grp) {
+    const auto ks = source_for(p, comp, loop, dtype, w_shared, al, grp, ng);
+    const cgf::Kernel k = cgf::load_kernel(*ks);
+    const int warps = k.threads / 32;
+    const std::int64_t need = (items + warps - 1) / warps;
+    const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(need, k.max_grid));
+    Args c = a;
+    void* args[] = {&c.x, &c.y, &c.w, &c.gz, &c.da, &c.db, &c.dc, &c.o0, &c.o1, &c.o2, &c.o3, &c.rows,
+                    &c.rp, &c.nb, &c.eid, &c.edges};
+    CU_CHECK(cgf::drv::cuLaunchKernel(k.fn, grid, 1, 1, k.threads, 1, 1, k.smem_bytes,
+                                      reinterpret_cast<CUstream>(stream), args, nullptr));
+  }
 }
 
 // The plan's uvw scratch buffer `name` for (current context, stream), at
@@ -1139,12 +1206,36 @@ int cgf_plan_kernel_source(cgf_plan* p, int comp, int loop, int dtype, int w_sha
   return rc == CGF_OK ? n : -rc;
 }
 
+int cgf_plan_kernel_groups(const cgf_plan* p, int comp, int loop, int dtype) {
+  if (!p || comp < 0 || comp > 4 || loop < 0 || loop > 3) return -CGF_E_INVALID;
+  return kernel_groups(p, static_cast<cgf::Comp>(comp), static_cast<cgf::Loop>(loop), dtype);
+}
+
+int cgf_plan_kernel_source_group(cgf_plan* p, int comp, int loop, int dtype, int w_shared, int aligned, int group,
+                                 char* buf, int cap) {
+  int n = 0;
+  const int rc = guarded([&] {
+    need(p, "plan");
+    if (comp < 0 || comp > 4 || loop < 0 || loop > 3) throw std::invalid_argument("bad comp / loop");
+    const int ng = cgf_plan_kernel_groups(p, comp, loop, dtype);
+    if (group < 0 || group >= ng) throw std::invalid_argument("kernel group out of range");
+    const auto ks = source_for(p, static_cast<cgf::Comp>(comp), static_cast<cgf::Loop>(loop), dtype, w_shared, aligned,
+                               group, ng);
+    n = copy_out(ks->source, buf, cap);
+  });
+  return rc == CGF_OK ? n : -rc;
+}
+
 int cgf_plan_kernel_compile(cgf_plan* p, int comp, int loop, int dtype, int w_shared, int aligned) {
   return guarded([&] {
     need(p, "plan");
     if (comp < 0 || comp > 4 || loop < 0 || loop > 3) throw std::invalid_argument("bad comp / loop");
-    const auto ks = source_for(p, static_cast<cgf::Comp>(comp), static_cast<cgf::Loop>(loop), dtype, w_shared, aligned);
-    cgf::compile_cubin(ks->source, ks->name);
+    const int ng = kernel_groups(p, static_cast<cgf::Comp>(comp), static_cast<cgf::Loop>(loop), dtype);
+    for (int grp = 0; grp < ng; ++grp) {
+      const auto ks = source_for(p, static_cast<cgf::Comp>(comp), static_cast<cgf::Loop>(loop), dtype, w_shared,
+                                 aligned, grp, ng);
+      cgf::compile_cubin(ks->source, ks->name);
+    }
   });
 }
 

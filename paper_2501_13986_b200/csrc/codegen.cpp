@@ -146,6 +146,12 @@ class Gen {
   int max_dz_ = 1, max_dx_ = 1, max_piece_ = 1;
   bool has_c_ = false;
   std::uint32_t scr_words_ = 0, off_zs_ = 0, off_wt_ = 0, off_ct_ = 0, off_gya_ = 0, off_gxs_ = 0;
+  // ConvByInput: the row's gx-type accumulator holds only this kernel's x
+  // chunks, packed: class k's unit kc, chunk c sits at
+  // gx_base_[k] + kc * gx_unit_[k] + gx_pre_[k][c] (affine in kc).
+  std::vector<std::uint32_t> gx_base_, gx_unit_;
+  std::vector<std::vector<std::uint32_t>> gx_pre_;
+  std::uint32_t gx_words_ = 0;
 
   bool reads_gz() const { return cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdX; }
   bool dual() const { return cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX; }
@@ -341,12 +347,25 @@ void Gen::layout() {
     L.words = std::max<std::uint32_t>(L.words, A());
     lay_.push_back(std::move(L));
   }
+  for (size_t k = 0; k < cls_.size(); ++k) {
+    const Unit& u = units_[cls_[k].u0];
+    std::vector<std::uint32_t> pre;
+    std::uint32_t w = 0;
+    for (const auto& xc : u.x_chunks) {
+      pre.push_back(w);
+      w += xc.words;
+    }
+    gx_base_.push_back(gx_words_);
+    gx_unit_.push_back(w);
+    gx_pre_.push_back(pre);
+    gx_words_ += w * static_cast<std::uint32_t>(cls_[k].n);
+  }
   const std::uint32_t stage = up(static_cast<std::uint32_t>(std::max(max_piece_, 32 * max_dx_)));
   scr_words_ = stage;
   off_gya_ = scr_words_;
   scr_words_ += up(static_cast<std::uint32_t>(p_.dim_y));
   off_gxs_ = scr_words_;
-  if (by_input()) scr_words_ += up(static_cast<std::uint32_t>(p_.dim_x));
+  if (by_input()) scr_words_ += up(gx_words_);
   off_zs_ = scr_words_;
   if (has_c_) {
     scr_words_ += up(2u * 32u * max_dz_);
@@ -793,13 +812,13 @@ void Gen::emit_gy_reduce(const std::string& rowexpr) {
     for (int j = j0; j < std::min(dy, j0 + 32); ++j)
       o_ << "      { const T s_ = warp_sum(gy[" << j << "]); if (lane == " << j - j0 << ") mine = s_; }\n";
     o_ << "      if (lane < " << std::min(dy - j0, 32) << ") O1[" << rowexpr << " * (i64)" << dy << " + " << j0
-       << " + lane] = mine; }\n";
+       << " + lane] " << (cfg_.gy_accum ? "+=" : "=") << " mine; }\n";
   }
 }
 
 void Gen::emit_gy_flush_row(const std::string& rowexpr) {
   o_ << "    __syncwarp();\n    for (int j = lane; j < " << p_.dim_y << "; j += 32) { O1[" << rowexpr << " * (i64)"
-     << p_.dim_y << " + j] = gya[j]; gya[j] = 0; }\n    __syncwarp();\n";
+     << p_.dim_y << " + j] " << (cfg_.gy_accum ? "+=" : "=") << " gya[j]; gya[j] = 0; }\n    __syncwarp();\n";
 }
 
 std::string zero_init(const std::string& name, int n) { return "T " + name + "[" + S(n) + "] = {};"; }
@@ -979,7 +998,8 @@ void Gen::emit_conv_loop() {
         const int dx = xdx[xc.off];
         o_ << "      if (lane < " << xb[xc.off] << ") {";
         for (int i = 0; i < dx; ++i)
-          o_ << " gxs[" << O(xc.off, C.xstep[c]) << " + lane * " << dx << " + " << i << "] += ax" << c << "[" << i << "];";
+          o_ << " gxs[" << O(gx_base_[k] + gx_pre_[k][c], gx_unit_[k]) << " + lane * " << dx << " + " << i << "] += ax" << c
+             << "[" << i << "];";
         o_ << " }\n";
       }
       emit_release();
@@ -992,13 +1012,23 @@ void Gen::emit_conv_loop() {
         emit_gy_reduce("eid");
     }
     o_ << "    }\n";
-    const bool vec = cfg_.aligned && al16(p_.dim_x);
+    // the row's packed x chunks -> their places in the output row
     o_ << "    __syncwarp();\n";
-    if (vec)
-      o_ << "    coop_store16(O0 + row * (i64)" << p_.dim_x << ", gxs, " << p_.dim_x * sz_ / 16 << ", lane);\n";
-    else
-      o_ << "    coop_store(O0 + row * (i64)" << p_.dim_x << ", gxs, " << p_.dim_x << ", lane);\n";
-    o_ << "    __syncwarp();\n    for (int j = lane; j < " << p_.dim_x << "; j += 32) gxs[j] = 0;\n    __syncwarp();\n";
+    for (size_t k = 0; k < cls_.size(); ++k) {
+      const UClass& C = cls_[k];
+      const Unit& u = U0(static_cast<int>(k));
+      o_ << "#pragma unroll 1\n    for (int kc = 0; kc < " << C.n << "; ++kc) {\n";
+      for (size_t c = 0; c < u.x_chunks.size(); ++c) {
+        const auto& xc = u.x_chunks[c];
+        const bool vec = cfg_.aligned && al16(p_.dim_x) && al16(xc.off) && al16(C.xstep[c]) && al16(xc.words) &&
+                         al16(gx_base_[k] + gx_pre_[k][c]) && al16(gx_unit_[k]);
+        o_ << "      " << (vec ? "coop_store16(" : "coop_store(") << "O0 + row * (i64)" << p_.dim_x << " + "
+           << O(xc.off, C.xstep[c]) << ", gxs + " << O(gx_base_[k] + gx_pre_[k][c], gx_unit_[k]) << ", "
+           << (vec ? xc.words * sz_ / 16 : xc.words) << ", lane);\n";
+      }
+      o_ << "    }\n";
+    }
+    o_ << "    __syncwarp();\n    for (int j = lane; j < " << gx_words_ << "; j += 32) gxs[j] = 0;\n    __syncwarp();\n";
   }
   o_ << "  }\n";
 }
@@ -1036,7 +1066,8 @@ KernelSource Gen::run() {
   static const char* loopn[] = {"tp", "convo", "convi", "conve"};
   KernelSource ks;
   ks.name = std::string("cgf_") + loopn[static_cast<int>(cfg_.loop)] + "_" + compn[static_cast<int>(cfg_.comp)] +
-            (cfg_.f64 ? "_f64" : "_f32") + (cfg_.w_shared ? "_ws" : "") + (cfg_.aligned ? "" : "_u");
+            (cfg_.f64 ? "_f64" : "_f32") + (cfg_.w_shared ? "_ws" : "") + (cfg_.aligned ? "" : "_u") +
+            (cfg_.tag.empty() ? "" : "_" + cfg_.tag);
   ks.threads = warps * 32;
   ks.smem_bytes = static_cast<int>(wb * warps + 8ull * depth * warps);
   ks.units = static_cast<int>(units_.size());
@@ -1068,7 +1099,7 @@ KernelSource Gen::run() {
   o_ << "  T* gya = scr + " << off_gya_ << "; (void)gya;\n"
      << "  for (int j = lane; j < " << p_.dim_y << "; j += 32) gya[j] = 0;\n";
   if (by_input())
-    o_ << "  T* gxs = scr + " << off_gxs_ << ";\n  for (int j = lane; j < " << p_.dim_x << "; j += 32) gxs[j] = 0;\n";
+    o_ << "  T* gxs = scr + " << off_gxs_ << ";\n  for (int j = lane; j < " << gx_words_ << "; j += 32) gxs[j] = 0;\n";
   o_ << "  u64* bars = (u64*)(smem_raw + NW * WARP_BYTES) + wid * D;\n"
         "  if (lane == 0) { for (int d = 0; d < D; ++d) mbar_init(&bars[d], " << (cfg_.lane_copy && !cfg_.par_bulk ? 32 : 1) << "); mbar_fence_init(); }\n"
         "  __syncwarp();\n"

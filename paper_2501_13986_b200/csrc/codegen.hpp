@@ -63,6 +63,11 @@ struct KernelConfig {
   bool y_window = false;    // stage y as a 16-byte window even when its rows are aligned (A/B)
   bool lane_copy = true;    // stage inputs with per-lane 16-byte cp.async (whole warp) instead of
                             // one lane's cp.async.bulk: no single-lane issue loop per range
+  // ConvByInput over a GROUP of units (the kernel is given a unit subset):
+  // gy-type per-edge outputs add to what earlier groups wrote (read-modify-
+  // write in group order, deterministic) instead of overwriting.
+  bool gy_accum = false;
+  std::string tag;          // appended to the kernel name (e.g. the group "g1of3")
 };
 
 // Applies "k=v,flag,..." overrides (env CGF_GEN) to a config: depth=N,

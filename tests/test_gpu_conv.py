@@ -251,3 +251,36 @@ def test_c4_full_graph_sampled(dt):
     check(host(gx)[rows], wx[rows], dt, "C4 sampled g_node_x")
     check(host(gy[eidx]), wy, dt, "C4 sampled g_edge_y")
     check(host(gw[eidx]), ww, dt, "C4 sampled g_edge_w")
+
+
+@pytest.mark.parametrize("groups", [1, 2, 3, 5])
+@pytest.mark.parametrize("dt", DTYPES, ids=["f32", "f64"])
+def test_grouped_kernels_match_oracle(groups, dt, monkeypatch):
+    """The by-neighbour conv kernels (backward, double-backward pass 2) and
+    the batched TP double-backward run their units in G groups, one kernel
+    each, with the per-edge / per-row dy summed in group order: any G gives
+    the oracle's results (C2 TP on a ragged lattice graph, plus 300 TP rows)."""
+    monkeypatch.setenv("CGF_CONVI_GROUPS", str(groups))
+    monkeypatch.setenv("CGF_ROW_GROUPS", str(groups))
+    js = config("c2")
+    o, pkg = O.Oracle(js), P()
+    plan = pkg.TpPlan(js)
+    cp = pkg.ConvPlan(plan)
+    og = graphs()["ragged5"]
+    g = pkg.Graph(og.nodes, og.src, og.nbr)
+    nx, ey, ew, gnz, dgx, dgy, dgw = conv_inputs(o, og, dt, seed=55)
+    outs = cp.backward(g, dev(nx), dev(ey), dev(ew), dev(gnz))
+    for got, want, n in zip(outs, o.conv_backward(og, nx, ey, ew, gnz), ("gx", "gy", "gw")):
+        check(host(got), want, dt, f"G={groups} conv {n}")
+    outs = cp.double_backward(g, dev(nx), dev(ey), dev(ew), dev(gnz), (dev(dgx), dev(dgy), dev(dgw)))
+    want = o.conv_double_backward(og, nx, ey, ew, gnz, dgx, dgy, dgw)
+    for got, wv, n in zip(outs, want, ("dx", "dy", "dw", "dgz")):
+        check(host(got), wv, dt, f"G={groups} conv double-backward {n}")
+    rows = 300
+    gen = O.NormalGen(77)
+    x, y, w = (gen.normal_vec(rows * d, dt).reshape(rows, -1) for d in (o.dim_x, o.dim_y, o.n_w))
+    gz, da = (gen.normal_vec(rows * d, dt).reshape(rows, -1) for d in (o.dim_z, o.dim_x))
+    db, dc = (gen.normal_vec(rows * d, dt).reshape(rows, -1) for d in (o.dim_y, o.n_w))
+    outs = plan.double_backward(dev(x), dev(y), dev(w), dev(gz), (dev(da), dev(db), dev(dc)))
+    for got, wv, n in zip(outs, o.double_backward(x, y, w, gz, da, db, dc), ("dx", "dy", "dw", "dgz")):
+        check(host(got), wv, dt, f"G={groups} TP double-backward {n}")

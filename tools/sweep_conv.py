@@ -20,7 +20,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2501_13986_b200 as cgf  # noqa: E402
-from oracle import oracle as O  # noqa: E402
+from paper_2501_13986_b200 import dist as cdist  # noqa: E402
+from paper_2501_13986_b200.configs import config_json  # noqa: E402
 
 CASES = {"c4": ("c2", 29), "c5": ("c1", 58), "c4_c1tp": ("c1", 29)}
 
@@ -43,11 +44,12 @@ def main():
     pk = peak()
     for case in a.cases.split(","):
         prob, n = CASES[case]
-        og = O.radius_graph(O.cubic_lattice(n), 3.0)
-        plan = cgf.TpPlan(O.config_json(prob))
+        nodes, src, nbr = cdist.lattice_radius_graph(n, 1.0, 3.0)
+        plan = cgf.TpPlan(config_json(prob))
         cp = cgf.ConvPlan(plan)
-        g = cgf.Graph(og.nodes, og.src, og.nbr)
-        V, E = og.nodes, og.edges
+        g = cgf.Graph(nodes, src, nbr)
+        del src, nbr
+        V, E = g.nodes, g.edges
         for dts in a.dtypes.split(","):
             tdt = torch.float32 if dts == "f32" else torch.float64
             es = 4 if dts == "f32" else 8
@@ -92,7 +94,8 @@ def main():
                         del r
                     ms = statistics.median(ts)
                     gbs = words * es / (ms / 1e3) / 1e9
-                    rec = {"case": case, "tp": prob, "mode": mode_name, "nodes": V, "edges": E, "op": op, "dtype": dts, "ms": ms,
+                    rec = {"case": case, "tp": prob, "mode": mode_name, "env": {k: v for k, v in os.environ.items()
+                                                                               if k.startswith("CGF_")}, "nodes": V, "edges": E, "op": op, "dtype": dts, "ms": ms,
                            "edges/s": E / (ms / 1e3), "GB/s": gbs, "frac_hbm": gbs / pk,
                            "GFLOP/s": flops / (ms / 1e3) / 1e9}
                 except Exception as exc:
