@@ -42,11 +42,11 @@ struct cgf_plan {
   std::map<ScratchKey, CUdeviceptr> wimg;
   std::map<ScratchKey, std::size_t> scratch_cap;  // bytes of each buffer in wimg
   // host-pointer path: two streams + double-buffered device staging per context
-  static constexpr int kPipe = 3;  // chunks in flight: H2D(c+1) | kernels(c) | D2H(c-1)
+  static constexpr int kPipe = 4;  // max chunks in flight: H2D(c+1) | kernels(c) | D2H(c-1) | ...
   struct HostPipe {
     CUstream s[kPipe] = {};
     CUdeviceptr buf[kPipe] = {};
-    std::size_t cap = 0;
+    std::size_t cap[kPipe] = {};
   };
   std::map<CUcontext, HostPipe> pipes;
   std::mutex host_mu;
@@ -957,10 +957,15 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
     if (out[i]) (orow[i] ? row_words : fixed_words) += ow[i];
   const bool one_chunk = ws && op != CGF_OP_FORWARD;
   std::int64_t chunk = rows;
+  // staging per chunk (CGF_HOST_CHUNK_MB, default 128): large enough that each
+  // copy runs at PCIe speed, small enough that the pipeline fills quickly;
+  // CGF_HOST_DEPTH (2..4, default 3) chunks in flight
+  const char* mb_env = std::getenv("CGF_HOST_CHUNK_MB");
+  const char* dp_env = std::getenv("CGF_HOST_DEPTH");
+  const std::size_t chunk_bytes = (mb_env ? std::max(1, std::atoi(mb_env)) : 128) * (1ull << 20);
+  const int K = dp_env ? std::clamp(std::atoi(dp_env), 2, static_cast<int>(cgf_plan::kPipe)) : 3;
   if (!one_chunk) {
-    // ~128 MB of staging per chunk: large enough that each copy runs at PCIe
-    // speed, small enough that the pipeline fills quickly
-    const std::int64_t target = static_cast<std::int64_t>((128ull << 20) / std::max<std::size_t>(1, row_words * es));
+    const std::int64_t target = static_cast<std::int64_t>(chunk_bytes / std::max<std::size_t>(1, row_words * es));
     chunk = std::min<std::int64_t>(rows, std::max<std::int64_t>(1024, target / 128 * 128));
   }
   const std::size_t need = (fixed_words + static_cast<std::size_t>(chunk) * row_words) * es + 11 * 256;
@@ -971,20 +976,18 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
     std::lock_guard<std::mutex> g(p->mu);
     pipe = &p->pipes[ctx];
   }
-  constexpr int K = cgf_plan::kPipe;
   if (!pipe->s[0])
-    for (int k = 0; k < K; ++k) CU_CHECK(cgf::drv::cuStreamCreate(&pipe->s[k], CU_STREAM_NON_BLOCKING));
-  if (pipe->cap < need) {
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < cgf_plan::kPipe; ++k) CU_CHECK(cgf::drv::cuStreamCreate(&pipe->s[k], CU_STREAM_NON_BLOCKING));
+  for (int k = 0; k < K; ++k)
+    if (!pipe->buf[k] || pipe->cap[k] < need) {
       if (pipe->buf[k]) {
         CU_CHECK(cgf::drv::cuStreamSynchronize(pipe->s[k]));
         cgf::drv::cuMemFree(pipe->buf[k]);
+        pipe->buf[k] = 0;
       }
-      pipe->buf[k] = 0;
       CU_CHECK(cgf::drv::cuMemAlloc(&pipe->buf[k], need));
+      pipe->cap[k] = need;
     }
-    pipe->cap = need;
-  }
   const std::int64_t nchunks = (rows + chunk - 1) / chunk;
   for (std::int64_t c = 0; c < nchunks; ++c) {
     const int k = static_cast<int>(c % K);

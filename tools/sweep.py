@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_2501_13986_b200 as cgf  # noqa: E402
-from oracle.oracle import config_json  # noqa: E402
+from paper_2501_13986_b200.configs import config_json  # noqa: E402
 
 ROWS = {"c1": 50_000, "c2": 1_000_000, "c3": 1_000_000}
 
@@ -90,6 +90,7 @@ def main():
                     ms = statistics.median(ts)
                     gbs = words * es / (ms / 1e3) / 1e9
                     rec = {"config": cname, "op": op, "dtype": dts, "rows": R, "w_shared": ws, "ms": ms, "burst": burst,
+                           "env": {k: v for k, v in os.environ.items() if k.startswith("CGF_")},
                            "GB/s": gbs, "frac_hbm": gbs / pk, "GFLOP/s": flops / (ms / 1e3) / 1e9,
                            "rows/s": R / (ms / 1e3)}
                 except Exception as exc:
