@@ -365,7 +365,7 @@ class _TorchShardStandIn:
     def __init__(self, plan):
         self.plan = plan
 
-    def forward_shard(self, sh, x_all, ey, ew):
+    def forward_shard(self, sh, x_all, ey, ew, mode=0):
         import torch
         d = sh.device(x_all.device)
         src = torch.repeat_interleave(torch.arange(sh.out_nodes), d["row_ptr"].diff())
@@ -373,7 +373,7 @@ class _TorchShardStandIn:
         z[:, :self.plan.dim_x].index_add_(0, src, x_all[d["nbr"].long()])
         return z
 
-    def backward_shard(self, sh, x_all, ey, ew, gz):
+    def backward_shard(self, sh, x_all, ey, ew, gz, mode=0):
         import torch
         d = sh.device(x_all.device)
         src = torch.repeat_interleave(torch.arange(sh.out_nodes), d["row_ptr"].diff())

@@ -119,34 +119,50 @@ bool covers(const std::vector<std::pair<std::uint32_t, std::uint32_t>>& pieces, 
   return true;
 }
 
-// The by-neighbour conv kernels (backward, double-backward pass 2) gather
-// g_node_z[s] (dim_z words) for every edge; the rows of the sources a grid
-// works on at one time exceed L2 when dim_z is large (C4: ~6K rows x 36 KB).
-// Running the units in G groups, one kernel launch each, shrinks each pass's
-// gz working set (and the per-warp gx accumulator) G-fold; per-edge gy is
-// summed across the groups in group order. G from the row size; CGF_CONVI_GROUPS
-// overrides.
-int convi_groups(const cgf_plan* p, int dtype) {
-  if (const char* env = std::getenv("CGF_CONVI_GROUPS")) return std::clamp(std::atoi(env), 1, static_cast<int>(p->units.size()));
-  const std::size_t zbytes = static_cast<std::size_t>(p->problem.dim_z) * (dtype == CGF_F64 ? 8 : 4);
-  return std::clamp(static_cast<int>((zbytes + 16383) / 16384), 1, static_cast<int>(p->units.size()));
+// Kernels that run a problem's units in G groups, one launch each (the
+// generator is given the unit subset; per-row / per-edge dy-type outputs are
+// summed across groups in group order, every other output has one owner):
+//
+//  * by-neighbour conv (backward, double-backward pass 2): each edge gathers
+//    g_node_z[s] (dim_z words); with dim_z large the rows the grid touches at
+//    once overflow L2 (C4 FP64: 2.4x the algorithmic DRAM bytes,
+//    profiles/r01_ncu_v5_summary.txt) and the per-warp gx accumulator caps
+//    occupancy at 4 warps / SM. G groups cut both G-fold.
+//  * batched double-backward (and backward): seven ops per CG entry make one
+//    kernel's code overflow the instruction cache (no_instruction stalls,
+//    profiles/r01_ncu_v8_dbwd.txt); G smaller kernels fit.
+//
+// Defaults from the sweep in profiles/r02_sweep_groups.jsonl (C4 / C5 conv,
+// C1 / C2 TP); CGF_CONVI_GROUPS / CGF_ROW_GROUPS(_BWD) override.
+int group_env(const char* name, int nu) {
+  const char* env = std::getenv(name);
+  return env ? std::clamp(std::atoi(env), 1, nu) : 0;
 }
 
-// The batched double-backward computes seven ops per CG entry: with every unit
-// in one kernel its code overflows the instruction cache (no_instruction was
-// its top stall, profiles/r01_ncu_v8_dbwd.txt). Units split into groups, one
-// kernel each, keep each kernel's code small; the only shared outputs are the
-// per-row dy (dim_y words, summed in group order). CGF_ROW_GROUPS overrides.
+int convi_groups(const cgf_plan* p, cgf::Comp comp, int dtype) {
+  const int nu = static_cast<int>(p->units.size());
+  if (const int g = group_env("CGF_CONVI_GROUPS", nu)) return g;
+  const std::size_t zbytes = static_cast<std::size_t>(p->problem.dim_z) * (dtype == CGF_F64 ? 8 : 4);
+  int g = 1;
+  if (comp == cgf::Comp::Bwd)  // FP64 C4: 164 -> 83 ms at G = 8; FP32 C4 / C5: G = 1 is fastest
+    g = dtype == CGF_F64 && zbytes > 32768 ? 8 : 1;
+  else  // DBwdX: C4 FP32 110 -> 90 ms (G = 4), C4 FP64 290 -> 189 ms (G = 2), C5 139 -> 127 ms (G = 2)
+    g = dtype == CGF_F32 && zbytes > 16384 ? 4 : 2;
+  return std::clamp(g, 1, nu);
+}
+
 int row_groups(const cgf_plan* p, cgf::Comp comp, int dtype) {
   const int nu = static_cast<int>(p->units.size());
-  if (comp != cgf::Comp::DBwd) return 1;
-  if (const char* env = std::getenv("CGF_ROW_GROUPS")) return std::clamp(std::atoi(env), 1, nu);
-  (void)dtype;
-  return 1;
+  if (comp != cgf::Comp::DBwd && comp != cgf::Comp::Bwd) return 1;
+  if (const int g = group_env(comp == cgf::Comp::DBwd ? "CGF_ROW_GROUPS" : "CGF_ROW_GROUPS_BWD", nu)) return g;
+  if (comp == cgf::Comp::Bwd) return 1;
+  // C2 FP32 33.9 -> 28.2 ms (G = 6), FP64 29.1 -> 25.0 ms (G = 2); C1 FP32 0.29 -> 0.26 ms (G = 2)
+  const int g = dtype == CGF_F32 ? std::min(6, (nu + 1) / 2) : (nu >= 8 ? 2 : 1);
+  return std::clamp(g, 1, nu);
 }
 
 int kernel_groups(const cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype) {
-  if (loop == cgf::Loop::ConvByInput) return convi_groups(p, dtype);
+  if (loop == cgf::Loop::ConvByInput) return convi_groups(p, comp, dtype);
   if (loop == cgf::Loop::Rows) return row_groups(p, comp, dtype);
   return 1;
 }
@@ -184,8 +200,7 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
                                    aligned ? 1 : 0, flags + "|" + std::to_string(group) + "/" + std::to_string(ngroups));
   auto it = p->sources.find(key);
   if (it != p->sources.end()) return it->second;
-  if (w_shared && comp != cgf::Comp::Fwd && !(comp == cgf::Comp::Bwd && cgf::uvw_eligible(p->problem) && dtype == CGF_F32))
-    throw cgf::UnsupportedError("shared-weight backward / double-backward: only the FP32 uvw tensor-core path");
+  if (w_shared && loop != cgf::Loop::Rows) throw cgf::UnsupportedError("shared weights: batched TP only");
   cgf::KernelConfig cfg;
   cfg.comp = comp;
   cfg.loop = loop;
@@ -537,6 +552,63 @@ bool dbwd_split(int dtype) {
   return false;
 }
 
+// Stream-ordered device scratch.
+struct Scratch {
+  void* ptr = nullptr;
+  void* st = nullptr;
+  bool owned = true;
+  Scratch(std::size_t bytes, void* stream) : st(stream) { ptr = cgf::gops::scratch_alloc(bytes, stream); }
+  Scratch(void* borrowed, void* stream) : ptr(borrowed), st(stream), owned(false) {}
+  ~Scratch() {
+    if (owned) cgf::gops::scratch_free(ptr, st);
+  }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+bool dbwd_split(int dtype);
+
+// Backward / double-backward with ONE shared W on the SIMT kernels (FP64, and
+// shapes or ops the tcgen05 path does not cover): the kernel writes each row's
+// weight gradient into a row-indexed workspace, which a fixed-order column sum
+// folds into the shared gradient; rows run in chunks so the workspace stays
+// bounded (<= 2 GiB). Deterministic: the chunking depends on rows and n_w only.
+void shared_w_grad(cgf_plan* p, int op, int dtype, const Args& a, void* stream) {
+  const auto& pr = p->problem;
+  const std::size_t es = dtype == CGF_F64 ? 8 : 4;
+  std::int64_t per = std::max<std::int64_t>(1, static_cast<std::int64_t>((2ull << 30) / (pr.n_w * es)));
+  if (const char* env = std::getenv("CGF_SHARED_W_CHUNK_ROWS")) per = std::max(1, std::atoi(env));  // tests
+  const std::int64_t chunk = std::min(a.rows, per);
+  Scratch ws(static_cast<std::size_t>(chunk) * pr.n_w * es, stream);
+  const auto off = [&](const void* q, std::int64_t r0, int dim) -> const void* {
+    return q ? static_cast<const char*>(q) + es * static_cast<std::size_t>(r0) * dim : nullptr;
+  };
+  const auto moff = [&](void* q, std::int64_t r0, int dim) -> void* {
+    return q ? static_cast<char*>(q) + es * static_cast<std::size_t>(r0) * dim : nullptr;
+  };
+  for (std::int64_t r0 = 0; r0 < a.rows; r0 += chunk) {
+    Args c = a;
+    c.rows = std::min(chunk, a.rows - r0);
+    c.x = off(a.x, r0, pr.dim_x);
+    c.y = off(a.y, r0, pr.dim_y);
+    c.gz = off(a.gz, r0, pr.dim_z);
+    c.da = off(a.da, r0, pr.dim_x);
+    c.db = off(a.db, r0, pr.dim_y);
+    c.o0 = moff(a.o0, r0, pr.dim_x);
+    c.o1 = moff(a.o1, r0, pr.dim_y);
+    c.o3 = moff(a.o3, r0, pr.dim_z);
+    c.o2 = ws.ptr;  // per-row weight gradients of this chunk
+    if (op == CGF_OP_DOUBLE_BACKWARD && dbwd_split(dtype)) {
+      run_kernel(p, cgf::Comp::DBwdZ, cgf::Loop::Rows, dtype, 1, c, stream);
+      run_kernel(p, cgf::Comp::DBwdX, cgf::Loop::Rows, dtype, 1, c, stream);
+    } else {
+      run_kernel(p, static_cast<cgf::Comp>(op), cgf::Loop::Rows, dtype, 1, c, stream);
+    }
+    cgf::gops::column_sum(dtype == CGF_F64, ws.ptr, c.rows, pr.n_w, a.o2, r0 > 0, stream);
+  }
+}
+
 void launch(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, const void* x,
             const void* y, const void* w, const void* gz, const void* da, const void* db,
             const void* dc, void* o0, void* o1, void* o2, void* o3, void* stream) {
@@ -560,6 +632,10 @@ void launch(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, con
       run_uvw(p, "bwdx", gz, pr.dim_z, y, w, o0, rows, stream);
       run_uvw_grad_yw(p, x, y, w, gz, o1, o2, rows, stream);
     }
+    return;
+  }
+  if (w_shared && op != CGF_OP_FORWARD) {
+    shared_w_grad(p, op, dtype, a, stream);
     return;
   }
   if (op == CGF_OP_DOUBLE_BACKWARD && dbwd_split(dtype)) {
@@ -611,37 +687,24 @@ void check_edge_list(std::int64_t nodes, std::int64_t edges, const std::int32_t*
 // Atomic-mode conv (Mode::atomic, conv.cpp:311-324 / 470-486) over an edge
 // list: one item per (edge, unit); z / gx contributions accumulate at the
 // edge's src / dst nodes with float atomics into zeroed node arrays.
-void conv_atomic(cgf_plan* p, int dtype, cgf::Comp comp, std::int64_t nodes, std::int64_t edges, const std::int32_t* src,
-                 const std::int32_t* dst, Args a, void* stream) {
-  if (nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
-  if (edges > 0 && nodes == 0) throw cgf::ShapeError("edges without nodes");
+void conv_atomic(cgf_plan* p, int dtype, cgf::Comp comp, std::int64_t out_nodes, std::int64_t in_nodes,
+                 std::int64_t edges, const std::int32_t* src, const std::int32_t* dst, Args a, void* stream) {
+  if (out_nodes < 0 || in_nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+  if (edges > 0 && (out_nodes == 0 || in_nodes == 0)) throw cgf::ShapeError("edges without nodes");
   const std::size_t es = dtype == CGF_F64 ? 8 : 4;
   const auto& pr = p->problem;
-  if (a.o3 || comp == cgf::Comp::Fwd) memzero(comp == cgf::Comp::Fwd ? a.o0 : a.o3, es * nodes * pr.dim_z, stream);
-  if (comp != cgf::Comp::Fwd) memzero(a.o0, es * nodes * pr.dim_x, stream);
+  // z-type outputs live on the output nodes, x-type ones on the neighbours
+  if (a.o3 || comp == cgf::Comp::Fwd) memzero(comp == cgf::Comp::Fwd ? a.o0 : a.o3, es * out_nodes * pr.dim_z, stream);
+  if (comp != cgf::Comp::Fwd) memzero(a.o0, es * in_nodes * pr.dim_x, stream);
   if (edges == 0) return;
   need(src, "src"); need(dst, "dst");
-  a.rows = nodes;
+  a.rows = out_nodes;
   a.edges = edges;
   a.eid = src;
   a.nb = dst;
   run_kernel(p, comp, cgf::Loop::ConvEdges, dtype, 0, a, stream);
 }
 
-// Stream-ordered device scratch.
-struct Scratch {
-  void* ptr = nullptr;
-  void* st = nullptr;
-  bool owned = true;
-  Scratch(std::size_t bytes, void* stream) : st(stream) { ptr = cgf::gops::scratch_alloc(bytes, stream); }
-  Scratch(void* borrowed, void* stream) : ptr(borrowed), st(stream), owned(false) {}
-  ~Scratch() {
-    if (owned) cgf::gops::scratch_free(ptr, st);
-  }
-  Scratch(const Scratch&) = delete;
-  Scratch& operator=(const Scratch&) = delete;
-  template <class T> T* as() const { return static_cast<T*>(ptr); }
-};
 
 // Per-edge output node of a device CSR, for the CSR entry points called with
 // CGF_CONV_ATOMIC and for the unfused backward's g_node_z gather.
@@ -654,6 +717,26 @@ struct CsrSrc : Scratch {
   }
   const std::int32_t* get() const { return as<const std::int32_t>(); }
 };
+
+// Atomic-mode conv given only the transposed CSR (the shard backward's
+// arguments): the edge list is rebuilt in edge order on the device.
+void atomic_transposed(cgf_plan* p, int dtype, cgf::Comp comp, std::int64_t out_nodes, std::int64_t in_nodes,
+                       std::int64_t edges, const std::int64_t* t_row_ptr, const std::int32_t* t_out,
+                       const std::int32_t* t_eid, const void* x, const void* y, const void* w, const void* gz,
+                       const void* da, const void* db, const void* dc, void* o0, void* o1, void* o2, void* o3,
+                       void* stream) {
+  Scratch el(edges > 0 ? 8ull * edges : 0, stream);
+  if (edges > 0) {
+    need(t_out, "t_src"); need(t_eid, "t_eid");
+    cgf::gops::untranspose(t_row_ptr, in_nodes, t_out, t_eid, el.as<std::int32_t>(), el.as<std::int32_t>() + edges,
+                           stream);
+  }
+  Args a;
+  a.x = x; a.y = y; a.w = w; a.gz = gz; a.da = da; a.db = db; a.dc = dc;
+  a.o0 = o0; a.o1 = o1; a.o2 = o2; a.o3 = o3;
+  conv_atomic(p, dtype, comp, out_nodes, in_nodes, edges, el.as<std::int32_t>(), el.as<std::int32_t>() + edges, a,
+              stream);
+}
 
 // Unfused comparator (conv.cpp:530-616): gather x per edge, batched TP over
 // |E| rows, then per-node sums in edge order. The output node's edges are
@@ -957,12 +1040,13 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
     if (out[i]) (orow[i] ? row_words : fixed_words) += ow[i];
   const bool one_chunk = ws && op != CGF_OP_FORWARD;
   std::int64_t chunk = rows;
-  // staging per chunk (CGF_HOST_CHUNK_MB, default 128): large enough that each
+  // staging per chunk (CGF_HOST_CHUNK_MB, default 256: 146 -> 140 ms per C2 e2e step
+  // vs 128, profiles/r02_sweep_e2e.jsonl): large enough that each
   // copy runs at PCIe speed, small enough that the pipeline fills quickly;
   // CGF_HOST_DEPTH (2..4, default 3) chunks in flight
   const char* mb_env = std::getenv("CGF_HOST_CHUNK_MB");
   const char* dp_env = std::getenv("CGF_HOST_DEPTH");
-  const std::size_t chunk_bytes = (mb_env ? std::max(1, std::atoi(mb_env)) : 128) * (1ull << 20);
+  const std::size_t chunk_bytes = (mb_env ? std::max(1, std::atoi(mb_env)) : 256) * (1ull << 20);
   const int K = dp_env ? std::clamp(std::atoi(dp_env), 2, static_cast<int>(cgf_plan::kPipe)) : 3;
   if (!one_chunk) {
     const std::int64_t target = static_cast<std::int64_t>(chunk_bytes / std::max<std::size_t>(1, row_words * es));
@@ -1280,10 +1364,17 @@ int cgf_conv_forward_shard(cgf_plan* p, int dtype, int64_t out_nodes, int64_t in
                            const void* edge_w, void* node_z, int mode, void* stream) {
   return guarded([&] {
     need(p, "plan");
-    if (mode != CGF_CONV_DETERMINISTIC) throw cgf::UnsupportedError("only the deterministic conv mode is built");
+    if (mode != CGF_CONV_DETERMINISTIC && mode != CGF_CONV_ATOMIC) throw std::invalid_argument("bad conv mode");
     if (out_nodes < 0 || in_nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
     if (out_nodes == 0) return;
     need(row_ptr, "row_ptr"); need(node_z, "node_z");
+    if (mode == CGF_CONV_ATOMIC) {  // Mode::atomic over the shard's CSR expanded to an edge list
+      const CsrSrc src(row_ptr, out_nodes, edges, stream);
+      Args a;
+      a.x = node_x; a.y = edge_y; a.w = edge_w; a.o0 = node_z;
+      conv_atomic(p, dtype, cgf::Comp::Fwd, out_nodes, in_nodes, edges, src.get(), nbr, a, stream);
+      return;
+    }
     if (edges > 0) { need(node_x, "node_x"); need(nbr, "nbr"); need(edge_y, "edge_y"); need(edge_w, "edge_w"); }
     const std::size_t es = dtype == CGF_F64 ? 8 : 4;
     if (!p->z_covered) memzero(node_z, es * out_nodes * p->problem.dim_z, stream);
@@ -1313,10 +1404,18 @@ int cgf_conv_backward_shard(cgf_plan* p, int dtype, int64_t out_nodes, int64_t i
                             void* g_edge_y, void* g_edge_w, int mode, void* stream) {
   return guarded([&] {
     need(p, "plan");
-    if (mode != CGF_CONV_DETERMINISTIC) throw cgf::UnsupportedError("only the deterministic conv mode is built");
+    if (mode != CGF_CONV_DETERMINISTIC && mode != CGF_CONV_ATOMIC) throw std::invalid_argument("bad conv mode");
     if (out_nodes < 0 || in_nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
     if (in_nodes == 0) return;
     need(t_row_ptr, "t_row_ptr"); need(node_x, "node_x"); need(g_node_x, "g_node_x");
+    if (mode == CGF_CONV_ATOMIC) {
+      // the transposed CSR as an edge list in transposed order: position q
+      // is edge t_eid[q] = (t_src[q], its neighbour); per-edge outputs are
+      // addressed through t_eid, so the edge arrays are permuted views
+      atomic_transposed(p, dtype, cgf::Comp::Bwd, out_nodes, in_nodes, edges, t_row_ptr, t_out, t_eid, node_x, edge_y,
+                        edge_w, g_node_z, nullptr, nullptr, nullptr, g_node_x, g_edge_y, g_edge_w, nullptr, stream);
+      return;
+    }
     if (edges > 0) {
       need(g_node_z, "g_node_z"); need(t_out, "t_src"); need(t_eid, "t_eid"); need(edge_y, "edge_y");
       need(edge_w, "edge_w"); need(g_edge_y, "g_edge_y"); need(g_edge_w, "g_edge_w");
@@ -1355,8 +1454,18 @@ int cgf_conv_double_backward_shard(cgf_plan* p, int dtype, int64_t out_nodes, in
                                    void* o_edge_w, void* o_g_node_z, int mode, void* stream) {
   return guarded([&] {
     need(p, "plan");
-    if (mode != CGF_CONV_DETERMINISTIC) throw cgf::UnsupportedError("only the deterministic conv mode is built");
+    if (mode != CGF_CONV_DETERMINISTIC && mode != CGF_CONV_ATOMIC) throw std::invalid_argument("bad conv mode");
     if (out_nodes < 0 || in_nodes < 0 || edges < 0) throw cgf::ShapeError("negative graph size");
+    if (mode == CGF_CONV_ATOMIC) {  // one pass over the edge list (dx at dst, dgz at src)
+      if (out_nodes > 0) need(row_ptr, "row_ptr");
+      if (edges > 0) need(nbr, "nbr");
+      const CsrSrc src(row_ptr, out_nodes, edges, stream);
+      Args a;
+      a.x = node_x; a.y = edge_y; a.w = edge_w; a.gz = g_node_z; a.da = d_gx; a.db = d_gy; a.dc = d_gw;
+      a.o0 = o_node_x; a.o1 = o_edge_y; a.o2 = o_edge_w; a.o3 = o_g_node_z;
+      conv_atomic(p, dtype, cgf::Comp::DBwd, out_nodes, in_nodes, edges, src.get(), nbr, a, stream);
+      return;
+    }
     const std::size_t es = dtype == CGF_F64 ? 8 : 4;
     // Pass 1, by output node: dL/dg_node_z = sum_e op3 + op6 + op7.
     if (out_nodes > 0) {
@@ -1410,7 +1519,7 @@ int cgf_conv_forward_atomic(cgf_plan* p, int dtype, int64_t nodes, int64_t edges
     if (edges > 0) { need(node_x, "node_x"); need(edge_y, "edge_y"); need(edge_w, "edge_w"); }
     Args a;
     a.x = node_x; a.y = edge_y; a.w = edge_w; a.o0 = node_z;
-    conv_atomic(p, dtype, cgf::Comp::Fwd, nodes, edges, src, dst, a, stream);
+    conv_atomic(p, dtype, cgf::Comp::Fwd, nodes, nodes, edges, src, dst, a, stream);
   });
 }
 
@@ -1427,7 +1536,7 @@ int cgf_conv_backward_atomic(cgf_plan* p, int dtype, int64_t nodes, int64_t edge
     Args a;
     a.x = node_x; a.y = edge_y; a.w = edge_w; a.gz = g_node_z;
     a.o0 = g_node_x; a.o1 = g_edge_y; a.o2 = g_edge_w;
-    conv_atomic(p, dtype, cgf::Comp::Bwd, nodes, edges, src, dst, a, stream);
+    conv_atomic(p, dtype, cgf::Comp::Bwd, nodes, nodes, edges, src, dst, a, stream);
   });
 }
 
@@ -1445,7 +1554,7 @@ int cgf_conv_double_backward_atomic(cgf_plan* p, int dtype, int64_t nodes, int64
     Args a;
     a.x = node_x; a.y = edge_y; a.w = edge_w; a.gz = g_node_z; a.da = d_gx; a.db = d_gy; a.dc = d_gw;
     a.o0 = o_node_x; a.o1 = o_edge_y; a.o2 = o_edge_w; a.o3 = o_g_node_z;
-    conv_atomic(p, dtype, cgf::Comp::DBwd, nodes, edges, src, dst, a, stream);
+    conv_atomic(p, dtype, cgf::Comp::DBwd, nodes, nodes, edges, src, dst, a, stream);
   });
 }
 

@@ -608,7 +608,9 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
   const Unit& u = U0(k);
   const Layout& L = lay_[k];
   const std::string nw = S(p_.n_w);
-  const std::string wrow = cfg_.w_shared ? "0" : idx(e_src());
+  // weight-gradient rows: per item (with shared W the caller passes a per-row
+  // workspace and reduces it over rows)
+  const std::string wrow = idx(e_src());
   const int nsub = static_cast<int>(u.subs.size());
   const int m = (cfg_.joint && u.merged > 1 && nsub % u.merged == 0) ? u.merged : 1;
   const int n = nsub / m;

@@ -122,6 +122,39 @@ __global__ void k_expand(const i64* __restrict__ rp, i64 nodes, int* __restrict_
     for (i64 e = rp[v]; e < rp[v + 1]; ++e) src[e] = static_cast<int>(v);
 }
 
+// dst[c] (+)= sum over r < rows of src[r * n + c], summed in row order (the
+// shared-W weight gradient's reduction over per-row partials; deterministic).
+template <typename T>
+__global__ void k_colsum(const T* __restrict__ src, i64 rows, i64 n, T* __restrict__ dst, int accumulate) {
+  for (i64 c = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; c < n;
+       c += static_cast<i64>(gridDim.x) * blockDim.x) {
+    T acc = accumulate ? dst[c] : T(0);
+    i64 r = 0;
+    for (; r + 8 <= rows; r += 8) {
+      T v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldg(src + (r + k) * n + c);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc += v[k];
+    }
+    for (; r < rows; ++r) acc += __ldg(src + r * n + c);
+    dst[c] = acc;
+  }
+}
+
+// transposed CSR -> edge list in edge order: position q of bucket d is edge
+// t_eid[q] = (t_src[q], d)
+__global__ void k_untranspose(const i64* __restrict__ trp, i64 in_nodes, const int* __restrict__ t_src,
+                              const int* __restrict__ t_eid, int* __restrict__ src, int* __restrict__ dst) {
+  for (i64 d = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; d < in_nodes;
+       d += static_cast<i64>(gridDim.x) * blockDim.x)
+    for (i64 q = trp[d]; q < trp[d + 1]; ++q) {
+      const int e = t_eid[q];
+      src[e] = t_src[q];
+      dst[e] = static_cast<int>(d);
+    }
+}
+
 __global__ void k_validate(const int* __restrict__ src, const int* __restrict__ dst, i64 edges, i64 nodes,
                            int allow_self, u64* first_bad) {
   for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < edges;
@@ -289,6 +322,27 @@ void segment_sum(bool f64, const void* rows, const std::int64_t* rp, const std::
 void rowptr_expand(const std::int64_t* rp, std::int64_t nodes, std::int32_t* src, void* stream) {
   if (nodes <= 0) return;
   k_expand<<<grid_for(nodes, 256), 256, 0, S(stream)>>>(reinterpret_cast<const i64*>(rp), nodes, src);
+  CK(cudaGetLastError());
+}
+
+void column_sum(bool f64, const void* src, std::int64_t rows, std::int64_t n, void* dst, bool accumulate,
+                void* stream) {
+  if (n <= 0) return;
+  const int acc = accumulate ? 1 : 0;
+  if (f64)
+    k_colsum<double><<<grid_for(n, 128), 128, 0, S(stream)>>>(static_cast<const double*>(src), rows, n,
+                                                              static_cast<double*>(dst), acc);
+  else
+    k_colsum<float><<<grid_for(n, 128), 128, 0, S(stream)>>>(static_cast<const float*>(src), rows, n,
+                                                             static_cast<float*>(dst), acc);
+  CK(cudaGetLastError());
+}
+
+void untranspose(const std::int64_t* t_row_ptr, std::int64_t in_nodes, const std::int32_t* t_src,
+                 const std::int32_t* t_eid, std::int32_t* src, std::int32_t* dst, void* stream) {
+  if (in_nodes <= 0) return;
+  k_untranspose<<<grid_for(in_nodes, 256), 256, 0, S(stream)>>>(reinterpret_cast<const i64*>(t_row_ptr), in_nodes,
+                                                                 t_src, t_eid, src, dst);
   CK(cudaGetLastError());
 }
 

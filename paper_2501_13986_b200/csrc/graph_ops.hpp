@@ -24,6 +24,16 @@ void segment_sum(bool f64, const void* rows, const std::int64_t* rp, const std::
 // src[e] = v for e in [rp[v], rp[v+1]) (CSR -> per-edge output node).
 void rowptr_expand(const std::int64_t* rp, std::int64_t nodes, std::int32_t* src, void* stream);
 
+// dst[c] = (accumulate ? dst[c] : 0) + sum over r < rows of src[r][c], in row
+// order (deterministic).
+void column_sum(bool f64, const void* src, std::int64_t rows, std::int64_t n, void* dst, bool accumulate,
+                void* stream);
+
+// Transposed CSR (t_row_ptr by neighbour, t_src, t_eid) -> the edge list in
+// edge order: src[e], dst[e] (the atomic-mode shard backward's input).
+void untranspose(const std::int64_t* t_row_ptr, std::int64_t in_nodes, const std::int32_t* t_src,
+                 const std::int32_t* t_eid, std::int32_t* src, std::int32_t* dst, void* stream);
+
 // ---- graph construction (conv.cpp:64-151) ---------------------------------
 
 // make_graph (conv.cpp:64-87): validates (first offending edge in edge order

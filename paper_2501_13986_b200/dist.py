@@ -103,11 +103,13 @@ class DistConvPlan:
     Inputs / outputs of each call are the rank's own slices: node-indexed
     arrays have ``shard.out_nodes`` rows (the rank's node range), edge arrays
     ``shard.edges`` rows. ``local`` computes the shard (default: the CUDA
-    ``ConvPlan``); ``group`` is the torch.distributed process group."""
+    ``ConvPlan``); ``group`` is the torch.distributed process group; ``mode``
+    DETERMINISTIC (default) or ATOMIC (Mode::atomic within each shard)."""
 
-    def __init__(self, plan, shard: GraphShard, group=None, local=None):
-        from . import ConvPlan
+    def __init__(self, plan, shard: GraphShard, group=None, local=None, mode=None):
+        from . import ConvPlan, DETERMINISTIC
         self.plan, self.shard, self.group = plan, shard, group
+        self.mode = DETERMINISTIC if mode is None else mode
         self.local = local if local is not None else ConvPlan(plan)
         self._gather_cache = {}
 
@@ -150,11 +152,11 @@ class DistConvPlan:
     # -- the three entry points -------------------------------------------------
     def forward(self, node_x, edge_y, edge_w):
         x_all = self._all_gather(node_x)
-        return self.local.forward_shard(self.shard, x_all, edge_y, edge_w)
+        return self.local.forward_shard(self.shard, x_all, edge_y, edge_w, mode=self.mode)
 
     def backward(self, node_x, edge_y, edge_w, g_node_z, node_x_all=None):
         x_all = self._all_gather(node_x) if node_x_all is None else node_x_all
-        gx_part, gy, gw = self.local.backward_shard(self.shard, x_all, edge_y, edge_w, g_node_z)
+        gx_part, gy, gw = self.local.backward_shard(self.shard, x_all, edge_y, edge_w, g_node_z, mode=self.mode)
         return self._reduce_scatter(gx_part), gy, gw
 
     def double_backward(self, node_x, edge_y, edge_w, g_node_z, upstream):
@@ -162,7 +164,7 @@ class DistConvPlan:
         x_all = self._all_gather(node_x)
         dgx_all = self._all_gather(d_gx)
         ox_part, oy, ow, ogz = self.local.double_backward_shard(self.shard, x_all, edge_y, edge_w, g_node_z,
-                                                                dgx_all, d_gy, d_gw)
+                                                                dgx_all, d_gy, d_gw, mode=self.mode)
         return self._reduce_scatter(ox_part), oy, ow, ogz
 
     def gather_x(self, node_x):

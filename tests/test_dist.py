@@ -111,16 +111,16 @@ class OracleShardConv:
         out[:a.shape[0]] = a
         return out
 
-    def forward_shard(self, sh, x_all, ey, ew):
+    def forward_shard(self, sh, x_all, ey, ew, mode=0):
         z = self.o.conv_forward(self._graph(sh), x_all.numpy(), ey.numpy(), ew.numpy())
         return torch.from_numpy(np.ascontiguousarray(z[:sh.out_nodes]))
 
-    def backward_shard(self, sh, x_all, ey, ew, gz):
+    def backward_shard(self, sh, x_all, ey, ew, gz, mode=0):
         gzp = self._pad(gz.numpy(), sh.in_nodes)
         gx, gy, gw = self.o.conv_backward(self._graph(sh), x_all.numpy(), ey.numpy(), ew.numpy(), gzp)
         return tuple(torch.from_numpy(np.ascontiguousarray(a)) for a in (gx, gy, gw))
 
-    def double_backward_shard(self, sh, x_all, ey, ew, gz, dgx_all, dgy, dgw):
+    def double_backward_shard(self, sh, x_all, ey, ew, gz, dgx_all, dgy, dgw, mode=0):
         gzp = self._pad(gz.numpy(), sh.in_nodes)
         ox, oy, ow, ogz = self.o.conv_double_backward(self._graph(sh), x_all.numpy(), ey.numpy(), ew.numpy(), gzp,
                                                       dgx_all.numpy(), dgy.numpy(), dgw.numpy())

@@ -32,10 +32,13 @@ def _inputs(o, g, dt):
     return nx, ey, ew, gnz, dgx, dgy, dgw
 
 
+@pytest.mark.parametrize("mode", ["det", "atomic"])
 @pytest.mark.parametrize("dt", [np.float32, np.float64], ids=["f32", "f64"])
 @pytest.mark.parametrize("world", [2, 3, 8])
 @pytest.mark.parametrize("cname", ["c1", "c2"])
-def test_sharded_conv_equals_whole_graph(cname, world, dt):
+def test_sharded_conv_equals_whole_graph(cname, world, dt, mode):
+    """mode "atomic": the *_shard entry points with CGF_CONV_ATOMIC (the
+    shard's CSR / transposed CSR expanded to an edge list on the device)."""
     import paper_2501_13986_b200 as p
     from paper_2501_13986_b200 import dist
     js = config(cname)
@@ -45,6 +48,7 @@ def test_sharded_conv_equals_whole_graph(cname, world, dt):
     g = p.Graph(n, src, nbr)
     nx, ey, ew, gnz, dgx, dgy, dgw = _inputs(o, og, dt)
     cp = p.ConvPlan(p.TpPlan(js))
+    M = p.ATOMIC if mode == "atomic" else p.DETERMINISTIC
     shards = [dist.GraphShard(g, world, r) for r in range(world)]
     chunk = shards[0].chunk
 
@@ -61,13 +65,13 @@ def test_sharded_conv_equals_whole_graph(cname, world, dt):
     ox_sum = torch.zeros_like(gx_sum)
     for s in shards:
         n0, n1, e0, e1 = s.node0, s.node0 + s.out_nodes, s.edge0, s.edge0 + s.edges
-        z.append(cp.forward_shard(s, x_all, D(ey[e0:e1]), D(ew[e0:e1])).cpu().numpy())
-        a, b, c = cp.backward_shard(s, x_all, D(ey[e0:e1]), D(ew[e0:e1]), D(gnz[n0:n1]))
+        z.append(cp.forward_shard(s, x_all, D(ey[e0:e1]), D(ew[e0:e1]), mode=M).cpu().numpy())
+        a, b, c = cp.backward_shard(s, x_all, D(ey[e0:e1]), D(ew[e0:e1]), D(gnz[n0:n1]), mode=M)
         gx_sum += a
         gy.append(b.cpu().numpy())
         gw.append(c.cpu().numpy())
         a, b, c, d = cp.double_backward_shard(s, x_all, D(ey[e0:e1]), D(ew[e0:e1]), D(gnz[n0:n1]), dgx_all,
-                                              D(dgy[e0:e1]), D(dgw[e0:e1]))
+                                              D(dgy[e0:e1]), D(dgw[e0:e1]), mode=M)
         ox_sum += a
         oy.append(b.cpu().numpy())
         ow.append(c.cpu().numpy())

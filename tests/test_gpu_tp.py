@@ -238,3 +238,32 @@ def test_random_problem_sweep(seed, rows, dt):
     outs = plan.double_backward(dev(x), dev(y), dev(w), dev(gz), (dev(da), dev(db), dev(dc)))
     for g, r, n in zip(outs, o.double_backward(x, y, w, gz, da, db, dc), ("dx", "dy", "dw", "dgz")):
         check(host(g), r, dt, n)
+
+
+SHARED_CASES = [("c3", config("c3"), 300), ("paper", config("paper"), 257), ("rand301", random_problem(301), 129),
+                ("rand2", random_problem(2), 77)]
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f32", "f64"])
+@pytest.mark.parametrize("name,js,rows", SHARED_CASES, ids=[c[0] for c in SHARED_CASES])
+def test_shared_w_backward_and_double_backward(name, js, rows, dt, monkeypatch):
+    """One W shared by every row (the C3 superset) on the SIMT kernels: the
+    per-row weight gradients go to a workspace reduced over rows in a fixed
+    order. Backward (FP64, or any shape the tcgen05 path does not take) and
+    double-backward (dL/dC shared too) against the oracle's w_shared mode;
+    small chunks (CGF_SHARED_W_CHUNK_ROWS) exercise the chunked reduction."""
+    monkeypatch.setenv("CGF_SHARED_W_CHUNK_ROWS", "100")
+    o, plan = O.Oracle(js), P().TpPlan(js)
+    x, y, w, gz, da, db, dc = inputs(o, rows, dt, seed=17, w_shared=True)
+    dc = dc[:1]
+    monkeypatch.setenv("CGF_UVW", "0")  # the SIMT path, also for C3 FP32
+    outs = plan.backward(dev(x), dev(y), dev(w), dev(gz), w_shared=True)
+    want = o.backward(x, y, w, gz, w_shared=True)
+    for got, wv, n in zip(outs, want, ("gx", "gy", "gw")):
+        check(host(got).reshape(wv.shape), wv, dt, f"shared-W {n}")
+    again = plan.backward(dev(x), dev(y), dev(w), dev(gz), w_shared=True)
+    assert all(torch.equal(a, b) for a, b in zip(outs, again))  # deterministic
+    outs = plan.double_backward(dev(x), dev(y), dev(w), dev(gz), (dev(da), dev(db), dev(dc)), w_shared=True)
+    want = o.double_backward(x, y, w, gz, da, db, dc, w_shared=True)
+    for got, wv, n in zip(outs, want, ("dx", "dy", "dw", "dgz")):
+        check(host(got).reshape(wv.shape), wv, dt, f"shared-W double-backward {n}")
