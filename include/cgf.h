@@ -328,6 +328,47 @@ int cgf_conv_double_backward_shard(cgf_plan* plan, int dtype, int64_t out_nodes,
                                    const void* d_gy, const void* d_gw, void* o_node_x, void* o_edge_y,
                                    void* o_edge_w, void* o_g_node_z, int mode, void* stream);
 
+/* ---- multi-GPU fused convolution (destination-partitioned, NCCL) ----------
+ * One process (or thread) per GPU, one rank each. The reference runs the conv
+ * on one host only (conv.cpp:234-528); SURVEY.md §8e's partition: rank r owns
+ * a contiguous range of output nodes (~|E|/P edges) with their node rows and
+ * their edges' y / W. Per call one exchange: the forward all-gathers node_x
+ * (padded [world x chunk] layout), the backward reduces the partial g_node_x
+ * with an all-to-all (ncclSend / ncclRecv) and a rank-ordered sum on the device
+ * (bitwise independent of NCCL's algorithm), the double-backward does both.
+ * NCCL is resolved at run time from libnccl.so.2 (the caller's instance when
+ * already loaded); `nccl_comm` is an ncclComm_t of `world` ranks. */
+typedef struct cgf_conv_shard cgf_conv_shard;
+/* NCCL bootstrap for callers without NCCL headers: a 128-byte unique id on
+ * one rank, shared out of band, then one communicator per rank. */
+int cgf_nccl_unique_id(char id[128]);
+int cgf_nccl_comm_create(int world, int rank, const char id[128], void** nccl_comm);
+int cgf_nccl_comm_destroy(void* nccl_comm);
+/* Rank `rank`'s shard of a host GraphCSR (row_ptr int64 [nodes + 1], nbr
+ * int32, sorted by (src, dst)): device CSR + transposed CSR in the padded
+ * neighbour space. info = {out_nodes, in_nodes, chunk, edges, node0, edge0}:
+ * the rank passes node rows [node0, node0 + out_nodes) and edges
+ * [edge0, edge0 + edges) of the global arrays. */
+int cgf_conv_shard_create(int64_t nodes, int64_t edges, const int64_t* row_ptr, const int32_t* nbr, int world,
+                          int rank, cgf_conv_shard** shard);
+int cgf_conv_shard_info(const cgf_conv_shard* shard, int64_t info[6]);
+void cgf_conv_shard_destroy(cgf_conv_shard* shard);
+/* ConvPlan::forward / backward (conv.hpp:99-111) and the double-backward over
+ * the partition; device pointers to the rank's rows, mode CGF_CONV_*. */
+int cgf_dist_conv_forward(cgf_plan* plan, int dtype, const cgf_conv_shard* shard, void* nccl_comm,
+                          const void* node_x, const void* edge_y, const void* edge_w, void* node_z, int mode,
+                          void* stream);
+int cgf_dist_conv_backward(cgf_plan* plan, int dtype, const cgf_conv_shard* shard, void* nccl_comm,
+                           const void* node_x, const void* edge_y, const void* edge_w, const void* g_node_z,
+                           void* g_node_x, void* g_edge_y, void* g_edge_w, int mode, void* stream);
+int cgf_dist_conv_double_backward(cgf_plan* plan, int dtype, const cgf_conv_shard* shard, void* nccl_comm,
+                                  const void* node_x, const void* edge_y, const void* edge_w, const void* g_node_z,
+                                  const void* d_gx, const void* d_gy, const void* d_gw, void* o_node_x,
+                                  void* o_edge_y, void* o_edge_w, void* o_g_node_z, int mode, void* stream);
+/* Deterministic all-reduce (sum) of `count` words in place: all-gather + a
+ * rank-ordered sum (the shared-W gradient of data-parallel replicas). */
+int cgf_dist_allreduce_ordered(int dtype, void* nccl_comm, int world, void* buf, int64_t count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -142,6 +142,16 @@ def lib():
     L.cgf_conv_unfused_workspace.restype = C.c_size_t
     L.cgf_conv_unfused_forward_host.argtypes = [P, I, I64, I64] + [P] * 6
     L.cgf_conv_unfused_backward_host.argtypes = [P, I, I64, I64] + [P] * 9
+    L.cgf_nccl_unique_id.argtypes = [C.c_char_p]
+    L.cgf_nccl_comm_create.argtypes = [I, I, C.c_char_p, C.POINTER(P)]
+    L.cgf_nccl_comm_destroy.argtypes = [P]
+    L.cgf_conv_shard_create.argtypes = [I64, I64, P, P, I, I, C.POINTER(P)]
+    L.cgf_conv_shard_info.argtypes = [P, P]
+    L.cgf_conv_shard_destroy.argtypes = [P]
+    L.cgf_dist_conv_forward.argtypes = [P, I, P, P] + [P] * 4 + [I, P]
+    L.cgf_dist_conv_backward.argtypes = [P, I, P, P] + [P] * 7 + [I, P]
+    L.cgf_dist_conv_double_backward.argtypes = [P, I, P, P] + [P] * 11 + [I, P]
+    L.cgf_dist_allreduce_ordered.argtypes = [I, P, I, P, I64, P]
     L.cgf_graph_make.argtypes = [I64, I64, P, P, I, P, P, P, P, P]
     L.cgf_graph_transpose.argtypes = [I64, I64, I64, P, P, P, P, P, P]
     L.cgf_graph_radius.argtypes = [I64, P, C.c_double, P, P, I64, P, P]

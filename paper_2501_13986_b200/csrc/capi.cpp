@@ -155,7 +155,8 @@ int row_groups(const cgf_plan* p, cgf::Comp comp, int dtype) {
   const int nu = static_cast<int>(p->units.size());
   if (comp != cgf::Comp::DBwd && comp != cgf::Comp::Bwd) return 1;
   if (const int g = group_env(comp == cgf::Comp::DBwd ? "CGF_ROW_GROUPS" : "CGF_ROW_GROUPS_BWD", nu)) return g;
-  if (comp == cgf::Comp::Bwd) return 1;
+  // backward: FP64 C2 12.4 -> 10.9 ms at G = 2 (profiles/r02_sweep_rowbwd.jsonl); FP32 G = 1 is fastest
+  if (comp == cgf::Comp::Bwd) return dtype == CGF_F64 && nu >= 8 ? 2 : 1;
   // C2 FP32 33.9 -> 28.2 ms (G = 6), FP64 29.1 -> 25.0 ms (G = 2); C1 FP32 0.29 -> 0.26 ms (G = 2)
   const int g = dtype == CGF_F32 ? std::min(6, (nu + 1) / 2) : (nu >= 8 ? 2 : 1);
   return std::clamp(g, 1, nu);
@@ -824,6 +825,10 @@ void host_bucket(std::int64_t nodes, std::int64_t edges, const std::int32_t* key
 }
 
 }  // namespace
+
+namespace cgf {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace cgf
 
 extern "C" {
 

@@ -43,6 +43,17 @@ DEVI void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
 DEVI void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_addr(dst)), "l"(src) : "memory");
 }
+// L2 eviction priorities (conv loops): gathered node rows that neighbouring
+// items re-read are kept (evict_last), per-edge streams go first (evict_first).
+DEVI u64 l2_policy_last() { u64 p; asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p)); return p; }
+DEVI u64 l2_policy_first() { u64 p; asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p)); return p; }
+DEVI void cp_async16_h(void* dst, const void* src, u64 pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(smem_addr(dst)), "l"(src), "l"(pol) : "memory");
+}
+DEVI void bulk_g2s_h(void* dst, const void* src, u32 bytes, u64* bar, u64 pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol) : "memory");
+}
 // Arrive on the mbarrier once all of this thread's prior cp.async completed
 // (the barrier counts one arrival per lane).
 DEVI void cp_async_arrive(u64* b) {
@@ -187,6 +198,7 @@ class Gen {
   std::string wsrc(const Sub& s, long long step, const std::string& arr) const;
   void emit_gy_reduce(const std::string& rowexpr);
   void emit_gy_flush_row(const std::string& rowexpr);
+  void emit_gy_resume(const std::string& rowexpr);
   void emit_class_loop_open(int k);
   void emit_class_loop_close(int k);
   void emit_rows_loop();
@@ -415,12 +427,17 @@ void Gen::emit_issue() {
     for (const auto& L : lay_)
       for (const auto& r : L.ranges)
         if (r.bulk && !r.window) base_id(r);
+  const bool hints = cfg_.l2_hints && conv();
+  // a range re-read by neighbouring items (node rows) vs a per-edge stream
+  auto keep = [&](const SlotRange& r) { return r.src != Src::Edge; };
+  auto pol = [&](const SlotRange& r) { return std::string(keep(r) ? "PL" : "PF"); };
   o_ << "__device__ __noinline__ void issue_unit(int u, i64 row, i64 nbr, i64 eid, i64 rows_tot, i64 edges_tot, T* sl,"
         " u64* bar, const T* __restrict__ X, const T* __restrict__ Y, const T* __restrict__ W,"
         " const T* __restrict__ GZ, const T* __restrict__ DA, const T* __restrict__ DB, const T* __restrict__ DC"
      << (lc ? ", int lane" : "") << ") {\n"
         "  (void)nbr; (void)eid; (void)rows_tot; (void)edges_tot;\n"
-     << (lc && !pb ? "" : "  fence_proxy_async();\n");
+     << (lc && !pb ? "" : "  fence_proxy_async();\n")
+     << (hints ? "  const u64 PL = l2_policy_last(), PF = l2_policy_first();\n" : "");
   int wlane = 31;  // parallel bulk: window ranges take lanes 31, 30, ...
   if (lc) {
     for (size_t i = 0; i < bases.size(); ++i) {
@@ -433,7 +450,7 @@ void Gen::emit_issue() {
       o_ << "  const char* B" << i << " = (const char*)(" << arr << " + " << I << " * (i64)" << stride << ");\n";
     }
     o_ << "  char* sb = (char*)sl;\n";
-    if (pb) o_ << "  u32 tx = 0; const char* s_ = nullptr; int d_ = 0; u32 b_ = 0;\n";
+    if (pb) o_ << "  u32 tx = 0; const char* s_ = nullptr; int d_ = 0; u32 b_ = 0;" << (hints ? " u64 p_ = 0;" : "") << "\n";
     // window ranges (y, db): same slot offsets in every class (laid out first)
     for (const auto& r : lay_[0].ranges) {
       if (!(r.bulk && r.window)) continue;
@@ -444,7 +461,8 @@ void Gen::emit_issue() {
         o_ << "  { const i64 b0 = " << I << " * " << r.stride << ", a0 = b0 & ~(i64)" << A() - 1 << ", a1 = (b0 + "
            << r.words << " + " << A() - 1 << ") & ~(i64)" << A() - 1 << ";\n    if (a1 <= " << tot << " * (i64)" << r.stride
            << ") { const u32 n_ = (u32)((a1 - a0) * sizeof(T)); tx += n_; if (lane == " << wlane << ") { s_ = (const char*)("
-           << r.arr << " + a0); d_ = " << r.slot_off * sz_ << "; b_ = n_; } } }\n";
+           << r.arr << " + a0); d_ = " << r.slot_off * sz_ << "; b_ = n_;" << (hints ? " p_ = " + pol(r) + ";" : "")
+           << " } } }\n";
         --wlane;
         continue;
       }
@@ -485,7 +503,9 @@ void Gen::emit_issue() {
       o_ << "    tx += " << fixed << "u;\n";
       for (size_t i = 0; i < runs.size(); ++i)
         o_ << "    " << (i ? "else " : "") << "if (lane == " << i << ") { s_ = B" << runs[i].base << " + "
-           << O(runs[i].off, runs[i].step) << "; d_ = " << runs[i].dst << "; b_ = " << runs[i].bytes << "u; }\n";
+           << O(runs[i].off, runs[i].step) << "; d_ = " << runs[i].dst << "; b_ = " << runs[i].bytes << "u;"
+           << (hints ? std::string(" p_ = ") + (bases[runs[i].base].second != Src::Edge ? "PL" : "PF") + ";" : "")
+           << " }\n";
     } else if (lc) {
       std::vector<std::pair<int, int>> pieces;  // (range, piece)
       for (size_t ri = 0; ri < L.ranges.size(); ++ri) {
@@ -495,7 +515,7 @@ void Gen::emit_issue() {
       }
       for (size_t t0 = 0; t0 < pieces.size(); t0 += 32) {
         const size_t t1 = std::min(pieces.size(), t0 + 32);
-        o_ << "    { const char* s_ = nullptr; int d_ = 0;\n";
+        o_ << "    { const char* s_ = nullptr; int d_ = 0;" << (hints ? " u64 p_ = 0;" : "") << "\n";
         size_t a = t0;
         bool first = true;
         while (a < t1) {
@@ -509,11 +529,15 @@ void Gen::emit_issue() {
                << ") + " << 16 * p0 << "; d_ = " << r.slot_off * sz_ + 16 * p0 << "; }\n";
           else
             o_ << "      " << (first ? "" : "else ") << "if (lane < " << b - t0 << ") { s_ = B" << base_id(r) << " + "
-               << O(r.off * sz_ + 16 * p0, r.step * sz_) << "; d_ = " << r.slot_off * sz_ + 16 * p0 << "; }\n";
+               << O(r.off * sz_ + 16 * p0, r.step * sz_) << "; d_ = " << r.slot_off * sz_ + 16 * p0 << ";"
+               << (hints ? " p_ = " + pol(r) + ";" : "") << " }\n";
           first = false;
           a = b;
         }
-        o_ << "      if (lane < " << t1 - t0 << ") cp_async16(sb + d_ + 16 * lane, s_ + 16 * lane); }\n";
+        if (hints)
+          o_ << "      if (lane < " << t1 - t0 << ") cp_async16_h(sb + d_ + 16 * lane, s_ + 16 * lane, p_); }\n";
+        else
+          o_ << "      if (lane < " << t1 - t0 << ") cp_async16(sb + d_ + 16 * lane, s_ + 16 * lane); }\n";
       }
     } else {
       o_ << "    u32 tx = " << L.fixed_bulk_bytes << "u; (void)tx;\n";
@@ -540,7 +564,8 @@ void Gen::emit_issue() {
     o_ << "  }\n";
   }
   if (pb)
-    o_ << "  if (lane == 0) mbar_expect_tx(bar, tx);\n  __syncwarp();\n  if (b_) bulk_g2s(sb + d_, s_, b_, bar);\n";
+    o_ << "  if (lane == 0) mbar_expect_tx(bar, tx);\n  __syncwarp();\n  if (b_) "
+       << (hints ? "bulk_g2s_h(sb + d_, s_, b_, bar, p_);\n" : "bulk_g2s(sb + d_, s_, b_, bar);\n");
   else if (lc)
     o_ << "  cp_async_arrive(bar);\n";
   o_ << "}\n\n";
@@ -618,7 +643,7 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
   const bool zx_on = cfg_.comp == Comp::Fwd || cfg_.comp == Comp::Bwd || cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ;
   const bool zab = cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX;
   const bool gfl = gy_flush();
-  const bool yq = !yreg() && m > 1;
+  const bool yq = !yreg() && (m > 1 || cfg_.y_item);
   if (yq) {
     // joint chunks: the item's y (and db) into registers once, so the products
     // below are shared across chunks; otherwise y is read from the slot at each
@@ -627,6 +652,29 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
     for (int j = 0; j < p_.dim_y; ++j)
       o_ << " yq[" << j << "] = sl[ys + " << j << "];" << (dual() ? " dbq[" + S(j) + "] = sl[dbs + " + S(j) + "];" : "");
     o_ << "\n";
+  }
+  if (cfg_.x_regs) {
+    // the unit's x (and dL/da) chunks into registers once: every sub reading a
+    // chunk then takes it from there instead of reloading the slot
+    for (size_t c = 0; c < u.x_chunks.size(); ++c) {
+      int dxc = 1, bpc = 0;
+      for (int si : u.subs)
+        if (p_.subs[si].x_off == u.x_chunks[c].off) {
+          dxc = p_.subs[si].dx();
+          bpc = p_.subs[si].bp;
+        }
+      const std::uint32_t xs = L.x_slot.at(u.x_chunks[c].off);
+      o_ << "      T xr" << c << "[" << dxc << "];" << (dual() ? " T ar" + S(c) + "[" + S(dxc) + "];" : "")
+         << "\n      if (lane < " << bpc << ") {";
+      for (int i = 0; i < dxc; ++i) o_ << " xr" << c << "[" << i << "] = sl[" << xs << " + lane * " << dxc << " + " << i << "];";
+      if (dual())
+        for (int i = 0; i < dxc; ++i)
+          o_ << " ar" << c << "[" << i << "] = sl[" << L.a_slot.at(u.x_chunks[c].off) << " + lane * " << dxc << " + " << i
+             << "];";
+      o_ << " } else {";
+      for (int i = 0; i < dxc; ++i) o_ << " xr" << c << "[" << i << "] = 0;" << (dual() ? " ar" + S(c) + "[" + S(i) + "] = 0;" : "");
+      o_ << " }\n";
+    }
   }
   auto Y = [&](int j) { return yreg() ? "y[" + S(j) + "]" : yq ? "yq[" + S(j) + "]" : "sl[ys + " + S(j) + "]"; };
   auto DB = [&](int j) { return yreg() ? "db[" + S(j) + "]" : yq ? "dbq[" + S(j) + "]" : "sl[dbs + " + S(j) + "]"; };
@@ -646,6 +694,13 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
       const long long swq = Cl.sw[qi];
       if (gfl && out_y()) o_ << "        T gyl" << X << "[" << s.dy() << "] = {};\n";
       const std::uint32_t xs = L.x_slot.at(s.x_off);
+      if (cfg_.x_regs) {
+        const int xc = u.x_chunk_of(s);
+        o_ << "        T xv" << X << "[" << dx << "];" << (dual() ? " T av" + X + "[" + S(dx) + "];" : "") << "\n       ";
+        for (int i = 0; i < dx; ++i)
+          o_ << " xv" << X << "[" << i << "] = xr" << xc << "[" << i << "];" << (dual() ? " av" + X + "[" + S(i) + "] = ar" + S(xc) + "[" + S(i) + "];" : "");
+        o_ << "\n";
+      } else {
       o_ << "        T xv" << X << "[" << dx << "];" << (dual() ? " T av" + X + "[" + S(dx) + "];" : "")
          << "\n        if (lane < " << s.bp << ") {";
       for (int i = 0; i < dx; ++i) o_ << " xv" << X << "[" << i << "] = sl[" << xs << " + lane * " << dx << " + " << i << "];";
@@ -657,6 +712,7 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
       if (dual())
         for (int i = 0; i < dx; ++i) o_ << " av" << X << "[" << i << "] = 0;";
       o_ << " }\n";
+      }
       std::string gzs;
       if (reads_gz()) {
         gzs = S(L.gz_slot.at(s.z_off));
@@ -818,9 +874,18 @@ void Gen::emit_gy_reduce(const std::string& rowexpr) {
   }
 }
 
+// A later group of a grouped kernel continues the running dy sum where the
+// earlier groups left it (in O1): the per-sub additions then happen in the
+// same order as in one ungrouped kernel, so any grouping gives bit-identical
+// dy (and a single-edge conv equals one TP call bitwise).
+void Gen::emit_gy_resume(const std::string& rowexpr) {
+  o_ << "    for (int j = lane; j < " << p_.dim_y << "; j += 32) gya[j] = O1[" << rowexpr << " * (i64)" << p_.dim_y
+     << " + j];\n    __syncwarp();\n";
+}
+
 void Gen::emit_gy_flush_row(const std::string& rowexpr) {
   o_ << "    __syncwarp();\n    for (int j = lane; j < " << p_.dim_y << "; j += 32) { O1[" << rowexpr << " * (i64)"
-     << p_.dim_y << " + j] " << (cfg_.gy_accum ? "+=" : "=") << " gya[j]; gya[j] = 0; }\n    __syncwarp();\n";
+     << p_.dim_y << " + j] = gya[j]; gya[j] = 0; }\n    __syncwarp();\n";
 }
 
 std::string zero_init(const std::string& name, int n) { return "T " + name + "[" + S(n) + "] = {};"; }
@@ -876,6 +941,7 @@ void Gen::emit_rows_loop() {
     o_ << " }\n";
   }
   if (out_y() && !gy_flush()) o_ << "    " << zero_init("gy", p_.dim_y) << "\n";
+  if (gy_flush() && cfg_.gy_accum) emit_gy_resume(it);
   for (size_t k = 0; k < cls_.size(); ++k) {
     const UClass& C = cls_[k];
     const Unit& u = U0(static_cast<int>(k));
@@ -983,6 +1049,7 @@ void Gen::emit_conv_loop() {
     // gxs[dim_x]; each item adds its register partials (lane-owned, conflict-free).
     o_ << "    for (i64 q = q0; q < q1; ++q) {\n      const i64 eid = EID[q]; const i64 nbr = NB[q]; (void)nbr;\n";
     if (out_y() && !gy_flush()) o_ << "      " << zero_init("gy", p_.dim_y) << "\n";
+    if (gy_flush() && cfg_.gy_accum) emit_gy_resume("eid");
     for (size_t k = 0; k < cls_.size(); ++k) {
       const UClass& C = cls_[k];
       const Unit& u = U0(static_cast<int>(k));
@@ -1149,6 +1216,12 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "newissue") cfg.old_issue = false;
     else if (k == "noywin") cfg.y_window = false;
     else if (k == "joint") cfg.joint = true;
+    else if (k == "l2hint") cfg.l2_hints = true;
+    else if (k == "nol2hint") cfg.l2_hints = false;
+    else if (k == "xregs") cfg.x_regs = true;
+    else if (k == "noxregs") cfg.x_regs = false;
+    else if (k == "yitem") cfg.y_item = true;
+    else if (k == "noyitem") cfg.y_item = false;
   }
 }
 

@@ -125,7 +125,7 @@ __global__ void k_expand(const i64* __restrict__ rp, i64 nodes, int* __restrict_
 // dst[c] (+)= sum over r < rows of src[r * n + c], summed in row order (the
 // shared-W weight gradient's reduction over per-row partials; deterministic).
 template <typename T>
-__global__ void k_colsum(const T* __restrict__ src, i64 rows, i64 n, T* __restrict__ dst, int accumulate) {
+__global__ void k_colsum(const T* __restrict__ src, i64 rows, i64 n, i64 ld, T* __restrict__ dst, int accumulate) {
   for (i64 c = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; c < n;
        c += static_cast<i64>(gridDim.x) * blockDim.x) {
     T acc = accumulate ? dst[c] : T(0);
@@ -133,11 +133,11 @@ __global__ void k_colsum(const T* __restrict__ src, i64 rows, i64 n, T* __restri
     for (; r + 8 <= rows; r += 8) {
       T v[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = __ldg(src + (r + k) * n + c);
+      for (int k = 0; k < 8; ++k) v[k] = __ldg(src + (r + k) * ld + c);
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc += v[k];
     }
-    for (; r < rows; ++r) acc += __ldg(src + r * n + c);
+    for (; r < rows; ++r) acc += __ldg(src + r * ld + c);
     dst[c] = acc;
   }
 }
@@ -326,14 +326,15 @@ void rowptr_expand(const std::int64_t* rp, std::int64_t nodes, std::int32_t* src
 }
 
 void column_sum(bool f64, const void* src, std::int64_t rows, std::int64_t n, void* dst, bool accumulate,
-                void* stream) {
+                void* stream, std::int64_t ld) {
   if (n <= 0) return;
+  if (ld <= 0) ld = n;
   const int acc = accumulate ? 1 : 0;
   if (f64)
-    k_colsum<double><<<grid_for(n, 128), 128, 0, S(stream)>>>(static_cast<const double*>(src), rows, n,
+    k_colsum<double><<<grid_for(n, 128), 128, 0, S(stream)>>>(static_cast<const double*>(src), rows, n, ld,
                                                               static_cast<double*>(dst), acc);
   else
-    k_colsum<float><<<grid_for(n, 128), 128, 0, S(stream)>>>(static_cast<const float*>(src), rows, n,
+    k_colsum<float><<<grid_for(n, 128), 128, 0, S(stream)>>>(static_cast<const float*>(src), rows, n, ld,
                                                              static_cast<float*>(dst), acc);
   CK(cudaGetLastError());
 }

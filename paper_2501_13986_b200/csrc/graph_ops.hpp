@@ -24,10 +24,10 @@ void segment_sum(bool f64, const void* rows, const std::int64_t* rp, const std::
 // src[e] = v for e in [rp[v], rp[v+1]) (CSR -> per-edge output node).
 void rowptr_expand(const std::int64_t* rp, std::int64_t nodes, std::int32_t* src, void* stream);
 
-// dst[c] = (accumulate ? dst[c] : 0) + sum over r < rows of src[r][c], in row
-// order (deterministic).
+// dst[c] = (accumulate ? dst[c] : 0) + sum over r < rows of src[r * ld + c]
+// (c < n; ld = 0 means n), in row order (deterministic).
 void column_sum(bool f64, const void* src, std::int64_t rows, std::int64_t n, void* dst, bool accumulate,
-                void* stream);
+                void* stream, std::int64_t ld = 0);
 
 // Transposed CSR (t_row_ptr by neighbour, t_src, t_eid) -> the edge list in
 // edge order: src[e], dst[e] (the atomic-mode shard backward's input).

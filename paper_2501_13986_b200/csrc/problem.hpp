@@ -37,6 +37,9 @@ struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// Sets cgf_last_error()'s message on this thread (capi.cpp).
+void set_last_error(const std::string& msg);
+
 // ----------------------------------------------------------------- irreps --
 struct MulIrrep {
   int mult = 1;

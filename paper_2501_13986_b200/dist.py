@@ -33,7 +33,8 @@ import numpy as np
 
 from . import ShapeError, lib, _check
 
-__all__ = ["partition_bounds", "GraphShard", "DistConvPlan", "lattice_radius_graph"]
+__all__ = ["partition_bounds", "GraphShard", "DistConvPlan", "lattice_radius_graph", "NcclComm", "DeviceShard",
+           "CAbiDistConvPlan", "allreduce_ordered"]
 
 
 def partition_bounds(row_ptr: np.ndarray, world: int) -> np.ndarray:
@@ -196,3 +197,107 @@ def lattice_radius_graph(n: int, spacing: float = 1.0, r_cut: float = 3.0):
     src = s_idx.astype(np.int64)
     nbr = src + delta[t_idx]
     return nodes, src, nbr
+
+
+# ------------------------------------------------ the C ABI's multi-GPU path --
+
+class NcclComm:
+    """An NCCL communicator made through the C ABI (cgf_nccl_*): for callers
+    that drive the C-ABI multi-GPU conv without torch.distributed. ``uid`` is
+    the 128-byte id from ``NcclComm.unique_id()`` on one rank, shared out of
+    band."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+        buf = C.create_string_buffer(128)
+        _check(lib().cgf_nccl_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, world: int, rank: int, uid: bytes):
+        import ctypes as C
+        h = C.c_void_p()
+        _check(lib().cgf_nccl_comm_create(world, rank, uid, C.byref(h)))
+        self.world, self.rank, self.h = world, rank, h
+
+    def close(self):
+        if self.h:
+            _check(lib().cgf_nccl_comm_destroy(self.h))
+            self.h = None
+
+
+class DeviceShard:
+    """cgf_conv_shard: rank ``rank``'s part of a host CSR graph, partitioned
+    and uploaded by libcgf (the same partition as GraphShard)."""
+
+    def __init__(self, graph, world: int, rank: int):
+        import ctypes as C
+        h = C.c_void_p()
+        _check(lib().cgf_conv_shard_create(graph.nodes, graph.edges, graph.row_ptr.ctypes.data,
+                                           graph.nbr.ctypes.data if graph.edges else None, world, rank, C.byref(h)))
+        self.h = h
+        info = np.zeros(6, np.int64)
+        _check(lib().cgf_conv_shard_info(h, info.ctypes.data))
+        self.out_nodes, self.in_nodes, self.chunk, self.edges, self.node0, self.edge0 = (int(v) for v in info)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().cgf_conv_shard_destroy(self.h)
+            self.h = None
+
+
+class CAbiDistConvPlan:
+    """The multi-GPU conv through the C ABI (cgf_dist_conv_*): NCCL all-gather
+    of node_x / all-to-all + rank-ordered reduction of g_node_x inside libcgf,
+    on torch CUDA tensors of the rank's rows."""
+
+    def __init__(self, plan, shard: DeviceShard, comm: NcclComm, mode=None):
+        from . import DETERMINISTIC
+        self.plan, self.shard, self.comm = plan, shard, comm
+        self.mode = DETERMINISTIC if mode is None else mode
+
+    def _call(self, fn, dt, *arrays, ref):
+        import ctypes as C
+        import torch
+        from . import _dtype_code
+        st = C.c_void_p(torch.cuda.current_stream(ref.device).cuda_stream)
+        _check(fn(self.plan._h, _dtype_code(ref), self.shard.h, self.comm.h,
+                  *(C.c_void_p(a.data_ptr()) for a in arrays), self.mode, st))
+
+    def forward(self, node_x, edge_y, edge_w):
+        p, sh = self.plan, self.shard
+        z = node_x.new_empty((sh.out_nodes, p.dim_z))
+        self._call(lib().cgf_dist_conv_forward, None, node_x, edge_y, edge_w, z, ref=node_x)
+        return z
+
+    def backward(self, node_x, edge_y, edge_w, g_node_z):
+        p, sh = self.plan, self.shard
+        gx = node_x.new_empty((sh.out_nodes, p.dim_x))
+        gy, gw = torch_like(edge_y), torch_like(edge_w)
+        self._call(lib().cgf_dist_conv_backward, None, node_x, edge_y, edge_w, g_node_z, gx, gy, gw, ref=node_x)
+        return gx, gy, gw
+
+    def double_backward(self, node_x, edge_y, edge_w, g_node_z, upstream):
+        p, sh = self.plan, self.shard
+        d_gx, d_gy, d_gw = upstream
+        ox = node_x.new_empty((sh.out_nodes, p.dim_x))
+        oy, ow = torch_like(edge_y), torch_like(edge_w)
+        ogz = node_x.new_empty((sh.out_nodes, p.dim_z))
+        self._call(lib().cgf_dist_conv_double_backward, None, node_x, edge_y, edge_w, g_node_z, d_gx, d_gy, d_gw,
+                   ox, oy, ow, ogz, ref=node_x)
+        return ox, oy, ow, ogz
+
+
+def torch_like(a):
+    return a.new_empty(a.shape)
+
+
+def allreduce_ordered(buf, comm: NcclComm):
+    """In-place deterministic sum over ranks (cgf_dist_allreduce_ordered)."""
+    import ctypes as C
+    import torch
+    from . import _dtype_code
+    st = C.c_void_p(torch.cuda.current_stream(buf.device).cuda_stream)
+    _check(lib().cgf_dist_allreduce_ordered(_dtype_code(buf), comm.h, comm.world, C.c_void_p(buf.data_ptr()),
+                                            buf.numel(), st))
+    return buf

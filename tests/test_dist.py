@@ -214,3 +214,4 @@ def test_bench_gpus_2_launches_two_ranks_cpu_harness():
     rec = json.loads(lines[0])
     assert rec["harness"] and rec["n_gpus"] == 2 and rec["conv"]["n_gpus"] == 2
     assert "all_to_all_single" in rec["conv"]["collectives"]
+

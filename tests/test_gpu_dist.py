@@ -90,3 +90,41 @@ def test_sharded_conv_equals_whole_graph(cname, world, dt, mode):
                             (np.concatenate(ogz), want_d[3], "dg_node_z")):
         err = O.rel_error(got, want)
         assert err <= TOL[dt], f"{what}: {err:.3e}"
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64], ids=["f32", "f64"])
+def test_cabi_multi_gpu_conv_world1(dt):
+    """The C ABI's multi-GPU conv (cgf_dist_conv_*, NCCL inside libcgf) on a
+    1-rank communicator: partition, padded all-gather, all-to-all reduction and
+    the ordered sum run for real; results equal the whole-graph ConvPlan
+    bitwise (one rank: the same kernels on the same rows). The shard layout
+    matches dist.GraphShard's for 3 ranks."""
+    import paper_2501_13986_b200 as p
+    from paper_2501_13986_b200 import dist
+    js = config("c1")
+    o = O.Oracle(js)
+    n, src, nbr = dist.lattice_radius_graph(5, 1.0, 1.8)
+    og = O.make_graph(n, src, nbr)
+    g = p.Graph(n, src, nbr)
+    for r in range(3):
+        ds, gs = dist.DeviceShard(g, 3, r), dist.GraphShard(g, 3, r)
+        assert (ds.out_nodes, ds.in_nodes, ds.chunk, ds.edges, ds.node0, ds.edge0) == \
+            (gs.out_nodes, gs.in_nodes, gs.chunk, gs.edges, gs.node0, gs.edge0)
+    nx, ey, ew, gnz, dgx, dgy, dgw = _inputs(o, og, dt)
+    D = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    plan = p.TpPlan(js)
+    comm = dist.NcclComm(1, 0, dist.NcclComm.unique_id())
+    try:
+        dc = dist.CAbiDistConvPlan(plan, dist.DeviceShard(g, 1, 0), comm)
+        cp = p.ConvPlan(plan)
+        args = (D(nx), D(ey), D(ew))
+        assert torch.equal(dc.forward(*args), cp.forward(g, *args))
+        for a, b in zip(dc.backward(*args, D(gnz)), cp.backward(g, *args, D(gnz))):
+            assert torch.equal(a, b)
+        up = (D(dgx), D(dgy), D(dgw))
+        for a, b in zip(dc.double_backward(*args, D(gnz), up), cp.double_backward(g, *args, D(gnz), up)):
+            assert torch.equal(a, b)
+        buf = D(gnz[:7].copy())
+        assert torch.equal(dist.allreduce_ordered(buf.clone(), comm), buf)
+    finally:
+        comm.close()
