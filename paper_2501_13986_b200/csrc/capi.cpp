@@ -249,6 +249,11 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
     // profiles/r01_ab_pbulk_small.log); for the C2 TP's conv they are slower
     if (small && (loop == cgf::Loop::ConvByOutput || loop == cgf::Loop::ConvByInput)) cfg.par_bulk = true;
   }
+  // x chunks / y in registers once per staged item: C4 conv double-backward
+  // FP64 189.6 -> 179.4 ms, FP32 91.0 -> 88.0; C2 FP64 backward 11.40 -> 10.87
+  // ms; the forward kernels are neutral or slower (profiles/r02_ab_flags.jsonl)
+  cfg.x_regs = cfg.y_item = (comp != cgf::Comp::Fwd && comp != cgf::Comp::Bwd) ||
+                            (comp == cgf::Comp::Bwd && loop == cgf::Loop::Rows && dtype == CGF_F64);
   cgf::apply_gen_flags(cfg, flags);
   std::vector<cgf::Unit> subset;
   if (ngroups > 1) {
