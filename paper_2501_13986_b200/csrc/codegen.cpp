@@ -33,6 +33,15 @@ DEVI bool mbar_try(u64* b, u32 parity) {
   return ok != 0;
 }
 DEVI void mbar_wait(u64* b, u32 parity) { while (!mbar_try(b, parity)) { } }
+// try_wait with a suspend-time hint (ns): a waiting warp is suspended by the
+// hardware until the phase completes or the hint expires, not spinning.
+DEVI bool mbar_try_sleep(u64* b, u32 parity) {
+  u32 ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
+               : "=r"(ok) : "r"(smem_addr(b)), "r"(parity), "r"(1000000u) : "memory");
+  return ok != 0;
+}
+DEVI void mbar_wait_sleep(u64* b, u32 parity) { while (!mbar_try_sleep(b, parity)) { } }
 DEVI void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // TMA 1-D bulk copy global -> shared, completion counted on an mbarrier (bytes).
 DEVI void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
@@ -573,7 +582,8 @@ void Gen::emit_issue() {
 
 void Gen::emit_wait_and_sync(int k) {
   const Layout& L = lay_[k];
-  o_ << "      T* sl = wsm + slot * SLOT_WORDS;\n      mbar_wait(&bars[slot], phase);\n";
+  o_ << "      T* sl = wsm + slot * SLOT_WORDS;\n      " << (cfg_.wait_sleep ? "mbar_wait_sleep" : "mbar_wait")
+     << "(&bars[slot], phase);\n";
   bool sync = false;
   for (const auto& r : L.ranges) {
     if ((r.arr == "Y" || r.arr == "DB") && !r.window)
@@ -1216,6 +1226,8 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "newissue") cfg.old_issue = false;
     else if (k == "noywin") cfg.y_window = false;
     else if (k == "joint") cfg.joint = true;
+    else if (k == "waitsleep") cfg.wait_sleep = true;
+    else if (k == "nowaitsleep") cfg.wait_sleep = false;
     else if (k == "l2hint") cfg.l2_hints = true;
     else if (k == "nol2hint") cfg.l2_hints = false;
     else if (k == "xregs") cfg.x_regs = true;
