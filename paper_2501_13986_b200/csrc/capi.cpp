@@ -248,6 +248,11 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
     // range (C5: FP32 bwd 44.8 -> 40.5 ms, FP64 fwd 24.7 -> 21.9, FP64 bwd 140.8 -> 130.3;
     // profiles/r01_ab_pbulk_small.log); for the C2 TP's conv they are slower
     if (small && (loop == cgf::Loop::ConvByOutput || loop == cgf::Loop::ConvByInput)) cfg.par_bulk = true;
+    // the large-row conv forward is latency-bound at 2 CTAs / SM (235 registers):
+    // capping registers for 3 CTAs / SM measured C4 FP32 12.9 -> 11.1 ms (the
+    // backward and the small-TP (C5) kernels are slower that way,
+    // profiles/r02_ab_conv2.jsonl)
+    if (!small && loop == cgf::Loop::ConvByOutput && comp == cgf::Comp::Fwd && dtype == CGF_F32) cfg.min_blocks = 3;
   }
   // x chunks / y in registers once per staged item: C4 conv double-backward
   // FP64 189.6 -> 179.4 ms, FP32 91.0 -> 88.0; C2 FP64 backward 11.40 -> 10.87
