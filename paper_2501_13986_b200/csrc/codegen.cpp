@@ -184,6 +184,9 @@ class Gen {
   bool edges() const { return cfg_.loop == Loop::ConvEdges; }
   bool yreg() const { return cfg_.y_regs && (cfg_.loop == Loop::Rows || edges()); }
   bool gy_flush() const { return out_y() && (dual() || cfg_.f64); }
+  int eb() const {
+    return cfg_.loop == Loop::ConvByOutput && cfg_.lane_copy ? std::max(1, cfg_.edges_per_item) : 1;
+  }
   Src x_src() const { return cfg_.loop == Loop::ConvByOutput || edges() ? Src::Nbr : Src::Row; }
   Src z_src() const { return cfg_.loop == Loop::ConvByInput ? Src::Nbr : Src::Row; }
   Src e_src() const { return conv() ? Src::Edge : Src::Row; }
@@ -198,7 +201,7 @@ class Gen {
   void layout();
   std::string range_src(const SlotRange& r) const;
   void emit_issue();
-  void emit_wait_and_sync(int k);
+  void emit_wait_and_sync(int k, bool with_wait = true);
   void emit_release();
   void emit_store(const std::string& dst, const std::string& rowexpr, std::uint32_t stride, long long off,
                   long long step, std::uint32_t words, int guard_rows, int width, const std::string& reg,
@@ -443,7 +446,7 @@ void Gen::emit_issue() {
   o_ << "__device__ __noinline__ void issue_unit(int u, i64 row, i64 nbr, i64 eid, i64 rows_tot, i64 edges_tot, T* sl,"
         " u64* bar, const T* __restrict__ X, const T* __restrict__ Y, const T* __restrict__ W,"
         " const T* __restrict__ GZ, const T* __restrict__ DA, const T* __restrict__ DB, const T* __restrict__ DC"
-     << (lc ? ", int lane" : "") << ") {\n"
+     << (lc ? ", int lane" : "") << (lc ? ", bool v_" : "") << ") {\n"
         "  (void)nbr; (void)eid; (void)rows_tot; (void)edges_tot;\n"
      << (lc && !pb ? "" : "  fence_proxy_async();\n")
      << (hints ? "  const u64 PL = l2_policy_last(), PF = l2_policy_first();\n" : "");
@@ -460,6 +463,9 @@ void Gen::emit_issue() {
     }
     o_ << "  char* sb = (char*)sl;\n";
     if (pb) o_ << "  u32 tx = 0; const char* s_ = nullptr; int d_ = 0; u32 b_ = 0;" << (hints ? " u64 p_ = 0;" : "") << "\n";
+    // v_ false: an item slot past the row's last edge (multi-edge items) --
+    // no copies, but the lane still arrives so the barrier count holds
+    o_ << "  if (v_) {\n";
     // window ranges (y, db): same slot offsets in every class (laid out first)
     for (const auto& r : lay_[0].ranges) {
       if (!(r.bulk && r.window)) continue;
@@ -572,6 +578,7 @@ void Gen::emit_issue() {
     }
     o_ << "  }\n";
   }
+  if (lc) o_ << "  }\n";
   if (pb)
     o_ << "  if (lane == 0) mbar_expect_tx(bar, tx);\n  __syncwarp();\n  if (b_) "
        << (hints ? "bulk_g2s_h(sb + d_, s_, b_, bar, p_);\n" : "bulk_g2s(sb + d_, s_, b_, bar);\n");
@@ -580,10 +587,11 @@ void Gen::emit_issue() {
   o_ << "}\n\n";
 }
 
-void Gen::emit_wait_and_sync(int k) {
+void Gen::emit_wait_and_sync(int k, bool with_wait) {
   const Layout& L = lay_[k];
-  o_ << "      T* sl = wsm + slot * SLOT_WORDS;\n      " << (cfg_.wait_sleep ? "mbar_wait_sleep" : "mbar_wait")
-     << "(&bars[slot], phase);\n";
+  if (with_wait)
+    o_ << "      T* sl = wsm + slot * SLOT_WORDS;\n      " << (cfg_.wait_sleep ? "mbar_wait_sleep" : "mbar_wait")
+       << "(&bars[slot], phase);\n";
   bool sync = false;
   for (const auto& r : L.ranges) {
     if ((r.arr == "Y" || r.arr == "DB") && !r.window)
@@ -921,7 +929,7 @@ void Gen::emit_rows_loop() {
         "    const int s_ = (int)(pn % D);\\\n"
      << (edges() ? "    issue_unit(u_, (i64)EID[r_], (i64)NB[r_], r_, rows, edges_tot,"
                  : "    issue_unit(u_, r_, r_, r_, rows, rows,")
-     << " wsm + s_ * SLOT_WORDS, &bars[s_], X, Y, W, GZ, DA, DB, DC" << (cfg_.lane_copy ? ", lane" : "") << ");\\\n"
+     << " wsm + s_ * SLOT_WORDS, &bars[s_], X, Y, W, GZ, DA, DB, DC" << (cfg_.lane_copy ? ", lane, true" : "") << ");\\\n"
         "    ++pn; } } while (0)\n"
         "  " << (cfg_.lane_copy ? "" : "if (lane == 0) ") << "for (int d = 0; d < D; ++d) producer_next();\n"
         "  int slot = 0; u32 phase = 0;\n"
@@ -1021,11 +1029,21 @@ void Gen::emit_conv_loop() {
         "  " << (cfg_.lane_copy ? "" : "if (lane == 0) ") << "{ seek(); fetch_idx(); }\n"
         "  int pslot = 0;\n"
         "#define producer_next() do { if (pk < my_rows) {\\\n"
-        "    const i64 r_ = prow(pk);\\\n"
-        "    issue_unit(pu, r_, pnb, peid, rows, edges_tot, wsm + pslot * SLOT_WORDS, &bars[pslot], X, Y, W, GZ, DA, DB, DC" << (cfg_.lane_copy ? ", lane" : "") << ");\\\n"
-        "    if (++pslot == D) pslot = 0;\\\n";
-  o_ << (bi ? "    if (++pu == NU) { pu = 0; if (++pq == pq1) { ++pk; seek(); } fetch_idx(); }\\\n"
-            : "    if (++pq == pq1) { pq = pq0; if (++pu == NU) { pu = 0; ++pk; seek(); } } fetch_idx();\\\n");
+        "    const i64 r_ = prow(pk);\\\n";
+  if (eb() > 1) {
+    // EB consecutive edges of the row per item, each in its own sub-slot
+    o_ << "    for (int e_ = 0; e_ < EB; ++e_) { const bool v_ = pq + e_ < pq1; const i64 q_ = v_ ? pq + e_ : pq;\\\n"
+          "      issue_unit(pu, r_, (i64)NB[q_], q_, rows, edges_tot, wsm + pslot * SLOT_WORDS + e_ * LW, &bars[pslot],"
+          " X, Y, W, GZ, DA, DB, DC, lane, v_); }\\\n"
+          "    if (++pslot == D) pslot = 0;\\\n"
+          "    pq += EB; if (pq >= pq1) { pq = pq0; if (++pu == NU) { pu = 0; ++pk; seek(); } }\\\n";
+  } else {
+    o_ << "    issue_unit(pu, r_, pnb, peid, rows, edges_tot, wsm + pslot * SLOT_WORDS, &bars[pslot], X, Y, W, GZ, DA, DB, DC"
+       << (cfg_.lane_copy ? ", lane, true" : "") << ");\\\n"
+          "    if (++pslot == D) pslot = 0;\\\n";
+    o_ << (bi ? "    if (++pu == NU) { pu = 0; if (++pq == pq1) { ++pk; seek(); } fetch_idx(); }\\\n"
+              : "    if (++pq == pq1) { pq = pq0; if (++pu == NU) { pu = 0; ++pk; seek(); } } fetch_idx();\\\n");
+  }
   o_ << "  } } while (0)\n"
         "  " << (cfg_.lane_copy ? "" : "if (lane == 0) ") << "for (int d = 0; d < D; ++d) producer_next();\n"
         "  int slot = 0; u32 phase = 0;\n"
@@ -1042,11 +1060,24 @@ void Gen::emit_conv_loop() {
       }
       emit_class_loop_open(static_cast<int>(k));
       for (size_t z = 0; z < u.z_pieces.size(); ++z) o_ << "      " << zero_init("pz" + S(z), zdz[u.z_pieces[z].off]) << "\n";
-      o_ << "      for (i64 q = q0; q < q1; ++q) {\n      const i64 eid = q; const i64 nbr = NB[q]; (void)nbr;\n";
-      emit_wait_and_sync(static_cast<int>(k));
-      emit_unit_body(static_cast<int>(k));
-      emit_release();
-      o_ << "      }\n";
+      if (eb() > 1) {
+        o_ << "      for (i64 q = q0; q < q1; q += EB) {\n      T* sb_ = wsm + slot * SLOT_WORDS;\n      "
+           << (cfg_.wait_sleep ? "mbar_wait_sleep" : "mbar_wait") << "(&bars[slot], phase);\n"
+           << "      const int ne_ = (int)(q1 - q < EB ? q1 - q : EB);\n#pragma unroll 1\n"
+           << "      for (int e_ = 0; e_ < ne_; ++e_) {\n      const i64 eid = q + e_; const i64 nbr = NB[eid]; (void)nbr;\n"
+           << "      T* sl = sb_ + e_ * LW;\n";
+        emit_wait_and_sync(static_cast<int>(k), false);
+        emit_unit_body(static_cast<int>(k));
+        o_ << "      }\n";
+        emit_release();
+        o_ << "      }\n";
+      } else {
+        o_ << "      for (i64 q = q0; q < q1; ++q) {\n      const i64 eid = q; const i64 nbr = NB[q]; (void)nbr;\n";
+        emit_wait_and_sync(static_cast<int>(k));
+        emit_unit_body(static_cast<int>(k));
+        emit_release();
+        o_ << "      }\n";
+      }
       for (size_t z = 0; z < u.z_pieces.size(); ++z) {
         const auto& zp = u.z_pieces[z];
         emit_store(cfg_.comp == Comp::Fwd ? "O0" : "O3", "row", p_.dim_z, zp.off, C.zstep[z], zp.words, zb[zp.off],
@@ -1130,6 +1161,8 @@ KernelSource Gen::run() {
     slot_words = std::max(slot_words, L.words);
     for (const auto& r : L.ranges) (r.bulk ? bulk : sync)++;
   }
+  const std::uint32_t lw = up(slot_words);  // one edge's sub-slot (multi-edge items)
+  if (eb() > 1) slot_words = lw * static_cast<std::uint32_t>(eb());
   // Default ring depth: ~12 KB of staged inputs per warp, 2..4 slots.
   int depth = cfg_.depth > 0 ? cfg_.depth
                              : static_cast<int>(std::clamp<std::uint64_t>(12288 / std::max<std::uint64_t>(1, slot_words * sz_), 2, 4));
@@ -1159,7 +1192,7 @@ KernelSource Gen::run() {
      << " code classes; " << ks.name << "\n";
   o_ << "typedef " << (cfg_.f64 ? "double" : "float") << " T;\n";
   o_ << "#define NW " << warps << "\n#define D " << depth << "\n#define NU " << units_.size() << "\n#define SLOT_WORDS "
-     << slot_words << "\n#define WARP_BYTES " << wb << "\n\n";
+     << slot_words << "\n#define WARP_BYTES " << wb << "\n#define EB " << eb() << "\n#define LW " << lw << "\n\n";
   emit_issue();
   o_ << "extern \"C\" __global__ void __launch_bounds__(NW * 32"
      << (cfg_.min_blocks > 0 ? ", " + S(cfg_.min_blocks) : "") << ") " << ks.name
@@ -1180,7 +1213,7 @@ KernelSource Gen::run() {
   if (by_input())
     o_ << "  T* gxs = scr + " << off_gxs_ << ";\n  for (int j = lane; j < " << gx_words_ << "; j += 32) gxs[j] = 0;\n";
   o_ << "  u64* bars = (u64*)(smem_raw + NW * WARP_BYTES) + wid * D;\n"
-        "  if (lane == 0) { for (int d = 0; d < D; ++d) mbar_init(&bars[d], " << (cfg_.lane_copy && !cfg_.par_bulk ? 32 : 1) << "); mbar_fence_init(); }\n"
+        "  if (lane == 0) { for (int d = 0; d < D; ++d) mbar_init(&bars[d], " << (cfg_.lane_copy && !cfg_.par_bulk ? 32 : 1) * eb() << "); mbar_fence_init(); }\n"
         "  __syncwarp();\n"
         "  const i64 gwarp = (i64)blockIdx.x * NW + wid, nwarp = (i64)gridDim.x * NW;\n"
         "  const i64 n_items = " << (edges() ? "edges_tot" : "rows") << ";\n"
@@ -1226,6 +1259,7 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "newissue") cfg.old_issue = false;
     else if (k == "noywin") cfg.y_window = false;
     else if (k == "joint") cfg.joint = true;
+    else if (k == "epi") cfg.edges_per_item = std::max(1, v);
     else if (k == "waitsleep") cfg.wait_sleep = true;
     else if (k == "nowaitsleep") cfg.wait_sleep = false;
     else if (k == "l2hint") cfg.l2_hints = true;

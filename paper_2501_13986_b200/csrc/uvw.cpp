@@ -78,15 +78,10 @@ DEVI void mbar_wait_t(u64* b, u32 parity, int tag) {
   if ((threadIdx.x & 31) == 0) atomicAdd(&prof_s[tag], (unsigned long long)(clock64() - c0));
   return;
 #endif
-  // try_wait with a suspend-time hint: the warp sleeps in hardware until the
-  // phase completes (or the hint expires) instead of spinning -- the spin
-  // loop's branches, counters and timer reads took issue slots the producer
-  // warps on the same sub-partition needed (ncu: ~40 % of the forward's
-  // issued instructions were wait-loop overhead, profiles/r02_ncu_sass_uvw.txt)
   const u64 t0 = gtimer();
   for (u32 it = 1;; ++it) {
-    if (mbar_try_sleep(b, parity)) return;
-    if ((it & 15u) == 0 && gtimer() - t0 > 4000000000ull) {
+    if (mbar_try(b, parity)) return;
+    if ((it & 1023u) == 0 && gtimer() - t0 > 4000000000ull) {
       printf("cgf_uvw: mbarrier timeout tag=%d block=%d thread=%d parity=%u\n", tag, blockIdx.x, threadIdx.x, parity);
       __trap();
     }

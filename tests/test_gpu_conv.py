@@ -284,3 +284,23 @@ def test_grouped_kernels_match_oracle(groups, dt, monkeypatch):
     outs = plan.double_backward(dev(x), dev(y), dev(w), dev(gz), (dev(da), dev(db), dev(dc)))
     for got, wv, n in zip(outs, o.double_backward(x, y, w, gz, da, db, dc), ("dx", "dy", "dw", "dgz")):
         check(host(got), wv, dt, f"G={groups} TP double-backward {n}")
+
+
+@pytest.mark.parametrize("epi", [2, 3])
+@pytest.mark.parametrize("dt", DTYPES, ids=["f32", "f64"])
+@pytest.mark.parametrize("name", ["c1", "c2", "paper"])
+def test_multi_edge_items_match_oracle(name, dt, epi, monkeypatch):
+    """By-output conv kernels with EB consecutive edges of a row staged per
+    item (CGF_GEN=epi=EB): ragged rows (edge counts not multiples of EB,
+    isolated nodes) give the oracle's forward and double-backward dgz."""
+    monkeypatch.setenv("CGF_GEN", f"epi={epi}")
+    js = config(name)
+    o, pkg = O.Oracle(js), P()
+    cp = pkg.ConvPlan(pkg.TpPlan(js))
+    og = graphs()["ragged5"]
+    g = pkg.Graph(og.nodes, og.src, og.nbr)
+    nx, ey, ew, gnz, dgx, dgy, dgw = conv_inputs(o, og, dt, seed=66)
+    check(host(cp.forward(g, dev(nx), dev(ey), dev(ew))), o.conv_forward(og, nx, ey, ew), dt, f"EB={epi} forward")
+    outs = cp.double_backward(g, dev(nx), dev(ey), dev(ew), dev(gnz), (dev(dgx), dev(dgy), dev(dgw)))
+    want = o.conv_double_backward(og, nx, ey, ew, gnz, dgx, dgy, dgw)
+    check(host(outs[3]), want[3], dt, f"EB={epi} double-backward dgz")
