@@ -197,6 +197,20 @@ std::vector<std::int32_t> neighbours(const GraphCSR& g) {
   return nb;
 }
 
+// The CSR row pointer rebuilt from the (sorted) edge list: the reference's
+// conv reads only g.edges (conv.cpp:234-528), so a GraphCSR whose row_ptr is
+// stale or missing must still work.
+std::vector<std::int64_t> row_ptr_of(const GraphCSR& g) {
+  std::vector<std::int64_t> rp(static_cast<std::size_t>(g.node_count) + 1, 0);
+  for (const auto& e : g.edges) {
+    if (e.src < 0 || e.src >= g.node_count || e.dst < 0 || e.dst >= g.node_count)
+      throw std::invalid_argument("conv: edge endpoint out of range");
+    ++rp[static_cast<std::size_t>(e.src) + 1];
+  }
+  for (std::size_t v = 1; v < rp.size(); ++v) rp[v] += rp[v - 1];
+  return rp;
+}
+
 // ConvStats from libcgf's store / load model of the GPU kernels (cgf_conv_stats).
 ConvStats conv_stats(const engine::TpPlan& plan, int op, Mode mode, bool unfused, const GraphCSR& g) {
   std::uint64_t s[4] = {0, 0, 0, 0};
@@ -231,7 +245,7 @@ ConvStats ConvPlan::forward(const GraphCSR& g, const std::vector<T>& node_x, con
     check(cgf_conv_forward_atomic_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(), sources(g).data(),
                                        nb.data(), node_x.data(), edge_y.data(), edge_w.data(), node_z.data()));
   else if (g.node_count > 0)
-    check(cgf_conv_forward_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(), g.row_ptr.data(),
+    check(cgf_conv_forward_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(), row_ptr_of(g).data(),
                                 nb.data(), node_x.data(), edge_y.data(), edge_w.data(), node_z.data(),
                                 CGF_CONV_DETERMINISTIC));
   return conv_stats(*plan_, CGF_OP_FORWARD, mode, false, g);
@@ -259,7 +273,7 @@ ConvStats ConvPlan::backward(const GraphCSR& g, const std::vector<std::int64_t>&
                                         sources(g).data(), nb.data(), node_x.data(), edge_y.data(), edge_w.data(),
                                         g_node_z.data(), g_node_x.data(), g_edge_y.data(), g_edge_w.data()));
   else if (g.node_count > 0)
-    check(cgf_conv_backward_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(), g.row_ptr.data(),
+    check(cgf_conv_backward_host(plan_->impl().gpu, dtype<T>(), g.node_count, g.edge_count(), row_ptr_of(g).data(),
                                  nb.data(), node_x.data(), edge_y.data(), edge_w.data(), g_node_z.data(),
                                  g_node_x.data(), g_edge_y.data(), g_edge_w.data(), CGF_CONV_DETERMINISTIC));
   return conv_stats(*plan_, CGF_OP_BACKWARD, mode, false, g);
