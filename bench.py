@@ -308,6 +308,31 @@ def tp_leg(cgf, plan, name, R, dtype, ops, steps, dev, world, w_shared=False, pe
     return out
 
 
+# tcgen05 kind::tf32 peak measured on this part by tools/tc_bench.cu
+# (profiles/r01_tc_bench.log: M=128, N=128, K=8 MMAs, 2046 MAC / cycle / SM)
+TF32_MAC_PER_CLK_SM = 2046
+SM_COUNT = 148
+
+
+def uvw_mma_flops_per_row(cfg_name):
+    """Dense W contraction flops per row of a kind-C problem (sum over
+    instructions of 2 * (2 l3 + 1) * b * b'), from its problem JSON."""
+    from paper_2501_13986_b200.configs import CONFIGS
+    js = CONFIGS[cfg_name]
+    seg = lambda s: [(int(t.split("x")[0]), int(t.split("x")[1][:-1])) for t in s.replace(" ", "").split("+")]
+    X, Z = seg(js["x"]), seg(js["z"])
+    return sum(2 * (2 * Z[zs - 1][1] + 1) * Z[zs - 1][0] * X[xs - 1][0] for xs, _, zs, _ in js["instructions"])
+
+
+def tensor_roofline(ms, mma_flops, clk_mhz):
+    """3xTF32 tensor-core work (3 MMAs per product) against the measured tf32 peak."""
+    peak = TF32_MAC_PER_CLK_SM * 2 * SM_COUNT * clk_mhz * 1e6 / 1e12
+    achieved = 3 * mma_flops / (ms / 1e3) / 1e12
+    return {"bound": "tensor", "unit": "TFLOP/s", "achieved": achieved, "peak": peak, "frac": achieved / peak,
+            "peak_kind": f"measured tf32 MMA rate (tools/tc_bench.cu) at {clk_mhz:.0f} MHz",
+            "mma_flops_per_launch": 3 * mma_flops}
+
+
 def conv_single_leg(cgf, cdist, name, tp_name, n, dtypes_ops, steps, dev, peak):
     """Fused conv on one GPU (C4: C2 TP on radius_graph(cubic_lattice(n^3), 3.0))."""
     import torch
@@ -682,6 +707,12 @@ def main():
         run_leg("c3", lambda: tp_leg(cgf, c3, "c3: 64x0e+64x1o+64x2e x 0e+1o+2e, 11 uvw paths, shared W "
                                               "(tcgen05 kind::tf32, 3xTF32)", 1_000_000, "f32",
                                      ("forward", "backward"), ls, dev, world, w_shared=True, peak=peak))
+        if "forward" in legs.get("c3", {}):
+            mf = uvw_mma_flops_per_row("c3") * 1_000_000
+            clk = clk.summary().get("sm_mhz") or 1965.0
+            legs["c3"]["forward"]["tensor_roofline"] = tensor_roofline(legs["c3"]["forward"]["ms"], mf, clk)
+            # backward: gx (the transposed forward), gzp = gz W (gy) and the rows-contracted gW, 3x the forward's MMAs
+            legs["c3"]["backward"]["tensor_roofline"] = tensor_roofline(legs["c3"]["backward"]["ms"], 3 * mf, clk)
     if "c4" in want and world == 1:
         run_leg("c4", lambda: conv_single_leg(cgf, cdist, "c4", "c2", 29,
                                               (("f32", ("forward", "backward", "double_backward")),

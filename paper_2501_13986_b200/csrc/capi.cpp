@@ -253,6 +253,10 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
     // backward and the small-TP (C5) kernels are slower that way,
     // profiles/r02_ab_conv2.jsonl)
     if (!small && loop == cgf::Loop::ConvByOutput && comp == cgf::Comp::Fwd && dtype == CGF_F32) cfg.min_blocks = 3;
+    // two consecutive edges of a row per staged item for the large-row
+    // by-output kernels: C4 forward FP32 11.1 -> 10.5 ms, FP64 21.3 -> 19.5 ms
+    // (profiles/r02_ab_epi.jsonl); the small-TP (C5) kernels are slower
+    if (!small && loop == cgf::Loop::ConvByOutput) cfg.edges_per_item = 2;
   }
   // x chunks / y in registers once per staged item: C4 conv double-backward
   // FP64 189.6 -> 179.4 ms, FP32 91.0 -> 88.0; C2 FP64 backward 11.40 -> 10.87

@@ -95,6 +95,31 @@ DEVI void coop_red16(double* dst, const double* src, int n16, int lane) {
 template <class T> DEVI void coop_red(T* dst, const T* src, int n, int lane) {
   for (int i = lane; i < n; i += 32) atomicAdd(dst + i, src[i]);
 }
+// Paired FP32 (sm_100 FFMA2 / FMUL2): each half is an IEEE fma / mul of its
+// operands; scalar register pairs are allocated adjacently by ptxas.
+DEVI void fma2s(float a, float b0, float b1, float& c0, float& c1) {
+  u64 A, B, C;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(A) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(C) : "f"(c0), "f"(c1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(B));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(C));
+}
+DEVI void fma2v(float a0, float a1, float b0, float b1, float& c0, float& c1) {
+  u64 A, B, C;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(C) : "f"(c0), "f"(c1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(B));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(C));
+}
+DEVI void mul2s(float a, float b0, float b1, float& r0, float& r1) {
+  u64 A, B, R;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(A) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(R) : "l"(A), "l"(B));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r0), "=f"(r1) : "l"(R));
+}
 template <class T> DEVI T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -662,6 +687,8 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
   const bool zab = cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX;
   const bool gfl = gy_flush();
   const bool yq = !yreg() && (m > 1 || cfg_.y_item);
+  // paired FP32 emission of two merged chunks (FFMA2); forward / backward only
+  const bool f2 = cfg_.ffma2 && m == 2 && !cfg_.f64 && !dual();
   if (yq) {
     // joint chunks: the item's y (and db) into registers once, so the products
     // below are shared across chunks; otherwise y is read from the slot at each
@@ -785,6 +812,28 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
       std::ostringstream l;
       l << "        { const T cy = " << v << " * " << Y(J) << ";";
       if (dual()) l << " const T cb = " << v << " * " << DB(J) << ";";
+      if (f2) {
+        // the two chunks' identical streams as paired FP32 ops (FFMA2 / FMUL2:
+        // one instruction per pair, each half an IEEE fma / mul -> the same
+        // bits as the scalar form)
+        const Sub& s_0 = p_.subs[u.subs[g]];
+        const Sub& s_1 = p_.subs[u.subs[g + n]];
+        const std::string A0 = "ax" + S(u.x_chunk_of(s_0)), A1 = "ax" + S(u.x_chunk_of(s_1));
+        auto GYc = [&](int c, const Sub& s) { return gfl ? "gyl_" + S(c) + "[" + S(e.j) + "]" : "gy[" + S(s.y_off + e.j) + "]"; };
+        if (zx_on) l << " fma2s(cy, xv_0[" << I << "], xv_1[" << I << "], zx_0[" << K << "], zx_1[" << K << "]);";
+        if (cfg_.comp == Comp::Bwd) {
+          l << " fma2s(cy, gzp_0[" << K << "], gzp_1[" << K << "], " << A0 << "[" << I << "], " << A1 << "[" << I << "]);"
+            << " { T t0_, t1_; mul2s(" << v << ", xv_0[" << I << "], xv_1[" << I << "], t0_, t1_);";
+          if (gfl)
+            l << " fma2v(t0_, t1_, gzp_0[" << K << "], gzp_1[" << K << "], " << GYc(0, s_0) << ", " << GYc(1, s_1) << "); }";
+          else
+            l << " " << GYc(0, s_0) << " = fma(t0_, gzp_0[" << K << "], " << GYc(0, s_0) << "); " << GYc(1, s_1)
+              << " = fma(t1_, gzp_1[" << K << "], " << GYc(1, s_1) << "); }";
+        }
+        l << " }\n";
+        o_ << l.str();
+        continue;
+      }
       for (int c = 0; c < m; ++c) {
         const int qi = g + c * n;
         const Sub& s = p_.subs[u.subs[qi]];
@@ -1260,6 +1309,8 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "noywin") cfg.y_window = false;
     else if (k == "joint") cfg.joint = true;
     else if (k == "epi") cfg.edges_per_item = std::max(1, v);
+    else if (k == "ffma2") cfg.ffma2 = true;
+    else if (k == "noffma2") cfg.ffma2 = false;
     else if (k == "waitsleep") cfg.wait_sleep = true;
     else if (k == "nowaitsleep") cfg.wait_sleep = false;
     else if (k == "l2hint") cfg.l2_hints = true;
