@@ -217,6 +217,10 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   // Two 32-lane chunks per staged item / code body: measured -4 % fwd, -11 %
   // bwd (TP) and -13 % (conv) in FP32; FP64 runs out of registers (keep 1).
   cfg.merge = (dtype == CGF_F32 && (comp == cgf::Comp::Fwd || comp == cgf::Comp::Bwd)) ? 2 : 1;
+  // ... emitted side by side as paired FP32 ops (FFMA2 / FMUL2: one instruction
+  // per chunk pair): C2 forward 8.63 -> 8.39 ms, C4 conv forward 10.40 -> 9.44
+  // ms, C4 conv backward 29.9 -> 28.8 ms (profiles/r02_ab_ffma2.jsonl); same bits
+  cfg.joint = cfg.ffma2 = cfg.merge == 2;
   // Measured per kernel (profiles/r01_ab_issue.log, r01_sweep_issue_bases.log):
   // the batched forward keeps the per-range 64-bit source addresses in
   // issue_unit (9.0 vs 9.15 ms; the conv forward is faster with row bases,
