@@ -209,7 +209,13 @@ class Gen {
   bool edges() const { return cfg_.loop == Loop::ConvEdges; }
   bool yreg() const { return cfg_.y_regs && (cfg_.loop == Loop::Rows || edges()); }
   bool gy_flush() const { return out_y() && (dual() || cfg_.f64); }
+  // by-output forward, FP32, kind B only: two edges per item as paired ops
+  bool pair_edges() const {
+    return cfg_.pair_edges && cfg_.loop == Loop::ConvByOutput && cfg_.comp == Comp::Fwd && !cfg_.f64 && !has_c_ &&
+           cfg_.lane_copy;
+  }
   int eb() const {
+    if (pair_edges()) return 2;
     return cfg_.loop == Loop::ConvByOutput && cfg_.lane_copy ? std::max(1, cfg_.edges_per_item) : 1;
   }
   Src x_src() const { return cfg_.loop == Loop::ConvByOutput || edges() ? Src::Nbr : Src::Row; }
@@ -232,6 +238,7 @@ class Gen {
                   long long step, std::uint32_t words, int guard_rows, int width, const std::string& reg,
                   bool atomic = false);
   void emit_unit_body(int k, const std::function<void(int)>& post_sub = {});
+  void emit_unit_body_edge_pair(int k);
   std::string wsrc(const Sub& s, long long step, const std::string& arr) const;
   void emit_gy_reduce(const std::string& rowexpr);
   void emit_gy_flush_row(const std::string& rowexpr);
@@ -930,6 +937,39 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
   }
 }
 
+// The forward of two edges of a row (sub-slots sb_ and sb_ + LW, y in ya_ /
+// yb_) side by side as paired FP32 ops; edge b's contribution is added after
+// edge a's in every z piece (and skipped when the item has one edge).
+void Gen::emit_unit_body_edge_pair(int k) {
+  const Unit& u = U0(k);
+  const Layout& L = lay_[k];
+  for (int q = 0; q < static_cast<int>(u.subs.size()); ++q) {
+    const Sub& s = p_.subs[u.subs[q]];
+    const int dx = s.dx(), dz = s.dz();
+    const std::uint32_t xs = L.x_slot.at(s.x_off), ws = L.w_slot.at(q);
+    const std::string PZ = "pz" + S(u.z_piece_of(s));
+    if (q && cfg_.sub_barrier) o_ << "      asm volatile(\"\" ::: \"memory\");\n";
+    o_ << "      { // sub " << u.subs[q] << " (edge pair): l=(" << s.l1 << "," << s.l2 << "," << s.l3 << ") nnz="
+       << s.cg->entries.size() << "\n        T xa[" << dx << "], xb[" << dx << "];\n        if (lane < " << s.bp << ") {";
+    for (int i = 0; i < dx; ++i)
+      o_ << " xa[" << i << "] = sb_[" << xs << " + lane * " << dx << " + " << i << "]; xb[" << i << "] = sb_[LW + " << xs
+         << " + lane * " << dx << " + " << i << "];";
+    o_ << " } else {";
+    for (int i = 0; i < dx; ++i) o_ << " xa[" << i << "] = 0; xb[" << i << "] = 0;";
+    o_ << " }\n        const T wa = (lane < " << s.b << ") ? sb_[" << ws << " + lane] : (T)0, wb = (lane < " << s.b
+       << ") ? sb_[LW + " << ws << " + lane] : (T)0;\n        T za[" << dz << "] = {}, zb[" << dz << "] = {};\n";
+    for (const auto& e : s.cg->entries) {
+      const int J = s.y_off + e.j;
+      o_ << "        { T ca_, cb_; mul2s((T)" << hexd(e.v) << ", ya_[" << J << "], yb_[" << J << "], ca_, cb_); fma2v(ca_, cb_, xa["
+         << e.i << "], xb[" << e.i << "], za[" << e.k << "], zb[" << e.k << "]); }\n";
+    }
+    for (int kk = 0; kk < dz; ++kk)
+      o_ << "        " << PZ << "[" << kk << "] = fma(wa, za[" << kk << "], " << PZ << "[" << kk << "]); if (two_) " << PZ << "["
+         << kk << "] = fma(wb, zb[" << kk << "], " << PZ << "[" << kk << "]);\n";
+    o_ << "      }\n";
+  }
+}
+
 void Gen::emit_gy_reduce(const std::string& rowexpr) {
   const int dy = p_.dim_y;
   for (int j0 = 0; j0 < dy; j0 += 32) {
@@ -1109,7 +1149,24 @@ void Gen::emit_conv_loop() {
       }
       emit_class_loop_open(static_cast<int>(k));
       for (size_t z = 0; z < u.z_pieces.size(); ++z) o_ << "      " << zero_init("pz" + S(z), zdz[u.z_pieces[z].off]) << "\n";
-      if (eb() > 1) {
+      if (pair_edges()) {
+        // two edges per item computed as paired FP32 ops (FFMA2 / FMUL2);
+        // each z piece still accumulates edge by edge in order (same bits)
+        o_ << "      for (i64 q = q0; q < q1; q += 2) {\n      T* sb_ = wsm + slot * SLOT_WORDS;\n      "
+           << (cfg_.wait_sleep ? "mbar_wait_sleep" : "mbar_wait") << "(&bars[slot], phase);\n"
+           << "      const bool two_ = q + 1 < q1;\n      T ya_[" << p_.dim_y << "], yb_[" << p_.dim_y << "];\n";
+        for (int h = 0; h < 2; ++h) {
+          o_ << "      { const i64 eid = q + (two_ ? " << h << " : 0); const i64 nbr = NB[eid]; (void)nbr; T* sl = sb_ + "
+             << h << " * LW;\n";
+          emit_wait_and_sync(static_cast<int>(k), false);
+          o_ << "       ";
+          for (int j = 0; j < p_.dim_y; ++j) o_ << " y" << (h ? "b" : "a") << "_[" << j << "] = sl[ys + " << j << "];";
+          o_ << " }\n";
+        }
+        emit_unit_body_edge_pair(static_cast<int>(k));
+        emit_release();
+        o_ << "      }\n";
+      } else if (eb() > 1) {
         o_ << "      for (i64 q = q0; q < q1; q += EB) {\n      T* sb_ = wsm + slot * SLOT_WORDS;\n      "
            << (cfg_.wait_sleep ? "mbar_wait_sleep" : "mbar_wait") << "(&bars[slot], phase);\n"
            << "      const int ne_ = (int)(q1 - q < EB ? q1 - q : EB);\n#pragma unroll 1\n"
@@ -1309,6 +1366,8 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "noywin") cfg.y_window = false;
     else if (k == "joint") cfg.joint = true;
     else if (k == "epi") cfg.edges_per_item = std::max(1, v);
+    else if (k == "pairedges") cfg.pair_edges = true;
+    else if (k == "nopairedges") cfg.pair_edges = false;
     else if (k == "ffma2") cfg.ffma2 = true;
     else if (k == "noffma2") cfg.ffma2 = false;
     else if (k == "waitsleep") cfg.wait_sleep = true;

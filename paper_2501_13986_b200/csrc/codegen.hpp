@@ -69,7 +69,8 @@ struct KernelConfig {
   bool gy_accum = false;
   bool x_regs = false;      // each staged x (and dL/da) chunk loaded into registers once per item, not per sub
   bool y_item = false;      // y (and db) loaded into registers once per item, not per CG entry
-  bool ffma2 = false;       // with joint emission of 2 merged chunks: paired FP32 ops (FFMA2 / FMUL2)
+  bool ffma2 = false;
+  bool pair_edges = false;  // ConvByOutput FP32 forward: two edges per item as paired FP32 ops (forces EB = 2)       // with joint emission of 2 merged chunks: paired FP32 ops (FFMA2 / FMUL2)
   int edges_per_item = 1;   // ConvByOutput: consecutive edges of a row staged in one item (one wait / issue per EB edges)
   bool wait_sleep = false;  // consumer waits: mbarrier.try_wait with a suspend-time hint
   bool l2_hints = false;    // conv loops: L2 evict_last for gathered node rows, evict_first for per-edge streams
