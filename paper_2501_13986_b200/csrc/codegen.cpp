@@ -214,8 +214,13 @@ class Gen {
     return cfg_.pair_edges && cfg_.loop == Loop::ConvByOutput && cfg_.comp == Comp::Fwd && !cfg_.f64 && !has_c_ &&
            cfg_.lane_copy;
   }
+  // by-neighbour backward, FP32, kind B, one unit (small problems), no groups
+  bool pair_edges_bwd() const {
+    return cfg_.pair_edges && cfg_.loop == Loop::ConvByInput && cfg_.comp == Comp::Bwd && !cfg_.f64 && !has_c_ &&
+           cfg_.lane_copy && units_.size() == 1 && cls_.size() == 1 && !cfg_.gy_accum && !gy_flush();
+  }
   int eb() const {
-    if (pair_edges()) return 2;
+    if (pair_edges() || pair_edges_bwd()) return 2;
     return cfg_.loop == Loop::ConvByOutput && cfg_.lane_copy ? std::max(1, cfg_.edges_per_item) : 1;
   }
   Src x_src() const { return cfg_.loop == Loop::ConvByOutput || edges() ? Src::Nbr : Src::Row; }
@@ -239,8 +244,9 @@ class Gen {
                   bool atomic = false);
   void emit_unit_body(int k, const std::function<void(int)>& post_sub = {});
   void emit_unit_body_edge_pair(int k);
+  void emit_unit_body_edge_pair_bwd(int k);
   std::string wsrc(const Sub& s, long long step, const std::string& arr) const;
-  void emit_gy_reduce(const std::string& rowexpr);
+  void emit_gy_reduce(const std::string& rowexpr, const std::string& arr = "gy");
   void emit_gy_flush_row(const std::string& rowexpr);
   void emit_gy_resume(const std::string& rowexpr);
   void emit_class_loop_open(int k);
@@ -970,12 +976,58 @@ void Gen::emit_unit_body_edge_pair(int k) {
   }
 }
 
-void Gen::emit_gy_reduce(const std::string& rowexpr) {
+// The backward of two edges into node d (sub-slots sb_ / sb_ + LW; x is the
+// node's row, the same for both) side by side as paired FP32 ops. Per-edge
+// accumulators axa / axb, gya / gyb and the gW of each edge keep the
+// one-edge-per-item order of every addition.
+void Gen::emit_unit_body_edge_pair_bwd(int k) {
+  const Unit& u = U0(k);
+  const Layout& L = lay_[k];
+  const std::string nw = S(p_.n_w);
+  for (int q = 0; q < static_cast<int>(u.subs.size()); ++q) {
+    const Sub& s = p_.subs[u.subs[q]];
+    const int dx = s.dx(), dz = s.dz();
+    const std::uint32_t xs = L.x_slot.at(s.x_off), ws = L.w_slot.at(q), gs = L.gz_slot.at(s.z_off);
+    const std::string AX = S(u.x_chunk_of(s));
+    if (q && cfg_.sub_barrier) o_ << "      asm volatile(\"\" ::: \"memory\");\n";
+    o_ << "      { // sub " << u.subs[q] << " (edge pair): l=(" << s.l1 << "," << s.l2 << "," << s.l3 << ") nnz="
+       << s.cg->entries.size() << "\n        T xv[" << dx << "], ga[" << dz << "], gb[" << dz << "];\n        if (lane < "
+       << s.bp << ") {";
+    for (int i = 0; i < dx; ++i) o_ << " xv[" << i << "] = sb_[" << xs << " + lane * " << dx << " + " << i << "];";
+    o_ << " } else {";
+    for (int i = 0; i < dx; ++i) o_ << " xv[" << i << "] = 0;";
+    o_ << " }\n        if (lane < " << s.b << ") {";
+    for (int kk = 0; kk < dz; ++kk)
+      o_ << " ga[" << kk << "] = sb_[" << gs << " + lane * " << dz << " + " << kk << "]; gb[" << kk << "] = sb_[LW + " << gs
+         << " + lane * " << dz << " + " << kk << "];";
+    o_ << " } else {";
+    for (int kk = 0; kk < dz; ++kk) o_ << " ga[" << kk << "] = 0; gb[" << kk << "] = 0;";
+    o_ << " }\n        const T wa = (lane < " << s.b << ") ? sb_[" << ws << " + lane] : (T)0, wb = (lane < " << s.b
+       << ") ? sb_[LW + " << ws << " + lane] : (T)0;\n        T pa[" << dz << "], pb[" << dz << "], za[" << dz
+       << "] = {}, zb[" << dz << "] = {};\n       ";
+    for (int kk = 0; kk < dz; ++kk) o_ << " pa[" << kk << "] = wa * ga[" << kk << "]; pb[" << kk << "] = wb * gb[" << kk << "];";
+    o_ << "\n";
+    for (const auto& e : s.cg->entries) {
+      const std::string v = "(T)" + hexd(e.v), I = S(e.i), K = S(e.k), Jg = S(s.y_off + e.j);
+      o_ << "        { T ca_, cb_; mul2s(" << v << ", ya_[" << Jg << "], yb_[" << Jg << "], ca_, cb_);"
+         << " fma2v(ca_, cb_, pa[" << K << "], pb[" << K << "], axa" << AX << "[" << I << "], axb" << AX << "[" << I << "]);"
+         << " { const T t_ = " << v << " * xv[" << I << "]; fma2s(t_, pa[" << K << "], pb[" << K << "], gya[" << Jg
+         << "], gyb[" << Jg << "]); }"
+         << " fma2s(xv[" << I << "], ca_, cb_, za[" << K << "], zb[" << K << "]); }\n";
+    }
+    o_ << "        { T ea = 0, eb = 0;";
+    for (int kk = 0; kk < dz; ++kk) o_ << " fma2v(ga[" << kk << "], gb[" << kk << "], za[" << kk << "], zb[" << kk << "], ea, eb);";
+    o_ << "\n          if (lane < " << s.b << ") { O2[eida * (i64)" << nw << " + " << s.w_off << " + lane] = ea; if (two_) O2[eidb * (i64)"
+       << nw << " + " << s.w_off << " + lane] = eb; } }\n      }\n";
+  }
+}
+
+void Gen::emit_gy_reduce(const std::string& rowexpr, const std::string& arr) {
   const int dy = p_.dim_y;
   for (int j0 = 0; j0 < dy; j0 += 32) {
     o_ << "    { T mine = 0;\n";
     for (int j = j0; j < std::min(dy, j0 + 32); ++j)
-      o_ << "      { const T s_ = warp_sum(gy[" << j << "]); if (lane == " << j - j0 << ") mine = s_; }\n";
+      o_ << "      { const T s_ = warp_sum(" << arr << "[" << j << "]); if (lane == " << j - j0 << ") mine = s_; }\n";
     o_ << "      if (lane < " << std::min(dy - j0, 32) << ") O1[" << rowexpr << " * (i64)" << dy << " + " << j0
        << " + lane] " << (cfg_.gy_accum ? "+=" : "=") << " mine; }\n";
   }
@@ -1122,7 +1174,7 @@ void Gen::emit_conv_loop() {
   if (eb() > 1) {
     // EB consecutive edges of the row per item, each in its own sub-slot
     o_ << "    for (int e_ = 0; e_ < EB; ++e_) { const bool v_ = pq + e_ < pq1; const i64 q_ = v_ ? pq + e_ : pq;\\\n"
-          "      issue_unit(pu, r_, (i64)NB[q_], q_, rows, edges_tot, wsm + pslot * SLOT_WORDS + e_ * LW, &bars[pslot],"
+          "      issue_unit(pu, r_, (i64)NB[q_], " << (bi ? "(i64)EID[q_]" : "q_") << ", rows, edges_tot, wsm + pslot * SLOT_WORDS + e_ * LW, &bars[pslot],"
           " X, Y, W, GZ, DA, DB, DC, lane, v_); }\\\n"
           "    if (++pslot == D) pslot = 0;\\\n"
           "    pq += EB; if (pq >= pq1) { pq = pq0; if (++pu == NU) { pu = 0; ++pk; seek(); } }\\\n";
@@ -1194,6 +1246,51 @@ void Gen::emit_conv_loop() {
   } else {
     // gx-type outputs accumulate over the row's edges in the warp's shared
     // gxs[dim_x]; each item adds its register partials (lane-owned, conflict-free).
+    if (pair_edges_bwd()) {
+      // two edges of the node per item as paired FP32 ops; every output is
+      // still accumulated edge by edge in order (same bits as one edge per item)
+      const Unit& u = U0(0);
+      std::map<std::uint32_t, int> xdx, xb;
+      for (int si : u.subs) {
+        xdx[p_.subs[si].x_off] = p_.subs[si].dx();
+        xb[p_.subs[si].x_off] = p_.subs[si].bp;
+      }
+      o_ << "    for (i64 q = q0; q < q1; q += 2) {\n      const bool two_ = q + 1 < q1;\n"
+            "      const i64 eida = EID[q], eidb = EID[two_ ? q + 1 : q];\n"
+         << "      " << zero_init("gya", p_.dim_y) << " " << zero_init("gyb", p_.dim_y) << "\n";
+      for (size_t c = 0; c < u.x_chunks.size(); ++c)
+        o_ << "      " << zero_init("axa" + S(c), xdx[u.x_chunks[c].off]) << " "
+           << zero_init("axb" + S(c), xdx[u.x_chunks[c].off]) << "\n";
+      o_ << "      T* sb_ = wsm + slot * SLOT_WORDS;\n      " << (cfg_.wait_sleep ? "mbar_wait_sleep" : "mbar_wait")
+         << "(&bars[slot], phase);\n      T ya_[" << p_.dim_y << "], yb_[" << p_.dim_y << "];\n";
+      for (int h = 0; h < 2; ++h) {
+        o_ << "      { const i64 eid = " << (h ? "eidb" : "eida") << "; const i64 nbr = NB[q + (two_ ? " << h
+           << " : 0)]; (void)nbr; T* sl = sb_ + " << h << " * LW;\n";
+        emit_wait_and_sync(0, false);
+        o_ << "       ";
+        for (int j = 0; j < p_.dim_y; ++j) o_ << " y" << (h ? "b" : "a") << "_[" << j << "] = sl[ys + " << j << "];";
+        o_ << " }\n";
+      }
+      emit_unit_body_edge_pair_bwd(0);
+      for (const char* h : {"a", "b"}) {
+        if (h[0] == 'b') o_ << "      if (two_) {\n";
+        for (size_t c = 0; c < u.x_chunks.size(); ++c) {
+          const auto& xc = u.x_chunks[c];
+          const int dx = xdx[xc.off];
+          o_ << "      if (lane < " << xb[xc.off] << ") {";
+          for (int i = 0; i < dx; ++i)
+            o_ << " gxs[" << gx_base_[0] + gx_pre_[0][c] << " + lane * " << dx << " + " << i << "] += ax" << h << c << "["
+               << i << "];";
+          o_ << " }\n";
+        }
+        if (h[0] == 'b') o_ << "      }\n";
+      }
+      emit_release();
+      emit_gy_reduce("eida", "gya");
+      o_ << "    if (two_) {\n";
+      emit_gy_reduce("eidb", "gyb");
+      o_ << "    }\n    }\n";
+    } else {
     o_ << "    for (i64 q = q0; q < q1; ++q) {\n      const i64 eid = EID[q]; const i64 nbr = NB[q]; (void)nbr;\n";
     if (out_y() && !gy_flush()) o_ << "      " << zero_init("gy", p_.dim_y) << "\n";
     if (gy_flush() && cfg_.gy_accum) emit_gy_resume("eid");
@@ -1228,6 +1325,7 @@ void Gen::emit_conv_loop() {
         emit_gy_reduce("eid");
     }
     o_ << "    }\n";
+    }
     // the row's packed x chunks -> their places in the output row
     o_ << "    __syncwarp();\n";
     for (size_t k = 0; k < cls_.size(); ++k) {
