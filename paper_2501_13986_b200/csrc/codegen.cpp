@@ -700,8 +700,8 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
   const bool zab = cfg_.comp == Comp::DBwd || cfg_.comp == Comp::DBwdZ || cfg_.comp == Comp::DBwdX;
   const bool gfl = gy_flush();
   const bool yq = !yreg() && (m > 1 || cfg_.y_item);
-  // paired FP32 emission of two merged chunks (FFMA2); forward / backward only
-  const bool f2 = cfg_.ffma2 && m == 2 && !cfg_.f64 && !dual();
+  // paired FP32 emission of two merged chunks (FFMA2)
+  const bool f2 = cfg_.ffma2 && m == 2 && !cfg_.f64;
   if (yq) {
     // joint chunks: the item's y (and db) into registers once, so the products
     // below are shared across chunks; otherwise y is read from the slot at each
@@ -834,6 +834,22 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
         const std::string A0 = "ax" + S(u.x_chunk_of(s_0)), A1 = "ax" + S(u.x_chunk_of(s_1));
         auto GYc = [&](int c, const Sub& s) { return gfl ? "gyl_" + S(c) + "[" + S(e.j) + "]" : "gy[" + S(s.y_off + e.j) + "]"; };
         if (zx_on) l << " fma2s(cy, xv_0[" << I << "], xv_1[" << I << "], zx_0[" << K << "], zx_1[" << K << "]);";
+        if (zab)
+          l << " fma2s(cy, av_0[" << I << "], av_1[" << I << "], za_0[" << K << "], za_1[" << K << "]);"
+            << " fma2s(cb, xv_0[" << I << "], xv_1[" << I << "], zb_0[" << K << "], zb_1[" << K << "]);";
+        if (need_gzc) {
+          // AX = fma(cb, gzp, fma(cy, gzc, AX)); GY = fma(v a, gzp, fma(v x, gzc, GY)) per chunk
+          l << " fma2s(cy, gzc_0[" << K << "], gzc_1[" << K << "], " << A0 << "[" << I << "], " << A1 << "[" << I << "]);"
+            << " fma2s(cb, gzp_0[" << K << "], gzp_1[" << K << "], " << A0 << "[" << I << "], " << A1 << "[" << I << "]);"
+            << " { T t0_, t1_, u0_, u1_; mul2s(" << v << ", xv_0[" << I << "], xv_1[" << I << "], t0_, t1_); mul2s(" << v
+            << ", av_0[" << I << "], av_1[" << I << "], u0_, u1_);";
+          if (gfl)
+            l << " fma2v(t0_, t1_, gzc_0[" << K << "], gzc_1[" << K << "], " << GYc(0, s_0) << ", " << GYc(1, s_1) << ");"
+              << " fma2v(u0_, u1_, gzp_0[" << K << "], gzp_1[" << K << "], " << GYc(0, s_0) << ", " << GYc(1, s_1) << "); }";
+          else
+            l << " " << GYc(0, s_0) << " = fma(u0_, gzp_0[" << K << "], fma(t0_, gzc_0[" << K << "], " << GYc(0, s_0) << "));"
+              << " " << GYc(1, s_1) << " = fma(u1_, gzp_1[" << K << "], fma(t1_, gzc_1[" << K << "], " << GYc(1, s_1) << ")); }";
+        }
         if (cfg_.comp == Comp::Bwd) {
           l << " fma2s(cy, gzp_0[" << K << "], gzp_1[" << K << "], " << A0 << "[" << I << "], " << A1 << "[" << I << "]);"
             << " { T t0_, t1_; mul2s(" << v << ", xv_0[" << I << "], xv_1[" << I << "], t0_, t1_);";
