@@ -261,6 +261,23 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
     // by-output kernels: C4 forward FP32 11.1 -> 10.5 ms, FP64 21.3 -> 19.5 ms
     // (profiles/r02_ab_epi.jsonl); the small-TP (C5) kernels are slower
     if (!small && loop == cgf::Loop::ConvByOutput) cfg.edges_per_item = 2;
+    // small problems' conv kernels (C5), profiles/r02_ab_occ.jsonl and r02_ab_pair_*.jsonl:
+    //  * forward: two edges per item as paired FP32 ops (FFMA2): 14.0 -> 12.9 ms
+    //  * backward: edge pairs + one slot per warp + 3 CTAs / SM (more warps beat a
+    //    deeper ring here): 40.4 -> 34.5 ms
+    //  * double-backward passes: one slot per warp, 4 CTAs / SM: 123 -> 116 ms
+    // and the FP64 large-row backward: one slot per warp, 82.6 -> 75.4 ms (C4)
+    if (small && dtype == CGF_F32 && loop == cgf::Loop::ConvByOutput && comp == cgf::Comp::Fwd) cfg.pair_edges = true;
+    if (small && dtype == CGF_F32 && loop == cgf::Loop::ConvByInput && comp == cgf::Comp::Bwd) {
+      cfg.pair_edges = true;
+      cfg.depth = 1;
+      cfg.min_blocks = 3;
+    }
+    if (small && dtype == CGF_F32 && (comp == cgf::Comp::DBwdZ || comp == cgf::Comp::DBwdX)) {
+      cfg.depth = 1;
+      cfg.min_blocks = 4;
+    }
+    if (!small && dtype == CGF_F64 && loop == cgf::Loop::ConvByInput && comp == cgf::Comp::Bwd) cfg.depth = 1;
   }
   // x chunks / y in registers once per staged item: C4 conv double-backward
   // FP64 189.6 -> 179.4 ms, FP32 91.0 -> 88.0; C2 FP64 backward 11.40 -> 10.87

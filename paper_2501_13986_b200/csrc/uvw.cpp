@@ -114,6 +114,15 @@ DEVI void tc_st8(u32 taddr, const float* v) {
                   "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
                   "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])) : "memory");
 }
+DEVI void tc_st16(u32 taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+               :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                  "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                  "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+                  "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+                  "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+                  "r"(__float_as_uint(v[15])) : "memory");
+}
 DEVI void tc_st4(u32 taddr, const float* v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
                :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
@@ -922,7 +931,7 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
   // channels)) and x-tile ring depth; env overrides for A/B runs.
   const int pw = std::getenv("CGF_UVW_PW") ? std::atoi(std::getenv("CGF_UVW_PW")) : kProdWarps;
   const int nx = std::getenv("CGF_UVW_NX") ? std::atoi(std::getenv("CGF_UVW_NX")) : 3;
-  if (pw != 8 && pw != 16) throw UnsupportedError("CGF_UVW_PW must be 8 or 16");
+  if (pw != 4 && pw != 8 && pw != 16) throw UnsupportedError("CGF_UVW_PW must be 4, 8 or 16");
   const int cpt = kCh * 4 / pw;  // channels per producer thread
   const int nwr = std::getenv("CGF_UVW_NW") ? std::atoi(std::getenv("CGF_UVW_NW")) : 6;  // W ring depth
   // A blocks per TMEM-store round (<= NS / 2 so a batch is written while the other half is consumed);
