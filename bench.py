@@ -636,7 +636,9 @@ def main():
 
     # ---- end to end through the public API with HOST buffers --------------
     pcie = measure_pcie(dev)
-    Re = args.e2e_rows
+    # per rank; halved beyond 2 ranks so N ranks' pinned buffers (13 GB each
+    # at 131,072 rows) stay well inside the host's memory
+    Re = args.e2e_rows if world <= 2 else args.e2e_rows // 2
     gh = torch.Generator().manual_seed(99 + rank)
     pin = lambda *s: torch.randn(s, dtype=tdt, generator=gh).pin_memory()
     hx, hy, hw, hg = pin(Re, plan.dim_x), pin(Re, plan.dim_y), pin(Re, plan.n_w), pin(Re, plan.dim_z)
@@ -685,7 +687,9 @@ def main():
 
     # ---- sub-legs ------------------------------------------------------------
     legs = {}
-    want = [s for s in args.legs.split(",") if s]
+    # the sub-legs are per-GPU replicas: measured at N = 1 only (at N > 1 a
+    # failure on one rank inside a leg's collective would stall the others)
+    want = [s for s in args.legs.split(",") if s] if world == 1 else []
     ls = args.leg_steps
 
     def run_leg(name, fn):
