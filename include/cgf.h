@@ -328,6 +328,16 @@ int cgf_conv_double_backward_shard(cgf_plan* plan, int dtype, int64_t out_nodes,
                                    const void* d_gy, const void* d_gw, void* o_node_x, void* o_edge_y,
                                    void* o_edge_w, void* o_g_node_z, int mode, void* stream);
 
+/* ---- array files (array_io.cpp:15-68) --------------------------------------
+ * The reference CLI's array format: <base>.bin raw little-endian values and a
+ * <base>.json sidecar {"cols":C,"dtype":"fp32"|"fp64","rows":R}. Files written
+ * here are byte-identical to the reference's save_array. cgf_array_load reads
+ * into a host buffer (device = 0) or, through pinned staging, into device
+ * memory on `stream` (device != 0); `capacity` is in elements. */
+int cgf_array_save(const char* base, int dtype, const void* host_data, int64_t rows, int64_t cols);
+int cgf_array_meta(const char* base, int64_t shape[2], int* dtype);
+int cgf_array_load(const char* base, int dtype, void* dst, int64_t capacity, int device, void* stream);
+
 /* ---- multi-GPU fused convolution (destination-partitioned, NCCL) ----------
  * One process (or thread) per GPU, one rank each. The reference runs the conv
  * on one host only (conv.cpp:234-528); SURVEY.md §8e's partition: rank r owns

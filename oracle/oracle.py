@@ -498,6 +498,7 @@ def ref_lib():
         L.cgr_plan_split.argtypes = [P, P, C.c_int]
         L.cgr_emit_text.argtypes = [P, C.c_int, C.c_int, C.c_char_p, C.c_int]
         L.cgr_schedule_json.argtypes = [P, C.c_char_p, C.c_int]
+        L.cgr_save_array.argtypes = [C.c_char_p, P, C.c_int64, C.c_int64, C.c_int]
         L.cgr_cg_block.argtypes = [C.c_int] * 4 + [P] * 4
         L.cgr_rng_new.restype = P
         L.cgr_rng_new.argtypes = [C.c_uint64]

@@ -22,6 +22,7 @@
 
 #include "cgforge/cg.hpp"
 #include "cgforge/conv.hpp"
+#include "cgforge/array_io.hpp"
 #include "cgforge/engine.hpp"
 #include "cgforge/kernelgen.hpp"
 #include "cgforge/rng.hpp"
@@ -409,6 +410,18 @@ int cgr_emit_text(void* h, int pos, int backward, char* buf, int cap) {
   std::memcpy(buf, t.data(), n);
   buf[n] = 0;
   return static_cast<int>(t.size());
+}
+
+// array_io::save_array (array_io.cpp:15-38), for byte comparisons.
+int cgr_save_array(const char* base, const void* data, std::int64_t rows, std::int64_t cols, int f64) {
+  try {
+    if (f64) array_io::save_array(base, static_cast<const double*>(data), rows, cols);
+    else array_io::save_array(base, static_cast<const float*>(data), rows, cols);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
 }
 
 // scheduler::schedule_to_json of the plan's schedule (scheduler.cpp:406-445).

@@ -27,6 +27,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcgf.so")
 
 __all__ = [
+    "save_array", "load_array", "read_meta",
     "TpPlan", "ConvPlan", "Graph", "DeviceGraph", "make_graph_device", "radius_graph_device", "cg_block", "lib", "CgfError", "ParseError", "ValidationError", "ShapeError",
     "BudgetError", "TriangleError", "InvalidArgument", "CudaError", "JitError",
     "UnsupportedError", "F32", "F64", "OP_FORWARD", "OP_BACKWARD", "OP_DOUBLE_BACKWARD", "DETERMINISTIC", "ATOMIC",
@@ -142,6 +143,9 @@ def lib():
     L.cgf_conv_unfused_workspace.restype = C.c_size_t
     L.cgf_conv_unfused_forward_host.argtypes = [P, I, I64, I64] + [P] * 6
     L.cgf_conv_unfused_backward_host.argtypes = [P, I, I64, I64] + [P] * 9
+    L.cgf_array_save.argtypes = [C.c_char_p, I, P, I64, I64]
+    L.cgf_array_meta.argtypes = [C.c_char_p, P, C.POINTER(I)]
+    L.cgf_array_load.argtypes = [C.c_char_p, I, P, I64, I, P]
     L.cgf_nccl_unique_id.argtypes = [C.c_char_p]
     L.cgf_nccl_comm_create.argtypes = [I, I, C.c_char_p, C.POINTER(P)]
     L.cgf_nccl_comm_destroy.argtypes = [P]
@@ -766,6 +770,41 @@ class ConvPlan:
             *(TpPlan._p(a) for a in (node_x_all, edge_y, edge_w, g_node_z, d_gx_all, d_gy, d_gw, ox, oy, ow, ogz)),
             mode, TpPlan._stream(node_x_all)))
         return ox, oy, ow, ogz
+
+
+# ------------------------------------------------------------ array files --
+
+def save_array(base: str, a):
+    """array_io::save_array (array_io.cpp:15-38): <base>.bin + <base>.json;
+    a 2-D float32 / float64 numpy array or CUDA tensor (copied to the host)."""
+    if _is_torch(a):
+        a = a.detach().cpu().numpy()
+    a = np.ascontiguousarray(a)
+    if a.ndim != 2:
+        raise ShapeError("save_array: expected a 2-D array")
+    _check(lib().cgf_array_save(base.encode(), _dtype_code(a), a.ctypes.data, a.shape[0], a.shape[1]))
+
+
+def read_meta(base: str):
+    """(rows, cols, dtype code) of an array file (array_io.cpp:40-50)."""
+    shape = np.zeros(2, np.int64)
+    dt = C.c_int()
+    _check(lib().cgf_array_meta(base.encode(), shape.ctypes.data, C.byref(dt)))
+    return int(shape[0]), int(shape[1]), dt.value
+
+
+def load_array(base: str, device=None):
+    """array_io::load_array (array_io.cpp:52-68): a numpy array, or with
+    ``device`` a CUDA tensor filled through pinned staging."""
+    rows, cols, dt = read_meta(base)
+    if device is None:
+        out = np.empty((rows, cols), np.float64 if dt == F64 else np.float32)
+        _check(lib().cgf_array_load(base.encode(), dt, out.ctypes.data, out.size, 0, None))
+        return out
+    import torch
+    out = torch.empty((rows, cols), dtype=torch.float64 if dt == F64 else torch.float32, device=device)
+    _check(lib().cgf_array_load(base.encode(), dt, C.c_void_p(out.data_ptr()), out.numel(), 1, _stream_of(out.device)))
+    return out
 
 
 def _kernel_source(plan: TpPlan, comp, loop, dtype=F32, w_shared=False, aligned=True) -> str:

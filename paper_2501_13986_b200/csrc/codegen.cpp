@@ -1311,7 +1311,6 @@ void Gen::emit_conv_loop() {
     if (out_y() && !gy_flush()) o_ << "      " << zero_init("gy", p_.dim_y) << "\n";
     if (gy_flush() && cfg_.gy_accum) emit_gy_resume("eid");
     for (size_t k = 0; k < cls_.size(); ++k) {
-      const UClass& C = cls_[k];
       const Unit& u = U0(static_cast<int>(k));
       std::map<std::uint32_t, int> xdx, xb;
       for (int si : u.subs) {

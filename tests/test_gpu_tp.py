@@ -267,3 +267,14 @@ def test_shared_w_backward_and_double_backward(name, js, rows, dt, monkeypatch):
     want = o.double_backward(x, y, w, gz, da, db, dc, w_shared=True)
     for got, wv, n in zip(outs, want, ("dx", "dy", "dw", "dgz")):
         check(host(got).reshape(wv.shape), wv, dt, f"shared-W double-backward {n}")
+
+
+def test_array_file_to_device(tmp_path):
+    """cgf_array_load into device memory through pinned staging (several
+    64 MB pieces) equals the host load."""
+    pkg = P()
+    a = np.random.default_rng(4).standard_normal((3000, 9001)).astype(np.float32)  # 108 MB
+    base = str(tmp_path / "big")
+    pkg.save_array(base, a)
+    d = pkg.load_array(base, device="cuda")
+    assert torch.equal(d.cpu(), torch.from_numpy(a))

@@ -105,3 +105,31 @@ def test_schedule_and_listings_match_live_reference_random(seed):
     for pos in range(plan.n_split):
         for bwd in (False, True):
             assert plan.listing(pos, bwd) == ref.emit_text(pos, bwd)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_array_files_round_trip_and_match_reference_bytes(tmp_path, dt):
+    """array_io (array_io.cpp:15-68): libcgf writes the reference's exact
+    .bin / .json bytes, reads them back, and rejects a dtype mismatch and a
+    short .bin like the reference."""
+    a = np.random.default_rng(3).standard_normal((5, 7)).astype(dt)
+    base = str(tmp_path / "ours")
+    cgf.save_array(base, a)
+    assert cgf.read_meta(base) == (5, 7, cgf.F64 if dt == np.float64 else cgf.F32)
+    assert np.array_equal(cgf.load_array(base), a)
+    if O.ref_available():
+        import ctypes as C
+        rb = str(tmp_path / "ref")
+        assert O.ref_lib().cgr_save_array(rb.encode(), a.ctypes.data, 5, 7, int(dt == np.float64)) == 0
+        for ext in (".bin", ".json"):
+            assert open(base + ext, "rb").read() == open(rb + ext, "rb").read(), ext
+    other = np.float32 if dt == np.float64 else np.float64
+    import ctypes as C
+    buf = np.empty(35, other)
+    rc = cgf.lib().cgf_array_load(base.encode(), cgf.F32 if other == np.float32 else cgf.F64, buf.ctypes.data, 35, 0,
+                                  None)
+    assert rc != 0 and "expected" in cgf.lib().cgf_last_error().decode()
+    with open(base + ".bin", "r+b") as f:
+        f.truncate(8)
+    with pytest.raises(cgf.CgfError, match="shorter"):
+        cgf.load_array(base)
