@@ -939,7 +939,14 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
   const int kb = std::max(1, std::min(std::getenv("CGF_UVW_KB") ? std::atoi(std::getenv("CGF_UVW_KB")) : 1, na / 2));
   // warps: producers | MMA | 4 epilogue | W loader | x loader
   const int mma_warp = pw, wload_warp = pw + 5, xload_warp = pw + 6, nwarps = pw + 7;
-  const int smem = 1024 /*align*/ + nx * xslot + nwr * wslot + 1024 /*barriers*/;
+  // epilogue staging (CGF_UVW_EPI=1): per epilogue warp, 32 rows x (8 dz + 4)
+  // floats, so each z row piece leaves as contiguous full-sector stores
+  int max_dz = 1;
+  for (const auto& sg : segs) max_dz = std::max(max_dz, sg.dz);
+  const bool epi_stage = std::getenv("CGF_UVW_EPI") && std::atoi(std::getenv("CGF_UVW_EPI")) == 1;
+  const int epi_stride = 8 * max_dz + 4;
+  const int epi_bytes = epi_stage ? 4 * 32 * epi_stride * 4 : 0;
+  const int smem = 1024 /*align*/ + nx * xslot + nwr * wslot + 1024 /*barriers*/ + epi_bytes;
   if (smem > 227 * 1024) throw UnsupportedError("uvw tensor-core path: shared memory too small");
   const int acol0 = kTmemCols - 32 * na;  // A ring columns [acol0, 512)
 
@@ -1229,6 +1236,8 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
   // epilogue: per segment (compile-time dz, n), TMEM -> registers -> z row
   o << "  else {\n"
        "    const int qd = warp & 3, m = 32 * qd + lane;\n"
+    << (epi_stage ? "    float* stg = (float*)((unsigned char*)bars + 1024) + qd * " + S(32 * epi_stride) + ";\n" : "")
+    << ""
        "    const u32 tq = tmem + ((u32)(32 * qd) << 16);\n"
        "    i64 lt = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {\n"
@@ -1244,6 +1253,29 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
       << "          float v[" << sg.dz << "][8];\n";
     for (int k = 0; k < sg.dz; ++k)
       o << "          tc_ld8(tq + (u32)(" << sg.col + k * sg.n << " + r0), v[" << k << "]);\n";
+    if (epi_stage) {
+      // rows -> the warp's staging rows (stride 8 dz + 4 floats: conflict-free
+      // v4 stores), then lanes walk the 32 rows' contiguous 8 dz floats
+      const int st = 8 * sg.dz + 4, nq = 2 * sg.dz;
+      o << "          tc_wait_ld();\n          {\n            float* sr = stg + lane * " << st << ";\n";
+      for (int t = 0; t < nq; ++t) {
+        o << "            sts128((unsigned char*)(sr + " << 4 * t << "), make_float4(";
+        for (int a = 0; a < 4; ++a) {
+          const int f = 4 * t + a, rr = f / sg.dz, kk = f % sg.dz;
+          o << (a ? ", " : "") << "v[" << kk << "][" << rr << "]";
+        }
+        o << "));\n";
+      }
+      o << "          }\n          __syncwarp();\n"
+        << "          if (!(UVW_EXP & 1))\n"
+        << "          for (int i = lane; i < " << 32 * nq << "; i += 32) {\n"
+        << "            const int rw = i / " << nq << ", pq = i - rw * " << nq << ";\n"
+        << "            const i64 grow = tile * 128 + 32 * qd + rw;\n"
+        << "            if (grow < rows) __stcs((float4*)(Z + grow * DIMZ + " << sg.z_off << " + r0 * " << sg.dz
+        << ") + pq, lds128((const unsigned char*)(stg + rw * " << st << " + 4 * pq)));\n          }\n"
+        << "          __syncwarp();\n";
+      o << "        }\n        tc_fence_before();\n        __syncwarp();\n";
+    } else {
     o << "          tc_wait_ld();\n          if (valid && !(UVW_EXP & 1)) {\n            float4* dst = (float4*)(zr + r0 * " << sg.dz << ");\n";
     for (int t = 0; t < 2 * sg.dz; ++t) {
       o << "            __stcs(dst + " << t << ", make_float4(";
@@ -1253,7 +1285,9 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
       }
       o << "));\n";
     }
-    o << "          }\n        }\n        tc_fence_before();\n        __syncwarp();\n"
+    o << "          }\n        }\n        tc_fence_before();\n        __syncwarp();\n";
+    }
+    o << ""
       << "        if (lane == 0) mbar_arrive(&sdrained[" << si << "]);\n      }\n";
   }
   o << "    }\n  }\n";
