@@ -937,13 +937,17 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
   // A blocks per TMEM-store round (<= NS / 2 so a batch is written while the other half is consumed);
   // batches of 2 measured 3.45 ms vs 3.36 ms for 1 (profiles/r01_uvw_kb.log), so 1 is the default
   const int kb = std::max(1, std::min(std::getenv("CGF_UVW_KB") ? std::atoi(std::getenv("CGF_UVW_KB")) : 1, na / 2));
+  const bool pipe = std::getenv("CGF_UVW_PIPE") && std::atoi(std::getenv("CGF_UVW_PIPE")) == 1;
   // warps: producers | MMA | 4 epilogue | W loader | x loader
   const int mma_warp = pw, wload_warp = pw + 5, xload_warp = pw + 6, nwarps = pw + 7;
-  // epilogue staging (CGF_UVW_EPI=1): per epilogue warp, 32 rows x (8 dz + 4)
-  // floats, so each z row piece leaves as contiguous full-sector stores
+  // epilogue staging: per epilogue warp, 32 rows x (8 dz + 4) floats, so each
+  // z row piece leaves as contiguous full-sector stores (each thread's own-row
+  // float4 stores touched 32 lines per instruction, half a sector each)
   int max_dz = 1;
   for (const auto& sg : segs) max_dz = std::max(max_dz, sg.dz);
-  const bool epi_stage = std::getenv("CGF_UVW_EPI") && std::atoi(std::getenv("CGF_UVW_EPI")) == 1;
+  // staged epilogue: C3 forward 3.19 -> 2.79 ms, gx 15.48 -> 15.05 ms of the
+  // backward (profiles/r02_ab_uvw2.jsonl); CGF_UVW_EPI=0 restores row stores
+  const bool epi_stage = !(std::getenv("CGF_UVW_EPI") && std::atoi(std::getenv("CGF_UVW_EPI")) == 0);
   const int epi_stride = 8 * max_dz + 4;
   const int epi_bytes = epi_stage ? 4 * 32 * epi_stride * 4 : 0;
   const int smem = 1024 /*align*/ + nx * xslot + nwr * wslot + 1024 /*barriers*/ + epi_bytes;
@@ -990,7 +994,7 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
     o << "// instruction " << q << ": l=(" << s.l1 << "," << s.l2 << "," << s.l3 << ") b=" << s.b << " b'=" << s.bp
       << " nnz=" << s.cg->entries.size() << "\n";
     o << "DEVI void produce_" << q << "(const unsigned char* xs, const float* yv, int m, int sub,"
-         " u32 tq, u64* afull, u64* aempty, u64* xempty, u32& slot, u32& ph) {\n";
+         " u32 tq, u64* afull, u64* aempty, u64* xempty, u32& slot, u32& ph, u32& pend, u32& pslot) {\n";
     // x: cpt channels x dx floats = cpt * dx / 4 float4 chunks of the staged SW64 tile
     const int nch = cpt * dx / 4;
     o << "  float xv[" << cpt * dx << "];\n#pragma unroll\n  for (int t = 0; t < " << nch
@@ -1012,6 +1016,26 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
     // Blocks go out in batches of kb: all of a batch's values are computed
     // before its slots are awaited, and one tcgen05.wait::st + fence + arrive
     // round covers the batch (the per-block round trip dominated the loop).
+    if (pipe) {
+      // Software-pipelined TMEM stores: block k's stores are issued, and their
+      // completion (tcgen05.wait::st) + the afull arrive happen only after
+      // block k+1's values are computed -- the store round trip overlaps the
+      // next block's FMAs instead of stalling the warp (pend / pslot carry the
+      // outstanding block across units; the caller flushes it at the end).
+      for (int k = 0; k < dz; ++k) {
+        o << "  {\n    float h[" << cpt << "], l[" << cpt << "];\n#pragma unroll\n    for (int c = 0; c < " << cpt
+          << "; ++c) {\n      float z = 0.f;\n#pragma unroll\n      for (int i = 0; i < " << dx
+          << "; ++i) z = fmaf(q[" << k << "][i], xv[c * " << dx << " + i], z);\n"
+          << "      h[c] = tf32_hi(z); l[c] = z - h[c];\n    }\n"
+          << "    if (pend) { tc_wait_st(); tc_fence_before(); __syncwarp(); if ((threadIdx.x & 31) == 0) mbar_arrive(&afull[pslot]); pend = 0; }\n"
+          << "    mbar_wait_t(&aempty[slot], ph ^ 1u, 1);\n    tc_fence_after();\n"
+          << "    { const u32 ta = tq + ACOL0 + 32 * slot + " << cpt << " * sub;\n"
+          << "      if (!(UVW_EXP & 4)) { tc_st" << cpt << "(ta, h); tc_st" << cpt << "(ta + 16, l); } }\n"
+          << "    pslot = slot; pend = 1;\n    if (++slot == NS) { slot = 0; ph ^= 1u; }\n  }\n";
+      }
+      o << "}\n\n";
+      continue;
+    }
     for (int k0 = 0; k0 < dz; k0 += kb) {
       const int nk = std::min(kb, dz - k0);
       o << "  {\n    float h[" << nk << "][" << cpt << "], l[" << nk << "][" << cpt << "];\n";
@@ -1120,7 +1144,7 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
     << ") {\n"
        "    const int m = 32 * (warp & 3) + lane, sub = warp >> 2;\n"
        "    const u32 tq = tmem + ((u32)(32 * (warp & 3)) << 16);\n"
-       "    u32 slot = 0, ph = 0, gx = 0;\n"
+       "    u32 slot = 0, ph = 0, gx = 0, pend = 0, pslot = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
        "      const i64 row = tile * 128 + m;\n"
        "      const bool valid = row < rows;\n"
@@ -1133,9 +1157,11 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
        "        const unsigned char* xsl = xbase + xs_ * XSLOT;\n"
        "        switch (U_INS[u]) {\n";
   for (int q = 0; q < np; ++q)
-    o << "          case " << q << ": produce_" << q << "(xsl, yv, m, sub, tq, afull, aempty, &xempty[xs_], slot, ph); break;\n";
+    o << "          case " << q << ": produce_" << q << "(xsl, yv, m, sub, tq, afull, aempty, &xempty[xs_], slot, ph, pend, pslot); break;\n";
   o << "        }\n      }\n";
-  o << "    }\n  }\n";
+  o << "    }\n"
+       "    if (pend) { tc_wait_st(); tc_fence_before(); __syncwarp(); if (lane == 0) mbar_arrive(&afull[pslot]); }\n"
+       "  }\n";
 
   // MMA issuer
   o << "  else if (warp == " << mma_warp
