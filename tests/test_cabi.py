@@ -113,3 +113,44 @@ def test_device_entry_points_fail_loudly_without_cuda():
     }
     for name, call in calls.items():
         assert call() == cgf.CudaError.code, name
+
+
+def test_output_arrays_are_shape_checked_before_any_compute():
+    """TpPlan.forward / backward / forward_backward reject a z (or gx, gy, gw)
+    of the wrong shape, or a non-contiguous / read-only numpy output, with
+    ShapeError before the C ABI is called (no device needed)."""
+    import numpy as np
+    import paper_2501_13986_b200 as cgf
+    from paper_2501_13986_b200.configs import config_json
+    plan = cgf.TpPlan(config_json("c1"))
+    x = np.zeros((4, plan.dim_x), np.float32)
+    y = np.zeros((4, plan.dim_y), np.float32)
+    w = np.zeros((4, plan.n_w), np.float32)
+    gz = np.zeros((4, plan.dim_z), np.float32)
+    for bad in (np.zeros((3, plan.dim_z), np.float32), np.zeros((4, plan.dim_z + 1), np.float32),
+                np.zeros((plan.dim_z, 4), np.float32).T):
+        with pytest.raises(cgf.ShapeError):
+            plan.forward(x, y, w, z=bad)
+    ro = np.zeros((4, plan.dim_z), np.float32)
+    ro.flags.writeable = False
+    with pytest.raises(cgf.ShapeError):
+        plan.forward(x, y, w, z=ro)
+    with pytest.raises(cgf.ShapeError):
+        plan.backward(x, y, w, gz, out=(np.zeros((4, plan.dim_x), np.float32), np.zeros((4, plan.dim_y), np.float32),
+                                        np.zeros((3, plan.n_w), np.float32)))
+    with pytest.raises(cgf.ShapeError):
+        plan.forward_backward(x, y, w, gz, out=(np.zeros((4, plan.dim_z), np.float32),) * 4)
+
+
+def test_device_traffic_model():
+    """cgf_tp_traffic: the compulsory words of each op."""
+    import paper_2501_13986_b200 as cgf
+    from paper_2501_13986_b200.configs import config_json
+    p = cgf.TpPlan(config_json("c2"))
+    X, Y, W, Z = p.dim_x, p.dim_y, p.n_w, p.dim_z
+    assert p.traffic(cgf.OP_FORWARD, 10) == (10 * (X + Y + W), 10 * Z)
+    assert p.traffic(cgf.OP_BACKWARD, 10) == (10 * (X + Y + W + Z), 10 * (X + Y + W))
+    assert p.traffic(cgf.OP_DOUBLE_BACKWARD, 10) == (10 * (3 * (X + Y + W) + Z), 10 * (X + Y + W + Z))
+    assert p.traffic(cgf.OP_FORWARD, 10, w_shared=True) == (10 * (X + Y) + W, 10 * Z)
+    # the bench's C2 per-row figures (SURVEY.md §8d): 12,432 / 15,776 words
+    assert sum(p.traffic(cgf.OP_FORWARD, 1)) == 12_432 and sum(p.traffic(cgf.OP_BACKWARD, 1)) == 15_776
