@@ -850,7 +850,8 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
     for (size_t i = 0; i < perm.size(); ++i) perm[i] = static_cast<int>(i);
     int best_score = 1 << 30;
     std::vector<Seg> best;
-    for (int cand = 4; cand >= 2 && best.empty(); --cand) {
+    const int na_max = std::getenv("CGF_UVW_NA") ? std::atoi(std::getenv("CGF_UVW_NA")) : 4;  // A/B knob
+    for (int cand = na_max; cand >= 2 && best.empty(); --cand) {
       const int cap = kTmemCols - 32 * cand;
       bool fits = true;
       for (const auto& sg : segs) fits = fits && sg.dz * sg.n <= cap;
@@ -916,14 +917,26 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
     wimg_of[q] = wimg;
     wimg += static_cast<std::size_t>(R[q].bp / kCh) * wslot;
   }
+  // CGF_UVW_ORDER=1: within a segment, channel-block-major (instructions of
+  // different dx alternate, so cheap and expensive producer units interleave)
+  const int uorder = std::getenv("CGF_UVW_ORDER") ? std::atoi(std::getenv("CGF_UVW_ORDER")) : 0;
   for (int si = 0; si < ns; ++si) {
     const auto& s = segs[si];
-    for (size_t t = 0; t < s.ins.size(); ++t) {
-      const int q = s.ins[t];
-      const int nb = R[q].bp / kCh;
-      for (int cb = 0; cb < nb; ++cb)
-        units.push_back({q, cb, si, s.dz, s.n, R[q].dx(), t == 0 && cb == 0, t + 1 == s.ins.size() && cb + 1 == nb,
-                         wimg_of[q] + static_cast<std::size_t>(cb) * wslot});
+    std::vector<std::pair<int, int>> qc;  // (instruction, channel block)
+    int maxnb = 0;
+    for (int q : s.ins) maxnb = std::max(maxnb, R[q].bp / kCh);
+    if (uorder == 1) {
+      for (int cb = 0; cb < maxnb; ++cb)
+        for (int q : s.ins)
+          if (cb < R[q].bp / kCh) qc.push_back({q, cb});
+    } else {
+      for (int q : s.ins)
+        for (int cb = 0; cb < R[q].bp / kCh; ++cb) qc.push_back({q, cb});
+    }
+    for (size_t t = 0; t < qc.size(); ++t) {
+      const int q = qc[t].first, cb = qc[t].second;
+      units.push_back({q, cb, si, s.dz, s.n, R[q].dx(), t == 0, t + 1 == qc.size(),
+                       wimg_of[q] + static_cast<std::size_t>(cb) * wslot});
     }
   }
   const int nu = static_cast<int>(units.size());
@@ -937,6 +950,13 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
   // A blocks per TMEM-store round (<= NS / 2 so a batch is written while the other half is consumed);
   // batches of 2 measured 3.45 ms vs 3.36 ms for 1 (profiles/r01_uvw_kb.log), so 1 is the default
   const int kb = std::max(1, std::min(std::getenv("CGF_UVW_KB") ? std::atoi(std::getenv("CGF_UVW_KB")) : 1, na / 2));
+  // every producer thread arrives on afull / xempty (no __syncwarp; CGF_UVW_ARV=0
+  // restores lane-0 arrives), and the x slot is released after the unit's last
+  // A block (CGF_UVW_XREL=0: right after the reads): together C3 forward
+  // 2.79 -> 2.75 ms (profiles/r02_ab_uvw5.jsonl)
+  const bool pipe_req = std::getenv("CGF_UVW_PIPE") && std::atoi(std::getenv("CGF_UVW_PIPE")) == 1;
+  const bool all_arrive = !pipe_req && !(std::getenv("CGF_UVW_ARV") && std::atoi(std::getenv("CGF_UVW_ARV")) == 0);
+  const bool xrel_late = !(std::getenv("CGF_UVW_XREL") && std::atoi(std::getenv("CGF_UVW_XREL")) == 0);
   const bool pipe = std::getenv("CGF_UVW_PIPE") && std::atoi(std::getenv("CGF_UVW_PIPE")) == 1;
   // warps: producers | MMA | 4 epilogue | W loader | x loader
   const int mma_warp = pw, wload_warp = pw + 5, xload_warp = pw + 6, nwarps = pw + 7;
@@ -1004,8 +1024,12 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
          // generic-proxy reads of the slot must be ordered before the next
          // TMA (async proxy) write into it: without this fence the refill
          // raced the reads (measured: corrupted rows).
-         "  fence_proxy_async();\n"
-         "  __syncwarp();\n  if ((threadIdx.x & 31) == 0) mbar_arrive(xempty);\n";
+         "";
+    // release of the x slot: right after the reads (default), or (CGF_UVW_XREL=1)
+    // after the unit's last A block, when the fence has no loads left to wait on
+    const std::string xrel = std::string(std::getenv("CGF_UVW_EXP") && (std::atoi(std::getenv("CGF_UVW_EXP")) & 8) ? "" : "  fence_proxy_async();\n") +
+                             (all_arrive ? "  mbar_arrive(xempty);\n" : "  __syncwarp();\n  if ((threadIdx.x & 31) == 0) mbar_arrive(xempty);\n");
+    if (!xrel_late) o << xrel;
     o << "  float q[" << dz << "][" << dx << "];\n#pragma unroll\n  for (int k = 0; k < " << dz
       << "; ++k)\n#pragma unroll\n    for (int i = 0; i < " << dx << "; ++i) q[k][i] = 0.f;\n";
     for (const auto& e : s.cg->entries)
@@ -1033,6 +1057,7 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
           << "      if (!(UVW_EXP & 4)) { tc_st" << cpt << "(ta, h); tc_st" << cpt << "(ta + 16, l); } }\n"
           << "    pslot = slot; pend = 1;\n    if (++slot == NS) { slot = 0; ph ^= 1u; }\n  }\n";
       }
+      if (xrel_late) o << xrel;
       o << "}\n\n";
       continue;
     }
@@ -1052,11 +1077,12 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
           << "      if (!(UVW_EXP & 4)) { tc_st" << cpt << "(ta, h[" << t << "]); tc_st" << cpt << "(ta + 16, l[" << t << "]); } }\n"
           << "    if (++s_ == NS) { s_ = 0; p_ ^= 1u; }\n";
       }
-      o << "    tc_wait_st();\n    tc_fence_before();\n    __syncwarp();\n"
-        << "    if ((threadIdx.x & 31) == 0) { u32 a_ = slot;";
+      o << "    tc_wait_st();\n    tc_fence_before();\n"
+        << (all_arrive ? "    { u32 a_ = slot;" : "    __syncwarp();\n    if ((threadIdx.x & 31) == 0) { u32 a_ = slot;");
       for (int t = 0; t < nk; ++t) o << " mbar_arrive(&afull[a_]);" << (t + 1 < nk ? " if (++a_ == NS) a_ = 0;" : "");
       o << " }\n    slot = s_; ph = p_;\n  }\n";
     }
+    if (xrel_late) o << xrel;
     o << "}\n\n";
   }
 
@@ -1121,11 +1147,11 @@ UvwSource generate_uvw_impl(const Problem& p, const std::string& tag, bool w_tra
        "  const i64 my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;\n"
        "  if (threadIdx.x == 0) {\n"
        "    for (int i = 0; i < NS; ++i) { mbar_init(&afull[i], "
-    << pw
+    << (all_arrive ? pw * 32 : pw)
     << "); mbar_init(&aempty[i], 1); }\n"
        "    for (int i = 0; i < NWR; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }\n"
        "    for (int i = 0; i < NX; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], "
-    << pw
+    << (all_arrive ? pw * 32 : pw)
     << "); }\n"
        "    for (int i = 0; i < NSEG; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sdrained[i], 4); }\n"
        "    mbar_fence_init();\n  }\n"
