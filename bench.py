@@ -390,21 +390,29 @@ class _TorchShardStandIn:
     def __init__(self, plan):
         self.plan = plan
 
-    def forward_shard(self, sh, x_all, ey, ew, mode=0):
+    def forward_shard(self, sh, x_all, ey, ew, mode=0, rows=None, out=None):
         import torch
         d = sh.device(x_all.device)
         src = torch.repeat_interleave(torch.arange(sh.out_nodes), d["row_ptr"].diff())
         z = x_all.new_zeros((sh.out_nodes, self.plan.dim_z))
         z[:, :self.plan.dim_x].index_add_(0, src, x_all[d["nbr"].long()])
-        return z
+        if rows is None:
+            return z
+        out = x_all.new_zeros(z.shape) if out is None else out
+        out[rows[0]:rows[1]] = z[rows[0]:rows[1]]
+        return out
 
-    def backward_shard(self, sh, x_all, ey, ew, gz, mode=0):
+    def backward_shard(self, sh, x_all, ey, ew, gz, mode=0, rows=None, outs=None):
         import torch
         d = sh.device(x_all.device)
         src = torch.repeat_interleave(torch.arange(sh.out_nodes), d["row_ptr"].diff())
         gx = x_all.new_zeros((sh.in_nodes, self.plan.dim_x))
         gx.index_add_(0, d["nbr"].long(), gz[src, :self.plan.dim_x])
-        return gx, torch.zeros_like(ey), torch.zeros_like(ew)
+        if rows is None:
+            return gx, torch.zeros_like(ey), torch.zeros_like(ew)
+        outs = (x_all.new_zeros(gx.shape), torch.zeros_like(ey), torch.zeros_like(ew)) if outs is None else outs
+        outs[0][rows[0]:rows[1]] = gx[rows[0]:rows[1]]
+        return outs
 
 
 def conv_leg(args, rank, world, dev, harness=False):
@@ -447,6 +455,7 @@ def conv_leg(args, rank, world, dev, harness=False):
         return a.elapsed_time(b) if cuda else (b - a) * 1e3
 
     def step(record=False):
+        # unoverlapped: all-gather | forward kernel | backward kernel | exchange + ordered sum
         t0 = mark()
         x_all = dc.gather_x(nx)
         t1 = mark()
@@ -460,29 +469,46 @@ def conv_leg(args, rank, world, dev, harness=False):
             laps.append((t0, t1, t2, t3, t4))
         return z, gx, gy, gw
 
-    for _ in range(max(3, args.warmup)):
-        step()
-    if cuda:
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    if cuda:
-        torch.cuda.synchronize()
-    a = mark()
-    for _ in range(args.conv_steps):
-        step(record=True)
-    b = mark()
-    if cuda:
-        torch.cuda.synchronize()
-    ms = lap(a, b) / args.conv_steps
-    f_ms = sum(lap(t[1], t[2]) for t in laps) / len(laps)
-    b_ms = sum(lap(t[2], t[3]) for t in laps) / len(laps)
-    ag_ms = sum(lap(t[0], t[1]) for t in laps) / len(laps)
-    rs_ms = sum(lap(t[3], t[4]) for t in laps) / len(laps)
-    t = torch.tensor([ms, f_ms, b_ms, ag_ms, rs_ms], dtype=torch.float64, device=dev)
+    def step_overlap(record=False):
+        # overlapped (DistConvPlan default at N > 1): local-neighbour rows run
+        # during the all-gather, own neighbour rows during the exchange
+        t0 = mark()
+        z, x_all = dc.forward_gathered(nx, ey, ew)
+        t1 = mark()
+        gx, gy, gw = dc.backward(nx, ey, ew, gnz, node_x_all=x_all)
+        t2 = mark()
+        if record:
+            laps.append((t0, t1, t2))
+        return z, gx, gy, gw
+
+    def timed(fn):
+        laps.clear()
+        for _ in range(max(3, args.warmup)):
+            fn()
+        if cuda:
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        if cuda:
+            torch.cuda.synchronize()
+        a = mark()
+        for _ in range(args.conv_steps):
+            fn(record=True)
+        b = mark()
+        if cuda:
+            torch.cuda.synchronize()
+        return lap(a, b) / args.conv_steps, [sum(lap(t[i], t[i + 1]) for t in laps) / len(laps)
+                                             for i in range(len(laps[0]) - 1)]
+
+    ms, (ag_ms, f_ms, b_ms, rs_ms) = timed(step)
+    ov_ms, ov_f, ov_b = (ms, f_ms + ag_ms, b_ms + rs_ms) if world == 1 else (lambda r: (r[0], *r[1]))(
+        timed(step_overlap))
+    t = torch.tensor([ms, f_ms, b_ms, ag_ms, rs_ms, ov_ms, ov_f, ov_b], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, f_mx, b_mx, ag_mx, rs_mx = (float(v) for v in t.tolist())
+    ms, f_mx, b_mx, ag_mx, rs_mx, ov_mx, ovf_mx, ovb_mx = (float(v) for v in t.tolist())
+    unoverlapped_ms = ms
+    ms = ov_mx  # the DistConvPlan default (overlapped at N > 1; the same step at N = 1)
     E, Vo, Vi = sh.edges, sh.out_nodes, sh.in_nodes
     fb = (E * (plan.dim_y + plan.n_w) + Vi * plan.dim_x + Vo * plan.dim_z) * es
     bb = (2 * E * (plan.dim_y + plan.n_w) + Vi * 2 * plan.dim_x + Vo * plan.dim_z) * es
@@ -492,10 +518,16 @@ def conv_leg(args, rank, world, dev, harness=False):
                     f"{nodes} nodes / {g.edges} edges, fwd+bwd, destination-partitioned",
         "edges_per_s": g.edges / (ms / 1e3), "ms_per_step": ms, "steps": args.conv_steps, "n_gpus": world,
         "scaling": "strong", "dtype": args.dtype,
-        "collectives": "all_gather_into_tensor(node_x) + all_to_all_single(g_node_x partials) + rank-ordered sum"
+        "collectives": "in-place all_gather_into_tensor(node_x) overlapped with the local-neighbour rows; "
+                       "point-to-point exchange of g_node_x partials overlapped with the own neighbour rows; "
+                       "rank-ordered sum (step_unoverlapped: all_to_all_single after the kernels)"
         if world > 1 else "none (1 rank)",
         "max_over_ranks_ms": {"step": ms, "forward_kernel": f_mx, "backward_kernel": b_mx,
-                              "all_gather": ag_mx, "reduce": rs_mx},
+                              "all_gather": ag_mx, "reduce": rs_mx, "step_unoverlapped": unoverlapped_ms,
+                              "step_overlapped": ov_mx, "forward_with_all_gather_overlapped": ovf_mx,
+                              "backward_with_exchange_overlapped": ovb_mx},
+        "overlap": {"local_rows": list(sh.local_rows()), "own_neighbour_rows": list(sh.own_rows()),
+                    "out_nodes": sh.out_nodes, "in_nodes": sh.in_nodes} if world > 1 else None,
         "rank0_roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
                            "forward": {"GB/s": fb / (f_ms / 1e3) / 1e9, "frac": fb / (f_ms / 1e3) / 1e9 / peak},
                            "backward": {"GB/s": bb / (b_ms / 1e3) / 1e9, "frac": bb / (b_ms / 1e3) / 1e9 / peak}},

@@ -727,29 +727,70 @@ class ConvPlan:
         if not _is_torch(ref):
             raise ShapeError("conv: pass torch CUDA tensors")
 
-    def forward_shard(self, sh, node_x_all, edge_y, edge_w, mode=DETERMINISTIC):
-        """Local output rows of the conv; node_x_all spans sh.in_nodes rows."""
+    @staticmethod
+    def _row_range(rows, n, what):
+        """(r0, r1) of a row-range shard call: 0 <= r0 <= r1 <= n, r0 a multiple of
+        4 so every row-indexed array keeps the 16-byte alignment of its base."""
+        r0, r1 = (0, n) if rows is None else (int(rows[0]), int(rows[1]))
+        if not 0 <= r0 <= r1 <= n:
+            raise ShapeError(f"conv shard: {what} rows [{r0}, {r1}) outside [0, {n})")
+        if r0 % 4:
+            raise ShapeError(f"conv shard: {what} row range must start at a multiple of 4, got {r0}")
+        return r0, r1
+
+    def _outs(self, outs, ref, shapes):
+        if outs is None:
+            return [TpPlan._empty_like(ref, s) for s in shapes]
+        for a, s in zip(outs, shapes):
+            if tuple(a.shape) != s:
+                raise ShapeError(f"conv shard: output shape mismatch: expected {s}, got {tuple(a.shape)}")
+            TpPlan._same(ref, a)
+        return list(outs)
+
+    def forward_shard(self, sh, node_x_all, edge_y, edge_w, mode=DETERMINISTIC, rows=None, out=None):
+        """Local output rows of the conv; node_x_all spans sh.in_nodes rows.
+
+        ``rows=(r0, r1)`` computes output rows [r0, r1) only, into ``out`` (the
+        [out_nodes, dim_z] result, allocated when None): the row-range launches
+        of the overlapped multi-GPU forward (``dist.DistConvPlan``). Rows are
+        independent and each keeps its edge order, so any split is bit-identical
+        to one launch over the shard."""
         p = self.plan
         self._check_shard(sh, node_x_all=node_x_all, edge_y=edge_y, edge_w=edge_w)
-        z = TpPlan._empty_like(node_x_all, (sh.out_nodes, p.dim_z))
+        (z,) = self._outs(None if out is None else (out,), node_x_all, [(sh.out_nodes, p.dim_z)])
+        r0, r1 = self._row_range(rows, sh.out_nodes, "output")
+        if rows is not None and mode != DETERMINISTIC:
+            raise ShapeError("conv shard: row ranges are for the deterministic mode")
         d = self._shard_ptrs(sh, node_x_all)
-        _check(lib().cgf_conv_forward_shard(p._h, _dtype_code(node_x_all), sh.out_nodes, sh.in_nodes, sh.edges,
-                                            d["row_ptr"], d["nbr"], TpPlan._p(node_x_all), TpPlan._p(edge_y),
-                                            TpPlan._p(edge_w), TpPlan._p(z), mode, TpPlan._stream(node_x_all)))
+        es = node_x_all.element_size()
+        _check(lib().cgf_conv_forward_shard(p._h, _dtype_code(node_x_all), r1 - r0, sh.in_nodes, sh.edges,
+                                            C.c_void_p(d["row_ptr"].value + 8 * r0), d["nbr"],
+                                            TpPlan._p(node_x_all), TpPlan._p(edge_y), TpPlan._p(edge_w),
+                                            C.c_void_p(z.data_ptr() + r0 * p.dim_z * es), mode,
+                                            TpPlan._stream(node_x_all)))
         return z
 
-    def backward_shard(self, sh, node_x_all, edge_y, edge_w, g_node_z, mode=DETERMINISTIC):
-        """(partial g_node_x over sh.in_nodes rows, g_edge_y, g_edge_w)."""
+    def backward_shard(self, sh, node_x_all, edge_y, edge_w, g_node_z, mode=DETERMINISTIC, rows=None, outs=None):
+        """(partial g_node_x over sh.in_nodes rows, g_edge_y, g_edge_w).
+
+        ``rows=(r0, r1)`` runs the transposed-CSR rows (neighbour nodes) [r0, r1)
+        only, writing their g_node_x rows and their edges' g_edge_y / g_edge_w
+        into ``outs`` = (gx, gy, gw) (allocated when None); the overlapped
+        multi-GPU backward runs the other ranks' rows first and sends them while
+        its own rows compute."""
         p = self.plan
         self._check_shard(sh, node_x_all=node_x_all, edge_y=edge_y, edge_w=edge_w, g_node_z=g_node_z)
-        gx = TpPlan._empty_like(node_x_all, (sh.in_nodes, p.dim_x))
-        gy = TpPlan._empty_like(node_x_all, (sh.edges, p.dim_y))
-        gw = TpPlan._empty_like(node_x_all, (sh.edges, p.n_w))
+        gx, gy, gw = self._outs(outs, node_x_all, [(sh.in_nodes, p.dim_x), (sh.edges, p.dim_y), (sh.edges, p.n_w)])
+        r0, r1 = self._row_range(rows, sh.in_nodes, "neighbour")
+        if rows is not None and mode != DETERMINISTIC:
+            raise ShapeError("conv shard: row ranges are for the deterministic mode")
         d = self._shard_ptrs(sh, node_x_all)
-        _check(lib().cgf_conv_backward_shard(p._h, _dtype_code(node_x_all), sh.out_nodes, sh.in_nodes, sh.edges,
-                                             d["t_row_ptr"], d["t_src"], d["t_eid"], TpPlan._p(node_x_all),
-                                             TpPlan._p(edge_y), TpPlan._p(edge_w), TpPlan._p(g_node_z),
-                                             TpPlan._p(gx), TpPlan._p(gy), TpPlan._p(gw), mode,
+        off = r0 * p.dim_x * node_x_all.element_size()
+        _check(lib().cgf_conv_backward_shard(p._h, _dtype_code(node_x_all), sh.out_nodes, r1 - r0, sh.edges,
+                                             C.c_void_p(d["t_row_ptr"].value + 8 * r0), d["t_src"], d["t_eid"],
+                                             C.c_void_p(node_x_all.data_ptr() + off), TpPlan._p(edge_y),
+                                             TpPlan._p(edge_w), TpPlan._p(g_node_z),
+                                             C.c_void_p(gx.data_ptr() + off), TpPlan._p(gy), TpPlan._p(gw), mode,
                                              TpPlan._stream(node_x_all)))
         return gx, gy, gw
 

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -37,9 +38,20 @@ struct cgf_conv_shard {
   // device CSR of the shard (rows = owned output nodes, nbr in the padded
   // neighbour space) and its transposed CSR
   void *row_ptr = nullptr, *nbr = nullptr, *t_row_ptr = nullptr, *t_src = nullptr, *t_eid = nullptr;
+  // overlap (dist.DistConvPlan's scheme): [la, lb) = the longest run of output
+  // rows whose neighbours are all this rank's nodes (they run during the
+  // all-gather), [oa, ob) = this rank's own slot of the neighbour rows (they run
+  // during the exchange); both 4-aligned. The collectives of an overlapped call
+  // run on `comm_stream`, ordered against the caller's stream by the events.
+  std::int64_t la = 0, lb = 0, oa = 0, ob = 0;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
   ~cgf_conv_shard() {
     for (void* p : {row_ptr, nbr, t_row_ptr, t_src, t_eid})
       if (p) cudaFree(p);
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
   }
 };
 
@@ -199,6 +211,17 @@ void ordered_reduce(const cgf_conv_shard* sh, int dtype, void* comm, const void*
                         false, stream, static_cast<std::int64_t>(sh->chunk) * dim);
 }
 
+// Overlapped collectives: on by default for P > 1 in the deterministic mode;
+// CGF_DIST_OVERLAP=0 turns them off, =force also overlaps on one rank (tests).
+bool overlap_on(const cgf_conv_shard* sh, int mode) {
+  const char* e = std::getenv("CGF_DIST_OVERLAP");
+  if (mode != CGF_CONV_DETERMINISTIC || (e && std::strcmp(e, "0") == 0)) return false;
+  return sh->world > 1 || (e && std::strcmp(e, "force") == 0);
+}
+
+std::int64_t ceil4(std::int64_t v) { return (v + 3) / 4 * 4; }
+std::int64_t floor4(std::int64_t v) { return v / 4 * 4; }
+
 }  // namespace
 
 extern "C" {
@@ -259,6 +282,25 @@ int cgf_conv_shard_create(int64_t nodes, int64_t edges, const int64_t* row_ptr, 
     std::vector<std::int32_t> tsrc(std::max<std::int64_t>(sh->edges, 1)), teid(std::max<std::int64_t>(sh->edges, 1));
     rc_check(cgf_conv_transpose_shard_host(sh->out_nodes, sh->in_nodes, sh->edges, rp.data(), nb.data(), trp.data(),
                                            tsrc.data(), teid.data()));
+    {  // overlap ranges (dist.GraphShard.local_rows / own_rows)
+      const std::int64_t lo = static_cast<std::int64_t>(rank) * sh->chunk, hi = lo + sh->out_nodes;
+      std::int64_t a = 0, ba = 0, bb = 0;
+      for (std::int64_t v = 0; v <= sh->out_nodes; ++v) {
+        bool inner = v < sh->out_nodes;
+        for (std::int64_t e = inner ? rp[v] : 0; inner && e < rp[v + 1]; ++e) inner = nb[e] >= lo && nb[e] < hi;
+        if (inner) continue;
+        if (v - a > bb - ba) { ba = a; bb = v; }
+        a = v + 1;
+      }
+      sh->la = ceil4(ba);
+      sh->lb = floor4(bb);
+      if (sh->la >= sh->lb) sh->la = sh->lb = 0;
+      sh->oa = ceil4(lo);
+      sh->ob = floor4(lo + sh->chunk);
+      if (sh->oa >= sh->ob) sh->oa = sh->ob = 0;
+      cuda_check(cudaStreamCreateWithFlags(&sh->comm_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      for (auto& e : sh->ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    }
     sh->row_ptr = upload(rp);
     sh->nbr = upload(nb);
     sh->t_row_ptr = upload(trp);
@@ -284,13 +326,40 @@ int cgf_dist_conv_forward(cgf_plan* plan, int dtype, const cgf_conv_shard* sh, v
     if (!plan || !sh || !comm) throw std::invalid_argument("null pointer");
     int64_t d[6];
     rc_check(cgf_plan_dims(plan, d));
-    const int dx = static_cast<int>(d[0]);
+    const int dx = static_cast<int>(d[0]), dz = static_cast<int>(d[2]);
     const std::size_t es = dtype == CGF_F64 ? 8 : 4;
-    DevScratch pad(es * dx * sh->chunk, stream), all(es * dx * sh->in_nodes, stream);
-    all_gather(sh, dtype, comm, node_x, dx, all.p, pad, stream);
-    rc_check(cgf_conv_forward_shard(plan, dtype, sh->out_nodes, sh->in_nodes, sh->edges,
-                                    static_cast<const int64_t*>(sh->row_ptr), static_cast<const int32_t*>(sh->nbr),
-                                    all.p, edge_y, edge_w, node_z, mode, stream));
+    const auto rp = static_cast<const int64_t*>(sh->row_ptr);
+    const auto nb = static_cast<const int32_t*>(sh->nbr);
+    if (!overlap_on(sh, mode) || sh->la >= sh->lb) {
+      DevScratch pad(es * dx * sh->chunk, stream), all(es * dx * sh->in_nodes, stream);
+      all_gather(sh, dtype, comm, node_x, dx, all.p, pad, stream);
+      rc_check(cgf_conv_forward_shard(plan, dtype, sh->out_nodes, sh->in_nodes, sh->edges, rp, nb, all.p, edge_y,
+                                      edge_w, node_z, mode, stream));
+      return;
+    }
+    // in-place all-gather on the comm stream while the local-neighbour rows run
+    cudaStream_t st = static_cast<cudaStream_t>(stream), cs = sh->comm_stream;
+    const std::size_t row = es * dx;
+    DevScratch all(row * sh->in_nodes, stream);
+    char* own = all.c() + row * sh->rank * sh->chunk;
+    cuda_check(cudaMemsetAsync(own + row * sh->out_nodes, 0, row * (sh->chunk - sh->out_nodes), st), "cudaMemsetAsync");
+    if (sh->out_nodes)
+      cuda_check(cudaMemcpyAsync(own, node_x, row * sh->out_nodes, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
+    cuda_check(cudaEventRecord(sh->ev[0], st), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(cs, sh->ev[0], 0), "cudaStreamWaitEvent");
+    nccl_check(nccl().allGather(own, all.p, static_cast<std::size_t>(sh->chunk) * dx, nccl_type(dtype),
+                                static_cast<ncclComm_t>(comm), cs), "ncclAllGather");
+    cuda_check(cudaEventRecord(sh->ev[1], cs), "cudaEventRecord");
+    char* z = static_cast<char*>(node_z);
+    auto rows = [&](std::int64_t r0, std::int64_t r1) {
+      if (r0 < r1)
+        rc_check(cgf_conv_forward_shard(plan, dtype, r1 - r0, sh->in_nodes, sh->edges, rp + r0, nb, all.p, edge_y,
+                                        edge_w, z + es * dz * r0, mode, stream));
+    };
+    rows(sh->la, sh->lb);
+    cuda_check(cudaStreamWaitEvent(st, sh->ev[1], 0), "cudaStreamWaitEvent");
+    rows(0, sh->la);
+    rows(sh->lb, sh->out_nodes);
   });
 }
 
@@ -306,11 +375,47 @@ int cgf_dist_conv_backward(cgf_plan* plan, int dtype, const cgf_conv_shard* sh, 
     DevScratch pad(es * dx * sh->chunk, stream), all(es * dx * sh->in_nodes, stream),
         part(es * dx * sh->in_nodes, stream);
     all_gather(sh, dtype, comm, node_x, dx, all.p, pad, stream);
-    rc_check(cgf_conv_backward_shard(plan, dtype, sh->out_nodes, sh->in_nodes, sh->edges,
-                                     static_cast<const int64_t*>(sh->t_row_ptr), static_cast<const int32_t*>(sh->t_src),
-                                     static_cast<const int32_t*>(sh->t_eid), all.p, edge_y, edge_w, g_node_z, part.p,
-                                     g_edge_y, g_edge_w, mode, stream));
-    ordered_reduce(sh, dtype, comm, part.p, dx, g_node_x, stream);
+    const auto trp = static_cast<const int64_t*>(sh->t_row_ptr);
+    const auto tsrc = static_cast<const int32_t*>(sh->t_src);
+    const auto teid = static_cast<const int32_t*>(sh->t_eid);
+    if (!overlap_on(sh, mode) || sh->oa >= sh->ob) {
+      rc_check(cgf_conv_backward_shard(plan, dtype, sh->out_nodes, sh->in_nodes, sh->edges, trp, tsrc, teid, all.p,
+                                       edge_y, edge_w, g_node_z, part.p, g_edge_y, g_edge_w, mode, stream));
+      ordered_reduce(sh, dtype, comm, part.p, dx, g_node_x, stream);
+      return;
+    }
+    // other ranks' neighbour rows first; their partials travel (comm stream)
+    // while the own rows run; then the rank-ordered sum, as ordered_reduce
+    cudaStream_t st = static_cast<cudaStream_t>(stream), cs = sh->comm_stream;
+    const std::size_t row = es * dx, block = row * static_cast<std::size_t>(sh->chunk);
+    auto rows = [&](std::int64_t r0, std::int64_t r1) {
+      if (r0 < r1)
+        rc_check(cgf_conv_backward_shard(plan, dtype, sh->out_nodes, r1 - r0, sh->edges, trp + r0, tsrc, teid,
+                                         all.c() + row * r0, edge_y, edge_w, g_node_z, part.c() + row * r0, g_edge_y,
+                                         g_edge_w, mode, stream));
+    };
+    rows(0, sh->oa);
+    rows(sh->ob, sh->in_nodes);
+    DevScratch parts(block * sh->world, stream);
+    cuda_check(cudaEventRecord(sh->ev[0], st), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(cs, sh->ev[0], 0), "cudaStreamWaitEvent");
+    const auto& n = nccl();
+    nccl_check(n.groupStart(), "ncclGroupStart");
+    for (int r = 0; r < sh->world; ++r) {
+      if (r == sh->rank) continue;
+      nccl_check(n.send(part.c() + block * r, block / es, nccl_type(dtype), r, static_cast<ncclComm_t>(comm), cs),
+                 "ncclSend");
+      nccl_check(n.recv(parts.c() + block * r, block / es, nccl_type(dtype), r, static_cast<ncclComm_t>(comm), cs),
+                 "ncclRecv");
+    }
+    nccl_check(n.groupEnd(), "ncclGroupEnd");
+    cuda_check(cudaEventRecord(sh->ev[1], cs), "cudaEventRecord");
+    rows(sh->oa, sh->ob);
+    cuda_check(cudaMemcpyAsync(parts.c() + block * sh->rank, part.c() + block * sh->rank, block,
+                               cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
+    cuda_check(cudaStreamWaitEvent(st, sh->ev[1], 0), "cudaStreamWaitEvent");
+    cgf::gops::column_sum(dtype == CGF_F64, parts.p, sh->world, static_cast<std::int64_t>(sh->out_nodes) * dx,
+                          g_node_x, false, stream, static_cast<std::int64_t>(sh->chunk) * dx);
   });
 }
 

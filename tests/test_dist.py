@@ -101,6 +101,7 @@ class OracleShardConv:
 
     def __init__(self, js):
         self.o = O.Oracle(js)
+        self.calls = []
 
     def _graph(self, sh):
         src = np.repeat(np.arange(sh.out_nodes), np.diff(sh.row_ptr))
@@ -111,14 +112,32 @@ class OracleShardConv:
         out[:a.shape[0]] = a
         return out
 
-    def forward_shard(self, sh, x_all, ey, ew, mode=0):
+    def forward_shard(self, sh, x_all, ey, ew, mode=0, rows=None, out=None):
         z = self.o.conv_forward(self._graph(sh), x_all.numpy(), ey.numpy(), ew.numpy())
-        return torch.from_numpy(np.ascontiguousarray(z[:sh.out_nodes]))
+        z = torch.from_numpy(np.ascontiguousarray(z[:sh.out_nodes]))
+        if rows is None:
+            return z
+        self.calls.append(("fwd", tuple(rows)))
+        out = torch.full_like(z, float("nan")) if out is None else out  # rows never written stay NaN
+        out[rows[0]:rows[1]] = z[rows[0]:rows[1]]
+        return out
 
-    def backward_shard(self, sh, x_all, ey, ew, gz, mode=0):
+    def backward_shard(self, sh, x_all, ey, ew, gz, mode=0, rows=None, outs=None):
         gzp = self._pad(gz.numpy(), sh.in_nodes)
         gx, gy, gw = self.o.conv_backward(self._graph(sh), x_all.numpy(), ey.numpy(), ew.numpy(), gzp)
-        return tuple(torch.from_numpy(np.ascontiguousarray(a)) for a in (gx, gy, gw))
+        full = tuple(torch.from_numpy(np.ascontiguousarray(a)) for a in (gx, gy, gw))
+        if rows is None:
+            return full
+        # the kernel contract: neighbour rows [r0, r1) write their g_node_x rows
+        # and the g_edge_y / g_edge_w of the edges whose neighbour they are
+        self.calls.append(("bwd", tuple(rows)))
+        outs = tuple(torch.full_like(a, float("nan")) for a in full) if outs is None else outs
+        r0, r1 = rows
+        outs[0][r0:r1] = full[0][r0:r1]
+        sel = torch.from_numpy((sh.nbr >= r0) & (sh.nbr < r1))
+        outs[1][sel] = full[1][sel]
+        outs[2][sel] = full[2][sel]
+        return outs
 
     def double_backward_shard(self, sh, x_all, ey, ew, gz, dgx_all, dgy, dgw, mode=0):
         gzp = self._pad(gz.numpy(), sh.in_nodes)
@@ -140,7 +159,7 @@ def _inputs(o, g, dt=np.float64):
     return nx, ey, ew, gnz, dgx, dgy, dgw
 
 
-def _rank_main(rank, world, port, js, outdir):
+def _rank_main(rank, world, port, js, outdir, overlap=True):
     import torch.distributed as tdist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     tdist.init_process_group("gloo", rank=rank, world_size=world)
@@ -150,7 +169,8 @@ def _rank_main(rank, world, port, js, outdir):
         o = O.Oracle(js)
         g = p.Graph(og.nodes, og.src, og.nbr)
         sh = dist.GraphShard(g, world, rank)
-        dc = dist.DistConvPlan(None, sh, local=OracleShardConv(js))
+        local = OracleShardConv(js)
+        dc = dist.DistConvPlan(None, sh, local=local, overlap=overlap)
         nx, ey, ew, gnz, dgx, dgy, dgw = _inputs(o, og)
         n0, n1 = sh.node0, sh.node0 + sh.out_nodes
         e0, e1 = sh.edge0, sh.edge0 + sh.edges
@@ -159,8 +179,9 @@ def _rank_main(rank, world, port, js, outdir):
         gx, gy, gw = dc.backward(T(nx[n0:n1]), T(ey[e0:e1]), T(ew[e0:e1]), T(gnz[n0:n1]))
         ox, oy, ow, ogz = dc.double_backward(T(nx[n0:n1]), T(ey[e0:e1]), T(ew[e0:e1]), T(gnz[n0:n1]),
                                              (T(dgx[n0:n1]), T(dgy[e0:e1]), T(dgw[e0:e1])))
-        np.savez(os.path.join(outdir, f"r{rank}.npz"), n0=n0, n1=n1, e0=e0, e1=e1, z=z.numpy(), gx=gx.numpy(),
-                 gy=gy.numpy(), gw=gw.numpy(), ox=ox.numpy(), oy=oy.numpy(), ow=ow.numpy(), ogz=ogz.numpy())
+        np.savez(os.path.join(outdir, f"r{rank}_{int(overlap)}.npz"), n0=n0, n1=n1, e0=e0, e1=e1, z=z.numpy(),
+                 gx=gx.numpy(), gy=gy.numpy(), gw=gw.numpy(), ox=ox.numpy(), oy=oy.numpy(), ow=ow.numpy(),
+                 ogz=ogz.numpy(), calls=np.array([c[0] + str(c[1]) for c in local.calls] or [""]))
     finally:
         tdist.destroy_process_group()
 
@@ -173,11 +194,12 @@ def _free_port():
     return port
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_distributed_conv_matches_whole_graph(world, tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("overlap", [False, True])
+def test_gloo_distributed_conv_matches_whole_graph(world, overlap, tmp_path):
     import torch.multiprocessing as mp
     js = config("c1")
-    mp.spawn(_rank_main, args=(world, _free_port(), js, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_rank_main, args=(world, _free_port(), js, str(tmp_path), overlap), nprocs=world, join=True)
     og = small_graph()
     o = O.Oracle(js)
     nx, ey, ew, gnz, dgx, dgy, dgw = _inputs(o, og)
@@ -185,10 +207,14 @@ def test_gloo_distributed_conv_matches_whole_graph(world, tmp_path):
     want_b = o.conv_backward(og, nx, ey, ew, gnz)
     want_d = o.conv_double_backward(og, nx, ey, ew, gnz, dgx, dgy, dgw)
     got = {k: [] for k in ("z", "gx", "gy", "gw", "ox", "oy", "ow", "ogz")}
+    calls = []
     for r in range(world):
-        d = np.load(tmp_path / f"r{r}.npz")
+        d = np.load(tmp_path / f"r{r}_{int(overlap)}.npz")
         for k in got:
             got[k].append(d[k])
+        calls += [c for c in d["calls"].tolist() if c]
+    # the overlapped path really splits: row-range forward and backward launches
+    assert (any(c.startswith("fwd") for c in calls) and any(c.startswith("bwd") for c in calls)) == overlap
     cat = {k: np.concatenate(v) for k, v in got.items()}
     for k, want in (("z", want_z), ("gx", want_b[0]), ("gy", want_b[1]), ("gw", want_b[2]), ("ox", want_d[0]),
                     ("oy", want_d[1]), ("ow", want_d[2]), ("ogz", want_d[3])):

@@ -93,12 +93,110 @@ def test_sharded_conv_equals_whole_graph(cname, world, dt, mode):
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64], ids=["f32", "f64"])
-def test_cabi_multi_gpu_conv_world1(dt):
+@pytest.mark.parametrize("cname", ["c1", "c2"])
+def test_row_range_shard_calls_bitwise(cname, dt):
+    """The row-range shard launches the overlapped multi-GPU path makes
+    (dist.DistConvPlan: local-neighbour rows during the all-gather, the rest
+    after; other ranks' neighbour rows before the exchange, own rows during it)
+    reproduce one whole-shard launch bit for bit, for the ranges the shard
+    computes and for arbitrary 4-aligned splits."""
+    import paper_2501_13986_b200 as p
+    from paper_2501_13986_b200 import dist
+    js = config(cname)
+    o = O.Oracle(js)
+    n, src, nbr = dist.lattice_radius_graph(7, 1.0, 1.8)
+    og = O.make_graph(n, src, nbr)
+    g = p.Graph(n, src, nbr)
+    nx, ey, ew, gnz, _, _, _ = _inputs(o, og, dt)
+    cp = p.ConvPlan(p.TpPlan(js))
+    D = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    world = 3
+    shards = [dist.GraphShard(g, world, r) for r in range(world)]
+    chunk = shards[0].chunk
+    x_all = np.zeros((world * chunk, o.dim_x), dt)
+    for s in shards:
+        x_all[s.rank * chunk:s.rank * chunk + s.out_nodes] = nx[s.node0:s.node0 + s.out_nodes]
+    x_all = D(x_all)
+    for s in shards:
+        n0, n1, e0, e1 = s.node0, s.node0 + s.out_nodes, s.edge0, s.edge0 + s.edges
+        y, w, gz = D(ey[e0:e1]), D(ew[e0:e1]), D(gnz[n0:n1])
+        z_ref = cp.forward_shard(s, x_all, y, w)
+        b_ref = cp.backward_shard(s, x_all, y, w, gz)
+        a, b = s.local_rows()
+        for cuts in ([0, a, b, s.out_nodes], [0, 8, 20, s.out_nodes], [0, s.out_nodes]):
+            cuts = sorted(set(min(c, s.out_nodes) for c in cuts))
+            z = None
+            for r0, r1 in zip(cuts, cuts[1:]):
+                z = cp.forward_shard(s, x_all, y, w, rows=(r0, r1), out=z)
+            assert torch.equal(z, z_ref), (s.rank, cuts)
+        a, b = s.own_rows()
+        for order in ([(0, a), (b, s.in_nodes), (a, b)], [(0, 12), (12, s.in_nodes)]):
+            outs = None
+            for r0, r1 in order:
+                outs = cp.backward_shard(s, x_all, y, w, gz, rows=(r0, r1), outs=outs)
+            for got, want in zip(outs, b_ref):
+                assert torch.equal(got, want), (s.rank, order)
+    s = shards[0]
+    with pytest.raises(p.ShapeError):
+        cp.forward_shard(s, x_all, D(ey[:s.edges]), D(ew[:s.edges]), rows=(2, 5))  # unaligned start
+    with pytest.raises(p.ShapeError):
+        cp.forward_shard(s, x_all, D(ey[:s.edges]), D(ew[:s.edges]), rows=(0, s.out_nodes + 1))
+
+
+def test_overlapped_dist_conv_plan_nccl_one_rank():
+    """DistConvPlan's overlapped path (in-place async all-gather, row-range
+    launches on both sides of work.wait(), own-row backward during the
+    exchange, rank-ordered sum) forced on a 1-rank NCCL process group: the same
+    torch.distributed calls and streams as at N > 1, bit-identical to the
+    whole-graph ConvPlan."""
+    import os
+    import socket
+
+    import torch.distributed as tdist
+
+    import paper_2501_13986_b200 as p
+    from paper_2501_13986_b200 import dist
+    if tdist.is_initialized():
+        pytest.skip("a process group already exists in this process")
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        js = config("c1")
+        o = O.Oracle(js)
+        n, src, nbr = dist.lattice_radius_graph(7, 1.0, 1.8)
+        og = O.make_graph(n, src, nbr)
+        g = p.Graph(n, src, nbr)
+        D = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        nx, ey, ew, gnz, _, _, _ = (D(a) for a in _inputs(o, og, np.float32))
+        plan = p.TpPlan(js)
+        sh = dist.GraphShard(g, 1, 0)
+        assert sh.local_rows()[1] > 0 and sh.own_rows()[1] > 0
+        dc = dist.DistConvPlan(plan, sh, overlap="force")
+        assert dc.overlap
+        cp = p.ConvPlan(plan)
+        z, x_all = dc.forward_gathered(nx, ey, ew)
+        assert torch.equal(z, cp.forward(g, nx, ey, ew))
+        for a, b in zip(dc.backward(nx, ey, ew, gnz, node_x_all=x_all), cp.backward(g, nx, ey, ew, gnz)):
+            assert torch.equal(a, b)
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("overlap", ["0", "force"])
+@pytest.mark.parametrize("dt", [np.float32, np.float64], ids=["f32", "f64"])
+def test_cabi_multi_gpu_conv_world1(dt, overlap, monkeypatch):
     """The C ABI's multi-GPU conv (cgf_dist_conv_*, NCCL inside libcgf) on a
     1-rank communicator: partition, padded all-gather, all-to-all reduction and
     the ordered sum run for real; results equal the whole-graph ConvPlan
     bitwise (one rank: the same kernels on the same rows). The shard layout
-    matches dist.GraphShard's for 3 ranks."""
+    matches dist.GraphShard's for 3 ranks. overlap="force": the overlapped
+    scheme (in-place all-gather on the shard's comm stream during the
+    local-neighbour rows, own rows during the exchange) on the one rank."""
+    monkeypatch.setenv("CGF_DIST_OVERLAP", overlap)
     import paper_2501_13986_b200 as p
     from paper_2501_13986_b200 import dist
     js = config("c1")
