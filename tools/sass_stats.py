@@ -17,7 +17,7 @@ import tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-KEY = ("FFMA", "FMUL", "FADD", "DFMA", "DMUL", "DADD", "LDS", "STS", "LDG", "STG", "LDGSTS", "UBLKCP", "UTMALDG",
+KEY = ("FFMA", "FFMA2", "FMUL", "FMUL2", "FADD", "DFMA", "DMUL", "DADD", "LDS", "STS", "LDG", "STG", "LDGSTS", "UBLKCP", "UTMALDG",
        "UTMASTG", "UTCHMMA", "UTCQMMA", "UTCMMA", "LDTM", "STTM", "SYNCS", "RED", "ATOM", "BRA", "SHFL")
 
 
