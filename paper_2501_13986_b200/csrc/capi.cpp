@@ -191,14 +191,18 @@ std::vector<std::pair<int, int>> unit_groups(const cgf_plan* p, int n) {
   return out;
 }
 
+// variant 1: the ConvEdges backward writing g_node_x as per-edge partial rows
+// (the row-order conv backward, conv_backward_row_order)
 std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype,
-                                              int w_shared, int aligned, int group = 0, int ngroups = 1) {
+                                              int w_shared, int aligned, int group = 0, int ngroups = 1,
+                                              int variant = 0) {
   if (dtype != CGF_F32 && dtype != CGF_F64) throw std::invalid_argument("bad dtype");
   std::lock_guard<std::mutex> g(p->mu);
   const char* env = std::getenv("CGF_GEN");
   const std::string flags = env ? env : "";
   const auto key = std::make_tuple(static_cast<int>(comp), static_cast<int>(loop), dtype, w_shared ? 1 : 0,
-                                   aligned ? 1 : 0, flags + "|" + std::to_string(group) + "/" + std::to_string(ngroups));
+                                   aligned ? 1 : 0, flags + "|" + std::to_string(group) + "/" + std::to_string(ngroups) +
+                                                        "|v" + std::to_string(variant));
   auto it = p->sources.find(key);
   if (it != p->sources.end()) return it->second;
   if (w_shared && loop != cgf::Loop::Rows) throw cgf::UnsupportedError("shared weights: batched TP only");
@@ -208,6 +212,7 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   cfg.f64 = dtype == CGF_F64;
   cfg.w_shared = w_shared != 0;
   cfg.aligned = aligned != 0;
+  cfg.edge_partials = variant == 1;
   // Batched fwd / bwd keep y in registers (prefetched a row ahead); the
   // double-backward needs those registers for its three z' accumulators.
   // FP64 backward reads y from the slot instead: the 2 x dim_y doubles of
@@ -366,13 +371,14 @@ struct Args {
   std::int64_t edges = 0;
 };
 
-void run_kernel(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype, int w_shared, const Args& a, void* stream) {
+void run_kernel(cgf_plan* p, cgf::Comp comp, cgf::Loop loop, int dtype, int w_shared, const Args& a, void* stream,
+                int variant = 0) {
   const std::int64_t items = loop == cgf::Loop::ConvEdges ? a.edges : a.rows;
   if (items <= 0) return;
   const bool al = aligned16({a.x, a.y, a.w, a.gz, a.da, a.db, a.dc, a.o0, a.o1, a.o2, a.o3});
   const int ng = kernel_groups(p, comp, loop, dtype);
   for (int grp = 0; grp < ng; ++grp) {
-    const auto ks = source_for(p, comp, loop, dtype, w_shared, al, grp, ng);
+    const auto ks = source_for(p, comp, loop, dtype, w_shared, al, grp, ng, variant);
     const cgf::Kernel k = cgf::load_kernel(*ks);
     const int warps = k.threads / 32;
     const std::int64_t need = (items + warps - 1) / warps;
@@ -772,6 +778,52 @@ void atomic_transposed(cgf_plan* p, int dtype, cgf::Comp comp, std::int64_t out_
   a.o0 = o0; a.o1 = o1; a.o2 = o2; a.o3 = o3;
   conv_atomic(p, dtype, comp, out_nodes, in_nodes, edges, el.as<std::int32_t>(), el.as<std::int32_t>() + edges, a,
               stream);
+}
+
+// Conv backward traversal ("beware the g_node_z gather"). By
+// neighbour (default kernel, transposed CSR): each edge gathers g_node_z[s]
+// (dim_z words) and g_node_x[d] is summed in the warp. Row order: the edges in
+// CSR order (consecutive edges share s, so g_node_z[s] is re-read from cache),
+// g_node_x as per-edge partial rows (2 dim_x words of extra DRAM traffic per
+// edge: written, read back) and a segmented sum over the transposed CSR.
+// Chooser (whole-graph calls): CGF_CONV_BWD=row | nbr, else by neighbour. The
+// traffic model favours row order whenever dim_z > 2 dim_x (C4: 9,088 vs 2,304
+// words per edge; C5: 1,632 vs 576), but the kernels are issue-bound and the
+// per-(edge, unit) ConvEdges kernel measured 3.3x (C4 FP32) to 23x (C5 FP32)
+// slower than the by-neighbour one (profiles/r02_ab_rowbwd.jsonl), so the
+// measured default is by neighbour for every problem.
+bool conv_bwd_row_order(const cgf_plan* p, int dtype) {
+  (void)p; (void)dtype;
+  const char* e = std::getenv("CGF_CONV_BWD");
+  return e && std::strcmp(e, "row") == 0;
+}
+
+// Whole graph only (cgf_conv_backward): src / nbr per edge in CSR order.
+void conv_backward_row_order(cgf_plan* p, int dtype, std::int64_t nodes, std::int64_t edges,
+                             const std::int64_t* row_ptr, const std::int32_t* nbr, const std::int64_t* t_row_ptr,
+                             const std::int32_t* t_eid, const void* x, const void* y, const void* w, const void* gz,
+                             void* gx, void* gy, void* gw, void* stream) {
+  const std::size_t es = dtype == CGF_F64 ? 8 : 4;
+  const auto& pr = p->problem;
+  if (nodes == 0) return;
+  if (edges == 0) {
+    memzero(gx, es * nodes * pr.dim_x, stream);
+    return;
+  }
+  need(x, "node_x"); need(nbr, "nbr"); need(y, "edge_y"); need(w, "edge_w"); need(gz, "g_node_z");
+  need(t_row_ptr, "t_row_ptr"); need(t_eid, "t_eid"); need(gy, "g_edge_y"); need(gw, "g_edge_w"); need(gx, "g_node_x");
+  const CsrSrc src(row_ptr, nodes, edges, stream);
+  Scratch part(es * edges * pr.dim_x, stream);
+  if (!p->x_covered) memzero(part.ptr, es * edges * pr.dim_x, stream);
+  Args a;
+  a.x = x; a.y = y; a.w = w; a.gz = gz;
+  a.o0 = part.ptr; a.o1 = gy; a.o2 = gw;
+  a.rows = nodes;
+  a.edges = edges;
+  a.eid = src.get();
+  a.nb = nbr;
+  run_kernel(p, cgf::Comp::Bwd, cgf::Loop::ConvEdges, dtype, 0, a, stream, 1);
+  cgf::gops::segment_sum(dtype == CGF_F64, part.ptr, t_row_ptr, t_eid, gx, nodes, pr.dim_x, stream);
 }
 
 // Unfused comparator (conv.cpp:530-616): gather x per edge, batched TP over
@@ -1481,6 +1533,12 @@ int cgf_conv_backward(cgf_plan* p, int dtype, int64_t nodes, int64_t edges, cons
       if (cgf_conv_backward_atomic(p, dtype, nodes, edges, src.get(), nbr, node_x, edge_y, edge_w, g_node_z, g_node_x,
                                    g_edge_y, g_edge_w, stream) != CGF_OK)
         throw std::runtime_error(g_err);
+    });
+  if (mode == CGF_CONV_DETERMINISTIC && conv_bwd_row_order(p, dtype))
+    return guarded([&] {
+      need(p, "plan");
+      conv_backward_row_order(p, dtype, nodes, edges, row_ptr, nbr, t_row_ptr, t_eid, node_x, edge_y, edge_w, g_node_z,
+                              g_node_x, g_edge_y, g_edge_w, stream);
     });
   return cgf_conv_backward_shard(p, dtype, nodes, nodes, edges, t_row_ptr, t_out, t_eid, node_x, edge_y, edge_w,
                                  g_node_z, g_node_x, g_edge_y, g_edge_w, mode, stream);

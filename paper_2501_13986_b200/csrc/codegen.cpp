@@ -1152,8 +1152,8 @@ void Gen::emit_rows_loop() {
       if (out_x())
         for (int c : x_done[q]) {
           const auto& xc = u.x_chunks[c];
-          emit_store("O0", edges() ? "nbr" : "row", p_.dim_x, xc.off, C.xstep[c], xc.words, xb[xc.off],
-                     xdx[xc.off], "ax" + S(c), edges());
+          emit_store("O0", edges() ? (cfg_.edge_partials ? "eid" : "nbr") : "row", p_.dim_x, xc.off, C.xstep[c],
+                     xc.words, xb[xc.off], xdx[xc.off], "ax" + S(c), edges() && !cfg_.edge_partials);
         }
       if (out_z())
         for (int z : z_done[q]) {
@@ -1485,6 +1485,7 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "noffma2") cfg.ffma2 = false;
     else if (k == "waitsleep") cfg.wait_sleep = true;
     else if (k == "nowaitsleep") cfg.wait_sleep = false;
+    else if (k == "edgepart") cfg.edge_partials = true;
     else if (k == "l2hint") cfg.l2_hints = true;
     else if (k == "nol2hint") cfg.l2_hints = false;
     else if (k == "xregs") cfg.x_regs = true;

@@ -304,3 +304,33 @@ def test_multi_edge_items_match_oracle(name, dt, epi, monkeypatch):
     outs = cp.double_backward(g, dev(nx), dev(ey), dev(ew), dev(gnz), (dev(dgx), dev(dgy), dev(dgw)))
     want = o.conv_double_backward(og, nx, ey, ew, gnz, dgx, dgy, dgw)
     check(host(outs[3]), want[3], dt, f"EB={epi} double-backward dgz")
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f32", "f64"])
+@pytest.mark.parametrize("gname", ["lat4", "ragged5"])
+@pytest.mark.parametrize("name", ["paper", "c1", "c2"])
+def test_row_order_backward_matches_oracle(name, gname, dt, monkeypatch):
+    """The row-order conv backward (CGF_CONV_BWD=row: edges in CSR order, per-edge
+    g_node_x partial rows, segmented sum over the transposed CSR) against the
+    oracle; deterministic (two calls bitwise equal), and a single edge is still
+    one TP bit for bit."""
+    monkeypatch.setenv("CGF_CONV_BWD", "row")
+    js = config(name)
+    og = graphs()[gname]
+    o, pkg = O.Oracle(js), P()
+    plan = pkg.TpPlan(js)
+    cp = pkg.ConvPlan(plan)
+    g = pkg.Graph(og.nodes, og.src, og.nbr)
+    nx, ey, ew, gnz, *_ = conv_inputs(o, og, dt)
+    args = (dev(nx), dev(ey), dev(ew), dev(gnz))
+    outs = cp.backward(g, *args)
+    for a, b, n in zip(outs, o.conv_backward(og, nx, ey, ew, gnz), ("g_node_x", "g_edge_y", "g_edge_w")):
+        check(host(a), b, dt, n)
+    for a, b in zip(outs, cp.backward(g, *args)):
+        assert torch.equal(a, b)
+    g1 = pkg.Graph(2, [0], [1])
+    x1 = dev(nx[:2])
+    gx, gy, gw = cp.backward(g1, x1, dev(ey[:1]), dev(ew[:1]), dev(gnz[:2]))
+    tx, ty, tw = plan.backward(x1[1:2], dev(ey[:1]), dev(ew[:1]), dev(gnz[0:1]))
+    assert torch.equal(gx[1], tx[0]) and torch.equal(gy, ty) and torch.equal(gw, tw)
+    assert not gx[0].any()
