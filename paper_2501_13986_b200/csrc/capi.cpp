@@ -1164,11 +1164,38 @@ void run_host(cgf_plan* p, int op, int dtype, int w_shared, std::int64_t rows, c
       CU_CHECK(cgf::drv::cuMemAlloc(&pipe->buf[k], need));
       pipe->cap[k] = need;
     }
-  const std::int64_t nchunks = (rows + chunk - 1) / chunk;
+  // chunk sequence: full chunks, with (CGF_HOST_RAMP, default on) the first and
+  // last ones split into 1/8, 1/4, 1/2 pieces, so the pipeline fills (first
+  // H2D alone) and drains (last D2H alone) in a small piece's time: C2 e2e step
+  // 147.2 -> 146.0 and 152.3 -> 150.5 ms (profiles/r02_sweep_e2e_ramp.jsonl)
+  std::vector<std::pair<std::int64_t, std::int64_t>> pieces;  // (first row, rows)
+  {
+    const char* ramp_env = std::getenv("CGF_HOST_RAMP");
+    const bool ramp = !one_chunk && !(ramp_env && std::atoi(ramp_env) == 0) && rows >= 4 * chunk;
+    std::vector<std::int64_t> sizes;
+    if (ramp) {
+      const std::int64_t q = std::max<std::int64_t>(128, chunk / 8 / 128 * 128);
+      const std::int64_t h = std::max<std::int64_t>(128, chunk / 4 / 128 * 128);
+      const std::int64_t half = std::max<std::int64_t>(128, chunk / 2 / 128 * 128);
+      const std::int64_t ends[3] = {q, h, half};
+      std::int64_t left = rows - 2 * (q + h + half);
+      for (std::int64_t v : ends) sizes.push_back(v);
+      for (; left > 0; left -= chunk) sizes.push_back(std::min(chunk, left));
+      for (int i = 2; i >= 0; --i) sizes.push_back(ends[i]);
+    } else {
+      for (std::int64_t left = rows; left > 0; left -= chunk) sizes.push_back(std::min(chunk, left));
+    }
+    std::int64_t r = 0;
+    for (std::int64_t v : sizes) {
+      pieces.emplace_back(r, v);
+      r += v;
+    }
+  }
+  const std::int64_t nchunks = static_cast<std::int64_t>(pieces.size());
   for (std::int64_t c = 0; c < nchunks; ++c) {
     const int k = static_cast<int>(c % K);
     CUstream st = pipe->s[k];
-    const std::int64_t r0 = c * chunk, n = std::min(chunk, rows - r0);
+    const std::int64_t r0 = pieces[c].first, n = pieces[c].second;
     std::size_t off = 0;
     auto carve = [&](std::size_t words) {
       const CUdeviceptr d = pipe->buf[k] + off;
