@@ -236,3 +236,23 @@ def test_forward_backward_host_entry_matches_separate_calls():
     o = O.Oracle(js)
     s = np.array([0, 1, rows // 2, rows - 1])
     check(z[s], o.forward(x[s], y[s], w[s]), np.float32, "fused host entry z")
+
+
+@pytest.mark.parametrize("ramp", ["0", "1"])
+def test_host_pipeline_chunking_is_bitwise_neutral(ramp, monkeypatch):
+    """The host path's chunking (1024-row chunks here, CGF_HOST_CHUNK_MB=1; with
+    CGF_HOST_RAMP the first / last chunks split into 1/8, 1/4, 1/2 pieces)
+    changes nothing: forward_backward on host arrays equals the device calls
+    bitwise (C1 FP32, 10,000 rows, a ragged last chunk)."""
+    monkeypatch.setenv("CGF_HOST_CHUNK_MB", "1")
+    monkeypatch.setenv("CGF_HOST_RAMP", ramp)
+    plan = P().TpPlan(config("c1"))
+    rows = 10_000
+    rng = np.random.default_rng(9)
+    x, y, w, gz = (rng.standard_normal((rows, d)).astype(np.float32)
+                   for d in (plan.dim_x, plan.dim_y, plan.n_w, plan.dim_z))
+    got = plan.forward_backward(x, y, w, gz)
+    D = lambda a: torch.from_numpy(a).cuda()
+    want = (plan.forward(D(x), D(y), D(w)),) + tuple(plan.backward(D(x), D(y), D(w), D(gz)))
+    for a, b, n in zip(got, want, ("z", "gx", "gy", "gw")):
+        assert np.array_equal(a, host(b)), n
