@@ -285,6 +285,10 @@ DEVI void prod_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 // element (row r of the operand, K index k) of a K-major SW64 tile whose K
 // runs over the 128 batch rows: 16-row K blocks 4 KB apart (64 operand rows)
 DEVI u32 kmaj_rows(int r, int k) { return (u32)((k >> 4) * 4096 + sw64(r, (k & 15) >> 2) + (k & 3) * 4); }
+// the same element of a K-major SW128 tile of 32 batch rows (one 128-byte line
+// per operand row, 16-byte chunks XOR the row's index in its 8-row atom): 32
+// lanes holding consecutive K of one operand row store 128 contiguous bytes
+DEVI u32 kmaj128(int r, int k) { return (u32)((r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) ^ r) & 7) << 4) + (k & 3) * 4); }
 )";
 }
 
@@ -334,15 +338,20 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
       segs.push_back({sq.z_off, sq.dz()});
     }
   const int gz_bytes = 2 * kTileRows * 64 * 4;
-  const int nx = std::getenv("CGF_UVW_GY_NX") ? std::atoi(std::getenv("CGF_UVW_GY_NX")) : 3;
-  const int smem = 1024 + gz_bytes + nx * g.xslot + 4 * g.wslot + 1024 + 128 * p.dim_y * 4;
+  // gz_k tiles move as halves (32 r: hi + lo, 32 KB) through a ring of NGH
+  // stages, so the loader runs ahead of the MMAs (one whole-tile buffer left
+  // every k's TMA latency exposed): 3.71 -> 2.99 ms with 3 stages and a
+  // 2-tile x ring (profiles/r02_ab_gy.txt)
+  const int ngh = std::getenv("CGF_UVW_GY_NGH") ? std::clamp(std::atoi(std::getenv("CGF_UVW_GY_NGH")), 2, 6) : 3;
+  const int nx = std::getenv("CGF_UVW_GY_NX") ? std::atoi(std::getenv("CGF_UVW_GY_NX")) : 2;
+  const int smem = 1024 + ngh * (gz_bytes / 2) + nx * g.xslot + 4 * g.wslot + 1024 + 128 * p.dim_y * 4;
   if (smem > 227 * 1024) throw UnsupportedError("uvw gy kernel: shared memory too small");
   std::ostringstream o;
   if (std::getenv("CGF_UVW_DEBUG")) o << "#define CGF_UVW_DEBUG 1\n";
   o << device_runtime_source() << uvw_helpers() << grad_helpers();
   o << "// uvw gy: " << np << " instructions, " << nplanes << " gz planes\n#define DIMX " << p.dim_x << "\n#define DIMY "
     << p.dim_y << "\n#define DIMZ " << p.dim_z << "\n#define NP " << np << "\n#define WSLOT " << g.wslot
-    << "\n#define XSLOT " << g.xslot << "\n#define GZB " << gz_bytes << "\n#define NX " << nx << "\n#define NPLANES "
+    << "\n#define XSLOT " << g.xslot << "\n#define GZB " << gz_bytes << "\n#define NGH " << ngh << "\n#define NX " << nx << "\n#define NPLANES "
     << nplanes << "\n";
   emit_grad_tables(o, p);
   {
@@ -428,16 +437,17 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "const __grid_constant__ TMap tx7, const __grid_constant__ TMap tgh, const __grid_constant__ TMap tgl, "
        "const float* __restrict__ Y, const float* __restrict__ WIMG, float* __restrict__ GY, i64 rows) {\n"
     << grad_kernel_head()
-    << "  unsigned char* gzt = sm;                 // gz_k tile [rows][r]: hi [4][128][16], lo after GZB/2 (TMA)\n"
-       "  unsigned char* xs0 = gzt + GZB;          // x tile ring (TMA, SW64)\n"
+    << "  unsigned char* gzt = sm;                 // NGH half tiles of gz_k [rows][32 r]: hi 16 KB, lo 16 KB (TMA)\n"
+       "  unsigned char* xs0 = gzt + NGH * (GZB / 2);  // x tile ring (TMA, SW64)\n"
        "  unsigned char* ws = xs0 + NX * XSLOT;    // W^T images of one instruction (4 r-blocks)\n"
        "  u64* bars = (u64*)(ws + 4 * WSLOT);\n"
-       "  u64* gz_full = bars; u64* gz_empty = bars + 1; u64* gzp_full = bars + 2; u64* gzp_empty = bars + 3;\n"
-       "  u64* w_full = bars + 4; u64* w_empty = bars + 5; u64* x_full = bars + 6; u64* x_empty = bars + 6 + NX;\n"
-       "  u32* tmem_slot = (u32*)(bars + 6 + 2 * NX);\n"
-       "  float* gys = (float*)(bars + 16);\n"
+       "  u64* gz_full = bars; u64* gz_empty = bars + NGH; u64* gzp_full = bars + 2 * NGH; u64* gzp_empty = gzp_full + 1;\n"
+       "  u64* w_full = gzp_empty + 1; u64* w_empty = w_full + 1; u64* x_full = w_empty + 1; u64* x_empty = x_full + NX;\n"
+       "  u32* tmem_slot = (u32*)(x_empty + NX);\n"
+       "  float* gys = (float*)(bars + 32);\n"
        "  if (threadIdx.x == 0) {\n"
-       "    mbar_init(gz_full, 1); mbar_init(gz_empty, 1); mbar_init(gzp_full, 1); mbar_init(gzp_empty, 8);\n"
+       "    for (int i = 0; i < NGH; ++i) { mbar_init(&gz_full[i], 1); mbar_init(&gz_empty[i], 1); }\n"
+       "    mbar_init(gzp_full, 1); mbar_init(gzp_empty, 8);\n"
        "    mbar_init(w_full, 1); mbar_init(w_empty, 1);\n"
        "    for (int i = 0; i < NX; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n"
        "    mbar_fence_init();\n  }\n"
@@ -478,7 +488,7 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "    }\n"
        "  }\n"
        "  else if (warp == 8) {\n"
-       "    const u64 gzh = sdesc128(smem_addr(gzt)), gzl = gzh + (u64)((GZB / 2) >> 4);\n"
+       "    const u64 gzh0 = sdesc128(smem_addr(gzt));\n"
        "    const u64 wd = sdesc64(smem_addr(ws));\n"
        "    const u32 id_gzp = idesc_tf32(64);\n"
        "    u32 ug = 0, uq = 0;\n"
@@ -488,23 +498,28 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "        mbar_wait_t(gzp_empty, (uq & 1u) ^ 1u, 27);\n"
        "        tc_fence_after();\n"
        "        const int dz = P_DZ[q];\n"
-       "        for (int k = 0; k < dz; ++k, ++ug) {\n"
-       "          mbar_wait_t(gz_full, ug & 1u, 26);\n"
-       "          tc_fence_after();\n"
+       "        for (int k = 0; k < dz; ++k) {\n"
        "          const u32 dg = tmem + 64 * k;\n"
-       "          if (elect_one()) {\n"
-       "#pragma unroll\n            for (int s = 0; s < 8; ++s) {\n"
-       // gz (A): SW128 blocks of 32 r (16 KB: 128 rows x 128 B); W^T (B): SW64 blocks of 16
-       "              const u64 ao = (u64)(((s >> 2) * 16384 + (s & 3) * 32) >> 4);\n"
-       "              const u64 bo = (u64)(((s >> 1) * WSLOT + (s & 1) * 32) >> 4);\n"
-       "              tc_mma(dg, gzh + ao, wd + bo, id_gzp, s ? 1u : 0u);\n"
-       "              tc_mma(dg, gzh + ao, wd + bo + (u64)((64 * 64) >> 4), id_gzp, 1u);\n"
-       "              tc_mma(dg, gzl + ao, wd + bo, id_gzp, 1u);\n"
+       "          for (int j = 0; j < 2; ++j, ++ug) {  // r-block j: one half-tile stage\n"
+       "            const u32 hs = ug % NGH;\n"
+       "            mbar_wait_t(&gz_full[hs], (ug / NGH) & 1u, 26);\n"
+       "            tc_fence_after();\n"
+       "            if (elect_one()) {\n"
+       "              const u64 gzh = gzh0 + (u64)((hs * (GZB / 2)) >> 4), gzl = gzh + (u64)((GZB / 4) >> 4);\n"
+       "#pragma unroll\n              for (int t = 0; t < 4; ++t) {\n"
+       // gz (A): SW128, [128 rows][32 r] per half; W^T (B): SW64 blocks of 16
+       "                const int s = 4 * j + t;\n"
+       "                const u64 ao = (u64)((t * 32) >> 4);\n"
+       "                const u64 bo = (u64)(((s >> 1) * WSLOT + (s & 1) * 32) >> 4);\n"
+       "                tc_mma(dg, gzh + ao, wd + bo, id_gzp, s ? 1u : 0u);\n"
+       "                tc_mma(dg, gzh + ao, wd + bo + (u64)((64 * 64) >> 4), id_gzp, 1u);\n"
+       "                tc_mma(dg, gzl + ao, wd + bo, id_gzp, 1u);\n"
+       "              }\n"
+       "              tc_commit(&gz_empty[hs]);\n"
+       "              if (k == dz - 1 && j == 1) { tc_commit(gzp_full); tc_commit(w_empty); }\n"
        "            }\n"
-       "            tc_commit(gz_empty);\n"
-       "            if (k == dz - 1) { tc_commit(gzp_full); tc_commit(w_empty); }\n"
+       "            __syncwarp();\n"
        "          }\n"
-       "          __syncwarp();\n"
        "        }\n"
        "      }\n"
        "    }\n"
@@ -544,14 +559,15 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
        "      u32 ug = 0;\n"
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
        "        for (int q = 0; q < NP; ++q)\n"
-       "          for (int k = 0; k < P_DZ[q]; ++k, ++ug) {\n"
-       "            mbar_wait_t(gz_empty, (ug & 1u) ^ 1u, 31);\n"
-       "            mbar_expect_tx(gz_full, GZB);\n"
-       "            for (int j = 0; j < 2; ++j) {\n"
-       "              tma_load3(gzt + j * 16384, &tgh, 32 * j, (int)(tile * 128), P_PLANE[q] + k, gz_full);\n"
-       "              tma_load3(gzt + GZB / 2 + j * 16384, &tgl, 32 * j, (int)(tile * 128), P_PLANE[q] + k, gz_full);\n"
+       "          for (int k = 0; k < P_DZ[q]; ++k)\n"
+       "            for (int j = 0; j < 2; ++j, ++ug) {\n"
+       "              const u32 hs = ug % NGH;\n"
+       "              unsigned char* d = gzt + hs * (GZB / 2);\n"
+       "              mbar_wait_t(&gz_empty[hs], ((ug / NGH) & 1u) ^ 1u, 31);\n"
+       "              mbar_expect_tx(&gz_full[hs], GZB / 2);\n"
+       "              tma_load3(d, &tgh, 32 * j, (int)(tile * 128), P_PLANE[q] + k, &gz_full[hs]);\n"
+       "              tma_load3(d + GZB / 4, &tgl, 32 * j, (int)(tile * 128), P_PLANE[q] + k, &gz_full[hs]);\n"
        "            }\n"
-       "          }\n"
        "    }\n"
        "    __syncwarp();\n"
        "  }\n"
@@ -596,7 +612,15 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   // buffered so the next instruction's segment lands while this one is used
   // (single-buffered, the producers spent a third of their time waiting on it)
   const int nx = 4;  // x tiles per instruction
-  const int smem = 1024 + 4 * tb + 2 * nx * xslot + 1024;
+  // staging depths: gz^T tiles (the loader runs ahead of the MMAs) and x
+  // segments; with two of each the pass was TMA-latency bound (no MMAs and no
+  // producer math still took 2.0 of 2.7 ms, profiles/r02_ab_gw.txt); 6 gz^T
+  // stages: 2.64 + 2.92 -> 2.20 + 2.34 ms (r02_ab_gw2.txt; more z' stages: no
+  // change, r02_ab_gw3.txt)
+  const int ngz = std::getenv("CGF_UVW_NGZ") ? std::clamp(std::atoi(std::getenv("CGF_UVW_NGZ")), 2, 8) : 6;
+  const int nxb = std::getenv("CGF_UVW_NXB") ? std::clamp(std::atoi(std::getenv("CGF_UVW_NXB")), 2, 4) : 2;
+  const int nzs = std::getenv("CGF_UVW_NZS") ? std::clamp(std::atoi(std::getenv("CGF_UVW_NZS")), 2, 4) : 2;  // z' stages
+  const int smem = 1024 + (ngz + nzs) * tb + nxb * nx * xslot + 1024;
   if (smem > 227 * 1024) throw UnsupportedError("uvw gW kernel: shared memory too small");
   const std::string kname = "cgf_uvw_bwdw" + S(first) + "_f32";
   // gz planes (same numbering as the pre-pass): segment component -> plane
@@ -610,10 +634,12 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
   std::ostringstream o;
   if (std::getenv("CGF_UVW_DEBUG")) o << "#define CGF_UVW_DEBUG 1\n";
   o << device_runtime_source() << uvw_helpers() << grad_helpers();
+  // experiment knobs (A/B only): 16 = no MMAs, 32 = producers skip the z' values
+  o << "#define UVW_EXP " << (std::getenv("CGF_UVW_EXP") ? std::atoi(std::getenv("CGF_UVW_EXP")) : 0) << "\n";
   o << "// uvw gW: instructions [" << first << ", " << first + count << ")\n#define DIMX " << p.dim_x
     << "\n#define DIMY " << p.dim_y << "\n#define DIMZ " << p.dim_z << "\n#define NW_ " << p.n_w << "\n#define Q0 "
     << first << "\n#define Q1 " << first + count << "\n#define XSLOT " << xslot << "\n#define TB " << tb
-    << "\n#define KR " << kRows << "\n#define NX " << nx << "\n";
+    << "\n#define KR " << kRows << "\n#define NX " << nx << "\n#define NGZ " << ngz << "\n#define NXB " << nxb << "\n#define NZS " << nzs << "\n";
   emit_grad_tables(o, p);
   o << "__constant__ int P_PLANE[" << R.size() << "] = {";
   for (size_t q = 0; q < R.size(); ++q) o << (q ? "," : "") << plane_of_seg.at(R[q].z_off);
@@ -645,7 +671,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
         << "        xv[2 * t] = v.x; xv[2 * t + 1] = v.y;\n      }\n"
         << "#pragma unroll\n      for (int c = 0; c < 2; ++c) {\n        float zc = 0.f;\n";
       for (const auto& kv : qk) o << "        zc = fmaf(q" << kv.first << ", xv[c * " << dx << " + " << kv.first << "], zc);\n";
-      o << "        const float h = tf32_hi(zc);\n        const u32 off = kmaj_rows(16 * cb + 2 * sub + c, m);\n"
+      o << "        const float h = tf32_hi(zc);\n        const u32 off = kmaj128(16 * cb + 2 * sub + c, m);\n"
         << "        sts32(zt + off, h); sts32(zt + TB / 2 + off, zc - h);\n      }\n    }\n    break; }\n";
     }
     o << "  }\n}\n\n";
@@ -663,17 +689,17 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "  unsigned char* sm = (unsigned char*)(((unsigned long long)smem_raw + 1023) & ~1023ull);\n"
        "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n"
        "  const i64 ntiles = (rows + KR - 1) / KR;\n"
-       "  unsigned char* gzt = sm;                 // 2 x gz_k^T tile [r][KR rows] K-major: hi, lo after TB/2\n"
-       "  unsigned char* zt = sm + 2 * TB;         // 2 x z'_k^T tile [c][KR rows] K-major\n"
-       "  unsigned char* xs0 = zt + 2 * TB;        // 2 x segments of one instruction: NX tiles each (TMA, SW64)\n"
-       "  u64* bars = (u64*)(xs0 + 2 * NX * XSLOT);\n"
-       "  u64* gz_full = bars; u64* gz_empty = bars + 2; u64* z_full = bars + 4; u64* z_empty = bars + 6;\n"
-       "  u64* x_full = bars + 8; u64* x_empty = bars + 10; u64* done = bars + 12;\n"
+       "  unsigned char* gzt = sm;                 // NGZ x gz_k^T tile [r][KR rows] K-major: hi, lo after TB/2\n"
+       "  unsigned char* zt = sm + NGZ * TB;       // NZS x z'_k^T tile [c][KR rows] K-major\n"
+       "  unsigned char* xs0 = zt + NZS * TB;      // NXB x segments of one instruction: NX tiles each (TMA, SW64)\n"
+       "  u64* bars = (u64*)(xs0 + NXB * NX * XSLOT);\n"
+       "  u64* gz_full = bars; u64* gz_empty = bars + NGZ; u64* z_full = gz_empty + NGZ; u64* z_empty = z_full + NZS;\n"
+       "  u64* x_full = z_empty + NZS; u64* x_empty = x_full + NXB; u64* done = x_empty + NXB;\n"
        "  u32* tmem_slot = (u32*)(done + 1);\n"
        "  if (threadIdx.x == 0) {\n"
-       "    for (int i = 0; i < 2; ++i) {\n"
-       "      mbar_init(&gz_full[i], 1); mbar_init(&gz_empty[i], 1); mbar_init(&z_full[i], 8); mbar_init(&z_empty[i], 1);\n    }\n"
-       "    for (int i = 0; i < 2; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n"
+       "    for (int i = 0; i < NGZ; ++i) { mbar_init(&gz_full[i], 1); mbar_init(&gz_empty[i], 1); }\n"
+       "    for (int i = 0; i < NZS; ++i) { mbar_init(&z_full[i], 8); mbar_init(&z_empty[i], 1); }\n"
+       "    for (int i = 0; i < NXB; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 8); }\n"
        "    mbar_init(done, 1);\n    mbar_fence_init();\n  }\n"
        "  if (warp == 8) {\n"
        "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" :: \"r\"(smem_addr(tmem_slot)));\n"
@@ -691,15 +717,15 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "#pragma unroll\n      for (int j = 0; j < DIMY; ++j) yv[j] = valid ? __ldg(Y + row * DIMY + j) : 0.f;\n"
        "#pragma unroll 1\n      for (int q = Q0; q < Q1; ++q, ++uq) {\n"
        "        const int dz = P_DZ[q];\n"
-       "        const u32 xb = uq & 1u;\n"
-       "        mbar_wait_t(&x_full[xb], (uq >> 1) & 1u, 23);\n"
+       "        const u32 xb = uq % NXB;\n"
+       "        mbar_wait_t(&x_full[xb], (uq / NXB) & 1u, 23);\n"
        "#pragma unroll 1\n        for (int k = 0; k < dz; ++k, ++ug) {\n"
-       "          const u32 zs = ug & 1u;\n"
+       "          const u32 zs = ug % NZS;\n"
        "          unsigned char* z = zt + zs * TB;\n"
-       "          mbar_wait_t(&z_empty[zs], ((ug >> 1) & 1u) ^ 1u, 21);\n"
+       "          mbar_wait_t(&z_empty[zs], ((ug / NZS) & 1u) ^ 1u, 21);\n"
        "          {\n"
        "            const unsigned char* xs = xs0 + (xb * NX) * XSLOT;\n"
-       "            switch (q) {\n";
+       "            if (!(UVW_EXP & 32)) switch (q) {\n";
   for (int q = first; q < first + count; ++q)
     o << "              case " << q << ": zw_" << q << "(k, xs, yv, m, sub, z); break;\n";
   o << "            }\n"
@@ -729,31 +755,34 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "    }\n"
        "  }\n"
        "  else if (warp == 8) {\n"
-       "    const u64 gh0 = sdesc128(smem_addr(gzt)), zh0 = sdesc64(smem_addr(zt));\n"
+       "    const u64 gh0 = sdesc128(smem_addr(gzt)), zh0 = sdesc128(smem_addr(zt));\n"
        "    const u32 id_w = (1u << 4) | (2u << 7) | (2u << 10) | ((u32)(64 >> 3) << 17) | ((u32)(64 >> 4) << 24);\n"
        "    u32 ug = 0; i64 lt = 0;\n"
        "    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {\n"
        "      for (int q = Q0; q < Q1; ++q) {\n"
        "        const int dz = P_DZ[q];\n"
        "        for (int k = 0; k < dz; ++k, ++ug) {\n"
-       "          const u32 st = ug & 1u, ph = (ug >> 1) & 1u;\n"
-       "          mbar_wait_t(&gz_full[st], ph, 26);\n"
+          "          const u32 st = ug % NZS, ph = (ug / NZS) & 1u, gs = ug % NGZ;\n"
+       "          mbar_wait_t(&gz_full[gs], (ug / NGZ) & 1u, 26);\n"
        "          mbar_wait_t(&z_full[st], ph, 28);\n"
        "          tc_fence_after();\n"
        "          if (elect_one()) {\n"
-       "            const u64 gh = gh0 + (u64)((st * TB) >> 4), gl = gh + (u64)((TB / 2) >> 4);\n"
+       "            const u64 gh = gh0 + (u64)((gs * TB) >> 4), gl = gh + (u64)((TB / 2) >> 4);\n"
        "            const u64 zh = zh0 + (u64)((st * TB) >> 4), zl = zh + (u64)((TB / 2) >> 4);\n"
        "            const u32 dw = tmem + 64 * (q - Q0);\n"
        "            const u32 first = (lt == 0 && k == 0) ? 1u : 0u;\n"
        "#pragma unroll\n            for (int s = 0; s < KR / 8; ++s) {\n"
-       // z' (A): SW64 blocks of 16 rows (4 KB); gz (B): SW128 blocks of 32 rows (8 KB)
-       "              const u64 o = (u64)(((s >> 1) * 4096 + (s & 1) * 32) >> 4);\n"
+       // z' (A) and gz (B): SW128, one 128-byte line of 32 batch rows per operand row
+       // (z' was SW64 with 16-row blocks: its producer stores were 2-way bank conflicted)
+       "              const u64 o = (u64)(((s >> 2) * 8192 + (s & 3) * 32) >> 4);\n"
        "              const u64 ob = (u64)(((s >> 2) * 8192 + (s & 3) * 32) >> 4);\n"
+       "              if (!(UVW_EXP & 16)) {\n"
        "              tc_mma(dw, zh + o, gh + ob, id_w, (first && s == 0) ? 0u : 1u);\n"
        "              tc_mma(dw, zh + o, gl + ob, id_w, 1u);\n"
        "              tc_mma(dw, zl + o, gh + ob, id_w, 1u);\n"
+       "              }\n"
        "            }\n"
-       "            tc_commit(&gz_empty[st]);\n            tc_commit(&z_empty[st]);\n"
+       "            tc_commit(&gz_empty[gs]);\n            tc_commit(&z_empty[st]);\n"
        "          }\n"
        "          __syncwarp();\n"
        "        }\n"
@@ -766,8 +795,8 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "      u32 uq = 0;\n"
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
        "        for (int q = Q0; q < Q1; ++q, ++uq) {\n"
-       "          const u32 xb = uq & 1u;\n"
-       "          mbar_wait_t(&x_empty[xb], ((uq >> 1) & 1u) ^ 1u, 29);\n"
+       "          const u32 xb = uq % NXB;\n"
+       "          mbar_wait_t(&x_empty[xb], ((uq / NXB) & 1u) ^ 1u, 29);\n"
        "          const int dx = P_DX[q];\n"
        "          mbar_expect_tx(&x_full[xb], 4 * KR * 64 * dx);\n"
        "          const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
@@ -786,8 +815,8 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "      for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x)\n"
        "        for (int q = Q0; q < Q1; ++q)\n"
        "          for (int k = 0; k < P_DZ[q]; ++k, ++ug) {\n"
-       "            const u32 st = ug & 1u;\n"
-       "            mbar_wait_t(&gz_empty[st], ((ug >> 1) & 1u) ^ 1u, 31);\n"
+       "            const u32 st = ug % NGZ;\n"
+       "            mbar_wait_t(&gz_empty[st], ((ug / NGZ) & 1u) ^ 1u, 31);\n"
        "            mbar_expect_tx(&gz_full[st], TB);\n"
        "            unsigned char* d = gzt + st * TB;\n"
        "            for (int b = 0; b < KR / 32; ++b) {\n"
