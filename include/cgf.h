@@ -364,7 +364,12 @@ int cgf_conv_shard_create(int64_t nodes, int64_t edges, const int64_t* row_ptr, 
 int cgf_conv_shard_info(const cgf_conv_shard* shard, int64_t info[6]);
 void cgf_conv_shard_destroy(cgf_conv_shard* shard);
 /* ConvPlan::forward / backward (conv.hpp:99-111) and the double-backward over
- * the partition; device pointers to the rank's rows, mode CGF_CONV_*. */
+ * the partition; device pointers to the rank's rows, mode CGF_CONV_*. With
+ * P > 1 in the deterministic mode the forward's all-gather runs on the shard's
+ * own stream while the rows whose neighbours are all local compute, and the
+ * backward's exchange runs while the rank's own neighbour rows compute (events
+ * order both against `stream`); results are bit-identical to the unoverlapped
+ * path, which CGF_DIST_OVERLAP=0 selects. */
 int cgf_dist_conv_forward(cgf_plan* plan, int dtype, const cgf_conv_shard* shard, void* nccl_comm,
                           const void* node_x, const void* edge_y, const void* edge_w, void* node_z, int mode,
                           void* stream);
