@@ -125,6 +125,37 @@ template <class T> DEVI T warp_sum(T v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// Warp sums of 2^P per-lane values at once, by recursive halving: in the round
+// with lane offset o each lane keeps half of its values and adds the partner's
+// copy of that half (lanes with bit o set keep the upper half), so the values
+// in flight halve every round; the remaining rounds are plain butterflies.
+// Every lane returns the total of value index warp_sum_n_idx<P>(lane); the
+// lanes sharing the top P lane bits hold the same (bit-identical) total.
+// 2^P (+1 .. 5-P) shuffles instead of 5 per value.
+template <class T, int P> DEVI T warp_sum_n(T* v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < P; ++r) {
+    const int o = 16 >> r, k = (1 << P) >> (r + 1);
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < k; ++i) {
+      const T snd = up ? v[i] : v[i + k];
+      const T kp = up ? v[i + k] : v[i];
+      v[i] = kp + __shfl_xor_sync(0xffffffffu, snd, o);
+    }
+  }
+  T t = v[0];
+#pragma unroll
+  for (int o = 16 >> P; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+template <int P> DEVI int warp_sum_n_idx(int lane) {
+  int j = 0;
+#pragma unroll
+  for (int r = 0; r < P; ++r) j = (j << 1) | ((lane >> (4 - r)) & 1);
+  return j;
+}
 )RT";
 }
 
@@ -247,6 +278,7 @@ class Gen {
   void emit_unit_body_edge_pair_bwd(int k);
   std::string wsrc(const Sub& s, long long step, const std::string& arr) const;
   void emit_gy_reduce(const std::string& rowexpr, const std::string& arr = "gy");
+  void emit_multi_sum(int n, const std::function<std::string(int)>& src, const std::string& use);
   void emit_gy_flush_row(const std::string& rowexpr);
   void emit_gy_resume(const std::string& rowexpr);
   void emit_class_loop_open(int k);
@@ -948,10 +980,9 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
              << s.w_stride << " + lane] = g; }\n";
         }
       }
-      if (gfl && out_y())
-        for (int j = 0; j < s.dy(); ++j)
-          o_ << "        { const T s_ = warp_sum(gyl" << X << "[" << j << "]); if (lane == " << j % 32 << ") gya["
-             << s.y_off + j << "] += s_; }\n";
+      if (gfl && out_y())  // each gya entry is always updated by the same lane (same dy -> same mapping)
+        emit_multi_sum(s.dy(), [&](int j) { return "gyl" + X + "[" + S(j) + "]"; },
+                       "gya[" + S(s.y_off) + " + j_] += s_;");
     }
     o_ << "      }\n";
     if (post_sub)
@@ -1038,14 +1069,44 @@ void Gen::emit_unit_body_edge_pair_bwd(int k) {
   }
 }
 
+// The warp sums of n <= 32 per-lane values src(0 .. n-1) in one recursive-
+// halving reduction (warp_sum_n); `use(j, s)` consumes total j in one lane.
+void Gen::emit_multi_sum(int n, const std::function<std::string(int)>& src, const std::string& use) {
+  if (n == 1 || !cfg_.multi_sum) {  // one butterfly per value (CGF_GEN=nomsum: the A/B baseline)
+    for (int j = 0; j < n; ++j)
+      o_ << "      { const T s_ = warp_sum(" << src(j) << "); if (lane == " << j << ") { const int j_ = " << j << "; "
+         << use << " } }\n";
+    return;
+  }
+  // split n into reductions of 2^P values (zero-padded) minimising issued
+  // instructions: a halving round costs 2 selects + a shuffle + an add per value
+  // pair (FP64: 4 + 2 + 1), a plain round a shuffle + an add (FP64: 2 + 1)
+  const int pair = cfg_.f64 ? 7 : 4, plain = cfg_.f64 ? 3 : 2;
+  auto cost = [&](int P) { return pair * ((1 << P) - 1) + plain * (5 - P); };
+  std::vector<int> best(n + 1, 1 << 30), pick(n + 1, 0);
+  best[0] = 0;
+  for (int m = 1; m <= n; ++m)
+    for (int P = 0; P <= 5; ++P) {
+      const int c = cost(P) + best[m - std::min(m, 1 << P)];
+      if (c < best[m]) { best[m] = c; pick[m] = P; }
+    }
+  for (int done = 0; done < n;) {
+    const int P = pick[n - done], cnt = std::min(n - done, 1 << P);
+    o_ << "      { T v_[" << (1 << P) << "] = {";
+    for (int j = 0; j < (1 << P); ++j) o_ << (j ? ", " : "") << (j < cnt ? src(done + j) : std::string("(T)0"));
+    o_ << "};\n        const T s_ = warp_sum_n<T, " << P << ">(v_); const int j_ = " << done << " + warp_sum_n_idx<" << P
+       << ">(lane);\n        if ((lane & " << (1 << (5 - P)) - 1 << ") == 0 && j_ < " << done + cnt << ") { " << use
+       << " } }\n";
+    done += cnt;
+  }
+}
+
 void Gen::emit_gy_reduce(const std::string& rowexpr, const std::string& arr) {
   const int dy = p_.dim_y;
   for (int j0 = 0; j0 < dy; j0 += 32) {
-    o_ << "    { T mine = 0;\n";
-    for (int j = j0; j < std::min(dy, j0 + 32); ++j)
-      o_ << "      { const T s_ = warp_sum(" << arr << "[" << j << "]); if (lane == " << j - j0 << ") mine = s_; }\n";
-    o_ << "      if (lane < " << std::min(dy - j0, 32) << ") O1[" << rowexpr << " * (i64)" << dy << " + " << j0
-       << " + lane] " << (cfg_.gy_accum ? "+=" : "=") << " mine; }\n";
+    const int n = std::min(dy - j0, 32);
+    emit_multi_sum(n, [&](int j) { return arr + "[" + S(j0 + j) + "]"; },
+                   "O1[" + rowexpr + " * (i64)" + S(dy) + " + " + S(j0) + " + j_] " + (cfg_.gy_accum ? "+=" : "=") + " s_;");
   }
 }
 
@@ -1486,6 +1547,7 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "waitsleep") cfg.wait_sleep = true;
     else if (k == "nowaitsleep") cfg.wait_sleep = false;
     else if (k == "edgepart") cfg.edge_partials = true;
+    else if (k == "nomsum") cfg.multi_sum = false;
     else if (k == "l2hint") cfg.l2_hints = true;
     else if (k == "nol2hint") cfg.l2_hints = false;
     else if (k == "xregs") cfg.x_regs = true;
