@@ -798,6 +798,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "          const u32 xb = uq % NXB;\n"
        "          mbar_wait_t(&x_empty[xb], ((uq / NXB) & 1u) ^ 1u, 29);\n"
        "          const int dx = P_DX[q];\n"
+       "          if (UVW_EXP & 64) { mbar_arrive(&x_full[xb]); continue; }\n"
        "          mbar_expect_tx(&x_full[xb], 4 * KR * 64 * dx);\n"
        "          const TMap* mp = dx == 1 ? &tx1 : dx == 3 ? &tx3 : dx == 5 ? &tx5 : &tx7;\n"
        "          for (int cb = 0; cb < 4; ++cb)\n"
@@ -817,6 +818,7 @@ UvwSource generate_uvw_backward_w(const Problem& p, int first, int count) {
        "          for (int k = 0; k < P_DZ[q]; ++k, ++ug) {\n"
        "            const u32 st = ug % NGZ;\n"
        "            mbar_wait_t(&gz_empty[st], ((ug / NGZ) & 1u) ^ 1u, 31);\n"
+       "            if (UVW_EXP & 128) { mbar_arrive(&gz_full[st]); continue; }\n"
        "            mbar_expect_tx(&gz_full[st], TB);\n"
        "            unsigned char* d = gzt + st * TB;\n"
        "            for (int b = 0; b < KR / 32; ++b) {\n"
