@@ -213,6 +213,10 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   cfg.w_shared = w_shared != 0;
   cfg.aligned = aligned != 0;
   cfg.edge_partials = variant == 1;
+  // output stores by compile-time-unrolled lane loops: the batched double-
+  // backward -2 % (FP32) / -8 % (FP64); the forward and single backward kernels
+  // are 2-7 % slower with them (profiles/r02_ab_ustore.jsonl)
+  cfg.unrolled_stores = comp == cgf::Comp::DBwd && loop == cgf::Loop::Rows;
   // Batched fwd / bwd keep y in registers (prefetched a row ahead); the
   // double-backward needs those registers for its three z' accumulators.
   // FP64 backward reads y from the slot instead: the 2 x dim_y doubles of

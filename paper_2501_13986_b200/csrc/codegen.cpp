@@ -80,6 +80,20 @@ DEVI void coop_store16(void* dst, const void* src, int n16, int lane) {
   float4* d = (float4*)dst;
   for (int i = lane; i < n16; i += 32) __stcs(d + i, s[i]);
 }
+// The same with the count known at compile time: the lane loop is unrolled
+// (no per-iteration index / compare / branch / descriptor moves).
+template <int N> DEVI void coop_store16n(void* dst, const void* src, int lane) {
+  const float4* s = (const float4*)src;
+  float4* d = (float4*)dst;
+#pragma unroll
+  for (int i0 = 0; i0 < N; i0 += 32)
+    if (N % 32 == 0 || i0 + lane < N) __stcs(d + i0 + lane, s[i0 + lane]);
+}
+template <int N, class T> DEVI void coop_storen(T* __restrict__ dst, const T* src, int lane) {
+#pragma unroll
+  for (int i0 = 0; i0 < N; i0 += 32)
+    if (N % 32 == 0 || i0 + lane < N) dst[i0 + lane] = src[i0 + lane];
+}
 // Atomic accumulation of a staged run into global memory (atomic-mode conv):
 // 16-byte vector reductions for FP32, scalar for FP64; results unused -> RED.
 DEVI void coop_red16(float* dst, const float* src, int n16, int lane) {
@@ -702,12 +716,17 @@ void Gen::emit_store(const std::string& dst, const std::string& rowexpr, std::ui
   for (int k = 0; k < width; ++k) o_ << " scr[lane * " << width << " + " << k << "] = " << reg << "[" << k << "];";
   o_ << " }\n      __syncwarp();\n";
   const bool vec = cfg_.aligned && al16(stride) && al16(off) && al16(step) && al16(words);
-  if (vec)
-    o_ << "      " << (atomic ? "coop_red16(" : "coop_store16(") << dst << " + " << rowexpr << " * (i64)" << stride
-       << " + " << O(off, step) << ", scr, " << words * sz_ / 16 << ", lane);\n";
+  const std::string at = dst + " + " + rowexpr + " * (i64)" + S(stride) + " + " + O(off, step);
+  if (atomic)
+    o_ << "      " << (vec ? "coop_red16(" : "coop_red(") << at << ", scr, " << (vec ? words * sz_ / 16 : words)
+       << ", lane);\n";
+  else if (!cfg_.unrolled_stores)
+    o_ << "      " << (vec ? "coop_store16(" : "coop_store(") << at << ", scr, " << (vec ? words * sz_ / 16 : words)
+       << ", lane);\n";
+  else if (vec)
+    o_ << "      coop_store16n<" << words * sz_ / 16 << ">(" << at << ", scr, lane);\n";
   else
-    o_ << "      " << (atomic ? "coop_red(" : "coop_store(") << dst << " + " << rowexpr << " * (i64)" << stride << " + "
-       << O(off, step) << ", scr, " << words << ", lane);\n";
+    o_ << "      coop_storen<" << words << ">(" << at << ", scr, lane);\n";
   o_ << "      __syncwarp();\n";
 }
 
@@ -1412,9 +1431,15 @@ void Gen::emit_conv_loop() {
         const auto& xc = u.x_chunks[c];
         const bool vec = cfg_.aligned && al16(p_.dim_x) && al16(xc.off) && al16(C.xstep[c]) && al16(xc.words) &&
                          al16(gx_base_[k] + gx_pre_[k][c]) && al16(gx_unit_[k]);
-        o_ << "      " << (vec ? "coop_store16(" : "coop_store(") << "O0 + row * (i64)" << p_.dim_x << " + "
-           << O(xc.off, C.xstep[c]) << ", gxs + " << O(gx_base_[k] + gx_pre_[k][c], gx_unit_[k]) << ", "
-           << (vec ? xc.words * sz_ / 16 : xc.words) << ", lane);\n";
+        const std::string at = "O0 + row * (i64)" + S(p_.dim_x) + " + " + O(xc.off, C.xstep[c]);
+        const std::string from = "gxs + " + O(gx_base_[k] + gx_pre_[k][c], gx_unit_[k]);
+        if (!cfg_.unrolled_stores)
+          o_ << "      " << (vec ? "coop_store16(" : "coop_store(") << at << ", " << from << ", "
+             << (vec ? xc.words * sz_ / 16 : xc.words) << ", lane);\n";
+        else if (vec)
+          o_ << "      coop_store16n<" << xc.words * sz_ / 16 << ">(" << at << ", " << from << ", lane);\n";
+        else
+          o_ << "      coop_storen<" << xc.words << ">(" << at << ", " << from << ", lane);\n";
       }
       o_ << "    }\n";
     }
@@ -1548,6 +1573,8 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "nowaitsleep") cfg.wait_sleep = false;
     else if (k == "edgepart") cfg.edge_partials = true;
     else if (k == "nomsum") cfg.multi_sum = false;
+    else if (k == "loopstores") cfg.unrolled_stores = false;
+    else if (k == "ustores") cfg.unrolled_stores = true;
     else if (k == "l2hint") cfg.l2_hints = true;
     else if (k == "nol2hint") cfg.l2_hints = false;
     else if (k == "xregs") cfg.x_regs = true;
