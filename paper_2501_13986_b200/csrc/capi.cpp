@@ -532,7 +532,8 @@ void run_uvw_grad_yw(cgf_plan* p, const void* x, const void* y, const void* w, c
   {
     const cgf::Kernel planes = cgf::load_kernel(us_y->prep);
     void* pargs[] = {&gza, &yh, &yl, &wh, &wl, &nrows, &pitch};
-    const unsigned pgrid = static_cast<unsigned>(std::min<std::int64_t>((rows + 31) / 32, planes.max_grid));
+    const std::int64_t pr = us_y->prep_rows;
+    const unsigned pgrid = static_cast<unsigned>(std::min<std::int64_t>((rows + pr - 1) / pr, planes.max_grid));
     CU_CHECK(cgf::drv::cuLaunchKernel(planes.fn, pgrid, 1, 1, 256, 1, 1, us_y->prep.smem_bytes, st, pargs, nullptr));
   }
   auto plane_map = [&](CUtensorMap* m, void* base, bool rows_inner) {

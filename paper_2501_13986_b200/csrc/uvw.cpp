@@ -365,15 +365,21 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
   // kernels, one block per 32 rows staged in shared memory:
   //   gy:  YH / YL [plane][row][64 r]      (the gy MMA's A tiles, K = r)
   //   gW:  WH / WL [plane][64 r][pitch]    (the gW MMA's B tiles, K = rows)
+  // rows per block: 32 (3 blocks / SM, 128-byte gW-plane segments) measured
+  // 2.41 ms against 3.15 ms for 16 rows (6 blocks / SM, half-line segments;
+  // profiles/r02_ab_planes.txt)
+  const int pr = std::getenv("CGF_UVW_PLANE_ROWS") ? std::atoi(std::getenv("CGF_UVW_PLANE_ROWS")) : 32;
+  if (pr != 16 && pr != 32) throw UnsupportedError("CGF_UVW_PLANE_ROWS must be 16 or 32");
+  o << "#define PR " << pr << "\n";
   o << "extern \"C\" __global__ void __launch_bounds__(256) cgf_uvw_bwd_planes_f32(const float* __restrict__ GZ,"
        " float* __restrict__ YH, float* __restrict__ YL, float* __restrict__ WH, float* __restrict__ WL, i64 rows,"
        " i64 pitch) {\n"
-       "  extern __shared__ float t[];  // [32][DIMZ + 1] (odd pitch: conflict-free column reads)\n"
-       "  const i64 chunks = (rows + 31) / 32;\n"
+       "  extern __shared__ float t[];  // [PR][DIMZ + 1] (odd pitch: conflict-free column reads)\n"
+       "  const i64 chunks = (rows + PR - 1) / PR;\n"
        "  for (i64 cbk = blockIdx.x; cbk < chunks; cbk += gridDim.x) {\n"
-       "    const i64 r0 = cbk * 32;\n"
+       "    const i64 r0 = cbk * PR;\n"
        "    __syncthreads();\n"
-       "    for (int e = threadIdx.x; e < 8 * DIMZ; e += 256) {  // 16-byte loads\n"
+       "    for (int e = threadIdx.x; e < PR / 4 * DIMZ; e += 256) {  // 16-byte loads\n"
        "      const int rr = e / (DIMZ / 4), c = 4 * (e - rr * (DIMZ / 4));\n"
        "      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);\n"
        "      if (r0 + rr < rows) v = __ldg((const float4*)(GZ + (r0 + rr) * DIMZ + c));\n"
@@ -385,8 +391,8 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
     o << "    // segment " << si << ": z offset " << zoff << ", " << dz << " components, planes " << pl0 << ".."
       << pl0 + dz - 1 << "\n"
       // gy planes: 4 consecutive r per 16-byte store
-      << "    for (int e = threadIdx.x; e < 32 * 16 * " << dz << "; e += 256) {\n"
-      << "      const int j = e & 15, rr = (e >> 4) & 31, k = e >> 9;\n"
+      << "    for (int e = threadIdx.x; e < PR * 16 * " << dz << "; e += 256) {\n"
+      << "      const int j = e & 15, rr = (e >> 4) % PR, k = (e >> 4) / PR;\n"
       << "      if (r0 + rr < rows) {\n"
       << "        const float* sr = t + rr * (DIMZ + 1) + " << zoff << " + k;\n"
       << "        float v[4], h[4];\n#pragma unroll\n        for (int a = 0; a < 4; ++a) { v[a] = sr[(4 * j + a) * " << dz
@@ -395,8 +401,8 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
       << "        __stcs((float4*)(YH + o), make_float4(h[0], h[1], h[2], h[3]));\n"
       << "        __stcs((float4*)(YL + o), make_float4(v[0] - h[0], v[1] - h[1], v[2] - h[2], v[3] - h[3]));\n      }\n    }\n"
       // gW planes: 4 consecutive rows per 16-byte store
-      << "    for (int e = threadIdx.x; e < 8 * 64 * " << dz << "; e += 256) {\n"
-      << "      const int q4 = e & 7, r = (e >> 3) & 63, k = e >> 9;\n"
+      << "    for (int e = threadIdx.x; e < PR / 4 * 64 * " << dz << "; e += 256) {\n"
+      << "      const int q4 = e % (PR / 4), r = (e / (PR / 4)) & 63, k = e / (PR / 4) / 64;\n"
       << "      float v[4], h[4];\n#pragma unroll\n      for (int a = 0; a < 4; ++a) { v[a] = t[(4 * q4 + a) * (DIMZ + 1) + "
       << zoff << " + r * " << dz << " + k]; h[a] = tf32_hi(v[a]); }\n"
       << "      const i64 o = ((i64)(" << pl0 << " + k) * 64 + r) * pitch + r0 + 4 * q4;\n"
@@ -582,7 +588,8 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
   out.prep = out.main;
   out.prep.name = "cgf_uvw_bwd_planes_f32";
   out.prep.threads = 256;
-  out.prep.smem_bytes = 32 * (p.dim_z + 1) * 4;
+  out.prep.smem_bytes = pr * (p.dim_z + 1) * 4;
+  out.prep_rows = pr;
   out.wimg_bytes = 0;
   out.dims_x = nplanes;  // number of gz planes (the caller sizes the plane buffers)
   return out;

@@ -30,6 +30,7 @@ struct UvwSource {
   std::size_t wimg_bytes = 0;
   int tile_rows = 128;
   int dims_x = 0;
+  int prep_rows = 32;  // batch rows per block of the prep kernel (the gz planes pre-pass)
 };
 
 UvwSource generate_uvw_forward(const Problem& p);
