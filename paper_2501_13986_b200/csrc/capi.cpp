@@ -143,11 +143,12 @@ int convi_groups(const cgf_plan* p, cgf::Comp comp, int dtype) {
   const int nu = static_cast<int>(p->units.size());
   if (const int g = group_env("CGF_CONVI_GROUPS", nu)) return g;
   const std::size_t zbytes = static_cast<std::size_t>(p->problem.dim_z) * (dtype == CGF_F64 ? 8 : 4);
+  // Re-swept after the multi-value warp sums (profiles/r02_sweep_groups2.jsonl)
   int g = 1;
-  if (comp == cgf::Comp::Bwd)  // FP64 C4: 164 -> 83 ms at G = 8; FP32 C4 / C5: G = 1 is fastest
-    g = dtype == CGF_F64 && zbytes > 32768 ? 8 : 1;
-  else  // DBwdX: C4 FP32 110 -> 90 ms (G = 4), C4 FP64 290 -> 189 ms (G = 2), C5 139 -> 127 ms (G = 2)
-    g = dtype == CGF_F32 && zbytes > 16384 ? 4 : 2;
+  if (comp == cgf::Comp::Bwd)  // FP64 C4: 164 -> 59 ms at G = 8, C5 FP64: 119 -> 108 ms at G = 2; FP32: G = 1
+    g = dtype == CGF_F64 ? (zbytes > 32768 ? 8 : 2) : 1;
+  else  // DBwdX: C4 FP32 101 -> 83 ms and FP64 267 -> 158 ms at G = 2; C5 FP32 fastest at G = 1
+    g = dtype == CGF_F32 && zbytes <= 16384 ? 1 : 2;
   return std::clamp(g, 1, nu);
 }
 
