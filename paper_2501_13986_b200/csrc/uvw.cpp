@@ -282,12 +282,10 @@ DEVI void tc_ld32(u32 taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 DEVI void prod_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-// element (row r of the operand, K index k) of a K-major SW64 tile whose K
-// runs over the 128 batch rows: 16-row K blocks 4 KB apart (64 operand rows)
-DEVI u32 kmaj_rows(int r, int k) { return (u32)((k >> 4) * 4096 + sw64(r, (k & 15) >> 2) + (k & 3) * 4); }
-// the same element of a K-major SW128 tile of 32 batch rows (one 128-byte line
-// per operand row, 16-byte chunks XOR the row's index in its 8-row atom): 32
-// lanes holding consecutive K of one operand row store 128 contiguous bytes
+// element (row r of the operand, K index k) of a K-major SW128 tile whose K
+// runs over 32 batch rows (one 128-byte line per operand row, 16-byte chunks
+// XOR the row's index in its 8-row atom): 32 lanes holding consecutive K of
+// one operand row store 128 contiguous bytes
 DEVI u32 kmaj128(int r, int k) { return (u32)((r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) ^ r) & 7) << 4) + (k & 3) * 4); }
 )";
 }
@@ -599,11 +597,11 @@ UvwSource generate_uvw_backward_y(const Problem& p) {
 // for instructions [first, first + count) (count <= 6: one 64-column TMEM
 // accumulator each):
 //   gW_q[r][c] += sum_row sum_k gz[row][q.z][r][k] z'_k[row][c],  z'_k = CG(x, y)[.., k]
-// (kernelgen.cpp:639-650 summed over rows): tcgen05 M=64 (c), N=64 (r), K = 64
-// batch rows per stage, both operands K-major over the rows, 3xTF32. The z'
-// tiles are written transposed by the producers, the gz^T tiles come by TMA
-// from the transposed gz planes (cgf_uvw_bwd_planes_f32); both are double
-// buffered, so the producers write stage s+1 while the MMAs consume stage s.
+// (kernelgen.cpp:639-650 summed over rows): tcgen05 M=64 (c), N=64 (r), K = 32
+// batch rows per stage, both operands K-major over the rows (SW128), 3xTF32.
+// The z' tiles are written transposed by the producers (double buffered), the
+// gz^T tiles come by TMA from the transposed gz planes (cgf_uvw_bwd_planes_f32)
+// through a ring of NGZ stages that runs ahead of the MMAs.
 // Accumulators live in TMEM across all tiles of the CTA and are written once
 // as this CTA's partial; `prep` sums the partials over CTAs in a fixed order
 // (deterministic).
