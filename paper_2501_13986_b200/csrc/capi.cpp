@@ -277,7 +277,10 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
     //    deeper ring here): 40.4 -> 34.5 ms
     //  * double-backward passes: one slot per warp, 4 CTAs / SM: 123 -> 116 ms
     // and the FP64 large-row backward: one slot per warp, 82.6 -> 75.4 ms (C4)
-    if (small && dtype == CGF_F32 && loop == cgf::Loop::ConvByOutput && comp == cgf::Comp::Fwd) cfg.pair_edges = true;
+    if (small && dtype == CGF_F32 && loop == cgf::Loop::ConvByOutput && comp == cgf::Comp::Fwd) {
+      cfg.pair_edges = true;
+      cfg.min_blocks = 4;  // 4 CTAs / SM: C5 forward 12.96 -> 12.22 ms (profiles/r02_ab_c5occ.jsonl)
+    }
     if (small && dtype == CGF_F32 && loop == cgf::Loop::ConvByInput && comp == cgf::Comp::Bwd) {
       cfg.pair_edges = true;
       cfg.depth = 1;
