@@ -241,3 +241,29 @@ def test_bench_gpus_2_launches_two_ranks_cpu_harness():
     assert rec["harness"] and rec["n_gpus"] == 2 and rec["conv"]["n_gpus"] == 2
     assert "all_to_all_single" in rec["conv"]["collectives"]
 
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_overlap_row_ranges(world):
+    """GraphShard.local_rows: every row in the range reads only the rank's own
+    node rows (so it may run during the all-gather), 4-aligned; own_rows: the
+    rank's own slot of the padded neighbour rows, 4-aligned. On a lattice the
+    local fraction falls as the slabs thin out."""
+    p, dist = pkg()
+    n, src, nbr = dist.lattice_radius_graph(12, 1.0, 2.0)
+    g = p.Graph(n, src, nbr)
+    fracs = []
+    for r in range(world):
+        sh = dist.GraphShard(g, world, r)
+        a, b = sh.local_rows()
+        assert a % 4 == 0 and b % 4 == 0 and 0 <= a <= b <= sh.out_nodes
+        lo, hi = r * sh.chunk, r * sh.chunk + sh.out_nodes
+        e0, e1 = sh.row_ptr[a], sh.row_ptr[b]
+        assert ((sh.nbr[e0:e1] >= lo) & (sh.nbr[e0:e1] < hi)).all()
+        oa, ob = sh.own_rows()
+        assert oa % 4 == 0 and ob % 4 == 0 and r * sh.chunk <= oa and ob <= (r + 1) * sh.chunk
+        fracs.append((b - a) / max(sh.out_nodes, 1))
+    if world == 1:
+        assert fracs[0] > 0.99
+    else:
+        assert min(fracs) < 1.0
