@@ -937,6 +937,22 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
       o_ << l.str();
     }
     // ---- per-chunk epilogues ----
+    // forward, kind B, two merged chunks: the per-channel weight application of
+    // both chunks as one paired FP32 op per component (fma.rn.f32x2: each half
+    // the same fma as before, so the bits do not change)
+    bool w_paired = false;
+    if (f2 && out_z() && cfg_.comp == Comp::Fwd && cfg_.pair_weights) {
+      const Sub& s0 = p_.subs[u.subs[g]];
+      const Sub& s1 = p_.subs[u.subs[g + n]];
+      if (s0.kind == Kind::B && s1.kind == Kind::B && s0.dz() == dz && s1.dz() == dz) {
+        const std::string P0 = "pz" + S(u.z_piece_of(s0)), P1 = "pz" + S(u.z_piece_of(s1));
+        if (P0 != P1)
+        for (int kk = 0; kk < dz; ++kk)
+          o_ << "        fma2v(wt_0, wt_1, zx_0[" << kk << "], zx_1[" << kk << "], " << P0 << "[" << kk << "], " << P1
+             << "[" << kk << "]);\n";
+        w_paired = P0 != P1;
+      }
+    }
     for (int c = 0; c < m; ++c) {
       const int qi = g + c * n;
       const Sub& s = p_.subs[u.subs[qi]];
@@ -945,7 +961,7 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
       const long long swq = Cl.sw[qi];
       const std::string gzs = reads_gz() ? S(L.gz_slot.at(s.z_off)) : "";
       // weight application (z-type outputs)
-      if (out_z()) {
+      if (out_z() && !w_paired) {
         const bool dzm = cfg_.comp != Comp::Fwd;  // dgz = W.(za+zb) + dC.zx
         if (s.kind == Kind::B) {
           for (int kk = 0; kk < dz; ++kk) {
@@ -1575,6 +1591,8 @@ void apply_gen_flags(KernelConfig& cfg, const std::string& flags) {
     else if (k == "nomsum") cfg.multi_sum = false;
     else if (k == "loopstores") cfg.unrolled_stores = false;
     else if (k == "ustores") cfg.unrolled_stores = true;
+    else if (k == "pairw") cfg.pair_weights = true;
+    else if (k == "nopairw") cfg.pair_weights = false;
     else if (k == "l2hint") cfg.l2_hints = true;
     else if (k == "nol2hint") cfg.l2_hints = false;
     else if (k == "xregs") cfg.x_regs = true;

@@ -75,6 +75,7 @@ struct KernelConfig {
   bool wait_sleep = false;  // consumer waits: mbarrier.try_wait with a suspend-time hint
   bool l2_hints = false;    // conv loops: L2 evict_last for gathered node rows, evict_first for per-edge streams
   bool unrolled_stores = false;  // staged output pieces stored by a compile-time-unrolled lane loop (else a runtime loop)
+  bool pair_weights = true;  // forward, 2 merged kind-B chunks: the weight application as fma.rn.f32x2
   bool multi_sum = true;      // dy warp sums by recursive halving (warp_sum_n) instead of one butterfly per value
   bool edge_partials = false;  // ConvEdges backward: g_node_x as per-edge partial rows (O0 + eid * dim_x, plain stores)
   std::string tag;          // appended to the kernel name (e.g. the group "g1of3")
