@@ -127,6 +127,13 @@ DEVI void fma2v(float a0, float a1, float b0, float b1, float& c0, float& c1) {
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(B));
   asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(C));
 }
+DEVI void mul2v(float a0, float a1, float b0, float b1, float& r0, float& r1) {
+  u64 A, B, R;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(R) : "l"(A), "l"(B));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r0), "=f"(r1) : "l"(R));
+}
 DEVI void mul2s(float a, float b0, float b1, float& r0, float& r1) {
   u64 A, B, R;
   asm("mov.b64 %0, {%1, %1};" : "=l"(A) : "f"(a));
@@ -795,6 +802,13 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
     for (int c = 0; c < m; ++c) o_ << " " << u.subs[g + c * n];
     o_ << ": " << (s0.kind == Kind::B ? "B" : "C") << " l=(" << s0.l1 << "," << s0.l2 << "," << s0.l3 << ") b=" << s0.b
        << " b'=" << s0.bp << " nnz=" << s0.cg->entries.size() << (m > 1 ? " x" + S(m) + " chunks" : "") << "\n";
+    // two merged kind-B chunks of a backward: their gz*w products and their gW
+    // chains go out as paired FP32 ops (each half the same op, same bits)
+    bool pair_b = false;
+    if (f2 && cfg_.pair_weights && cfg_.comp == Comp::Bwd) {
+      const Sub& s1 = p_.subs[u.subs[g + n]];
+      pair_b = s0.kind == Kind::B && s1.kind == Kind::B && s1.dz() == dz && !cfg_.w_shared;
+    }
     // ---- per-chunk operands ----
     for (int c = 0; c < m; ++c) {
       const int qi = g + c * n;
@@ -843,7 +857,11 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
       }
       if (reads_gz()) {
         o_ << "        T gzp" << X << "[" << dz << "];" << (need_gzc ? " T gzc" + X + "[" + S(dz) + "];" : "") << "\n";
-        if (s.kind == Kind::B) {
+        if (s.kind == Kind::B && pair_b) {
+          if (c == 1)  // both chunks' operands are in place now
+            for (int kk = 0; kk < dz; ++kk)
+              o_ << "        mul2v(wt_0, wt_1, gz_0[" << kk << "], gz_1[" << kk << "], gzp_0[" << kk << "], gzp_1[" << kk << "]);\n";
+        } else if (s.kind == Kind::B) {
           for (int kk = 0; kk < dz; ++kk)
             o_ << "        gzp" << X << "[" << kk << "] = wt" << X << " * gz" << X << "[" << kk << "];"
                << (need_gzc ? " gzc" + X + "[" + S(kk) + "] = ct" + X + " * gz" + X + "[" + S(kk) + "];" : "") << "\n";
@@ -873,6 +891,12 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
     for (const auto& e : s0.cg->entries) {
       const std::string v = "(T)" + hexd(e.v), I = S(e.i), K = S(e.k);
       const int J = s0.y_off + e.j;
+      // v * (a0, a1) into (r0, r1): a paired multiply, or (|v| = 1, exact either way) a copy
+      auto mul2 = [&](const std::string& a0, const std::string& a1, const std::string& r0, const std::string& r1) {
+        if (e.v == 1.0) return " " + r0 + " = " + a0 + "; " + r1 + " = " + a1 + ";";
+        if (e.v == -1.0) return " " + r0 + " = -" + a0 + "; " + r1 + " = -" + a1 + ";";
+        return " mul2s(" + v + ", " + a0 + ", " + a1 + ", " + r0 + ", " + r1 + ");";
+      };
       std::ostringstream l;
       l << "        { const T cy = " << v << " * " << Y(J) << ";";
       if (dual()) l << " const T cb = " << v << " * " << DB(J) << ";";
@@ -892,8 +916,8 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
           // AX = fma(cb, gzp, fma(cy, gzc, AX)); GY = fma(v a, gzp, fma(v x, gzc, GY)) per chunk
           l << " fma2s(cy, gzc_0[" << K << "], gzc_1[" << K << "], " << A0 << "[" << I << "], " << A1 << "[" << I << "]);"
             << " fma2s(cb, gzp_0[" << K << "], gzp_1[" << K << "], " << A0 << "[" << I << "], " << A1 << "[" << I << "]);"
-            << " { T t0_, t1_, u0_, u1_; mul2s(" << v << ", xv_0[" << I << "], xv_1[" << I << "], t0_, t1_); mul2s(" << v
-            << ", av_0[" << I << "], av_1[" << I << "], u0_, u1_);";
+            << " { T t0_, t1_, u0_, u1_;" << mul2("xv_0[" + I + "]", "xv_1[" + I + "]", "t0_", "t1_")
+            << mul2("av_0[" + I + "]", "av_1[" + I + "]", "u0_", "u1_");
           if (gfl)
             l << " fma2v(t0_, t1_, gzc_0[" << K << "], gzc_1[" << K << "], " << GYc(0, s_0) << ", " << GYc(1, s_1) << ");"
               << " fma2v(u0_, u1_, gzp_0[" << K << "], gzp_1[" << K << "], " << GYc(0, s_0) << ", " << GYc(1, s_1) << "); }";
@@ -903,7 +927,7 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
         }
         if (cfg_.comp == Comp::Bwd) {
           l << " fma2s(cy, gzp_0[" << K << "], gzp_1[" << K << "], " << A0 << "[" << I << "], " << A1 << "[" << I << "]);"
-            << " { T t0_, t1_; mul2s(" << v << ", xv_0[" << I << "], xv_1[" << I << "], t0_, t1_);";
+            << " { T t0_, t1_;" << mul2("xv_0[" + I + "]", "xv_1[" + I + "]", "t0_", "t1_");
           if (gfl)
             l << " fma2v(t0_, t1_, gzp_0[" << K << "], gzp_1[" << K << "], " << GYc(0, s_0) << ", " << GYc(1, s_1) << "); }";
           else
@@ -1003,7 +1027,18 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
         auto zk = [&](int kk) {
           return cfg_.comp == Comp::Bwd ? "zx" + X + "[" + S(kk) + "]" : "(za" + X + "[" + S(kk) + "] + zb" + X + "[" + S(kk) + "])";
         };
-        if (s.kind == Kind::B) {
+        if (s.kind == Kind::B && pair_b) {
+          if (c == 1) {  // both chunks' chains side by side
+            const int q0 = g;
+            const Sub& sa = p_.subs[u.subs[q0]];
+            o_ << "        { T g0 = 0, g1 = 0;";
+            for (int kk = 0; kk < dz; ++kk)
+              o_ << " fma2v(gz_0[" << kk << "], gz_1[" << kk << "], zx_0[" << kk << "], zx_1[" << kk << "], g0, g1);";
+            o_ << " if (lane < " << sa.b << ") O2[" << wrow << " * (i64)" << nw << " + " << O(sa.w_off, Cl.sw[q0])
+               << " + lane] = g0; if (lane < " << s.b << ") O2[" << wrow << " * (i64)" << nw << " + " << O(s.w_off, swq)
+               << " + lane] = g1; }\n";
+          }
+        } else if (s.kind == Kind::B) {
           o_ << "        { T g = 0;";
           for (int kk = 0; kk < dz; ++kk) o_ << " g = fma(gz" << X << "[" << kk << "], " << zk(kk) << ", g);";
           o_ << " if (lane < " << s.b << ") O2[" << wrow << " * (i64)" << nw << " + " << O(s.w_off, swq) << " + lane] = g; }\n";
