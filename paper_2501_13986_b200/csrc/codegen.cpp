@@ -1063,6 +1063,14 @@ void Gen::emit_unit_body(int k, const std::function<void(int)>& post_sub) {
 // The forward of two edges of a row (sub-slots sb_ and sb_ + LW, y in ya_ /
 // yb_) side by side as paired FP32 ops; edge b's contribution is added after
 // edge a's in every z piece (and skipped when the item has one edge).
+// v * (a0, a1) into (r0, r1) as emitted code: a paired multiply, or for
+// |v| = 1 (exact either way) a copy / negation
+std::string mul2_coef(double v, const std::string& a0, const std::string& a1, const std::string& r0, const std::string& r1) {
+  if (v == 1.0) return " " + r0 + " = " + a0 + "; " + r1 + " = " + a1 + ";";
+  if (v == -1.0) return " " + r0 + " = -" + a0 + "; " + r1 + " = -" + a1 + ";";
+  return " mul2s((T)" + hexd(v) + ", " + a0 + ", " + a1 + ", " + r0 + ", " + r1 + ");";
+}
+
 void Gen::emit_unit_body_edge_pair(int k) {
   const Unit& u = U0(k);
   const Layout& L = lay_[k];
@@ -1083,7 +1091,7 @@ void Gen::emit_unit_body_edge_pair(int k) {
        << ") ? sb_[LW + " << ws << " + lane] : (T)0;\n        T za[" << dz << "] = {}, zb[" << dz << "] = {};\n";
     for (const auto& e : s.cg->entries) {
       const int J = s.y_off + e.j;
-      o_ << "        { T ca_, cb_; mul2s((T)" << hexd(e.v) << ", ya_[" << J << "], yb_[" << J << "], ca_, cb_); fma2v(ca_, cb_, xa["
+      o_ << "        { T ca_, cb_;" << mul2_coef(e.v, "ya_[" + S(J) + "]", "yb_[" + S(J) + "]", "ca_", "cb_") << " fma2v(ca_, cb_, xa["
          << e.i << "], xb[" << e.i << "], za[" << e.k << "], zb[" << e.k << "]); }\n";
     }
     for (int kk = 0; kk < dz; ++kk)
@@ -1122,11 +1130,13 @@ void Gen::emit_unit_body_edge_pair_bwd(int k) {
     o_ << " }\n        const T wa = (lane < " << s.b << ") ? sb_[" << ws << " + lane] : (T)0, wb = (lane < " << s.b
        << ") ? sb_[LW + " << ws << " + lane] : (T)0;\n        T pa[" << dz << "], pb[" << dz << "], za[" << dz
        << "] = {}, zb[" << dz << "] = {};\n       ";
-    for (int kk = 0; kk < dz; ++kk) o_ << " pa[" << kk << "] = wa * ga[" << kk << "]; pb[" << kk << "] = wb * gb[" << kk << "];";
+    for (int kk = 0; kk < dz; ++kk)
+      o_ << (cfg_.pair_weights ? " mul2v(wa, wb, ga[" + S(kk) + "], gb[" + S(kk) + "], pa[" + S(kk) + "], pb[" + S(kk) + "]);"
+                               : " pa[" + S(kk) + "] = wa * ga[" + S(kk) + "]; pb[" + S(kk) + "] = wb * gb[" + S(kk) + "];");
     o_ << "\n";
     for (const auto& e : s.cg->entries) {
       const std::string v = "(T)" + hexd(e.v), I = S(e.i), K = S(e.k), Jg = S(s.y_off + e.j);
-      o_ << "        { T ca_, cb_; mul2s(" << v << ", ya_[" << Jg << "], yb_[" << Jg << "], ca_, cb_);"
+      o_ << "        { T ca_, cb_;" << mul2_coef(e.v, "ya_[" + Jg + "]", "yb_[" + Jg + "]", "ca_", "cb_")
          << " fma2v(ca_, cb_, pa[" << K << "], pb[" << K << "], axa" << AX << "[" << I << "], axb" << AX << "[" << I << "]);"
          << " { const T t_ = " << v << " * xv[" << I << "]; fma2s(t_, pa[" << K << "], pb[" << K << "], gya[" << Jg
          << "], gyb[" << Jg << "]); }"
