@@ -266,7 +266,8 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
     // capping registers for 3 CTAs / SM measured C4 FP32 12.9 -> 11.1 ms (the
     // backward and the small-TP (C5) kernels are slower that way,
     // profiles/r02_ab_conv2.jsonl)
-    if (!small && loop == cgf::Loop::ConvByOutput && comp == cgf::Comp::Fwd && dtype == CGF_F32) cfg.min_blocks = 3;
+    // FP64 likewise: C4 FP64 19.55 -> 17.76 ms (profiles/r02_ab_conv3/4.jsonl; C5 FP64 is slower that way)
+    if (!small && loop == cgf::Loop::ConvByOutput && comp == cgf::Comp::Fwd) cfg.min_blocks = 3;
     // two consecutive edges of a row per staged item for the large-row
     // by-output kernels: C4 forward FP32 11.1 -> 10.5 ms, FP64 21.3 -> 19.5 ms
     // (profiles/r02_ab_epi.jsonl); the small-TP (C5) kernels are slower
