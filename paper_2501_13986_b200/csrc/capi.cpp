@@ -291,8 +291,14 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
       cfg.depth = 1;
       cfg.min_blocks = 4;
     }
-    if (!small && dtype == CGF_F64 && loop == cgf::Loop::ConvByInput && comp == cgf::Comp::Bwd) cfg.depth = 1;
+    if (dtype == CGF_F64 && loop == cgf::Loop::ConvByInput && comp == cgf::Comp::Bwd) cfg.depth = 1;
   }
+  // FP64 double-backward family (batched and both conv passes) and the small
+  // FP64 by-neighbour backward: one slot per warp beats a deeper ring (more
+  // CTAs resident): C4 conv dbl-bwd 157 -> 141 ms, C2 dbl-bwd 20.3 -> 19.1 ms,
+  // C5 backward 108 -> 92 ms (profiles/r02_ab_dbwd_knobs.jsonl)
+  if (dtype == CGF_F64 && (comp == cgf::Comp::DBwd || comp == cgf::Comp::DBwdZ || comp == cgf::Comp::DBwdX))
+    cfg.depth = 1;
   // x chunks / y in registers once per staged item: C4 conv double-backward
   // FP64 189.6 -> 179.4 ms, FP32 91.0 -> 88.0; C2 FP64 backward 11.40 -> 10.87
   // ms; the forward kernels are neutral or slower (profiles/r02_ab_flags.jsonl)
