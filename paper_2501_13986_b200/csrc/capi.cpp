@@ -299,6 +299,8 @@ std::shared_ptr<cgf::KernelSource> source_for(cgf_plan* p, cgf::Comp comp, cgf::
   // C5 backward 108 -> 92 ms (profiles/r02_ab_dbwd_knobs.jsonl)
   if (dtype == CGF_F64 && (comp == cgf::Comp::DBwd || comp == cgf::Comp::DBwdZ || comp == cgf::Comp::DBwdX))
     cfg.depth = 1;
+  // FP32 batched double-backward: two slots per warp, C2 25.7 -> 25.4 ms (profiles/r02_ab_c2dbwd.jsonl)
+  if (dtype == CGF_F32 && comp == cgf::Comp::DBwd && loop == cgf::Loop::Rows) cfg.depth = 2;
   // x chunks / y in registers once per staged item: C4 conv double-backward
   // FP64 189.6 -> 179.4 ms, FP32 91.0 -> 88.0; C2 FP64 backward 11.40 -> 10.87
   // ms; the forward kernels are neutral or slower (profiles/r02_ab_flags.jsonl)
