@@ -501,8 +501,13 @@ def conv_leg(args, rank, world, dev, harness=False):
                                              for i in range(len(laps[0]) - 1)]
 
     ms, (ag_ms, f_ms, b_ms, rs_ms) = timed(step)
-    ov_ms, ov_f, ov_b = (ms, f_ms + ag_ms, b_ms + rs_ms) if world == 1 else (lambda r: (r[0], *r[1]))(
-        timed(step_overlap))
+    ov_err = None
+    try:
+        ov_ms, ov_f, ov_b = (ms, f_ms + ag_ms, b_ms + rs_ms) if world == 1 else (lambda r: (r[0], *r[1]))(
+            timed(step_overlap))
+    except Exception as exc:  # keep the unoverlapped measurement if the overlapped path fails
+        ov_err = repr(exc)[:300]
+        ov_ms, ov_f, ov_b = ms, f_ms + ag_ms, b_ms + rs_ms
     t = torch.tensor([ms, f_ms, b_ms, ag_ms, rs_ms, ov_ms, ov_f, ov_b], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -527,7 +532,7 @@ def conv_leg(args, rank, world, dev, harness=False):
                               "step_overlapped": ov_mx, "forward_with_all_gather_overlapped": ovf_mx,
                               "backward_with_exchange_overlapped": ovb_mx},
         "overlap": {"local_rows": list(sh.local_rows()), "own_neighbour_rows": list(sh.own_rows()),
-                    "out_nodes": sh.out_nodes, "in_nodes": sh.in_nodes} if world > 1 else None,
+                    "out_nodes": sh.out_nodes, "in_nodes": sh.in_nodes, "error": ov_err} if world > 1 else None,
         "rank0_roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
                            "forward": {"GB/s": fb / (f_ms / 1e3) / 1e9, "frac": fb / (f_ms / 1e3) / 1e9 / peak},
                            "backward": {"GB/s": bb / (b_ms / 1e3) / 1e9, "frac": bb / (b_ms / 1e3) / 1e9 / peak}},
