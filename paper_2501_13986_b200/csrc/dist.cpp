@@ -330,7 +330,9 @@ int cgf_dist_conv_forward(cgf_plan* plan, int dtype, const cgf_conv_shard* sh, v
     const std::size_t es = dtype == CGF_F64 ? 8 : 4;
     const auto rp = static_cast<const int64_t*>(sh->row_ptr);
     const auto nb = static_cast<const int32_t*>(sh->nbr);
-    if (!overlap_on(sh, mode) || sh->la >= sh->lb) {
+    // the collective must not depend on this rank's ranges (an empty range just
+    // moves all rows after the all-gather)
+    if (!overlap_on(sh, mode)) {
       DevScratch pad(es * dx * sh->chunk, stream), all(es * dx * sh->in_nodes, stream);
       all_gather(sh, dtype, comm, node_x, dx, all.p, pad, stream);
       rc_check(cgf_conv_forward_shard(plan, dtype, sh->out_nodes, sh->in_nodes, sh->edges, rp, nb, all.p, edge_y,
@@ -378,7 +380,7 @@ int cgf_dist_conv_backward(cgf_plan* plan, int dtype, const cgf_conv_shard* sh, 
     const auto trp = static_cast<const int64_t*>(sh->t_row_ptr);
     const auto tsrc = static_cast<const int32_t*>(sh->t_src);
     const auto teid = static_cast<const int32_t*>(sh->t_eid);
-    if (!overlap_on(sh, mode) || sh->oa >= sh->ob) {
+    if (!overlap_on(sh, mode)) {
       rc_check(cgf_conv_backward_shard(plan, dtype, sh->out_nodes, sh->in_nodes, sh->edges, trp, tsrc, teid, all.p,
                                        edge_y, edge_w, g_node_z, part.p, g_edge_y, g_edge_w, mode, stream));
       ordered_reduce(sh, dtype, comm, part.p, dx, g_node_x, stream);

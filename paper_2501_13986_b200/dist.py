@@ -243,11 +243,13 @@ class DistConvPlan:
     def forward_gathered(self, node_x, edge_y, edge_w):
         """(node_z rows of this rank, the padded all-gathered node_x) — the
         latter reusable by ``backward(node_x_all=...)``."""
+        # the collective a rank issues must not depend on its own row ranges
+        # (ranks with an empty local range still take the overlapped path)
         sh = self.shard
-        a, b = sh.local_rows() if self.overlap else (0, 0)
-        if a == b:
+        if not self.overlap:
             x_all = self._all_gather(node_x)
             return self.local.forward_shard(sh, x_all, edge_y, edge_w, mode=self.mode), x_all
+        a, b = sh.local_rows()
         x_all, work = self._all_gather_async(node_x)
         z = self.local.forward_shard(sh, x_all, edge_y, edge_w, mode=self.mode, rows=(a, b))
         work.wait()
@@ -259,10 +261,12 @@ class DistConvPlan:
     def backward(self, node_x, edge_y, edge_w, g_node_z, node_x_all=None):
         sh = self.shard
         x_all = self._all_gather(node_x) if node_x_all is None else node_x_all
-        a, b = sh.own_rows() if self.overlap else (0, 0)
-        if a == b:
+        if not self.overlap:
             gx_part, gy, gw = self.local.backward_shard(sh, x_all, edge_y, edge_w, g_node_z, mode=self.mode)
             return self._reduce_scatter(gx_part), gy, gw
+        # every rank exchanges point to point here, also one whose own range is
+        # empty (then all its rows run before the exchange)
+        a, b = sh.own_rows()
         outs = None
         for r0, r1 in ((0, a), (b, sh.in_nodes)):  # other ranks' neighbour rows first
             if r0 < r1:

@@ -159,13 +159,22 @@ def _inputs(o, g, dt=np.float64):
     return nx, ey, ew, gnz, dgx, dgy, dgw
 
 
-def _rank_main(rank, world, port, js, outdir, overlap=True):
+def ring_graph(n):
+    """n nodes, each with its two ring neighbours (sorted CSR): tiny shards whose
+    own / local row ranges are empty on some ranks and not on others."""
+    src = np.repeat(np.arange(n), 2)
+    nbr = np.stack([(np.arange(n) - 1) % n, (np.arange(n) + 1) % n], 1).reshape(-1)
+    order = np.lexsort((nbr, src))
+    return O.make_graph(n, src[order], nbr[order])
+
+
+def _rank_main(rank, world, port, js, outdir, overlap=True, graph="small"):
     import torch.distributed as tdist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         p, dist = pkg()
-        og = small_graph()
+        og = small_graph() if graph == "small" else ring_graph(int(graph[4:]))
         o = O.Oracle(js)
         g = p.Graph(og.nodes, og.src, og.nbr)
         sh = dist.GraphShard(g, world, rank)
@@ -220,6 +229,27 @@ def test_gloo_distributed_conv_matches_whole_graph(world, overlap, tmp_path):
                     ("oy", want_d[1]), ("ow", want_d[2]), ("ogz", want_d[3])):
         assert cat[k].shape == want.shape, k
         assert O.rel_error(cat[k], want) <= 1e-12, k
+
+
+def test_gloo_overlap_with_empty_ranges_on_some_ranks(tmp_path):
+    """13-node ring over 3 ranks: rank 0 has a non-empty own neighbour range,
+    ranks 1 and 2 do not. Every rank must still issue the same collectives
+    (no rank-dependent fallback), and the result equals the whole graph."""
+    import torch.multiprocessing as mp
+    p, dist = pkg()
+    og = ring_graph(13)
+    g = p.Graph(og.nodes, og.src, og.nbr)
+    empty = [dist.GraphShard(g, 3, r).own_rows()[0] == dist.GraphShard(g, 3, r).own_rows()[1] for r in range(3)]
+    assert any(empty) and not all(empty)
+    js = config("c1")
+    mp.spawn(_rank_main, args=(3, _free_port(), js, str(tmp_path), True, "ring13"), nprocs=3, join=True)
+    o = O.Oracle(js)
+    nx, ey, ew, gnz, dgx, dgy, dgw = _inputs(o, og)
+    want_z = o.conv_forward(og, nx, ey, ew)
+    want_b = o.conv_backward(og, nx, ey, ew, gnz)
+    got = {k: np.concatenate([np.load(tmp_path / f"r{r}_1.npz")[k] for r in range(3)]) for k in ("z", "gx", "gy", "gw")}
+    for k, want in (("z", want_z), ("gx", want_b[0]), ("gy", want_b[1]), ("gw", want_b[2])):
+        assert O.rel_error(got[k], want) <= 1e-12, k
 
 
 def test_bench_gpus_2_launches_two_ranks_cpu_harness():
